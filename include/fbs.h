@@ -1,0 +1,199 @@
+/*
+ * fbs.h — C ABI of the B200-native bilateral-space solve
+ *         (Fast Bilateral Solver, Barron & Poole, arXiv 1511.03296).
+ *
+ * The library implements the hot path of the paper's method on sm_100a:
+ *   grid build      simplified bilateral grid            PAPER.md:114-116 (Sec. 2, Eq. equiv)
+ *   bistochastize   Alg. 1                               PAPER.md:656-672 (Supp. Sec. 1)
+ *   assemble        A = λ(Dm − Dn B̄ Dn) + diag(Sc), b = S(c∘t)   PAPER.md:124-127 (Eq. quad_min)
+ *   precondition    Jacobi / hierarchical                PAPER.md:227-285 (Sec. 4, Eq. hier_precond)
+ *   initialise      flat / hierarchical                  PAPER.md:238-241, 287-293 (Eq. flat_init)
+ *   solve           PCG, Alg. 2                          PAPER.md:710-742 (Supp. Sec. 1)
+ *   slice           x̂ = Sᵀ ŷ                             PAPER.md:137-140 (Eq. solution)
+ *   backward        ∂f/∂t, ∂f/∂c by one more solve       PAPER.md:191-201 (Sec. 3)
+ * Readings of the paper where it is silent or ambiguous are numbered #1..#19 in
+ * DESIGN.md §3 (same numbering as SURVEY.md §8(c)).
+ *
+ * Conventions (all entry points)
+ *   - Every pointer argument named *_dev is DEVICE memory owned by the caller and only
+ *     borrowed for the enqueued work; pointers named *_host are HOST memory.
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
+ *     fbs_grid_build synchronises `stream` once at its end (to learn the data-dependent
+ *     vertex and pyramid-level counts); all other compute calls only enqueue.
+ *   - Layouts: RGB is interleaved uint8 [frames][H][W][3]; pixel vectors are planar float
+ *     [frames][K][H][W] (pixel p = y·W + x); confidences float [frames][H][W];
+ *     vertex vectors are float [M][K] in CANONICAL vertex order: ascending packed key
+ *     frame(8)‖by(16)‖bx(16)‖bl(8)‖bu(8)‖bv(8) (reading #3), frames concatenated.
+ *   - Return value: FBS_OK (0) or an FBS_E* code; fbs_last_error() gives a thread-local
+ *     message.  Data-dependent outcomes (breakdown, non-convergence) are reported by
+ *     fbs_system_stats after the stream has been synchronised.  No exception crosses
+ *     the ABI.  There is no CPU fallback: without a CUDA device every call fails with
+ *     FBS_ECUDA.
+ *   - Handles own their internal device buffers (allocated stream-ordered from the
+ *     device's default memory pool) and release them in *_destroy, which enqueues the
+ *     frees on the stream the handle was created on.
+ *   - Thread safety: a built grid is immutable; concurrent fbs_solve calls on distinct
+ *     streams with distinct outputs are allowed.  A system handle must not be used by
+ *     two streams at once.
+ */
+#ifndef FBS_H
+#define FBS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* fbs_stream; /* == cudaStream_t */
+typedef struct fbs_grid_s* fbs_grid;
+typedef struct fbs_system_s* fbs_system;
+
+/* ---------------------------------------------------------------- status codes */
+#define FBS_OK 0
+#define FBS_EINVAL 1 /* bad argument (see each call)                                   */
+#define FBS_ENOMEM 2 /* device allocation failed                                       */
+#define FBS_ECUDA 3  /* CUDA runtime error (message in fbs_last_error)                 */
+#define FBS_ELIMIT 4 /* structural limit exceeded: a σxy cell holds > 64 pixels, or a  */
+                     /* pyramid coarse cell has > 4096 children          */
+#define FBS_ESTATE 5 /* handle used in the wrong state (e.g. backward before forward)  */
+
+/* bits of the `status` word returned by fbs_system_stats */
+#define FBS_ST_BREAKDOWN 1     /* a (frame, channel) stopped on ρ = 0 or dᵀq ≤ 0 (reading #11) */
+#define FBS_ST_NOTCONVERGED 2  /* TOL mode: max_iters reached before ‖r‖ ≤ tol‖b‖           */
+
+/* ---------------------------------------------------------------- options */
+typedef struct {
+    int n_bistoch;     /* Alg. 1 iterations, fixed count (reading #5); default 20          */
+    int build_pyramid; /* 1: build the Supp. Sec. 2 pyramid (needed by HIER precond/init) */
+} fbs_grid_opts;
+
+enum { FBS_PRECOND_JACOBI = 0, FBS_PRECOND_HIER = 1 };
+enum { FBS_INIT_FLAT = 0, FBS_INIT_HIER = 1, FBS_INIT_ZERO = 2 };
+enum { FBS_MODE_FIXED = 0, FBS_MODE_TOL = 1 };
+
+typedef struct {
+    int precond;          /* FBS_PRECOND_*; default HIER                          */
+    int init;             /* FBS_INIT_*; default HIER                              */
+    int mode;             /* FBS_MODE_FIXED: exactly `iters` iterations (Alg. 2);   */
+                          /* FBS_MODE_TOL: stop when ‖r_i‖₂ ≤ tol·‖b‖₂ (recurrence residual,     */
+                          /* tested before every iteration incl. i = 0, reading #11)            */
+    int iters;            /* FIXED iteration count; default 25                    */
+    double tol;           /* TOL relative residual; default 1e-6                                 */
+    int max_iters;        /* TOL cap; default 2000                                               */
+    double precond_alpha; /* z_weight α, β of the preconditioner; default 2, 5    */
+    double precond_beta;
+    double init_alpha;    /* z_weight α, β of the initialisation; default 4, 0    */
+    double init_beta;
+} fbs_solve_opts;
+
+void fbs_default_grid_opts(fbs_grid_opts* o);
+void fbs_default_solve_opts(fbs_solve_opts* o);
+
+/* ---------------------------------------------------------------- grid */
+/* Build the simplified bilateral grid of `frames` independent reference images.
+ *   rgb_dev   uint8 [frames][height][width][3], device.
+ *   sigma_*   bandwidths of Eq. bilateral_affinity.  Pixel (x, y) with
+ *             integer luma/chroma numerators Yn,Un,Vn (reading #1) maps to the vertex
+ *             (⌊x/σxy⌋, ⌊y/σxy⌋, ⌊Yn/256σl⌋, ⌊Un/256σuv⌋, ⌊Vn/256σuv⌋), each one IEEE
+ *             fp64 division then floor (reading #2).
+ * Then runs opts->n_bistoch iterations of Alg. 1 and (if opts->build_pyramid) builds the
+ * pyramid of PAPER.md:745-766 (reading #8).  Synchronises `stream` once at the end.
+ * Errors: FBS_EINVAL if a pointer is NULL, frames ∉ [1, 256], height or width ∉
+ * [1, 65535·σxy], σxy < 1, σl < 1 or σuv < 1 (8-bit key fields), or a σxy cell would hold
+ * more than 64 pixels (σxy > 8); FBS_ELIMIT (see above); FBS_ENOMEM; FBS_ECUDA. */
+int fbs_grid_build(const uint8_t* rgb_dev, int frames, int height, int width, double sigma_xy,
+                   double sigma_l, double sigma_uv, const fbs_grid_opts* opts, fbs_stream stream,
+                   fbs_grid* out);
+
+/* Sizes of a built grid (host outputs; any pointer may be NULL).
+ *   frame_vertices_host  int64 [frames]      vertices per frame
+ *   level_vertices_host  int64 [n_levels]    Σ over frames of level-k vertex counts
+ *   frame_levels_host    int32 [frames]      pyramid levels of each frame (until 1 vertex) */
+int fbs_grid_info(fbs_grid g, int64_t* n_pixels, int64_t* n_vertices, int* n_levels,
+                  int64_t* frame_vertices_host, int64_t* level_vertices_host,
+                  int32_t* frame_levels_host);
+
+/* Copy the grid to host memory in canonical order (synchronous; any pointer may be NULL).
+ *   keys_host  uint64 [M]      packed keys (reading #3), strictly ascending
+ *   vid_host   int32  [N]      vertex of each pixel (S as a hard assignment)
+ *   nbr_host   int32  [M][10]  ±1 neighbours, slots (x−,x+,y−,y+,l−,l+,u−,u+,v−,v+), −1 absent
+ *   m_host     int32  [M]      splat counts m = S1
+ *   n_host     float  [M]      Alg. 1 result n (Dn = diag(n))
+ *   bistoch_residual_host      max|n∘B̄n − m| / max m after the last Alg. 1 step */
+int fbs_grid_export(fbs_grid g, uint64_t* keys_host, int32_t* vid_host, int32_t* nbr_host,
+                    int32_t* m_host, float* n_host, float* bistoch_residual_host);
+
+/* Pyramid level `level` ≥ 1 in canonical order (synchronous):
+ *   keys_host    uint64 [M_level]       level keys (fields halved `level` times)
+ *   parent_host  int32  [M_{level−1}]   parent (in level) of each level−1 vertex = S_{level−1}
+ *   count_host   int32  [M_level]       P(1): level-0 vertices under each level vertex */
+int fbs_pyramid_export(fbs_grid g, int level, uint64_t* keys_host, int32_t* parent_host,
+                       int32_t* count_host);
+
+void fbs_grid_destroy(fbs_grid g);
+
+/* ---------------------------------------------------------------- solve */
+/* Solve A y = b for K channels sharing one A (reading #13) and slice.
+ *   t_dev      float [frames][K][H][W]   targets
+ *   c_dev      float [frames][H][W]      confidences, ≥ 0 (not checked on device)
+ *   lambda     > 0                       smoothness weight λ
+ *   x_dev      float [frames][K][H][W]   output x̂ = Sᵀŷ (may alias nothing else)
+ *   y_dev      float [M][K] or NULL      bilateral-space solution ŷ
+ *   sys_out    receives the system handle (A-state, M⁻¹, ŷ) for fbs_solve_backward and
+ *              the stats/export calls; NULL = destroy it after the solve.
+ * Each (frame, channel) runs its own PCG scalars and stopping rule (reading #13).
+ * Errors: FBS_EINVAL (NULL pointer, K ∉ [1, 64], λ ≤ 0 or not finite, HIER precond/init
+ * on a grid built without pyramid, bad opts); FBS_ENOMEM; FBS_ECUDA. */
+int fbs_solve(fbs_grid g, const float* t_dev, int K, const float* c_dev, double lambda,
+              const fbs_solve_opts* opts, float* x_dev, float* y_dev, fbs_system* sys_out,
+              fbs_stream stream);
+
+/* Backward pass: given g = ∂f/∂x̂ [frames][K][H][W], solve A d = S g
+ * with the forward's preconditioner and stopping rule from d = 0 (reading #14), then
+ *   ∂f/∂t = c ∘ Sᵀd              → dt_dev float [frames][K][H][W]
+ *   ∂f/∂c = Σ_k Sᵀ(−d_k∘ŷ_k) + (Sᵀd_k)∘t_k   → dc_dev float [frames][H][W] (reading #15)
+ * t_dev and c_dev must be the same arrays (unchanged) that were passed to fbs_solve. */
+int fbs_solve_backward(fbs_system sys, const float* dldx_dev, const float* t_dev,
+                       const float* c_dev, float* dt_dev, float* dc_dev, fbs_stream stream);
+
+/* Per-(frame, channel) results (host outputs, synchronous; any pointer may be NULL):
+ *   iterations_host   int32  [frames*K]  PCG iterations run (forward)
+ *   relres_host       double [frames*K]  recurrence ‖r‖₂/‖b‖₂ at exit (forward)
+ *   bwd_iterations_host int32 [frames*K] iterations of the last backward solve
+ *   status_host       FBS_ST_* bits */
+int fbs_system_stats(fbs_system sys, int32_t* iterations_host, double* relres_host,
+                     int32_t* bwd_iterations_host, int32_t* status_host);
+
+/* Copy the assembled system to host memory (synchronous; any pointer may be NULL):
+ *   sc_host [M]  S c;   b_host [M][K]  S(c∘t);   diagA_host [M]  diag(A);
+ *   y0_host [M][K]  initial state;   y_host [M][K]  solution ŷ;
+ *   db_host [M][K]  ∂f/∂b of the last backward (zeros before any backward). */
+int fbs_system_export(fbs_system sys, float* sc_host, float* b_host, float* diagA_host,
+                      float* y0_host, float* y_host, float* db_host);
+
+void fbs_system_destroy(fbs_system sys);
+
+/* ---------------------------------------------------------------- operators (device, async) */
+/* x̂ = Sᵀy: y_dev float [M][K] canonical → x_dev float [frames][K][H][W]. */
+int fbs_slice(fbs_grid g, const float* y_dev, int K, float* x_dev, fbs_stream stream);
+/* out = S p: p_dev float [frames][K][H][W] → out_dev float [M][K]. */
+int fbs_splat(fbs_grid g, const float* p_dev, int K, float* out_dev, fbs_stream stream);
+/* out = B̄ v: v_dev, out_dev float [M] (reading #4). */
+int fbs_blur(fbs_grid g, const float* v_dev, float* out_dev, fbs_stream stream);
+/* out = A y and out = M⁻¹ r for the system's A and preconditioner; float [M][K]. */
+int fbs_system_apply_A(fbs_system sys, const float* y_dev, float* out_dev, fbs_stream stream);
+int fbs_system_apply_precond(fbs_system sys, const float* r_dev, float* out_dev,
+                             fbs_stream stream);
+
+/* ---------------------------------------------------------------- misc */
+const char* fbs_last_error(void);
+int fbs_version(void);
+/* Number of CUDA kernels this library has launched in this process (monotone counter). */
+int64_t fbs_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBS_H */

@@ -1,0 +1,18 @@
+"""B200-native bilateral-space solve (Fast Bilateral Solver, arXiv 1511.03296).
+
+The product is libfbs.so (C ABI: include/fbs.h, sm_100a kernels in csrc/); this package
+is its thin ctypes binding.  Importing it fails loudly if the library is missing.
+"""
+from .fbs import (  # noqa: F401
+    FbsError,
+    Grid,
+    System,
+    blur,
+    grid_build,
+    launch_count,
+    make_opts,
+    slice_,
+    solve,
+    splat,
+    version,
+)

@@ -1,0 +1,831 @@
+// api.cu — C ABI (include/fbs.h) and host orchestration of the sm_100a bilateral solver.
+// Unity build: this translation unit includes every kernel header of csrc/.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "fbs_common.cuh"
+#include "grid_kernels.cuh"
+#include "pyramid_kernels.cuh"
+#include "solve_kernels.cuh"
+
+namespace fbs {
+
+std::atomic<long long> g_launches{0};
+
+namespace {
+
+thread_local std::string t_err;
+
+struct Err : std::runtime_error {
+    int code;
+    Err(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        const int code = (e == cudaErrorMemoryAllocation) ? FBS_ENOMEM : FBS_ECUDA;
+        throw Err(code, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
+    do {                                                                                 \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                       \
+        ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
+        ck(cudaGetLastError(), #kernel);                                                 \
+    } while (0)
+
+int g_num_sms = 0;
+
+void device_setup(int* dev) {
+    ck(cudaGetDevice(dev), "cudaGetDevice");
+    static bool pool_done[64] = {};
+    if (*dev < 64 && !pool_done[*dev]) {
+        cudaMemPool_t pool;
+        ck(cudaDeviceGetDefaultMemPool(&pool, *dev), "cudaDeviceGetDefaultMemPool");
+        uint64_t thr = UINT64_MAX;
+        ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr), "mempool threshold");
+        int sms = 0;
+        ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, *dev), "sm count");
+        g_num_sms = sms;
+        ck(cudaFuncSetAttribute(k_pyr_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kCoarseCap * (int)sizeof(unsigned long long)),
+           "k_pyr_level smem");
+        pool_done[*dev] = true;
+    }
+}
+
+template <class T>
+T* dalloc(std::vector<void*>& list, size_t count, cudaStream_t s) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    ck(cudaMallocAsync(&p, count * sizeof(T), s), "cudaMallocAsync");
+    list.push_back(p);
+    return static_cast<T*>(p);
+}
+
+void free_all(std::vector<void*>& list, cudaStream_t s) {
+    for (void* p : list) cudaFreeAsync(p, s);
+    list.clear();
+}
+
+inline int grid_for(int64_t n, int threads = kThreads, int cap_per_sm = 16) {
+    int64_t b = (n + threads - 1) / threads;
+    const int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * cap_per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+int bitlen(int64_t v) {
+    int b = 0;
+    while (v > 0) {
+        ++b;
+        v >>= 1;
+    }
+    return b;
+}
+
+int guard(const char* where, const std::function<void()>& body);
+
+}  // namespace
+}  // namespace fbs
+
+using namespace fbs;
+
+// ===================================================================================== grid
+static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy, double sl, double suv,
+                            const fbs_grid_opts* opts, cudaStream_t s, fbs_grid* out) {
+    if (!rgb || !out) throw Err(FBS_EINVAL, "null pointer");
+    if (F < 1 || F > 256) throw Err(FBS_EINVAL, "frames must be in [1, 256]");
+    if (!(sxy >= 1.0) || !(sl >= 1.0) || !(suv >= 1.0) || !std::isfinite(sxy) || !std::isfinite(sl) ||
+        !std::isfinite(suv))
+        throw Err(FBS_EINVAL, "sigma_xy, sigma_l, sigma_uv must be finite and >= 1");
+    if (H < 1 || W < 1) throw Err(FBS_EINVAL, "height and width must be >= 1");
+    const int ncx = (int)std::floor((double)(W - 1) / sxy) + 1;
+    const int ncy = (int)std::floor((double)(H - 1) / sxy) + 1;
+    if (ncx > 65536 || ncy > 65536) throw Err(FBS_EINVAL, "image too large for 16-bit spatial key fields");
+    // widest cell: ⌈σxy⌉ columns at most; the kernel re-checks every cell
+    const int cw = (int)std::ceil(sxy);
+    if ((int64_t)std::min(cw, W) * std::min(cw, H) > kCellMaxPx)
+        throw Err(FBS_EINVAL, "a sigma_xy cell would hold more than 64 pixels (sigma_xy > 8 is not supported)");
+    const int64_t N = (int64_t)F * H * W;
+    if (N >= (1ll << 31) - 1) throw Err(FBS_EINVAL, "too many pixels (>= 2^31)");
+
+    int dev = 0;
+    device_setup(&dev);
+    fbs_grid g = new fbs_grid_s();
+    try {
+        g->F = F; g->H = H; g->W = W; g->sxy = sxy; g->sl = sl; g->suv = suv;
+        g->ncx = ncx; g->ncy = ncy; g->ncells = (int64_t)F * ncx * ncy; g->N = N;
+        g->n_bistoch = opts ? opts->n_bistoch : 20;
+        if (g->n_bistoch < 0) throw Err(FBS_EINVAL, "n_bistoch must be >= 0");
+        const bool want_pyr = opts ? opts->build_pyramid != 0 : true;
+        g->stream = s;
+        g->device = dev;
+        auto& A = g->allocs;
+
+        g->colStart = dalloc<int>(A, ncx + 1, s);
+        g->rowStart = dalloc<int>(A, ncy + 1, s);
+        LAUNCH(k_axis_bins, grid_for(W), kThreads, 0, s, W, sxy, ncx, g->colStart);
+        LAUNCH(k_axis_bins, grid_for(H), kThreads, 0, s, H, sxy, ncy, g->rowStart);
+
+        const int64_t ntiles = (g->ncells + kCellsPerBlock - 1) / kCellsPerBlock;
+        const int64_t maxTiles = std::max<int64_t>(ntiles, 1);
+        // scratch: tile counter + look-back state (+ error flag, + residual words)
+        unsigned* counter = dalloc<unsigned>(A, 1, s);
+        int* err = dalloc<int>(A, 4, s);
+        unsigned long long* state = dalloc<unsigned long long>(A, maxTiles, s);
+        ck(cudaMemsetAsync(counter, 0, sizeof(unsigned), s), "memset");
+        ck(cudaMemsetAsync(err, 0, 4 * sizeof(int), s), "memset");
+        ck(cudaMemsetAsync(state, 0, maxTiles * sizeof(unsigned long long), s), "memset");
+        g->vid = dalloc<int>(A, N, s);
+        uint64_t* keysCap = dalloc<uint64_t>(A, N, s);
+        int* mCap = dalloc<int>(A, N, s);
+        g->cellOff = dalloc<int>(A, g->ncells + 1, s);
+        g->frameOff = dalloc<int>(A, F + 1, s);
+        CellGeom geo{F, H, W, ncx, ncy, g->colStart, g->rowStart};
+        LAUNCH(k_grid_cells, (unsigned)ntiles, 256, 0, s, rgb, geo, 256.0 * sl, 256.0 * suv, g->ncells, counter,
+               state, keysCap, mCap, g->vid, g->cellOff, err);
+        LAUNCH(k_frame_offsets, 1, 288, 0, s, g->cellOff, F, (int64_t)ncx * ncy, g->frameOff);
+
+        // ---- sync 1: vertex counts (sizes the vertex arrays and the pyramid capacities)
+        std::vector<int> fo(F + 1);
+        int errh[4];
+        ck(cudaMemcpyAsync(fo.data(), g->frameOff, (F + 1) * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaMemcpyAsync(errh, err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaStreamSynchronize(s), "sync");
+        if (errh[0]) throw Err(FBS_ELIMIT, "a sigma_xy cell holds more than 64 pixels");
+        g->M = fo[F];
+        g->frameOffH.assign(fo.begin(), fo.end());
+        g->maxFrameM = 0;
+        for (int f = 0; f < F; ++f) g->maxFrameM = std::max<int64_t>(g->maxFrameM, fo[f + 1] - fo[f]);
+        g->keys = keysCap;
+        g->m = mCap;
+        const int64_t M = g->M;
+
+        g->nearv = dalloc<uint2>(A, M, s);
+        g->yoff = dalloc<int2>(A, M, s);
+        LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 8), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
+               g->ncells, g->nearv, g->yoff, err);
+
+        // ---- Alg. 1 (reading #5: fixed n_bistoch iterations)
+        g->n = dalloc<float>(A, M, s);
+        float* ntmp = dalloc<float>(A, M, s);
+        float* cur = ntmp;
+        float* nxt = g->n;
+        if (g->n_bistoch % 2 == 0) std::swap(cur, nxt);  // make the last write land in g->n
+        for (int it = 0; it < g->n_bistoch; ++it) {
+            LAUNCH(k_bistoch, grid_for(M), kThreads, 0, s, g->nearv, g->yoff, g->m, cur, nxt, (int)M, it == 0);
+            std::swap(cur, nxt);
+        }
+        if (g->n_bistoch == 0) {
+            std::vector<float> ones(M, 1.f);
+            ck(cudaMemcpyAsync(g->n, ones.data(), M * sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
+            ck(cudaStreamSynchronize(s), "sync");
+        }
+        unsigned* res2 = reinterpret_cast<unsigned*>(err + 2);
+        LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nearv, g->yoff, g->m, g->n, (int)M, res2);
+
+        // ---- pyramid (Supp. Sec. 2), levels 1 .. Lmax-1
+        int Lmax = 1;
+        if (want_pyr) {
+            const int64_t lmax = (int64_t)std::floor(65280.0 / (256.0 * sl));
+            const int64_t uvmax = (int64_t)std::floor(65408.0 / (256.0 * suv));
+            const int bits = std::max({bitlen(ncy - 1), bitlen(ncx - 1), bitlen(lmax), bitlen(uvmax)});
+            Lmax = std::min(1 + bits, kMaxLevels);
+        }
+        const uint64_t* keysK = g->keys;
+        const int* cellOffK = g->cellOff;
+        int ncxK = ncx, ncyK = ncy;
+        const int* countK = nullptr;  // level 0: P(1) = 1
+        std::vector<int*> lvFrameOffDev(Lmax, nullptr);
+        for (int k = 1; k < Lmax; ++k) {
+            Level& L = g->lv[k];
+            L.ncx = ((ncx - 1) >> k) + 1;
+            L.ncy = ((ncy - 1) >> k) + 1;
+            L.ncells = (int64_t)F * L.ncx * L.ncy;
+            L.keys = dalloc<uint64_t>(A, M, s);
+            L.cellOff = dalloc<int>(A, L.ncells + 1, s);
+            L.parent = dalloc<int>(A, M, s);
+            L.childStart = dalloc<int>(A, M + 1, s);
+            L.childList = dalloc<int>(A, M, s);
+            L.count = dalloc<int>(A, M, s);
+            unsigned long long* st2 = dalloc<unsigned long long>(A, L.ncells, s);
+            unsigned* ctr2 = dalloc<unsigned>(A, 1, s);
+            ck(cudaMemsetAsync(st2, 0, L.ncells * sizeof(unsigned long long), s), "memset");
+            ck(cudaMemsetAsync(ctr2, 0, sizeof(unsigned), s), "memset");
+            LAUNCH(k_pyr_level, (unsigned)L.ncells, 256, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK,
+                   ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, L.keys, L.parent, L.childStart, L.childList,
+                   L.cellOff, err);
+            // P(1): upper bound M on the level size; the kernel stops at the true size via childStart
+            lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
+            LAUNCH(k_frame_offsets, 1, 288, 0, s, L.cellOff, F, (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
+            keysK = L.keys;
+            cellOffK = L.cellOff;
+            ncxK = L.ncx;
+            ncyK = L.ncy;
+        }
+        // ---- sync 2: level sizes
+        std::vector<std::vector<int>> lfo(Lmax);
+        for (int k = 1; k < Lmax; ++k) {
+            lfo[k].resize(F + 1);
+            ck(cudaMemcpyAsync(lfo[k].data(), lvFrameOffDev[k], (F + 1) * sizeof(int), cudaMemcpyDeviceToHost, s),
+               "d2h");
+        }
+        ck(cudaMemcpyAsync(errh, err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaStreamSynchronize(s), "sync");
+        if (errh[0] & 8) throw Err(FBS_ELIMIT, "a pyramid coarse cell has more than 4096 children");
+        if (errh[0] & ~8) throw Err(FBS_ECUDA, "internal grid-build check failed (code " + std::to_string(errh[0]) + ")");
+        {
+            float e, mm;
+            std::memcpy(&e, &errh[2], 4);
+            std::memcpy(&mm, &errh[3], 4);
+            g->bistoch_residual = (mm > 0.f) ? e / mm : 0.f;
+        }
+        // per-frame level counts: first level with a single vertex (reading #8)
+        g->frameLevelsH.assign(F, Lmax);
+        for (int f = 0; f < F; ++f) {
+            int Lf = 1;
+            if (fo[f + 1] - fo[f] > 1) {
+                Lf = Lmax;
+                for (int k = 1; k < Lmax; ++k)
+                    if (lfo[k][f + 1] - lfo[k][f] == 1) { Lf = k + 1; break; }
+            }
+            g->frameLevelsH[f] = Lf;
+        }
+        int L = 1;
+        for (int f = 0; f < F; ++f) L = std::max(L, g->frameLevelsH[f]);
+        g->L = L;
+        g->has_pyramid = want_pyr;
+        for (int k = 1; k < L; ++k) {
+            g->lv[k].M = lfo[k][F];
+            g->lv[k].frameOff.assign(lfo[k].begin(), lfo[k].end());
+            LAUNCH(k_lift_count, grid_for(g->lv[k].M), kThreads, 0, s, countK, g->lv[k].childStart,
+                   g->lv[k].childList, (int)g->lv[k].M, g->lv[k].count);
+            countK = g->lv[k].count;
+        }
+        g->frameLevels = dalloc<int>(A, F, s);
+        ck(cudaMemcpyAsync(g->frameLevels, g->frameLevelsH.data(), F * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
+        ck(cudaStreamSynchronize(s), "sync");  // host vector lifetime for the H2D copy
+    } catch (...) {
+        free_all(g->allocs, s);
+        delete g;
+        throw;
+    }
+    *out = g;
+}
+
+// ===================================================================================== solve
+namespace {
+
+VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
+    fbs_grid g = S->g;
+    VecArgs a{};
+    a.K = S->K;
+    a.BPF = S->BPF;
+    a.M = g->M;
+    a.lam = (float)S->lam;
+    a.frameOff = g->frameOff;
+    a.nearv = g->nearv;
+    a.yoff = g->yoff;
+    a.n = g->n;
+    a.sc = S->sc;
+    a.diagA = S->diagA;
+    a.x = x;
+    a.r = S->rh;
+    a.d = S->dh;
+    a.q = S->qh;
+    a.s = S->sh;
+    a.b = b;
+    a.w0 = S->w0;
+    a.mu0 = S->mu0;
+    a.parent0 = (g->L > 1) ? g->lv[1].parent : nullptr;
+    a.acc1 = (g->L > 1) ? S->lvBuf[1] : nullptr;
+    a.M1 = (g->L > 1) ? g->lv[1].M : 0;
+    a.partial = S->partial;
+    a.counters = S->counters;
+    a.sc_ = sc;
+    a.tol_mode = S->o.mode == FBS_MODE_TOL;
+    a.tol2 = S->o.tol * S->o.tol;
+    a.max_iters = (S->o.mode == FBS_MODE_TOL) ? S->o.max_iters : S->o.iters;
+    return a;
+}
+
+// lift level-0 input `in0` [C][M] through all levels into S->lvBuf[k]
+void lift_all(fbs_system S, const float* in0, int C, cudaStream_t s) {
+    fbs_grid g = S->g;
+    const float* in = in0;
+    int64_t Min = g->M;
+    for (int k = 1; k < g->L; ++k) {
+        const Level& L = g->lv[k];
+        LAUNCH(k_lift, grid_for(L.M), kThreads, 0, s, in, Min, L.childStart, L.childList, L.M, C, S->lvBuf[k]);
+        in = S->lvBuf[k];
+        Min = L.M;
+    }
+}
+
+// project levels L-1 .. 1 in place (mult = μ_k if use_mu, else hier-init weights)
+void project_all(fbs_system S, int C, bool use_mu, double alpha, double beta, cudaStream_t s) {
+    fbs_grid g = S->g;
+    for (int k = g->L - 1; k >= 1; --k) {
+        const Level& L = g->lv[k];
+        const bool top = (k == g->L - 1);
+        const float* up = top ? nullptr : S->lvBuf[k + 1];
+        const int64_t Mup = top ? 0 : g->lv[k + 1].M;
+        const int* parent = top ? nullptr : g->lv[k + 1].parent;
+        LAUNCH(k_project, grid_for(L.M), kThreads, 0, s, S->lvBuf[k], L.M, up, Mup, parent, C,
+               use_mu ? S->mu[k] : nullptr, L.count, L.keys, g->frameLevels, k, alpha, beta);
+    }
+}
+
+// s = M⁻¹ r (hier) given w0 written; finishes the ρ reduction
+void hier_precond(fbs_system S, const VecArgs& a, int first, cudaStream_t s) {
+    lift_all(S, S->w0, S->K, s);
+    project_all(S, S->K, true, 0, 0, s);
+    const int nb = S->g->F * S->BPF;
+    LAUNCH(k_precond_finish, nb, kThreads, 0, s, a, first);
+}
+
+void pcg_iteration(fbs_system S, const VecArgs& a, cudaStream_t s) {
+    const int nb = S->g->F * S->BPF;
+    const bool hier = S->o.precond == FBS_PRECOND_HIER;
+    LAUNCH(k_spmv, nb, kThreads, 0, s, a);
+    if (hier) {
+        LAUNCH(k_update<true>, nb, kThreads, 0, s, a);
+        hier_precond(S, a, 0, s);
+    } else {
+        LAUNCH(k_update<false>, nb, kThreads, 0, s, a);
+    }
+    LAUNCH(k_direction, nb, kThreads, 0, s, a, 0);
+}
+
+// Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.
+void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
+    fbs_grid g = S->g;
+    const int nb = g->F * S->BPF;
+    const int FK = g->F * S->K;
+    const bool hier = S->o.precond == FBS_PRECOND_HIER;
+    LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK);
+    if (hier) {
+        auto k1 = k_residual0<true, true>;
+        auto k2 = k_residual0<true, false>;
+        if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
+        else LAUNCH(k2, nb, kThreads, 0, s, a);
+        hier_precond(S, a, 1, s);
+    } else {
+        auto k1 = k_residual0<false, true>;
+        auto k2 = k_residual0<false, false>;
+        if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
+        else LAUNCH(k2, nb, kThreads, 0, s, a);
+    }
+    LAUNCH(k_direction, nb, kThreads, 0, s, a, 1);
+    if (S->o.mode == FBS_MODE_FIXED) {
+        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, s);
+        return;
+    }
+    // TOL: device-side per-channel stopping; the host polls the active count one chunk behind
+    int* pin = nullptr;
+    ck(cudaHostAlloc(&pin, 2 * sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
+    cudaEvent_t ev[2];
+    ck(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming), "event");
+    const int chunk = 8;
+    int done = 0, slot = 0, pending = -1;
+    try {
+        while (done < S->o.max_iters) {
+            const int nit = std::min(chunk, S->o.max_iters - done);
+            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, s);
+            done += nit;
+            ck(cudaMemcpyAsync(&pin[slot], a.sc_.n_active, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+            ck(cudaEventRecord(ev[slot], s), "event");
+            if (pending >= 0) {
+                ck(cudaEventSynchronize(ev[pending]), "event sync");
+                if (pin[pending] == 0) break;
+            }
+            pending = slot;
+            slot ^= 1;
+        }
+        ck(cudaStreamSynchronize(s), "sync");
+    } catch (...) {
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        cudaFreeHost(pin);
+        throw;
+    }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
+    cudaFreeHost(pin);
+}
+
+PcgScalars alloc_scalars(std::vector<void*>& A, int FK, cudaStream_t s) {
+    PcgScalars p;
+    p.rho = dalloc<double>(A, FK, s);
+    p.alpha = dalloc<double>(A, FK, s);
+    p.beta = dalloc<double>(A, FK, s);
+    p.bb = dalloc<double>(A, FK, s);
+    p.rr = dalloc<double>(A, FK, s);
+    p.active = dalloc<int>(A, FK, s);
+    p.iters = dalloc<int>(A, FK, s);
+    p.status = dalloc<int>(A, FK, s);
+    p.n_active = dalloc<int>(A, 1, s);
+    ck(cudaMemsetAsync(p.iters, 0, FK * sizeof(int), s), "memset");
+    ck(cudaMemsetAsync(p.status, 0, FK * sizeof(int), s), "memset");
+    ck(cudaMemsetAsync(p.rr, 0, FK * sizeof(double), s), "memset");
+    ck(cudaMemsetAsync(p.bb, 0, FK * sizeof(double), s), "memset");
+    return p;
+}
+
+void validate_opts(const fbs_solve_opts& o, fbs_grid g) {
+    if (o.precond != FBS_PRECOND_JACOBI && o.precond != FBS_PRECOND_HIER) throw Err(FBS_EINVAL, "bad precond");
+    if (o.init != FBS_INIT_FLAT && o.init != FBS_INIT_HIER && o.init != FBS_INIT_ZERO) throw Err(FBS_EINVAL, "bad init");
+    if (o.mode != FBS_MODE_FIXED && o.mode != FBS_MODE_TOL) throw Err(FBS_EINVAL, "bad mode");
+    if (o.mode == FBS_MODE_FIXED && o.iters < 0) throw Err(FBS_EINVAL, "iters must be >= 0");
+    if (o.mode == FBS_MODE_TOL && (o.max_iters < 0 || !(o.tol >= 0.0))) throw Err(FBS_EINVAL, "bad tol/max_iters");
+    if ((o.precond == FBS_PRECOND_HIER || o.init == FBS_INIT_HIER) && !g->has_pyramid)
+        throw Err(FBS_EINVAL, "hierarchical precond/init need a grid built with build_pyramid = 1");
+    if (o.precond == FBS_PRECOND_HIER && !(o.precond_alpha > 0.0)) throw Err(FBS_EINVAL, "precond_alpha must be > 0");
+    if (o.init == FBS_INIT_HIER && !(o.init_alpha > 0.0)) throw Err(FBS_EINVAL, "init_alpha must be > 0");
+}
+
+}  // namespace
+
+static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double lam, const fbs_solve_opts* opts,
+                       float* x, float* y, fbs_system* sys_out, cudaStream_t s) {
+    if (!g || !t || !c || !x) throw Err(FBS_EINVAL, "null pointer");
+    if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
+    if (!(lam > 0.0) || !std::isfinite(lam)) throw Err(FBS_EINVAL, "lambda must be finite and > 0");
+    fbs_solve_opts o;
+    if (opts) o = *opts; else fbs_default_solve_opts(&o);
+    validate_opts(o, g);
+    int dev = 0;
+    device_setup(&dev);
+
+    fbs_system S = new fbs_system_s();
+    try {
+        S->g = g;
+        S->K = K;
+        S->lam = lam;
+        S->o = o;
+        S->stream = s;
+        const int64_t M = g->M;
+        const int F = g->F;
+        auto& A = S->allocs;
+        // launch geometry of the per-frame kernels: BPF blocks per frame
+        int occ = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv, kThreads, 0), "occupancy");
+        const int64_t want = (g->maxFrameM + kThreads - 1) / kThreads;
+        const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
+        S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
+        S->C = K + 1;
+        const size_t KM = (size_t)K * M;
+        S->sc = dalloc<float>(A, M, s);
+        S->b = dalloc<float>(A, KM, s);
+        S->diagA = dalloc<float>(A, M, s);
+        S->mu0 = dalloc<float>(A, M, s);
+        S->y0 = dalloc<float>(A, KM, s);
+        S->xh = dalloc<float>(A, KM, s);
+        S->rh = dalloc<float>(A, KM, s);
+        S->dh = dalloc<float>(A, KM, s);
+        S->qh = dalloc<float>(A, KM, s);
+        S->sh = dalloc<float>(A, KM, s);
+        const bool hierP = o.precond == FBS_PRECOND_HIER, hierI = o.init == FBS_INIT_HIER;
+        if (hierP || hierI) {
+            S->w0 = dalloc<float>(A, (size_t)S->C * M, s);
+            for (int k = 1; k < g->L; ++k) {
+                S->lvBuf[k] = dalloc<float>(A, (size_t)S->C * g->lv[k].M, s);
+                if (hierP) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
+            }
+        }
+        S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * K, s);
+        S->counters = dalloc<unsigned>(A, F, s);
+        ck(cudaMemsetAsync(S->counters, 0, F * sizeof(unsigned), s), "memset");
+        S->fwd = alloc_scalars(A, F * K, s);
+
+        const int nb = F * S->BPF;
+        CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
+        // a4: splat Sc, b = S(c∘t)
+        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 8), 256, 0, s, geo, g->cellOff, g->vid, c, t, K, M, S->sc,
+               S->b);
+        // a5: assemble (+ flat/zero init)
+        VecArgs a = make_args(S, S->fwd, S->xh, S->b);
+        LAUNCH(k_assemble, nb, kThreads, 0, s, a, S->diagA, S->mu0, hierP ? S->w0 : nullptr, o.init, S->fwd);
+        // a6/a7: hierarchical preconditioner multipliers and init
+        if (hierP) {
+            lift_all(S, S->w0, 1, s);
+            for (int k = 1; k < g->L; ++k)
+                LAUNCH(k_mu, grid_for(g->lv[k].M), kThreads, 0, s, S->lvBuf[k], g->lv[k].count, g->lv[k].keys,
+                       g->frameLevels, g->lv[k].M, k, o.precond_alpha, o.precond_beta, S->mu[k]);
+        }
+        if (hierI) {
+            LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, K, S->w0);
+            lift_all(S, S->w0, K + 1, s);
+            project_all(S, K + 1, false, o.init_alpha, o.init_beta, s);
+            LAUNCH(k_init_finish, grid_for(M), kThreads, 0, s, S->w0, M, K, a.parent0, a.acc1, a.M1, S->xh);
+        }
+        ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
+        // a8: PCG
+        run_pcg(S, a, false, s);
+        // a9: slice
+        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, S->xh, M, K, F, (int64_t)g->H * g->W, 1, x);
+        if (y) LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, S->xh, M, K, y);
+    } catch (...) {
+        free_all(S->allocs, s);
+        delete S;
+        throw;
+    }
+    if (sys_out) {
+        *sys_out = S;
+    } else {
+        free_all(S->allocs, s);
+        delete S;
+    }
+}
+
+static void backward_impl(fbs_system S, const float* g_dldx, const float* t, const float* c, float* dt, float* dc,
+                          cudaStream_t s) {
+    if (!S || !g_dldx || !t || !c || !dt || !dc) throw Err(FBS_EINVAL, "null pointer");
+    fbs_grid g = S->g;
+    const int64_t M = g->M;
+    const int K = S->K;
+    const size_t KM = (size_t)K * M;
+    if (!S->xb) {
+        S->xb = dalloc<float>(S->allocs, KM, s);
+        S->u = dalloc<float>(S->allocs, KM, s);
+        S->bwd = alloc_scalars(S->allocs, g->F * K, s);
+    }
+    CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
+    // u = S g (∂f/∂b = A⁻¹(S ∂f/∂x̂)), solved from x0 = 0 (reading #14)
+    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 8), 256, 0, s, geo, g->cellOff, g->vid, nullptr, g_dldx, K,
+           M, nullptr, S->u);
+    VecArgs a = make_args(S, S->bwd, S->xb, S->u);
+    const int nb = g->F * S->BPF;
+    // k_assemble here only zeroes x and forms ‖u‖² (diag(A), μ0 are recomputed from the same inputs)
+    LAUNCH(k_assemble, nb, kThreads, 0, s, a, S->diagA, S->mu0, nullptr, FBS_INIT_ZERO, S->bwd);
+    run_pcg(S, a, true, s);
+    LAUNCH(k_bwd_finalize, grid_for(g->N), kThreads, 0, s, g->vid, S->xb, S->xh, c, t, M, K, g->F,
+           (int64_t)g->H * g->W, dt, dc);
+    S->has_backward = true;
+}
+
+// ===================================================================================== ABI
+namespace fbs {
+namespace {
+int guard(const char* where, const std::function<void()>& body) {
+    try {
+        body();
+        t_err.clear();
+        return FBS_OK;
+    } catch (const Err& e) {
+        t_err = std::string(where) + ": " + e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        t_err = std::string(where) + ": " + e.what();
+        return FBS_ECUDA;
+    } catch (...) {
+        t_err = std::string(where) + ": unknown error";
+        return FBS_ECUDA;
+    }
+}
+}  // namespace
+}  // namespace fbs
+
+extern "C" {
+
+void fbs_default_grid_opts(fbs_grid_opts* o) {
+    if (!o) return;
+    o->n_bistoch = 20;
+    o->build_pyramid = 1;
+}
+
+void fbs_default_solve_opts(fbs_solve_opts* o) {
+    if (!o) return;
+    o->precond = FBS_PRECOND_HIER;
+    o->init = FBS_INIT_HIER;
+    o->mode = FBS_MODE_FIXED;
+    o->iters = 25;
+    o->tol = 1e-6;
+    o->max_iters = 2000;
+    o->precond_alpha = 2.0;
+    o->precond_beta = 5.0;
+    o->init_alpha = 4.0;
+    o->init_beta = 0.0;
+}
+
+int fbs_grid_build(const uint8_t* rgb, int frames, int height, int width, double sxy, double sl, double suv,
+                   const fbs_grid_opts* opts, fbs_stream stream, fbs_grid* out) {
+    return guard("fbs_grid_build", [&] {
+        grid_build_impl(rgb, frames, height, width, sxy, sl, suv, opts, (cudaStream_t)stream, out);
+    });
+}
+
+int fbs_grid_info(fbs_grid g, int64_t* n_pixels, int64_t* n_vertices, int* n_levels, int64_t* frame_vertices,
+                  int64_t* level_vertices, int32_t* frame_levels) {
+    return guard("fbs_grid_info", [&] {
+        if (!g) throw Err(FBS_EINVAL, "null grid");
+        if (n_pixels) *n_pixels = g->N;
+        if (n_vertices) *n_vertices = g->M;
+        if (n_levels) *n_levels = g->L;
+        if (frame_vertices)
+            for (int f = 0; f < g->F; ++f) frame_vertices[f] = g->frameOffH[f + 1] - g->frameOffH[f];
+        if (level_vertices) {
+            level_vertices[0] = g->M;
+            for (int k = 1; k < g->L; ++k) level_vertices[k] = g->lv[k].M;
+        }
+        if (frame_levels)
+            for (int f = 0; f < g->F; ++f) frame_levels[f] = g->frameLevelsH[f];
+    });
+}
+
+int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int32_t* m, float* n, float* res) {
+    return guard("fbs_grid_export", [&] {
+        if (!g) throw Err(FBS_EINVAL, "null grid");
+        cudaStream_t s = g->stream;
+        const int64_t M = g->M;
+        if (keys) ck(cudaMemcpyAsync(keys, g->keys, M * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        if (vid) ck(cudaMemcpyAsync(vid, g->vid, g->N * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (m) ck(cudaMemcpyAsync(m, g->m, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (n) ck(cudaMemcpyAsync(n, g->n, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (nbr) {
+            std::vector<void*> tmp;
+            int* d = dalloc<int>(tmp, (size_t)M * 10, s);
+            LAUNCH(k_export_nbr, grid_for(M), kThreads, 0, s, g->nearv, g->yoff, (int)M, d);
+            ck(cudaMemcpyAsync(nbr, d, (size_t)M * 40, cudaMemcpyDeviceToHost, s), "d2h");
+            free_all(tmp, s);
+        }
+        if (res) *res = g->bistoch_residual;
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+int fbs_pyramid_export(fbs_grid g, int level, uint64_t* keys, int32_t* parent, int32_t* count) {
+    return guard("fbs_pyramid_export", [&] {
+        if (!g) throw Err(FBS_EINVAL, "null grid");
+        if (level < 1 || level >= g->L) throw Err(FBS_EINVAL, "level out of range");
+        cudaStream_t s = g->stream;
+        const Level& L = g->lv[level];
+        const int64_t Mprev = (level == 1) ? g->M : g->lv[level - 1].M;
+        if (keys) ck(cudaMemcpyAsync(keys, L.keys, L.M * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        if (parent) ck(cudaMemcpyAsync(parent, L.parent, Mprev * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (count) ck(cudaMemcpyAsync(count, L.count, L.M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+void fbs_grid_destroy(fbs_grid g) {
+    if (!g) return;
+    free_all(g->allocs, g->stream);
+    delete g;
+}
+
+int fbs_solve(fbs_grid g, const float* t, int K, const float* c, double lam, const fbs_solve_opts* opts, float* x,
+              float* y, fbs_system* sys_out, fbs_stream stream) {
+    return guard("fbs_solve", [&] { solve_impl(g, t, K, c, lam, opts, x, y, sys_out, (cudaStream_t)stream); });
+}
+
+int fbs_solve_backward(fbs_system S, const float* dldx, const float* t, const float* c, float* dt, float* dc,
+                       fbs_stream stream) {
+    return guard("fbs_solve_backward", [&] { backward_impl(S, dldx, t, c, dt, dc, (cudaStream_t)stream); });
+}
+
+int fbs_system_stats(fbs_system S, int32_t* iters, double* relres, int32_t* bwd_iters, int32_t* status) {
+    return guard("fbs_system_stats", [&] {
+        if (!S) throw Err(FBS_EINVAL, "null system");
+        cudaStream_t s = S->stream;
+        const int FK = S->g->F * S->K;
+        std::vector<double> rr(FK), bb(FK);
+        std::vector<int> st(FK), st2(FK, 0);
+        ck(cudaMemcpyAsync(rr.data(), S->fwd.rr, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaMemcpyAsync(bb.data(), S->fwd.bb, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaMemcpyAsync(st.data(), S->fwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (iters) ck(cudaMemcpyAsync(iters, S->fwd.iters, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (S->xb) {
+            ck(cudaMemcpyAsync(st2.data(), S->bwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+            if (bwd_iters) ck(cudaMemcpyAsync(bwd_iters, S->bwd.iters, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        } else if (bwd_iters) {
+            for (int i = 0; i < FK; ++i) bwd_iters[i] = 0;
+        }
+        ck(cudaStreamSynchronize(s), "sync");
+        if (relres)
+            for (int i = 0; i < FK; ++i) relres[i] = bb[i] > 0 ? std::sqrt(rr[i] / bb[i]) : std::sqrt(rr[i]);
+        if (status) {
+            int acc = 0;
+            for (int i = 0; i < FK; ++i) acc |= st[i] | st2[i];
+            *status = acc;
+        }
+    });
+}
+
+int fbs_system_export(fbs_system S, float* sc, float* b, float* diagA, float* y0, float* y, float* db) {
+    return guard("fbs_system_export", [&] {
+        if (!S) throw Err(FBS_EINVAL, "null system");
+        fbs_grid g = S->g;
+        cudaStream_t s = S->stream;
+        const int64_t M = g->M;
+        const int K = S->K;
+        const size_t KM = (size_t)K * M;
+        std::vector<void*> tmp;
+        float* d = dalloc<float>(tmp, KM, s);
+        auto vk = [&](const float* src, float* host) {
+            LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, src, M, K, d);
+            ck(cudaMemcpyAsync(host, d, KM * 4, cudaMemcpyDeviceToHost, s), "d2h");
+            ck(cudaStreamSynchronize(s), "sync");
+        };
+        if (sc) ck(cudaMemcpyAsync(sc, S->sc, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (diagA) ck(cudaMemcpyAsync(diagA, S->diagA, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(cudaStreamSynchronize(s), "sync");
+        if (b) vk(S->b, b);
+        if (y0) vk(S->y0, y0);
+        if (y) vk(S->xh, y);
+        if (db) {
+            if (S->xb) vk(S->xb, db);
+            else std::memset(db, 0, KM * 4);
+        }
+        free_all(tmp, s);
+        ck(cudaStreamSynchronize(s), "sync");
+    });
+}
+
+void fbs_system_destroy(fbs_system S) {
+    if (!S) return;
+    free_all(S->allocs, S->stream);
+    delete S;
+}
+
+int fbs_slice(fbs_grid g, const float* y, int K, float* x, fbs_stream stream) {
+    return guard("fbs_slice", [&] {
+        if (!g || !y || !x) throw Err(FBS_EINVAL, "null pointer");
+        if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
+        cudaStream_t s = (cudaStream_t)stream;
+        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, y, g->M, K, g->F, (int64_t)g->H * g->W, 0, x);
+    });
+}
+
+int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) {
+    return guard("fbs_splat", [&] {
+        if (!g || !p || !out) throw Err(FBS_EINVAL, "null pointer");
+        if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
+        cudaStream_t s = (cudaStream_t)stream;
+        std::vector<void*> tmp;
+        const size_t KM = (size_t)K * g->M;
+        float* planar = dalloc<float>(tmp, KM, s);
+        CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
+        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 8), 256, 0, s, geo, g->cellOff, g->vid, nullptr, p, K,
+               g->M, nullptr, planar);
+        LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, K, out);
+        free_all(tmp, s);
+    });
+}
+
+int fbs_blur(fbs_grid g, const float* v, float* out, fbs_stream stream) {
+    return guard("fbs_blur", [&] {
+        if (!g || !v || !out) throw Err(FBS_EINVAL, "null pointer");
+        LAUNCH(k_blur, grid_for(g->M), kThreads, 0, (cudaStream_t)stream, g->nearv, g->yoff, v, g->M, out);
+    });
+}
+
+int fbs_system_apply_A(fbs_system S, const float* y, float* out, fbs_stream stream) {
+    return guard("fbs_system_apply_A", [&] {
+        if (!S || !y || !out) throw Err(FBS_EINVAL, "null pointer");
+        cudaStream_t s = (cudaStream_t)stream;
+        fbs_grid g = S->g;
+        std::vector<void*> tmp;
+        const size_t KM = (size_t)S->K * g->M;
+        float* ys = dalloc<float>(tmp, KM, s);
+        LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, y, nullptr, g->M, S->K, ys);
+        VecArgs a = make_args(S, S->fwd, S->xh, S->b);
+        LAUNCH(k_apply_A, grid_for(g->M), kThreads, 0, s, a, ys, out);
+        free_all(tmp, s);
+    });
+}
+
+int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_stream stream) {
+    return guard("fbs_system_apply_precond", [&] {
+        if (!S || !r || !out) throw Err(FBS_EINVAL, "null pointer");
+        cudaStream_t s = (cudaStream_t)stream;
+        fbs_grid g = S->g;
+        std::vector<void*> tmp;
+        const size_t KM = (size_t)S->K * g->M;
+        float* w = (S->o.precond == FBS_PRECOND_HIER) ? S->w0 : dalloc<float>(tmp, KM, s);
+        LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, r, S->mu0, g->M, S->K, w);
+        const bool hier = S->o.precond == FBS_PRECOND_HIER && g->L > 1;
+        if (hier) {
+            lift_all(S, w, S->K, s);
+            project_all(S, S->K, true, 0, 0, s);
+        }
+        LAUNCH(k_precond_out, grid_for(g->M), kThreads, 0, s, w, S->mu0, hier ? g->lv[1].parent : nullptr,
+               hier ? S->lvBuf[1] : nullptr, hier ? g->lv[1].M : 0, g->M, S->K, out);
+        free_all(tmp, s);
+    });
+}
+
+const char* fbs_last_error(void) { return t_err.c_str(); }
+int fbs_version(void) { return 1; }
+int64_t fbs_launch_count(void) { return (int64_t)g_launches.load(); }
+
+}  // extern "C"

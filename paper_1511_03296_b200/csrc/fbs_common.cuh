@@ -1,0 +1,228 @@
+// fbs_common.cuh — shared device helpers and handle layouts of the sm_100a bilateral solver.
+// Unity build: api.cu includes every *.cuh of this directory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cuda/atomic>
+#include <vector>
+
+#include "fbs.h"
+
+namespace fbs {
+
+constexpr int kD = 5;                // XYLUV dims
+constexpr int kBbarDiag = 2 * kD;    // B̄_diag = 2D (reading #4)
+constexpr int kCellMaxPx = 64;       // level-0 cell = one warp, ≤ 2 px per lane
+constexpr int kCellsPerBlock = 8;    // 8 warps, one cell each
+constexpr int kCoarseCap = 4096;     // children of one pyramid coarse cell (smem sort capacity)
+constexpr int kMaxLevels = 24;
+constexpr int kThreads = 256;        // vertex-parallel kernels
+constexpr int kMaxK = 64;
+
+// ------------------------------------------------------------------ launch counter
+extern std::atomic<long long> g_launches;
+
+// ------------------------------------------------------------------ small device helpers
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Deterministic block sum (fixed tree).  All threads call; result valid in thread 0.
+// `sh` needs blockDim.x/32 doubles.  Contains __syncthreads.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (w == 0) {
+        r = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
+        r = warp_sum(r);
+    }
+    return r;
+}
+
+// Per-frame "last block done": every block of frame f calls this once after writing its
+// partials; returns true (in all threads) only in the last block to arrive, which then owns
+// the frame's final fixed-order reduction.  Resets the counter for the next launch.
+__device__ __forceinline__ bool last_block_of_frame(unsigned* counter, int bpf, int* sflag) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned prev = atomicAdd(counter, 1u);
+        *sflag = (prev == (unsigned)(bpf - 1));
+    }
+    __syncthreads();
+    const bool last = *sflag != 0;
+    if (last) {
+        __threadfence();
+        if (threadIdx.x == 0) *counter = 0u;
+    }
+    return last;
+}
+
+// ------------------------------------------------------------------ decoupled look-back scan
+// Tile state word: bits 63..62 flag (0 none, 1 aggregate, 2 inclusive prefix),
+// bits 61..31 second count (pyramid children), bits 30..0 first count (vertices).
+constexpr unsigned long long kLbAgg = 1ull << 62;
+constexpr unsigned long long kLbPre = 2ull << 62;
+constexpr unsigned long long kLbVal = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long lb_pack(unsigned a, unsigned b) {
+    return (unsigned long long)a | ((unsigned long long)b << 31);
+}
+__device__ __forceinline__ unsigned lb_first(unsigned long long v) { return (unsigned)(v & 0x7fffffffull); }
+__device__ __forceinline__ unsigned lb_second(unsigned long long v) {
+    return (unsigned)((v >> 31) & 0x7fffffffull);
+}
+
+// Single-thread look-back (thread 0 of the tile).  Tiles obtain their id from an atomic
+// counter, so every predecessor has already started: the spin is deadlock-free.
+// Returns the exclusive prefix (packed) of tile `t`.
+__device__ __forceinline__ unsigned long long lookback(unsigned long long* state, unsigned t,
+                                                       unsigned long long agg) {
+    cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(state[t]);
+    if (t == 0) {
+        me.store(kLbPre | agg, cuda::memory_order_relaxed);
+        return 0ull;
+    }
+    me.store(kLbAgg | agg, cuda::memory_order_relaxed);
+    unsigned long long excl = 0ull;
+    long long j = (long long)t - 1;
+    while (true) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(state[j]);
+        const unsigned long long s = a.load(cuda::memory_order_relaxed);
+        const unsigned long long fl = s & ~kLbVal;
+        if (fl == 0ull) {
+            __nanosleep(32);
+            continue;
+        }
+        excl += s & kLbVal;
+        if (fl == kLbPre) break;
+        --j;
+    }
+    me.store(kLbPre | (excl + agg), cuda::memory_order_relaxed);
+    return excl;
+}
+
+// ------------------------------------------------------------------ neighbour encoding
+// near: 8 signed bytes = relative offsets of the (x−, x+, l−, l+, u−, u+, v−, v+) neighbours
+// (0 = absent; |offset| ≤ 127 because a σxy cell holds ≤ 64 vertices and x-neighbours sit in
+// the adjacent cell of the same canonical row).  yoff: relative offsets of (y−, y+), 0 = absent.
+__device__ __forceinline__ int near_off(uint2 nr, int i) {
+    const unsigned w = (i < 4) ? nr.x : nr.y;
+    return (int)(int8_t)(w >> (8 * (i & 3)));
+}
+
+// Σ_{u ∈ N(v)} x[u] in fixed slot order (x−,x+,l−,l+,u−,u+,v−,v+,y−,y+).
+__device__ __forceinline__ float nbr_sum(const float* __restrict__ x, int v, uint2 nr, int2 yo) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int o = near_off(nr, i);
+        if (o) s += __ldg(x + v + o);
+    }
+    if (yo.x) s += __ldg(x + v + yo.x);
+    if (yo.y) s += __ldg(x + v + yo.y);
+    return s;
+}
+
+__device__ __forceinline__ bool is_isolated(uint2 nr, int2 yo) {
+    return (nr.x | nr.y | (unsigned)yo.x | (unsigned)yo.y) == 0u;
+}
+
+// ------------------------------------------------------------------ handles
+struct Level {          // pyramid level k ≥ 1
+    int64_t M = 0;      // vertices (all frames)
+    int ncx = 0, ncy = 0;
+    int64_t ncells = 0;
+    uint64_t* keys = nullptr;       // [M]
+    int* cellOff = nullptr;         // [ncells + 1]
+    int* parent = nullptr;          // [M_{k-1}]  level k-1 → k  (S_{k-1})
+    int* childStart = nullptr;      // [M + 1]
+    int* childList = nullptr;       // [M_{k-1}]  children grouped by parent, fixed order
+    int* count = nullptr;           // [M] P(1)
+    std::vector<int64_t> frameOff;  // host copy [F + 1]
+};
+
+struct PcgScalars {     // per (frame, channel), fk = f*K + k
+    double* rho = nullptr;
+    double* alpha = nullptr;
+    double* beta = nullptr;
+    double* bb = nullptr;   // ‖b‖²
+    double* rr = nullptr;   // last ‖r‖² (TOL)
+    int* active = nullptr;
+    int* iters = nullptr;
+    int* status = nullptr;
+    int* n_active = nullptr;  // single counter
+};
+
+}  // namespace fbs
+
+struct fbs_grid_s {
+    int F = 0, H = 0, W = 0;
+    double sxy = 0, sl = 0, suv = 0;
+    int ncx = 0, ncy = 0;
+    int64_t ncells = 0, N = 0, M = 0;
+    int n_bistoch = 20;
+    bool has_pyramid = false;
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    // level 0
+    int* colStart = nullptr;   // [ncx + 1]
+    int* rowStart = nullptr;   // [ncy + 1]
+    int* vid = nullptr;        // [N]
+    uint64_t* keys = nullptr;  // [N] capacity (first M valid)
+    int* m = nullptr;          // [N] capacity
+    int* cellOff = nullptr;    // [ncells + 1]
+    uint2* nearv = nullptr;    // [M]
+    int2* yoff = nullptr;      // [M]
+    float* n = nullptr;        // [M]
+    int* frameOff = nullptr;   // device [F + 1]
+    std::vector<int64_t> frameOffH;
+    int* frameLevels = nullptr;  // device [F]
+    std::vector<int> frameLevelsH;
+    float bistoch_residual = -1.f;
+    int L = 1;  // levels incl. base (max over frames)
+    fbs::Level lv[fbs::kMaxLevels];
+    int64_t maxFrameM = 0;
+    std::vector<void*> allocs;
+};
+
+struct fbs_system_s {
+    fbs_grid g = nullptr;
+    int K = 1;
+    double lam = 1.0;
+    fbs_solve_opts o{};
+    cudaStream_t stream = nullptr;
+    cudaStream_t capture = nullptr;
+    int BPF = 1;
+    // vertex arrays
+    float* sc = nullptr;      // [M]
+    float* b = nullptr;       // [K][M] S(c∘t)
+    float* u = nullptr;       // [K][M] S g (backward right-hand side)
+    float* diagA = nullptr;   // [M] Laplacian-form diag(A); 0 ⇔ dead vertex
+    float* mu0 = nullptr;     // [M] level-0 multiplier (1/diagA on live vertices)
+    float* y0 = nullptr;      // [K][M] initial state
+    float* xh = nullptr;      // [K][M] forward solution ŷ
+    float* xb = nullptr;      // [K][M] backward solution ∂f/∂b
+    float* rh = nullptr;
+    float* dh = nullptr;
+    float* qh = nullptr;
+    float* sh = nullptr;
+    float* w0 = nullptr;                   // [C][M] level-0 pyramid input
+    float* lvBuf[fbs::kMaxLevels] = {};    // [C][M_k] level values (k ≥ 1)
+    float* mu[fbs::kMaxLevels] = {};       // [M_k] precond multipliers (k ≥ 1)
+    int C = 1;
+    double* partial = nullptr;  // [F][BPF][2K]
+    unsigned* counters = nullptr;  // [F]
+    fbs::PcgScalars fwd, bwd;
+    bool has_backward = false;
+    std::vector<void*> allocs;
+};

@@ -1,0 +1,322 @@
+// grid_kernels.cuh — simplified bilateral grid on sm_100a.
+//
+// Canonical vertex order is ascending packed key frame‖by‖bx‖bl‖bu‖bv (reading #3).  The
+// (frame, by, bx) digits of a pixel's key follow from its position, so the vertices of one
+// σxy×σxy cell are contiguous and cells appear in raster order: the grid is built by a
+// cell-local sort of the 24-bit (bl, bu, bv) codes (one warp per cell) plus a single-pass
+// decoupled look-back scan of per-cell unique counts for the global vertex ids — no global
+// sort of N keys is needed.
+#pragma once
+#include "fbs_common.cuh"
+
+namespace fbs {
+
+// ---------------------------------------------------------------- axis bins (reading #2)
+// start[b] = first coordinate i with ⌊i/σ⌋ = b; start[nb] = len.  σ ≥ 1, so bins are dense.
+__global__ void k_axis_bins(int len, double sigma, int nb, int* __restrict__ start) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
+        const int b = (int)floor((double)i / sigma);
+        const int bp = (i == 0) ? -1 : (int)floor((double)(i - 1) / sigma);
+        if (b != bp) start[b] = i;
+        if (i == len - 1) start[nb] = len;
+    }
+}
+
+struct CellGeom {
+    int F, H, W, ncx, ncy;
+    const int* colStart;
+    const int* rowStart;
+};
+
+// ---------------------------------------------------------------- warp bitonic sort, 64 keys
+// element e = j*32 + lane (a0: j = 0, a1: j = 1); ascending.
+__device__ __forceinline__ void warp_bitonic64(uint32_t& a0, uint32_t& a1, int lane) {
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+        for (int s = k >> 1; s > 0; s >>= 1) {
+            if (s == 32) {
+                const bool asc = (lane & k) == 0;
+                const uint32_t lo = min(a0, a1), hi = max(a0, a1);
+                a0 = asc ? lo : hi;
+                a1 = asc ? hi : lo;
+            } else {
+                const uint32_t p0 = __shfl_xor_sync(0xffffffffu, a0, s);
+                const uint32_t p1 = __shfl_xor_sync(0xffffffffu, a1, s);
+                const bool lower = (lane & s) == 0;
+                const bool asc0 = (lane & k) == 0;
+                const bool asc1 = ((lane + 32) & k) == 0;
+                a0 = (lower == asc0) ? min(a0, p0) : max(a0, p0);
+                a1 = (lower == asc1) ? min(a1, p1) : max(a1, p1);
+            }
+        }
+    }
+}
+
+// (bl, bu, bv) code of one pixel: reading #1 integer YUV numerators, reading #2 fp64 floor.
+__device__ __forceinline__ uint32_t luv_code(const uint8_t* __restrict__ px, double dl, double duv) {
+    const int R = px[0], G = px[1], B = px[2];
+    const int Yn = 77 * R + 150 * G + 29 * B;
+    const int Un = -43 * R - 85 * G + 128 * B + 32768;
+    const int Vn = 128 * R - 107 * G - 21 * B + 32768;
+    const uint32_t bl = (uint32_t)floor((double)Yn / dl);
+    const uint32_t bu = (uint32_t)floor((double)Un / duv);
+    const uint32_t bv = (uint32_t)floor((double)Vn / duv);
+    return (bl << 16) | (bu << 8) | bv;
+}
+
+__device__ __forceinline__ void cell_of(const CellGeom& g, int64_t c, int& f, int& cy, int& cx) {
+    const int64_t per = (int64_t)g.ncx * g.ncy;
+    f = (int)(c / per);
+    const int64_t r = c - (int64_t)f * per;
+    cy = (int)(r / g.ncx);
+    cx = (int)(r - (int64_t)cy * g.ncx);
+}
+
+// ---------------------------------------------------------------- level-0 grid build
+// One warp per σxy cell (≤ 64 px), 8 cells per block = one look-back tile.
+// Outputs: keys[v], m[v] (= S1), vid[p], cellOff[c] (first vertex of each cell).
+__global__ void __launch_bounds__(256) k_grid_cells(
+    const uint8_t* __restrict__ rgb, CellGeom g, double dl, double duv, int64_t ncells,
+    unsigned* __restrict__ tile_counter, unsigned long long* __restrict__ tile_state,
+    uint64_t* __restrict__ keys, int* __restrict__ mcount, int* __restrict__ vid,
+    int* __restrict__ cellOff, int* __restrict__ err) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned s_cnt[kCellsPerBlock];
+    __shared__ unsigned s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)tile * kCellsPerBlock + warp;
+
+    uint32_t a0 = 0xffffffffu, a1 = 0xffffffffu;
+    int f = 0, cy = 0, cx = 0, x0 = 0, y0 = 0, w = 1, npx = 0;
+    if (c < ncells) {
+        cell_of(g, c, f, cy, cx);
+        x0 = g.colStart[cx];
+        y0 = g.rowStart[cy];
+        w = g.colStart[cx + 1] - x0;
+        const int h = g.rowStart[cy + 1] - y0;
+        npx = w * h;
+        if (npx > kCellMaxPx) {  // host validated σxy ≤ 8; keep the kernel safe anyway
+            if (lane == 0) atomicOr(err, 1);
+            npx = kCellMaxPx;
+        }
+        const uint8_t* base = rgb + (size_t)f * g.H * g.W * 3;
+        if (lane < npx) {
+            const int px = x0 + lane % w, py = y0 + lane / w;
+            a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, dl, duv) << 6) | (uint32_t)lane;
+        }
+        if (lane + 32 < npx) {
+            const int i = lane + 32;
+            const int px = x0 + i % w, py = y0 + i / w;
+            a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, dl, duv) << 6) | (uint32_t)i;
+        }
+    }
+    warp_bitonic64(a0, a1, lane);
+
+    // run heads in sorted order (same code ⇒ same vertex)
+    const uint32_t up0 = __shfl_up_sync(0xffffffffu, a0, 1);
+    const uint32_t up1 = __shfl_up_sync(0xffffffffu, a1, 1);
+    const uint32_t last0 = __shfl_sync(0xffffffffu, a0, 31);
+    const uint32_t prev1 = lane ? up1 : last0;
+    const bool v0 = a0 != 0xffffffffu, v1 = a1 != 0xffffffffu;
+    const bool h0 = v0 && (lane == 0 || (up0 >> 6) != (a0 >> 6));
+    const bool h1 = v1 && ((prev1 >> 6) != (a1 >> 6));
+    const unsigned hb0 = __ballot_sync(0xffffffffu, h0);
+    const unsigned hb1 = __ballot_sync(0xffffffffu, h1);
+    const unsigned le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
+    const int r0 = __popc(hb0 & le) - 1;
+    const int r1 = __popc(hb0) + __popc(hb1 & le) - 1;
+    const unsigned U = (unsigned)(__popc(hb0) + __popc(hb1));
+
+    if (lane == 0) s_cnt[warp] = (c < ncells) ? U : 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned agg = 0;
+        for (int i = 0; i < kCellsPerBlock; ++i) agg += s_cnt[i];
+        s_excl = lb_first(lookback(tile_state, tile, lb_pack(agg, 0u)));
+    }
+    __syncthreads();
+    if (c >= ncells) return;
+    unsigned off = s_excl;
+    for (int i = 0; i < warp; ++i) off += s_cnt[i];
+
+    const unsigned long long H64 = (unsigned long long)hb0 | ((unsigned long long)hb1 << 32);
+    const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)cy << 40) | ((uint64_t)cx << 24);
+    int* vbase = vid + (size_t)f * g.H * g.W;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const uint32_t a = j ? a1 : a0;
+        const bool valid = j ? v1 : v0;
+        const bool head = j ? h1 : h0;
+        const int r = j ? r1 : r0;
+        const int e = lane + 32 * j;
+        if (!valid) continue;
+        const unsigned v = off + (unsigned)r;
+        if (head) {
+            const unsigned long long rest = H64 & ~((2ull << e) - 1ull);
+            const int nxt = rest ? (__ffsll((long long)rest) - 1) : npx;
+            keys[v] = khi | (uint64_t)(a >> 6);
+            mcount[v] = nxt - e;
+        }
+        const int i = (int)(a & 63u);
+        const int px = x0 + i % w, py = y0 + i / w;
+        vbase[(size_t)py * g.W + px] = (int)v;
+    }
+    if (lane == 0) {
+        cellOff[c] = (int)off;
+        if (c == ncells - 1) cellOff[ncells] = (int)(off + U);
+    }
+}
+
+// ---------------------------------------------------------------- neighbours (B̄ structure)
+__device__ __forceinline__ int lower_bound_s(const uint32_t* a, int n, uint32_t q) {
+    int lo = 0;
+    while (n > 0) {
+        const int half = n >> 1;
+        if (a[lo + half] < q) {
+            lo += half + 1;
+            n -= half + 1;
+        } else {
+            n = half;
+        }
+    }
+    return lo;
+}
+
+// One warp per cell: stage the 24-bit codes of the cell and of its x∓ / y∓ neighbour cells in
+// shared memory, then each vertex binary-searches its 10 ±1 neighbours (reading #4).
+__global__ void __launch_bounds__(256) k_grid_neighbours(
+    const uint64_t* __restrict__ keys, const int* __restrict__ cellOff, int ncx, int ncy,
+    int64_t ncells, uint2* __restrict__ nearv, int2* __restrict__ yoff, int* __restrict__ err) {
+    __shared__ uint32_t sc[kCellsPerBlock][5][kCellMaxPx];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
+         c += (int64_t)gridDim.x * kCellsPerBlock) {
+        const int64_t per = (int64_t)ncx * ncy;
+        const int64_t r = c % per;
+        const int cy = (int)(r / ncx), cx = (int)(r % ncx);
+        int st[5], ln[5];
+        const int64_t cc[5] = {c, c - 1, c + 1, c - ncx, c + ncx};
+        const bool ok[5] = {true, cx > 0, cx < ncx - 1, cy > 0, cy < ncy - 1};
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+            st[s] = ok[s] ? cellOff[cc[s]] : 0;
+            ln[s] = ok[s] ? cellOff[cc[s] + 1] - st[s] : 0;
+            if (ln[s] > kCellMaxPx) {
+                if (lane == 0) atomicOr(err, 2);
+                ln[s] = kCellMaxPx;
+            }
+            for (int i = lane; i < ln[s]; i += 32) sc[warp][s][i] = (uint32_t)(keys[st[s] + i] & 0xffffffu);
+        }
+        __syncwarp();
+        for (int i = lane; i < ln[0]; i += 32) {
+            const uint32_t q = sc[warp][0][i];
+            const int v = st[0] + i;
+            const uint32_t l = (q >> 16) & 255u, u = (q >> 8) & 255u, vv = q & 255u;
+            // slot → (segment, target code, field-in-range)
+            const int seg[10] = {1, 2, 0, 0, 0, 0, 0, 0, 3, 4};
+            const uint32_t tq[10] = {q, q, q - (1u << 16), q + (1u << 16), q - (1u << 8), q + (1u << 8),
+                                     q - 1u, q + 1u, q, q};
+            const bool in[10] = {true, true, l > 0, l < 255, u > 0, u < 255, vv > 0, vv < 255, true, true};
+            int offs[10];
+#pragma unroll
+            for (int k = 0; k < 10; ++k) {
+                offs[k] = 0;
+                const int s = seg[k];
+                if (in[k] && ln[s] > 0) {
+                    const int j = lower_bound_s(sc[warp][s], ln[s], tq[k]);
+                    if (j < ln[s] && sc[warp][s][j] == tq[k]) offs[k] = st[s] + j - v;
+                }
+            }
+            unsigned bx = 0, by = 0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int o = offs[k];
+                if (o < -127 || o > 127) atomicOr(err, 4);
+                const unsigned b = (unsigned)(o & 0xff);
+                if (k < 4) bx |= b << (8 * k); else by |= b << (8 * (k - 4));
+            }
+            nearv[v] = make_uint2(bx, by);
+            yoff[v] = make_int2(offs[8], offs[9]);
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- Alg. 1 bistochastization
+// n ← sqrt((n ∘ m) / (B̄ n)),  B̄ n = 2D n_v + Σ_{u∈N(v)} n_u, fp32.
+__global__ void __launch_bounds__(256) k_bistoch(const uint2* __restrict__ nearv,
+                                                 const int2* __restrict__ yoff,
+                                                 const int* __restrict__ m,
+                                                 const float* __restrict__ nin,
+                                                 float* __restrict__ nout, int M, int first) {
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
+        const uint2 nr = nearv[v];
+        const int2 yo = yoff[v];
+        float nv, bn;
+        if (first) {
+            int deg = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) deg += near_off(nr, i) != 0;
+            deg += (yo.x != 0) + (yo.y != 0);
+            nv = 1.f;
+            bn = (float)kBbarDiag + (float)deg;
+        } else {
+            nv = nin[v];
+            bn = (float)kBbarDiag * nv + nbr_sum(nin, v, nr, yo);
+        }
+        nout[v] = sqrtf(nv * (float)m[v] / bn);
+    }
+}
+
+// max|n∘B̄n − m| and max m (order-independent max ⇒ deterministic), reporting only.
+__global__ void k_bistoch_residual(const uint2* __restrict__ nearv, const int2* __restrict__ yoff,
+                                   const int* __restrict__ m, const float* __restrict__ n, int M,
+                                   unsigned* __restrict__ out2) {
+    float e = 0.f, mm = 0.f;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
+        const float bn = (float)kBbarDiag * n[v] + nbr_sum(n, v, nearv[v], yoff[v]);
+        e = fmaxf(e, fabsf(n[v] * bn - (float)m[v]));
+        mm = fmaxf(mm, (float)m[v]);
+    }
+    for (int o = 16; o; o >>= 1) {
+        e = fmaxf(e, __shfl_xor_sync(0xffffffffu, e, o));
+        mm = fmaxf(mm, __shfl_xor_sync(0xffffffffu, mm, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(out2, __float_as_uint(e));
+        atomicMax(out2 + 1, __float_as_uint(mm));
+    }
+}
+
+// ---------------------------------------------------------------- exports
+__global__ void k_export_nbr(const uint2* __restrict__ nearv, const int2* __restrict__ yoff, int M,
+                             int* __restrict__ nbr10) {
+    // export slot order (x−,x+,y−,y+,l−,l+,u−,u+,v−,v+); internal near order (x−,x+,l−,l+,u−,u+,v−,v+)
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
+        const uint2 nr = nearv[v];
+        const int2 yo = yoff[v];
+        int* o = nbr10 + (size_t)v * 10;
+        int nb[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int d = near_off(nr, i);
+            nb[i] = d ? v + d : -1;
+        }
+        o[0] = nb[0];
+        o[1] = nb[1];
+        o[2] = yo.x ? v + yo.x : -1;
+        o[3] = yo.y ? v + yo.y : -1;
+        o[4] = nb[2];
+        o[5] = nb[3];
+        o[6] = nb[4];
+        o[7] = nb[5];
+        o[8] = nb[6];
+        o[9] = nb[7];
+    }
+}
+
+}  // namespace fbs

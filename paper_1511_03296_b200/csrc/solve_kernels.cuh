@@ -1,0 +1,568 @@
+// solve_kernels.cuh — bilateral-space solve on sm_100a.
+//
+// A is applied in Laplacian-difference form (reading #20):
+//   (A y)_v = λ n_v Σ_{u∈N(v)} n_u (y_v − y_u) + Sc_v y_v
+// which equals λ(Dm − Dn B̄ Dn) + diag(Sc) at Alg. 1's fixed point n∘B̄n = m.
+// It is positive semidefinite by construction in floating point (a weighted graph Laplacian plus
+// a non-negative diagonal), keeps constants in the null space of zero-confidence components,
+// and its differences (y_v − y_u) are exact for smooth y, so fp32 vectors reach the oracle's
+// solution.  Vectors are fp32 planar [K][M]; dots accumulate in fp64 with a fixed-order
+// per-frame reduction (block partials + last-block-done), so runs are bitwise reproducible.
+// Each (frame, channel) has its own α, β, ρ and stopping rule (reading #13).
+#pragma once
+#include "fbs_common.cuh"
+#include "grid_kernels.cuh"
+
+namespace fbs {
+
+struct VecArgs {
+    int K, BPF;
+    int64_t M;
+    float lam;
+    const int* frameOff;  // [F+1]
+    const uint2* nearv;
+    const int2* yoff;
+    const float* n;       // Alg. 1 result
+    const float* sc;      // S c
+    const float* diagA;   // diag(A) in Laplacian form; 0 ⇔ dead vertex (reading #6)
+    float* x;
+    float* r;
+    float* d;
+    float* q;
+    float* s;
+    const float* b;
+    float* w0;            // hier: level-0 pyramid input [K][M]
+    const float* mu0;     // level-0 multiplier 1/diag(A) on live vertices
+    const int* parent0;   // hier: level 0 → 1 (nullptr if single level)
+    const float* acc1;    // hier: projected level-1 values [C][M1]
+    int64_t M1;
+    double* partial;      // [F][BPF][2K]
+    unsigned* counters;   // [F]
+    PcgScalars sc_;
+    int tol_mode;
+    double tol2;
+    int max_iters;
+};
+
+// (A y)_v in Laplacian-difference form (see header): λ n_v Σ_u n_u (y_v − y_u) + Sc_v y_v,
+// neighbours in fixed slot order (x−,x+,l−,l+,u−,u+,v−,v+,y−,y+).
+__device__ __forceinline__ float apply_A_row(const float* __restrict__ y, const float* __restrict__ n, int v,
+                                            uint2 nr, int2 yo, float lam, float scv) {
+    const float yv = y[v];
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int o = near_off(nr, i);
+        if (o) acc += __ldg(n + v + o) * (yv - __ldg(y + v + o));
+    }
+    if (yo.x) acc += __ldg(n + v + yo.x) * (yv - __ldg(y + v + yo.x));
+    if (yo.y) acc += __ldg(n + v + yo.y) * (yv - __ldg(y + v + yo.y));
+    return lam * n[v] * acc + scv * yv;
+}
+
+// Σ_{u∈N(v)} n_u  (so that diag(A) = λ n_v Σ n_u + Sc_v)
+__device__ __forceinline__ float nbr_nsum(const float* __restrict__ n, int v, uint2 nr, int2 yo) {
+    return nbr_sum(n, v, nr, yo);
+}
+
+// ---------------------------------------------------------------- splat  S p
+// One warp per σxy cell.  Pixels of a vertex all lie in its cell; the per-vertex sum is formed
+// deterministically: lanes holding the same vertex are grouped with match_any, each group summed
+// in lane order (fp64), and the two half-cells added in fixed order.  WEIGHTED: Sc = S c and
+// b_k = S(c∘t_k) (Eq. quad_min); otherwise out_k = S p_k.
+template <bool WEIGHTED>
+__global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict__ cellOff,
+                                               const int* __restrict__ vid, const float* __restrict__ c,
+                                               const float* __restrict__ p, int K, int64_t M,
+                                               float* __restrict__ sc_out, float* __restrict__ out) {
+    __shared__ double acc[kCellsPerBlock][kCellMaxPx];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ncells = (int64_t)g.F * g.ncx * g.ncy;
+    const size_t HW = (size_t)g.H * g.W;
+    for (int64_t cell = (int64_t)blockIdx.x * kCellsPerBlock + warp; cell < ncells;
+         cell += (int64_t)gridDim.x * kCellsPerBlock) {
+        int f, cy, cx;
+        cell_of(g, cell, f, cy, cx);
+        const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
+        const int w = g.colStart[cx + 1] - x0, h = g.rowStart[cy + 1] - y0;
+        const int npx = min(w * h, kCellMaxPx);
+        const int vbeg = cellOff[cell], U = cellOff[cell + 1] - vbeg;
+        size_t pix[2];
+        int rk[2];
+        float cw[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int i = lane + 32 * j;
+            rk[j] = -1;
+            pix[j] = 0;
+            cw[j] = 0.f;
+            if (i < npx) {
+                pix[j] = (size_t)(y0 + i / w) * g.W + (x0 + i % w);
+                rk[j] = vid[(size_t)f * HW + pix[j]] - vbeg;
+                cw[j] = WEIGHTED ? c[(size_t)f * HW + pix[j]] : 1.f;
+            }
+        }
+        const unsigned pe0 = __match_any_sync(0xffffffffu, rk[0]);
+        const unsigned pe1 = __match_any_sync(0xffffffffu, rk[1]);
+        const int nch = WEIGHTED ? K + 1 : K;
+        for (int ch = 0; ch < nch; ++ch) {
+            // channel WEIGHTED&&ch==0: Sc; else b_k (k = ch - WEIGHTED)
+            const int k = WEIGHTED ? ch - 1 : ch;
+            for (int i = lane; i < U; i += 32) acc[warp][i] = 0.0;
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                double val = 0.0;
+                if (rk[j] >= 0) {
+                    if (WEIGHTED && ch == 0) {
+                        val = (double)cw[j];
+                    } else {
+                        const float pv = p[((size_t)f * K + k) * HW + pix[j]];
+                        val = WEIGHTED ? (double)cw[j] * (double)pv : (double)pv;
+                    }
+                }
+                const unsigned pe = j ? pe1 : pe0;
+                double sum = 0.0;
+                for (unsigned mm = pe; mm; mm &= mm - 1u) sum += __shfl_sync(pe, val, __ffs(mm) - 1);
+                if (rk[j] >= 0 && lane == __ffs(pe) - 1) acc[warp][rk[j]] += sum;
+                __syncwarp();
+            }
+            for (int i = lane; i < U; i += 32) {
+                const float v = (float)acc[warp][i];
+                if (WEIGHTED && ch == 0) sc_out[vbeg + i] = v;
+                else out[(size_t)k * M + vbeg + i] = v;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// ---------------------------------------------------------------- per-frame reductions
+// finish of the ρ-reduction (Alg. 2 lines 11-13 + stopping rule, reading #11), executed by the
+// last block of frame f.  first: the reduction right after initialisation (lines 2-4).
+__device__ void finish_rho(const VecArgs& a, int f, bool first, double* shd) {
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        if (!first && !a.sc_.active[fk]) continue;
+        double R = 0.0, RR = 0.0;
+        for (int j = threadIdx.x; j < a.BPF; j += blockDim.x) {
+            const double* pp = a.partial + ((size_t)f * a.BPF + j) * 2 * a.K + 2 * k;
+            R += __ldcg(pp);
+            RR += __ldcg(pp + 1);
+        }
+        R = block_sum(R, shd);
+        RR = block_sum(RR, shd);
+        if (threadIdx.x == 0) {
+            const bool conv = a.tol_mode && RR <= a.tol2 * a.sc_.bb[fk];
+            a.sc_.rr[fk] = RR;
+            if (first) {
+                a.sc_.rho[fk] = R;
+                a.sc_.beta[fk] = 0.0;
+                a.sc_.iters[fk] = 0;
+                const bool act = !conv && R != 0.0 && a.max_iters > 0;
+                a.sc_.active[fk] = act;
+                if (!act) atomicSub(a.sc_.n_active, 1);
+            } else {
+                a.sc_.beta[fk] = R / a.sc_.rho[fk];
+                a.sc_.rho[fk] = R;
+                const int it = a.sc_.iters[fk] + 1;
+                a.sc_.iters[fk] = it;
+                if (conv || R == 0.0 || it >= a.max_iters) {
+                    if (!conv && a.tol_mode && R != 0.0) atomicOr(a.sc_.status + fk, FBS_ST_NOTCONVERGED);
+                    a.sc_.active[fk] = 0;
+                    atomicSub(a.sc_.n_active, 1);
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void write_partials(const VecArgs& a, int f, int j, int k, double v0, double v1,
+                                               double* shd) {
+    v0 = block_sum(v0, shd);
+    v1 = block_sum(v1, shd);
+    if (threadIdx.x == 0) {
+        double* pp = a.partial + ((size_t)f * a.BPF + j) * 2 * a.K + 2 * k;
+        pp[0] = v0;
+        pp[1] = v1;
+    }
+}
+
+// ---------------------------------------------------------------- assemble (Eq. quad_min)
+// diag(A) = λ n_v Σ_u n_u + Sc_v (PAPER.md:230 at Alg. 1's fixed point; isolated vertex: Sc_v,
+// reading #6), μ0 = 1/diag(A) on live vertices (Jacobi), ‖b‖² per (frame, k), and
+// flat init y_flat = b/Sc (reading #9) or zero init.  Per-frame blocks.
+__global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__ diagA, float* __restrict__ mu0,
+                                                  float* __restrict__ w0diag, int init_mode, PcgScalars scal) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+        const float dA = a.lam * a.n[v] * nbr_nsum(a.n, v, a.nearv[v], a.yoff[v]) + a.sc[v];
+        const bool live = dA > 0.f;
+        diagA[v] = dA;
+        mu0[v] = live ? 1.f / dA : 0.f;
+        if (w0diag) w0diag[v] = dA;
+    }
+    for (int k = 0; k < a.K; ++k) {
+        double bb = 0.0;
+        const size_t off = (size_t)k * a.M;
+        for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+            const float b = a.b[off + v];
+            bb += (double)b * (double)b;
+            if (init_mode == FBS_INIT_FLAT) {
+                const float S = a.sc[v];
+                a.x[off + v] = (S > 0.f) ? b / S : 0.f;
+            } else if (init_mode == FBS_INIT_ZERO) {
+                a.x[off + v] = 0.f;
+            }
+        }
+        write_partials(a, f, j, k, bb, 0.0, shd);
+    }
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
+        for (int k = 0; k < a.K; ++k) {
+            double R = 0.0;
+            for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
+                R += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k);
+            R = block_sum(R, shd);
+            if (threadIdx.x == 0) scal.bb[f * a.K + k] = R;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- pyramid lift / project
+// lift: out[c][p] = Σ_{children j of p} in[c][j]   (P(y) bottom-up)
+__global__ void k_lift(const float* __restrict__ in, int64_t Min, const int* __restrict__ childStart,
+                       const int* __restrict__ childList, int64_t Mout, int C, float* __restrict__ out) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < Mout;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int s = childStart[p], e = childStart[p + 1];
+        for (int c = 0; c < C; ++c) {
+            const float* src = in + (size_t)c * Min;
+            float acc = 0.f;
+            for (int jj = s; jj < e; ++jj) acc += src[childList[jj]];
+            out[(size_t)c * Mout + p] = acc;
+        }
+    }
+}
+
+// μ_k = z_w(k) · P(1)_k / P(diag A)_k  (Eq. hier_precond); 0 where the
+// denominator is 0 (reading #10) or where the frame has fewer than k+1 levels.
+__global__ void k_mu(const float* __restrict__ PdA, const int* __restrict__ count,
+                     const uint64_t* __restrict__ keys, const int* __restrict__ frameLevels, int64_t Mk,
+                     int level, double alpha, double beta, float* __restrict__ mu) {
+    const double zw = pow(alpha, -(beta + (double)level));
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < Mk;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        const int f = (int)(keys[p] >> 56);
+        const float den = PdA[p];
+        mu[p] = (level < frameLevels[f] && den > 0.f) ? (float)(zw * (double)count[p] / (double)den) : 0.f;
+    }
+}
+
+// project: L_k[c][v] = mult_k(v) · L_k[c][v] + L_{k+1}[c][parent_k(v)]   (Pᵀ top-down)
+// mult_k = mu[v] (preconditioner) or z_w(k; α, β) / P(1)_k (hier init).
+__global__ void k_project(float* __restrict__ Lk, int64_t Mk, const float* __restrict__ up, int64_t Mup,
+                          const int* __restrict__ parent, int C, const float* __restrict__ mu,
+                          const int* __restrict__ count, const uint64_t* __restrict__ keys,
+                          const int* __restrict__ frameLevels, int level, double alpha, double beta) {
+    const double zw = (level == 0) ? 1.0 : pow(alpha, -(beta + (double)level));
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < Mk;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        float mult;
+        if (mu) {
+            mult = mu[v];
+        } else {
+            const int f = (int)(keys[v] >> 56);
+            mult = (level < frameLevels[f]) ? (float)(zw / (double)count[v]) : 0.f;
+        }
+        const int pa = up ? parent[v] : 0;
+        for (int c = 0; c < C; ++c) {
+            float val = mult * Lk[(size_t)c * Mk + v];
+            if (up) val += up[(size_t)c * Mup + pa];
+            Lk[(size_t)c * Mk + v] = val;
+        }
+    }
+}
+
+// hier init at level 0:  y_hier = Pᵀ(z∘P(b)/P(1)) / Pᵀ(z∘P(Sc)/P(1)), 0 where den = 0.
+// w0 holds [b_0..b_{K-1}, Sc]; the level-0 multiplier is z_w(0)/P(1)_0 = 1.
+__global__ void k_init_finish(const float* __restrict__ w0, int64_t M, int K, const int* __restrict__ parent0,
+                              const float* __restrict__ acc1, int64_t M1, float* __restrict__ x) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
+        const int pa = acc1 ? parent0[v] : 0;
+        float den = w0[(size_t)K * M + v];
+        if (acc1) den += acc1[(size_t)K * M1 + pa];
+        for (int k = 0; k < K; ++k) {
+            float num = w0[(size_t)k * M + v];
+            if (acc1) num += acc1[(size_t)k * M1 + pa];
+            x[(size_t)k * M + v] = (den > 0.f) ? num / den : 0.f;
+        }
+    }
+}
+
+__global__ void k_fill_init_w0(const float* __restrict__ b, const float* __restrict__ sc, int64_t M, int K,
+                               float* __restrict__ w0) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
+        for (int k = 0; k < K; ++k) w0[(size_t)k * M + v] = b[(size_t)k * M + v];
+        w0[(size_t)K * M + v] = sc[v];
+    }
+}
+
+// ---------------------------------------------------------------- PCG (Alg. 2)
+__global__ void k_init_scalars(PcgScalars s, int FK) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < FK) {
+        s.rho[i] = 0.0;
+        s.alpha[i] = 0.0;
+        s.beta[i] = 0.0;
+        s.rr[i] = 0.0;
+        s.active[i] = 1;
+        s.iters[i] = 0;
+        s.status[i] = 0;
+    }
+    if (i == 0) *s.n_active = FK;
+}
+
+// Alg. 2 lines 2-4:  r = b − A x;  s = M⁻¹ r;  ρ = rᵀs   (X_ZERO: x = 0 ⇒ r = b, backward).
+// HIER: writes w0 = mask∘r for the pyramid; the reduction finishes in k_precond_finish.
+template <bool HIER, bool X_ZERO>
+__global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = 0; k < a.K; ++k) {
+        const size_t off = (size_t)k * a.M;
+        double rho = 0.0, rr = 0.0;
+        for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+            float r = a.b[off + v];
+            if (!X_ZERO) r -= apply_A_row(a.x + off, a.n, v, a.nearv[v], a.yoff[v], a.lam, a.sc[v]);
+            a.r[off + v] = r;
+            const float m0 = a.mu0[v];
+            if (HIER) {
+                a.w0[off + v] = (m0 > 0.f) ? r : 0.f;
+            } else {
+                const float s = m0 * r;
+                a.s[off + v] = s;
+                rho += (double)r * (double)s;
+                rr += (double)r * (double)r;
+            }
+        }
+        if (!HIER) write_partials(a, f, j, k, rho, rr, shd);
+    }
+    if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, true, shd);
+}
+
+// Alg. 2 lines 6-7:  q = A d;  α = ρ / dᵀq  (breakdown guard dᵀq ≤ 0, reading #11)
+__global__ void __launch_bounds__(256) k_spmv(VecArgs a) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        double dq = 0.0;
+        if (a.sc_.active[fk]) {
+            const size_t off = (size_t)k * a.M;
+            const float* d = a.d + off;
+            for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+                const float q = apply_A_row(d, a.n, v, a.nearv[v], a.yoff[v], a.lam, a.sc[v]);
+                a.q[off + v] = q;
+                dq += (double)d[v] * (double)q;
+            }
+        }
+        write_partials(a, f, j, k, dq, 0.0, shd);
+    }
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
+        for (int k = 0; k < a.K; ++k) {
+            const int fk = f * a.K + k;
+            if (!a.sc_.active[fk]) continue;
+            double DQ = 0.0;
+            for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
+                DQ += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k);
+            DQ = block_sum(DQ, shd);
+            if (threadIdx.x == 0) {
+                if (DQ <= 0.0) {
+                    a.sc_.active[fk] = 0;
+                    a.sc_.alpha[fk] = 0.0;
+                    atomicOr(a.sc_.status + fk, FBS_ST_BREAKDOWN);
+                    atomicSub(a.sc_.n_active, 1);
+                } else {
+                    a.sc_.alpha[fk] = a.sc_.rho[fk] / DQ;
+                }
+            }
+        }
+    }
+}
+
+// Alg. 2 lines 8-12:  x += αd;  r −= αq;  s = M⁻¹r;  ρ_new = rᵀs.
+// Jacobi: s = r/diag(A) inline, reduction finished here.  HIER: writes w0 = mask∘r.
+template <bool HIER>
+__global__ void __launch_bounds__(256) k_update(VecArgs a) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        double rho = 0.0, rr = 0.0;
+        if (a.sc_.active[fk]) {
+            const float al = (float)a.sc_.alpha[fk];
+            const size_t off = (size_t)k * a.M;
+            for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+                a.x[off + v] += al * a.d[off + v];
+                const float r = a.r[off + v] - al * a.q[off + v];
+                a.r[off + v] = r;
+                const float m0 = a.mu0[v];
+                if (HIER) {
+                    a.w0[off + v] = (m0 > 0.f) ? r : 0.f;
+                } else {
+                    const float s = m0 * r;
+                    a.s[off + v] = s;
+                    rho += (double)r * (double)s;
+                    rr += (double)r * (double)r;
+                }
+            }
+        }
+        if (!HIER) write_partials(a, f, j, k, rho, rr, shd);
+    }
+    if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, false, shd);
+}
+
+// Hierarchical M⁻¹ at level 0 (Eq. hier_precond): s = mask∘(μ0∘w + the projected coarser
+// levels); ρ = rᵀs = wᵀs (w = mask∘r), ‖r‖² (reading #6: r = 0 on dead vertices).
+__global__ void __launch_bounds__(256) k_precond_finish(VecArgs a, int first) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        double rho = 0.0, rr = 0.0;
+        if (first || a.sc_.active[fk]) {
+            const size_t off = (size_t)k * a.M;
+            for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+                const float w = a.w0[off + v];
+                const float m0 = a.mu0[v];
+                float s = 0.f;
+                if (m0 > 0.f) {
+                    s = m0 * w;
+                    if (a.acc1) s += a.acc1[(size_t)k * a.M1 + a.parent0[v]];
+                }
+                a.s[off + v] = s;
+                const float r = a.r[off + v];
+                rho += (double)r * (double)s;
+                rr += (double)r * (double)r;
+            }
+        }
+        write_partials(a, f, j, k, rho, rr, shd);
+    }
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, first != 0, shd);
+}
+
+// Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
+__global__ void __launch_bounds__(256) k_direction(VecArgs a, int first) {
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        if (!first && !a.sc_.active[fk]) continue;
+        const float be = first ? 0.f : (float)a.sc_.beta[fk];
+        const size_t off = (size_t)k * a.M;
+        for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x)
+            a.d[off + v] = first ? a.s[off + v] : a.s[off + v] + be * a.d[off + v];
+    }
+}
+
+// ---------------------------------------------------------------- slice / export / backward
+// x̂ = Sᵀŷ.  ys planar [K][M] (planar = 1) or canonical [M][K].
+__global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ ys, int64_t M, int K, int F,
+                        int64_t HW, int planar, float* __restrict__ out) {
+    const int64_t N = (int64_t)F * HW;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+        const int v = vid[p];
+        const int f = (int)(p / HW);
+        const int64_t pp = p - (int64_t)f * HW;
+        for (int k = 0; k < K; ++k) {
+            const float y = planar ? ys[(size_t)k * M + v] : ys[(size_t)v * K + k];
+            out[((size_t)f * K + k) * HW + pp] = y;
+        }
+    }
+}
+
+// planar [K][M] → canonical [M][K]
+__global__ void k_export_vk(const float* __restrict__ src, int64_t M, int K, float* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / K;
+        const int k = (int)(i - v * K);
+        dst[i] = src[(size_t)k * M + v];
+    }
+}
+
+// canonical [M][K] → planar [K][M], optionally masked to live vertices (mu0 > 0)
+__global__ void k_import_vk(const float* __restrict__ src, const float* __restrict__ mask, int64_t M, int K,
+                            float* __restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = i / K;
+        const int k = (int)(i - v * K);
+        dst[(size_t)k * M + v] = (mask && !(mask[v] > 0.f)) ? 0.f : src[i];
+    }
+}
+
+// Backward finalisation:  ∂t_k = c ∘ Sᵀd_k;
+// ∂c = Σ_k Sᵀ(−d_k∘ŷ_k) + (Sᵀd_k)∘t_k   (reading #15).
+__global__ void k_bwd_finalize(const int* __restrict__ vid, const float* __restrict__ db,
+                               const float* __restrict__ y, const float* __restrict__ c, const float* __restrict__ t,
+                               int64_t M, int K, int F, int64_t HW, float* __restrict__ dt, float* __restrict__ dc) {
+    const int64_t N = (int64_t)F * HW;
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+        const int v = vid[p];
+        const int f = (int)(p / HW);
+        const int64_t pp = p - (int64_t)f * HW;
+        const float cp = c[p];
+        float acc = 0.f;
+        for (int k = 0; k < K; ++k) {
+            const float D = db[(size_t)k * M + v];
+            const float Y = y[(size_t)k * M + v];
+            const size_t ip = ((size_t)f * K + k) * HW + pp;
+            dt[ip] = cp * D;
+            acc += -D * Y + D * t[ip];
+        }
+        dc[p] = acc;
+    }
+}
+
+// B̄ v (reading #4), debug / parity operator.
+__global__ void k_blur(const uint2* __restrict__ nearv, const int2* __restrict__ yoff, const float* __restrict__ x,
+                       int64_t M, float* __restrict__ out) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x)
+        out[v] = (float)kBbarDiag * x[v] + nbr_sum(x, (int)v, nearv[v], yoff[v]);
+}
+
+// A y for planar y, written canonical [M][K] (debug / parity operator).
+__global__ void k_apply_A(VecArgs a, const float* __restrict__ ys, float* __restrict__ out) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.M; v += (int64_t)gridDim.x * blockDim.x)
+        for (int k = 0; k < a.K; ++k)
+            out[(size_t)v * a.K + k] =
+                apply_A_row(ys + (size_t)k * a.M, a.n, (int)v, a.nearv[v], a.yoff[v], a.lam, a.sc[v]);
+}
+
+// M⁻¹ r at level 0 for masked planar w, written canonical [M][K] (debug / parity operator).
+__global__ void k_precond_out(const float* __restrict__ w0, const float* __restrict__ mu0,
+                              const int* __restrict__ parent0, const float* __restrict__ acc1, int64_t M1,
+                              int64_t M, int K, float* __restrict__ out) {
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
+        for (int k = 0; k < K; ++k) {
+            float s = 0.f;
+            if (mu0[v] > 0.f) {
+                s = mu0[v] * w0[(size_t)k * M + v];
+                if (acc1) s += acc1[(size_t)k * M1 + parent0[v]];
+            }
+            out[(size_t)v * K + k] = s;
+        }
+    }
+}
+
+}  // namespace fbs

@@ -1,0 +1,307 @@
+"""Thin ctypes binding of include/fbs.h — argument marshalling only.
+
+Every step of the bilateral-space solve runs in libfbs.so's sm_100a kernels; this module
+checks tensor dtypes/devices/layouts, passes raw device pointers and the current CUDA
+stream, and turns FBS_E* codes into exceptions.  There is no CPU fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfbs.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing — build it with `python paper_1511_03296_b200/build.py` "
+                      "(the product path has no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+FBS_OK, FBS_EINVAL, FBS_ENOMEM, FBS_ECUDA, FBS_ELIMIT, FBS_ESTATE = range(6)
+FBS_ST_BREAKDOWN, FBS_ST_NOTCONVERGED = 1, 2
+PRECOND = {"jacobi": 0, "hier": 1}
+INIT = {"flat": 0, "hier": 1, "zero": 2}
+MODE = {"fixed": 0, "tol": 1}
+
+
+class GridOpts(C.Structure):
+    _fields_ = [("n_bistoch", C.c_int), ("build_pyramid", C.c_int)]
+
+
+class SolveOpts(C.Structure):
+    _fields_ = [("precond", C.c_int), ("init", C.c_int), ("mode", C.c_int), ("iters", C.c_int),
+                ("tol", C.c_double), ("max_iters", C.c_int), ("precond_alpha", C.c_double),
+                ("precond_beta", C.c_double), ("init_alpha", C.c_double), ("init_beta", C.c_double)]
+
+
+_vp, _i, _d, _i64 = C.c_void_p, C.c_int, C.c_double, C.c_int64
+_SIGS = {
+    "fbs_default_grid_opts": (None, [C.POINTER(GridOpts)]),
+    "fbs_default_solve_opts": (None, [C.POINTER(SolveOpts)]),
+    "fbs_grid_build": (_i, [_vp, _i, _i, _i, _d, _d, _d, C.POINTER(GridOpts), _vp, C.POINTER(_vp)]),
+    "fbs_grid_info": (_i, [_vp, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i), _vp, _vp, _vp]),
+    "fbs_grid_export": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fbs_pyramid_export": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "fbs_grid_destroy": (None, [_vp]),
+    "fbs_solve": (_i, [_vp, _vp, _i, _vp, _d, C.POINTER(SolveOpts), _vp, _vp, C.POINTER(_vp), _vp]),
+    "fbs_solve_backward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fbs_system_stats": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "fbs_system_export": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fbs_system_destroy": (None, [_vp]),
+    "fbs_slice": (_i, [_vp, _vp, _i, _vp, _vp]),
+    "fbs_splat": (_i, [_vp, _vp, _i, _vp, _vp]),
+    "fbs_blur": (_i, [_vp, _vp, _vp, _vp]),
+    "fbs_system_apply_A": (_i, [_vp, _vp, _vp, _vp]),
+    "fbs_system_apply_precond": (_i, [_vp, _vp, _vp, _vp]),
+    "fbs_last_error": (C.c_char_p, []),
+    "fbs_version": (_i, []),
+    "fbs_launch_count": (_i64, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+class FbsError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[fbs code {code}] {msg}")
+        self.code = code
+
+
+def _check(code: int):
+    if code != FBS_OK:
+        raise FbsError(code, _lib.fbs_last_error().decode())
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _np_ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _stream(stream) -> C.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev_tensor(x: torch.Tensor, dtype: torch.dtype, name: str, ndim: int) -> torch.Tensor:
+    if not isinstance(x, torch.Tensor) or not x.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if x.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {x.dtype}")
+    if x.dim() != ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got shape {tuple(x.shape)}")
+    return x.contiguous()
+
+
+def launch_count() -> int:
+    """Kernels launched by libfbs.so in this process (monotone)."""
+    return int(_lib.fbs_launch_count())
+
+
+def version() -> int:
+    return int(_lib.fbs_version())
+
+
+# ----------------------------------------------------------------------------- grid
+class Grid:
+    """Handle of a built simplified bilateral grid (fbs_grid)."""
+
+    def __init__(self, handle, frames, H, W):
+        self._h = handle
+        self.frames, self.H, self.W = frames, H, W
+        n, m, lv = _i64(), _i64(), _i()
+        _check(_lib.fbs_grid_info(self._h, C.byref(n), C.byref(m), C.byref(lv), None, None, None))
+        self.N, self.M, self.levels = n.value, m.value, lv.value
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        fv = np.zeros(self.frames, np.int64)
+        lv = np.zeros(self.levels, np.int64)
+        fl = np.zeros(self.frames, np.int32)
+        _check(_lib.fbs_grid_info(self._h, None, None, None, _np_ptr(fv), _np_ptr(lv), _np_ptr(fl)))
+        return {"N": self.N, "M": self.M, "levels": self.levels, "frame_vertices": fv,
+                "level_vertices": lv, "frame_levels": fl}
+
+    def export(self):
+        keys = np.zeros(self.M, np.uint64)
+        vid = np.zeros(self.N, np.int32)
+        nbr = np.zeros((self.M, 10), np.int32)
+        m = np.zeros(self.M, np.int32)
+        n = np.zeros(self.M, np.float32)
+        res = np.zeros(1, np.float32)
+        _check(_lib.fbs_grid_export(self._h, _np_ptr(keys), _np_ptr(vid), _np_ptr(nbr), _np_ptr(m),
+                                    _np_ptr(n), _np_ptr(res)))
+        return {"keys": keys, "vid": vid, "nbr": nbr, "m": m, "n": n, "bistoch_residual": float(res[0])}
+
+    def pyramid_level(self, level: int):
+        lv = self.info()["level_vertices"]
+        keys = np.zeros(int(lv[level]), np.uint64)
+        parent = np.zeros(int(lv[level - 1]), np.int32)
+        count = np.zeros(int(lv[level]), np.int32)
+        _check(_lib.fbs_pyramid_export(self._h, level, _np_ptr(keys), _np_ptr(parent), _np_ptr(count)))
+        return {"keys": keys, "parent": parent, "count": count}
+
+    def close(self):
+        if self._h is not None:
+            _lib.fbs_grid_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def grid_build(rgb: torch.Tensor, sigma_xy: float, sigma_l: float, sigma_uv: float, n_bistoch: int = 20,
+               build_pyramid: bool = True, stream=None) -> Grid:
+    """fbs_grid_build: rgb uint8 CUDA [F][H][W][3] (or [H][W][3])."""
+    if isinstance(rgb, torch.Tensor) and rgb.dim() == 3:
+        rgb = rgb.unsqueeze(0)
+    rgb = _dev_tensor(rgb, torch.uint8, "rgb", 4)
+    F, H, W, ch = rgb.shape
+    if ch != 3:
+        raise ValueError("rgb must be [F][H][W][3]")
+    o = GridOpts(int(n_bistoch), int(bool(build_pyramid)))
+    h = C.c_void_p()
+    _check(_lib.fbs_grid_build(_ptr(rgb), F, H, W, float(sigma_xy), float(sigma_l), float(sigma_uv),
+                               C.byref(o), _stream(stream), C.byref(h)))
+    return Grid(h, F, H, W)
+
+
+# ----------------------------------------------------------------------------- solve
+def make_opts(precond="hier", init="hier", mode="fixed", iters=25, tol=1e-6, max_iters=2000,
+              precond_alpha=2.0, precond_beta=5.0, init_alpha=4.0, init_beta=0.0) -> SolveOpts:
+    return SolveOpts(PRECOND[precond], INIT[init], MODE[mode], int(iters), float(tol), int(max_iters),
+                     float(precond_alpha), float(precond_beta), float(init_alpha), float(init_beta))
+
+
+class System:
+    """Handle of a solved system (fbs_system): A-state, M⁻¹ and ŷ, reused by backward."""
+
+    def __init__(self, handle, grid: Grid, K: int):
+        self._h = handle
+        self.grid = grid
+        self.K = K
+
+    def stats(self):
+        FK = self.grid.frames * self.K
+        it = np.zeros(FK, np.int32)
+        rel = np.zeros(FK, np.float64)
+        bit = np.zeros(FK, np.int32)
+        st = np.zeros(1, np.int32)
+        _check(_lib.fbs_system_stats(self._h, _np_ptr(it), _np_ptr(rel), _np_ptr(bit), _np_ptr(st)))
+        return {"iterations": it.reshape(self.grid.frames, self.K), "relres": rel.reshape(self.grid.frames, self.K),
+                "bwd_iterations": bit.reshape(self.grid.frames, self.K), "status": int(st[0])}
+
+    def export(self):
+        M, K = self.grid.M, self.K
+        sc = np.zeros(M, np.float32)
+        b = np.zeros((M, K), np.float32)
+        dA = np.zeros(M, np.float32)
+        y0 = np.zeros((M, K), np.float32)
+        y = np.zeros((M, K), np.float32)
+        db = np.zeros((M, K), np.float32)
+        _check(_lib.fbs_system_export(self._h, _np_ptr(sc), _np_ptr(b), _np_ptr(dA), _np_ptr(y0), _np_ptr(y),
+                                      _np_ptr(db)))
+        return {"sc": sc, "b": b, "diagA": dA, "y0": y0, "y": y, "db": db}
+
+    def backward(self, dldx: torch.Tensor, t: torch.Tensor, c: torch.Tensor, stream=None):
+        """fbs_solve_backward → (dL/dt [F][K][H][W], dL/dc [F][H][W])."""
+        g = self.grid
+        dldx = _dev_tensor(dldx, torch.float32, "dldx", 4)
+        t = _dev_tensor(t, torch.float32, "t", 4)
+        c = _dev_tensor(c, torch.float32, "c", 3)
+        dt = torch.empty_like(t)
+        dc = torch.empty_like(c)
+        _check(_lib.fbs_solve_backward(self._h, _ptr(dldx), _ptr(t), _ptr(c), _ptr(dt), _ptr(dc), _stream(stream)))
+        return dt, dc
+
+    def apply_A(self, y: torch.Tensor, stream=None) -> torch.Tensor:
+        y = _dev_tensor(y, torch.float32, "y", 2)
+        out = torch.empty_like(y)
+        _check(_lib.fbs_system_apply_A(self._h, _ptr(y), _ptr(out), _stream(stream)))
+        return out
+
+    def apply_precond(self, r: torch.Tensor, stream=None) -> torch.Tensor:
+        r = _dev_tensor(r, torch.float32, "r", 2)
+        out = torch.empty_like(r)
+        _check(_lib.fbs_system_apply_precond(self._h, _ptr(r), _ptr(out), _stream(stream)))
+        return out
+
+    def close(self):
+        if self._h is not None:
+            _lib.fbs_system_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(grid: Grid, t: torch.Tensor, c: torch.Tensor, lam: float, want_y: bool = False,
+          keep_system: bool = False, stream=None, out: Optional[torch.Tensor] = None, **opts):
+    """fbs_solve.  t float32 [F][K][H][W], c float32 [F][H][W] → x [F][K][H][W]
+    (+ y [M][K] if want_y, + System if keep_system)."""
+    t = _dev_tensor(t, torch.float32, "t", 4)
+    c = _dev_tensor(c, torch.float32, "c", 3)
+    F, K, H, W = t.shape
+    if (F, H, W) != (grid.frames, grid.H, grid.W) or tuple(c.shape) != (F, H, W):
+        raise ValueError("t/c shapes do not match the grid")
+    x = torch.empty_like(t) if out is None else out
+    y = torch.empty((grid.M, K), dtype=torch.float32, device=t.device) if want_y else None
+    o = make_opts(**opts)
+    h = C.c_void_p()
+    _check(_lib.fbs_solve(grid.handle, _ptr(t), K, _ptr(c), float(lam), C.byref(o), _ptr(x), _ptr(y),
+                          C.byref(h) if keep_system else None, _stream(stream)))
+    res = [x]
+    if want_y:
+        res.append(y)
+    if keep_system:
+        res.append(System(h, grid, K))
+    return res[0] if len(res) == 1 else tuple(res)
+
+
+# ----------------------------------------------------------------------------- operators
+def slice_(grid: Grid, y: torch.Tensor, stream=None) -> torch.Tensor:
+    y = _dev_tensor(y, torch.float32, "y", 2)
+    K = y.shape[1]
+    x = torch.empty((grid.frames, K, grid.H, grid.W), dtype=torch.float32, device=y.device)
+    _check(_lib.fbs_slice(grid.handle, _ptr(y), K, _ptr(x), _stream(stream)))
+    return x
+
+
+def splat(grid: Grid, p: torch.Tensor, stream=None) -> torch.Tensor:
+    p = _dev_tensor(p, torch.float32, "p", 4)
+    K = p.shape[1]
+    out = torch.empty((grid.M, K), dtype=torch.float32, device=p.device)
+    _check(_lib.fbs_splat(grid.handle, _ptr(p), K, _ptr(out), _stream(stream)))
+    return out
+
+
+def blur(grid: Grid, v: torch.Tensor, stream=None) -> torch.Tensor:
+    v = _dev_tensor(v, torch.float32, "v", 1)
+    out = torch.empty_like(v)
+    _check(_lib.fbs_blur(grid.handle, _ptr(v), _ptr(out), _stream(stream)))
+    return out
+
+
+def header_symbols():
+    """Function names declared in include/fbs.h (for ABI-completeness tests)."""
+    import re
+    with open(os.path.join(os.path.dirname(_HERE), "include", "fbs.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(fbs_[a-z_]+)\s*\(", text)))
