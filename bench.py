@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py — megapixels/s of the bilateral-space solve (grid build + Alg. 1 + pyramid + splat +
+assemble + hierarchical init + 25 PCG iterations + slice) on BASELINE.json configs[4] (batch
+scaling: independent 1920×1080 frames, 8 per GPU, sharded over ranks with no collective on the
+solve path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fbs|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (one rank per GPU, NCCL)
+
+Prints ONE JSON line on rank 0.  `value` = all ranks' pixels ÷ the max-over-ranks device time
+of exactly K steps (CUDA events, barrier + synchronize on both sides).  `--impl reference`
+times the fp64 oracle (oracle/, the CPU reference of this build) on a bounded sample instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixels/sec solved (grid+PCG+slice); PCG HBM GB/s vs peak; 1/2/4/8 GPUs"
+SIGMAS = (8.0, 4.0, 3.0)
+LAM = 128.0
+ITERS = 25
+
+# Algorithmic bytes per unit of each kernel: fp32 vectors, K = 1, neighbour
+# structure 16 B/vertex (8 int8 near offsets + 2 int32 y offsets).  Gathers of neighbour
+# values are cache-resident re-reads and are not counted.
+BYTES_PER_VERTEX = {
+    "k_spmv": 32,            # nbr 16 + d 4 + n 4 + Sc 4 + q write 4
+    "k_update<true>": 32,    # x rw 8 + r rw 8 + d 4 + q 4 + mu0 4 + w0 write 4
+    "k_update<false>": 32,   # x rw 8 + r rw 8 + d 4 + q 4 + mu0 4 + s write 4
+    "k_precond_finish": 24,  # w0 4 + mu0 4 + parent 4 + r 4 + s write 4 + acc1 gather (≈4)
+    "k_direction": 12,       # s 4 + d rw 8
+    "k_bistoch": 28,         # nbr 16 + m 4 + n 4 + n write 4
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["fbs", "reference"], default="fbs")
+    ap.add_argument("--frames-per-gpu", type=int, default=8)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid: str):
+        self.uuid = uuid
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons, n = [], [], set(), 0
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9 or (self.uuid and self.uuid not in f[0]):
+                continue
+            n += 1
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        loaded = [s for s in sm if smax and s > 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(smax) if smax else None, "reasons": sorted(reasons), "samples": n}
+
+
+# --------------------------------------------------------------------------- reference arm
+def oracle_run(w):
+    import oracle as O
+    opts = O.SolveOptions(precond=w.precond, init=w.init, mode=w.mode, iters=w.iters, n_bistoch=w.n_bistoch)
+    t0 = time.perf_counter()
+    O.solve(w.rgb, w.t, w.c, w.sigma_xy, w.sigma_l, w.sigma_uv, w.lam, opts)
+    return time.perf_counter() - t0
+
+
+def oracle_sample(args, frame, crop):
+    """Bounded sample of the workload for the CPU oracle: a crop of one frame."""
+    from workloads import make
+    W, H = crop
+    return make("c5", frames=1, first_frame=frame, W=W, H=H)
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    from threadpoolctl import threadpool_limits
+    crop = (min(args.width, 960), min(args.height, 540))
+    w = oracle_sample(args, 0, crop)
+    with threadpool_limits(1):
+        for _ in range(args.warmup):
+            oracle_run(w)
+        times = [oracle_run(w) for _ in range(args.steps)]
+    ms = 1e3 * sum(times) / len(times)
+    value = w.pixels / 1e6 / (ms / 1e3)
+    sample = f"frame 0 of c5_batch cropped to {crop[0]}x{crop[1]} (seed 5000), hier+hier, 25 PCG iters, fp64 oracle"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args),
+            "cpu_baseline": {"value": value, "unit": "MP/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(args):
+    return {"workload": f"c5_batch: {args.frames_per_gpu} independent {args.width}x{args.height} RGB frames per GPU "
+                        f"(300-cell Voronoi + gradients + noise 3, planar depth with 5% outliers), "
+                        f"sigma=(8,4,3), lambda=128, Alg.1 x20, hier precond+init, {ITERS} PCG iters, K=1",
+            "frames_per_gpu": args.frames_per_gpu, "width": args.width, "height": args.height,
+            "parallelism": f"frames sharded over {args.gpus} rank(s), no collective on the solve path",
+            "l2": "inputs larger than L2 (rgb+t+c = 11 B/px, 182 MB per GPU-step > 126 MB L2)"}
+
+
+# --------------------------------------------------------------------------- main arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1511_03296_b200 as fbs
+    from workloads import make
+
+    F = args.frames_per_gpu
+    w = make("c5", frames=F, first_frame=rank * F, W=args.width, H=args.height)
+    rgb_h = torch.from_numpy(w.rgb).pin_memory()
+    t_h = torch.from_numpy(w.t).pin_memory()
+    c_h = torch.from_numpy(w.c).pin_memory()
+    rgb_d, t_d, c_d = rgb_h.to(dev), t_h.to(dev), c_h.to(dev)
+    x_d = torch.empty_like(t_d)
+    x_h = torch.empty_like(t_h).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        g = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=20)
+        fbs.solve(g, t_d, c_d, LAM, precond="hier", init="hier", mode="fixed", iters=ITERS, out=x_d)
+        g.close()
+        return g
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device time, CUDA events on the launching stream)
+    uuid = str(torch.cuda.get_device_properties(dev).uuid) if hasattr(torch.cuda.get_device_properties(dev), "uuid") else ""
+    clocks = ClockSampler(uuid)
+    clocks.start()
+    barrier()
+    l0 = fbs.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = fbs.launch_count() - l0
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(ms)
+    pixels_all = w.pixels * world
+    value = pixels_all / 1e6 / (ms / 1e3 / args.steps)
+
+    # ---- per-kernel device times over a second pass of the same K steps (events per launch)
+    g_info = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=20)
+    M = g_info.M
+    info = g_info.info()
+    g_info.close()
+    fbs.profile_reset()
+    fbs.profile_enable(True)
+    barrier()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        step()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    fbs.profile_enable(False)
+    prof = fbs.profile_report()
+    prof_ms = p0.elapsed_time(p1)
+    kernels = {k: {"launches": n, "ms_per_step": tot / args.steps, "avg_us": 1e3 * tot / max(n, 1)}
+               for k, (n, tot) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    roof = None
+    cand = [(k, v) for k, v in kernels.items() if k in BYTES_PER_VERTEX]
+    if cand:
+        kname, kv = max(cand, key=lambda kv_: kv_[1]["ms_per_step"])
+        bytes_launch = BYTES_PER_VERTEX[kname] * M
+        achieved = bytes_launch / (kv["avg_us"] * 1e-6) / 1e9
+        peak, peak_src = 6545.6, "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                peak = float(json.load(fh)["hbm_gbs"])
+        except Exception:
+            peak, peak_src = 6650.0, "B200_PROFILING.md fallback"
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                traffic = json.load(fh).get(kname)
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": kname, "bytes_per_launch": bytes_launch,
+                "bytes_per_vertex": BYTES_PER_VERTEX[kname], "vertices": M, "avg_launch_us": kv["avg_us"],
+                "share_of_step": kv["ms_per_step"] / (prof_ms / args.steps), "peak_source": peak_src}
+    stages = {
+        "grid_build": ["k_axis_bins", "k_grid_cells", "k_frame_offsets", "k_grid_neighbours"],
+        "bistochastize": ["k_bistoch", "k_bistoch_residual"],
+        "pyramid": ["k_pyr_level", "k_lift_count"],
+        "splat_assemble": ["k_splat<true>", "k_assemble", "k_mu", "k_fill_init_w0", "k_init_finish"],
+        "pcg": ["k_spmv", "k_update<true>", "k_update<false>", "k_precond_finish", "k_direction", "k1", "k2",
+                "k_init_scalars", "k_lift", "k_project"],
+        "slice": ["k_slice"],
+    }
+    stages_ms = {s: sum(kernels[k]["ms_per_step"] for k in ks if k in kernels) for s, ks in stages.items()}
+    stages_ms["pcg_per_iteration"] = stages_ms["pcg"] / ITERS
+
+    # ---- end to end through the public API with host buffers (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        def step_e2e():
+            rgb_d.copy_(rgb_h, non_blocking=True)
+            t_d.copy_(t_h, non_blocking=True)
+            c_d.copy_(c_h, non_blocking=True)
+            step()
+            x_h.copy_(x_d, non_blocking=True)
+        step_e2e()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_e2e()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = max_over_ranks(e0.elapsed_time(e1))
+        h2d = rgb_h.numel() + 4 * t_h.numel() + 4 * c_h.numel()
+        e2e = {"value": pixels_all / 1e6 / (ems / 1e3 / args.steps), "unit": "MP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * x_h.numel()),
+               "ms_per_step": ems / args.steps}
+
+    # ---- CPU baseline: the oracle as it stands, one frame, host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from threadpoolctl import threadpool_limits
+        wf = make("c5", frames=2, first_frame=0, W=args.width, H=args.height)
+        with threadpool_limits(1):
+            sec = oracle_run(wf)
+        cpu = {"value": wf.pixels / 1e6 / sec, "unit": "MP/s", "cores": 1, "kind": "oracle",
+               "sample": f"frames 0-1 of the workload ({args.width}x{args.height}), fp64 numpy/scipy oracle, "
+                         f"hier+hier, 25 PCG iters, single thread ({sec:.1f} s)"}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": workload_config(args) | {"vertices_per_gpu": M,
+                                                   "levels": int(info["levels"])},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clk, "stages_ms_per_step": stages_ms, "kernels": kernels,
+                "profiled_ms_per_step": prof_ms / args.steps}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

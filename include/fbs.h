@@ -193,6 +193,14 @@ int fbs_version(void);
 /* Number of CUDA kernels this library has launched in this process (monotone counter). */
 int64_t fbs_launch_count(void);
 
+/* Per-kernel device timing.  While enabled, every launch is bracketed by two CUDA events
+ * recorded on its own stream.  fbs_profile_report synchronises those events and writes a JSON
+ * object {"<kernel>": [launches, total_ms], ...} into buf (NUL-terminated, truncated to len);
+ * it returns the number of bytes needed.  fbs_profile_reset clears the records. */
+int fbs_profile_enable(int on);
+int fbs_profile_report(char* buf, size_t len);
+int fbs_profile_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,6 +11,9 @@ from .fbs import (  # noqa: F401
     grid_build,
     launch_count,
     make_opts,
+    profile_enable,
+    profile_report,
+    profile_reset,
     slice_,
     solve,
     splat,

@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 #include <functional>
+#include <map>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -33,8 +35,48 @@ void ck(cudaError_t e, const char* what) {
     }
 }
 
+// ---- per-kernel event timing (fbs_profile_*)
+struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+};
+std::atomic<int> g_prof_on{0};
+std::vector<ProfRec> g_prof;
+std::vector<cudaEvent_t> g_ev_pool;
+std::mutex g_prof_mu;
+
+cudaEvent_t ev_get() {
+    if (!g_ev_pool.empty()) {
+        cudaEvent_t e = g_ev_pool.back();
+        g_ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+struct ProfScope {
+    int idx = -1;
+    cudaStream_t s;
+    ProfScope(const char* name, cudaStream_t st) : s(st) {
+        if (!g_prof_on.load(std::memory_order_relaxed)) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        ProfRec r{name, ev_get(), ev_get()};
+        ck(cudaEventRecord(r.a, s), "cudaEventRecord");
+        g_prof.push_back(r);
+        idx = (int)g_prof.size() - 1;
+    }
+    ~ProfScope() {
+        if (idx < 0) return;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        cudaEventRecord(g_prof[idx].b, s);
+    }
+};
+
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
     do {                                                                                 \
+        ::fbs::ProfScope _ps(#kernel, (stream));                                         \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                       \
         ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
         ck(cudaGetLastError(), #kernel);                                                 \
@@ -827,5 +869,53 @@ int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_strea
 const char* fbs_last_error(void) { return t_err.c_str(); }
 int fbs_version(void) { return 1; }
 int64_t fbs_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int fbs_profile_enable(int on) {
+    fbs::g_prof_on.store(on ? 1 : 0);
+    return FBS_OK;
+}
+
+int fbs_profile_reset(void) {
+    return guard("fbs_profile_reset", [&] {
+        std::lock_guard<std::mutex> lk(fbs::g_prof_mu);
+        for (auto& r : fbs::g_prof) {
+            fbs::g_ev_pool.push_back(r.a);
+            fbs::g_ev_pool.push_back(r.b);
+        }
+        fbs::g_prof.clear();
+    });
+}
+
+int fbs_profile_report(char* buf, size_t len) {
+    std::string js;
+    int rc = guard("fbs_profile_report", [&] {
+        std::lock_guard<std::mutex> lk(fbs::g_prof_mu);
+        std::map<std::string, std::pair<long long, double>> acc;
+        for (auto& r : fbs::g_prof) {
+            ck(cudaEventSynchronize(r.b), "cudaEventSynchronize");
+            float ms = 0.f;
+            ck(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+            auto& e = acc[r.name];
+            e.first += 1;
+            e.second += ms;
+        }
+        js = "{";
+        bool first = true;
+        for (auto& kv : acc) {
+            char tmp[256];
+            std::snprintf(tmp, sizeof(tmp), "%s\"%s\": [%lld, %.6f]", first ? "" : ", ", kv.first.c_str(),
+                          kv.second.first, kv.second.second);
+            js += tmp;
+            first = false;
+        }
+        js += "}";
+    });
+    if (rc != FBS_OK) return -rc;
+    if (buf && len > 0) {
+        std::strncpy(buf, js.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return (int)js.size() + 1;
+}
 
 }  // extern "C"

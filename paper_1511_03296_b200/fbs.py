@@ -60,6 +60,9 @@ _SIGS = {
     "fbs_last_error": (C.c_char_p, []),
     "fbs_version": (_i, []),
     "fbs_launch_count": (_i64, []),
+    "fbs_profile_enable": (_i, [_i]),
+    "fbs_profile_report": (_i, [C.c_char_p, C.c_size_t]),
+    "fbs_profile_reset": (_i, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -108,6 +111,26 @@ def launch_count() -> int:
 
 def version() -> int:
     return int(_lib.fbs_version())
+
+
+def profile_enable(on: bool = True):
+    """Bracket every library kernel launch with CUDA events (per-kernel device timing)."""
+    _lib.fbs_profile_enable(int(bool(on)))
+
+
+def profile_reset():
+    _check(_lib.fbs_profile_reset())
+
+
+def profile_report() -> dict:
+    """{kernel: (launches, total_ms)} of the launches recorded since the last reset."""
+    import json
+    need = _lib.fbs_profile_report(None, 0)
+    if need < 0:
+        _check(-need)
+    buf = C.create_string_buffer(need + 16)
+    _lib.fbs_profile_report(buf, len(buf))
+    return {k: (int(v[0]), float(v[1])) for k, v in json.loads(buf.value.decode()).items()}
 
 
 # ----------------------------------------------------------------------------- grid
