@@ -151,6 +151,24 @@ def workload_config(args):
             "l2": "inputs larger than L2 (rgb+t+c = 11 B/px, 182 MB per GPU-step > 126 MB L2)"}
 
 
+# --------------------------------------------------------------------------- sharding
+def shard_frames(rank: int, per_gpu: int):
+    """Frames of configs[4] owned by `rank`: [rank·per_gpu, (rank+1)·per_gpu).
+    Frames are independent systems, so no data-path collective is needed."""
+    return list(range(rank * per_gpu, (rank + 1) * per_gpu))
+
+
+def reduce_max(value: float, world: int, device=None) -> float:
+    """Max over ranks (device-timed ms), outside the timed region."""
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # --------------------------------------------------------------------------- main arm
 def main():
     args = parse()
@@ -171,7 +189,8 @@ def main():
     from workloads import make
 
     F = args.frames_per_gpu
-    w = make("c5", frames=F, first_frame=rank * F, W=args.width, H=args.height)
+    frames = shard_frames(rank, F)
+    w = make("c5", frames=F, first_frame=frames[0], W=args.width, H=args.height)
     rgb_h = torch.from_numpy(w.rgb).pin_memory()
     t_h = torch.from_numpy(w.t).pin_memory()
     c_h = torch.from_numpy(w.c).pin_memory()
@@ -192,11 +211,7 @@ def main():
         torch.cuda.synchronize()
 
     def max_over_ranks(v):
-        if world == 1:
-            return v
-        tt = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        return float(tt.item())
+        return reduce_max(v, world, dev)
 
     for _ in range(max(args.warmup, 0)):
         step()

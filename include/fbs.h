@@ -55,8 +55,8 @@ typedef struct fbs_system_s* fbs_system;
 #define FBS_EINVAL 1 /* bad argument (see each call)                                   */
 #define FBS_ENOMEM 2 /* device allocation failed                                       */
 #define FBS_ECUDA 3  /* CUDA runtime error (message in fbs_last_error)                 */
-#define FBS_ELIMIT 4 /* structural limit exceeded: a σxy cell holds > 64 pixels, or a  */
-                     /* pyramid coarse cell has > 4096 children          */
+#define FBS_ELIMIT 4 /* structural limit exceeded: a σxy cell holds > 64 pixels        */
+                     /* (reading #21)                                    */
 #define FBS_ESTATE 5 /* handle used in the wrong state (e.g. backward before forward)  */
 
 /* bits of the `status` word returned by fbs_system_stats */

@@ -247,6 +247,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         int ncxK = ncx, ncyK = ncy;
         const int* countK = nullptr;  // level 0: P(1) = 1
         std::vector<int*> lvFrameOffDev(Lmax, nullptr);
+        unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
         for (int k = 1; k < Lmax; ++k) {
             Level& L = g->lv[k];
             L.ncx = ((ncx - 1) >> k) + 1;
@@ -258,13 +259,13 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             L.childStart = dalloc<int>(A, M + 1, s);
             L.childList = dalloc<int>(A, M, s);
             L.count = dalloc<int>(A, M, s);
-            unsigned long long* st2 = dalloc<unsigned long long>(A, L.ncells, s);
+            unsigned long long* st2 = dalloc<unsigned long long>(A, 2 * L.ncells, s);
             unsigned* ctr2 = dalloc<unsigned>(A, 1, s);
-            ck(cudaMemsetAsync(st2, 0, L.ncells * sizeof(unsigned long long), s), "memset");
+            ck(cudaMemsetAsync(st2, 0, 2 * L.ncells * sizeof(unsigned long long), s), "memset");
             ck(cudaMemsetAsync(ctr2, 0, sizeof(unsigned), s), "memset");
             LAUNCH(k_pyr_level, (unsigned)L.ncells, 256, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK,
-                   ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, L.keys, L.parent, L.childStart, L.childList,
-                   L.cellOff, err);
+                   ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, st2 + L.ncells, pyrScratch, L.keys, L.parent,
+                   L.childStart, L.childList, L.cellOff);
             // P(1): upper bound M on the level size; the kernel stops at the true size via childStart
             lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
             LAUNCH(k_frame_offsets, 1, 288, 0, s, L.cellOff, F, (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
@@ -282,7 +283,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         }
         ck(cudaMemcpyAsync(errh, err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaStreamSynchronize(s), "sync");
-        if (errh[0] & 8) throw Err(FBS_ELIMIT, "a pyramid coarse cell has more than 4096 children");
         if (errh[0] & ~8) throw Err(FBS_ECUDA, "internal grid-build check failed (code " + std::to_string(errh[0]) + ")");
         {
             float e, mm;

@@ -46,24 +46,28 @@ __device__ __forceinline__ int block_excl_scan(int x, int* sh /*[33]*/, int* tot
     return sh[w] + incl - x;
 }
 
-// One block (T threads) per level-(k+1) coarse cell.
+// One block (T threads) per level-(k+1) coarse cell.  Two look-back chains: the children
+// prefix is published first (it is known before sorting), which also places the cell's slice of
+// a global scratch array; cells with more than kCoarseCap children sort there instead of in
+// shared memory (rare: dense pixel-noise images at σl = σuv = 1).
 __global__ void __launch_bounds__(256) k_pyr_level(
     const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK, int ncxK, int ncyK,
     int ncxN, int ncyN, int64_t ncellsN, unsigned* __restrict__ tile_counter,
-    unsigned long long* __restrict__ tile_state, uint64_t* __restrict__ keysN,
+    unsigned long long* __restrict__ stateC, unsigned long long* __restrict__ stateV,
+    unsigned long long* __restrict__ scratch, uint64_t* __restrict__ keysN,
     int* __restrict__ parentK, int* __restrict__ childStartN, int* __restrict__ childListN,
-    int* __restrict__ cellOffN, int* __restrict__ err) {
-    extern __shared__ unsigned long long sk[];  // [kCoarseCap]
+    int* __restrict__ cellOffN) {
+    extern __shared__ unsigned long long sk_smem[];  // [kCoarseCap]
     __shared__ unsigned s_tile;
     __shared__ int s_scan[33];
-    __shared__ unsigned long long s_excl;
+    __shared__ unsigned s_cexcl, s_vexcl;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const int64_t C = s_tile;
     const int T = blockDim.x;
 
     int f = 0, CY = 0, CX = 0, n0 = 0, n1 = 0, s0 = 0, s1 = 0;
-    if (C < ncellsN) {
+    {
         const int64_t per = (int64_t)ncxN * ncyN;
         f = (int)(C / per);
         const int64_t r = C - (int64_t)f * per;
@@ -78,14 +82,13 @@ __global__ void __launch_bounds__(256) k_pyr_level(
             if (a == 0) { s0 = st; n0 = en - st; } else { s1 = st; n1 = en - st; }
         }
     }
-    int nch = n0 + n1;
-    if (nch > kCoarseCap) {
-        if (threadIdx.x == 0) atomicOr(err, 8);
-        nch = 0;  // publish an empty cell so later tiles do not deadlock; grid build fails
-        n0 = n1 = 0;
-    }
+    const int nch = n0 + n1;
+    if (threadIdx.x == 0) s_cexcl = lb_first(lookback(stateC, (unsigned)C, lb_pack((unsigned)nch, 0u)));
+    __syncthreads();
+    const int cOff = (int)s_cexcl;
     int P = 1;
     while (P < nch) P <<= 1;
+    unsigned long long* sk = (nch <= kCoarseCap) ? sk_smem : scratch + 2 * (size_t)cOff;
     for (int i = threadIdx.x; i < P; i += T) {
         unsigned long long key = ~0ull;
         if (i < nch) {
@@ -119,14 +122,9 @@ __global__ void __launch_bounds__(256) k_pyr_level(
     }
     int U;
     const int before = block_excl_scan(myHeads, s_scan, &U);
-    if (threadIdx.x == 0) {
-        const unsigned long long ex =
-            (C < ncellsN) ? lookback(tile_state, (unsigned)C, lb_pack((unsigned)U, (unsigned)nch)) : 0ull;
-        s_excl = ex;
-    }
+    if (threadIdx.x == 0) s_vexcl = lb_first(lookback(stateV, (unsigned)C, lb_pack((unsigned)U, 0u)));
     __syncthreads();
-    if (C >= ncellsN) return;
-    const int vOff = (int)lb_first(s_excl), cOff = (int)lb_second(s_excl);
+    const int vOff = (int)s_vexcl;
     const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)CY << 40) | ((uint64_t)CX << 24);
     int r = before - 1;
     for (int e = 0; e < E; ++e) {
