@@ -14,6 +14,7 @@
 #include "grid_kernels.cuh"
 #include "pyramid_kernels.cuh"
 #include "solve_kernels.cuh"
+#include "hier_kernels.cuh"
 
 namespace fbs {
 
@@ -98,6 +99,11 @@ void device_setup(int* dev) {
         ck(cudaFuncSetAttribute(k_pyr_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kCoarseCap * (int)sizeof(unsigned long long)),
            "k_pyr_level smem");
+        const int big = 200 * 1024;
+        ck(cudaFuncSetAttribute(k_tile_up<UP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
+        ck(cudaFuncSetAttribute(k_tile_project<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
+        ck(cudaFuncSetAttribute(k_coarse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
+        ck(cudaFuncSetAttribute(k_tile_project<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
         pool_done[*dev] = true;
     }
 }
@@ -139,6 +145,12 @@ int guard(const char* where, const std::function<void()>& body);
 }  // namespace fbs
 
 using namespace fbs;
+
+namespace {
+HierArgs grid_hier(fbs_grid g);
+int n_tiles(const HierArgs& h);
+
+}  // namespace
 
 // ===================================================================================== grid
 static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy, double sl, double suv,
@@ -211,10 +223,14 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->m = mCap;
         const int64_t M = g->M;
 
-        g->nearv = dalloc<uint2>(A, M, s);
-        g->yoff = dalloc<int2>(A, M, s);
+        g->nbr = dalloc<int4>(A, M, s);
+        // per-tile maxima (sizes the tile kernels' shared memory): [0..3] pyramid tile levels,
+        // [7] staged vertices of the fused direction + SpMV tiles
+        int* tmax = dalloc<int>(A, 8, s);
+        ck(cudaMemsetAsync(tmax, 0, 8 * sizeof(int), s), "memset");
+
         LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 8), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
-               g->ncells, g->nearv, g->yoff, err);
+               g->ncells, g->nbr, err);
 
         // ---- Alg. 1 (reading #5: fixed n_bistoch iterations)
         g->n = dalloc<float>(A, M, s);
@@ -223,7 +239,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         float* nxt = g->n;
         if (g->n_bistoch % 2 == 0) std::swap(cur, nxt);  // make the last write land in g->n
         for (int it = 0; it < g->n_bistoch; ++it) {
-            LAUNCH(k_bistoch, grid_for(M), kThreads, 0, s, g->nearv, g->yoff, g->m, cur, nxt, (int)M, it == 0);
+            LAUNCH(k_bistoch, grid_for(M), kThreads, 0, s, g->nbr, g->m, cur, nxt, (int)M, it == 0);
             std::swap(cur, nxt);
         }
         if (g->n_bistoch == 0) {
@@ -232,7 +248,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             ck(cudaStreamSynchronize(s), "sync");
         }
         unsigned* res2 = reinterpret_cast<unsigned*>(err + 2);
-        LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nearv, g->yoff, g->m, g->n, (int)M, res2);
+        LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, res2);
 
         // ---- pyramid (Supp. Sec. 2), levels 1 .. Lmax-1
         int Lmax = 1;
@@ -263,7 +279,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             unsigned* ctr2 = dalloc<unsigned>(A, 1, s);
             ck(cudaMemsetAsync(st2, 0, 2 * L.ncells * sizeof(unsigned long long), s), "memset");
             ck(cudaMemsetAsync(ctr2, 0, sizeof(unsigned), s), "memset");
-            LAUNCH(k_pyr_level, (unsigned)L.ncells, 256, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK,
+            LAUNCH(k_pyr_level, (unsigned)L.ncells, 64, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK,
                    ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, st2 + L.ncells, pyrScratch, L.keys, L.parent,
                    L.childStart, L.childList, L.cellOff);
             // P(1): upper bound M on the level size; the kernel stops at the true size via childStart
@@ -274,6 +290,24 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             ncxK = L.ncx;
             ncyK = L.ncy;
         }
+        // per-level maximum vertex count of a level-T tile (T = min(3, Lmax−1)): sizes the tile
+        // kernels' shared memory (hier_kernels.cuh)
+        if (Lmax > 1) {
+            HierArgs hc{};
+            hc.T = std::min(kTileT, Lmax - 1);
+            hc.F = F;
+            for (int k = 0; k <= hc.T; ++k) {
+                hc.lv[k].cellOff = (k == 0) ? g->cellOff : g->lv[k].cellOff;
+                hc.lv[k].ncx = (k == 0) ? ncx : g->lv[k].ncx;
+                hc.lv[k].ncy = (k == 0) ? ncy : g->lv[k].ncy;
+            }
+            hc.ntx = hc.lv[hc.T].ncx;
+            hc.nty = hc.lv[hc.T].ncy;
+            const int nt = F * hc.ntx * hc.nty;
+            LAUNCH(k_tile_maxcounts, grid_for(nt), kThreads, 0, s, hc, nt, tmax);
+        }
+        int tmaxh[8] = {};
+        ck(cudaMemcpyAsync(tmaxh, tmax, sizeof(tmaxh), cudaMemcpyDeviceToHost, s), "d2h");
         // ---- sync 2: level sizes
         std::vector<std::vector<int>> lfo(Lmax);
         for (int k = 1; k < Lmax; ++k) {
@@ -312,8 +346,49 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
                    g->lv[k].childList, (int)g->lv[k].M, g->lv[k].count);
             countK = g->lv[k].count;
         }
+        for (int k = 0; k < 8; ++k) g->tileMax[k] = tmaxh[k];
+
         g->frameLevels = dalloc<int>(A, F, s);
         ck(cudaMemcpyAsync(g->frameLevels, g->frameLevelsH.data(), F * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
+        std::vector<int> lfoAll((size_t)L * (F + 1));
+        for (int f = 0; f <= F; ++f) lfoAll[f] = fo[f];
+        for (int k = 1; k < L; ++k)
+            for (int f = 0; f <= F; ++f) lfoAll[(size_t)k * (F + 1) + f] = lfo[k][f];
+        g->lvFrameOffDev = dalloc<int>(A, lfoAll.size(), s);
+        ck(cudaMemcpyAsync(g->lvFrameOffDev, lfoAll.data(), lfoAll.size() * sizeof(int), cudaMemcpyHostToDevice, s),
+           "h2d");
+        // tile level: 4 (16×16 cells) when its shared memory fits, else 3 (maxima counted for
+        // the level-min(4, Lmax−1) tiles bound the smaller tiles too)
+        g->tileT = std::min(kTileT, L - 1);
+        if (g->tileT == 4) {
+            size_t need = 0;
+            for (int k = 0; k <= 4; ++k) need += (size_t)(g->tileMax[k] + 31) / 32 * 32 * 4;
+            need += (size_t)prog_capacity(g->tileMax, 4) * 2;
+            if (need > 96 * 1024) g->tileT = 3;
+        }
+        if (L > 1) {  // shared-memory need of k_coarse_smem: Σ_k (2c_k + c_k[k<top] + (c_k+1 + c_{k−1})[k>T]) words
+            const int T = g->tileT, top = L - 1;
+            int64_t worst = 0;
+            for (int f = 0; f < F; ++f) {
+                auto cntk = [&](int k) -> int64_t { return k == 0 ? fo[f + 1] - fo[f] : lfo[k][f + 1] - lfo[k][f]; };
+                int64_t w = 0;
+                for (int k = T; k <= top; ++k) {
+                    w += 2 * cntk(k);
+                    if (k < top) w += cntk(k);
+                    if (k > T) w += cntk(k) + 1 + cntk(k - 1);
+                }
+                worst = std::max(worst, w);
+            }
+            g->coarseSmem = (int)std::min<int64_t>(worst * 4 + 64, INT32_MAX);
+        }
+        if (L > 1) {
+            g->tileProgCap = prog_capacity(g->tileMax, g->tileT);
+            HierArgs hg = grid_hier(g);
+            const int nt = n_tiles(hg);
+            g->tileProg = dalloc<uint16_t>(A, (size_t)nt * g->tileProgCap, s);
+            hg.prog = g->tileProg;
+            LAUNCH(k_tile_program, nt, kThreads, 0, s, hg, g->tileProgCap, g->tileProg);
+        }
         ck(cudaStreamSynchronize(s), "sync");  // host vector lifetime for the H2D copy
     } catch (...) {
         free_all(g->allocs, s);
@@ -334,14 +409,13 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     a.M = g->M;
     a.lam = (float)S->lam;
     a.frameOff = g->frameOff;
-    a.nearv = g->nearv;
-    a.yoff = g->yoff;
+    a.nbr = g->nbr;
     a.n = g->n;
     a.sc = S->sc;
     a.diagA = S->diagA;
     a.x = x;
     a.r = S->rh;
-    a.d = S->dh;
+    a.dn = S->dn;
     a.q = S->qh;
     a.s = S->sh;
     a.b = b;
@@ -359,52 +433,118 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     return a;
 }
 
-// lift level-0 input `in0` [C][M] through all levels into S->lvBuf[k]
-void lift_all(fbs_system S, const float* in0, int C, cudaStream_t s) {
+// ---- hierarchical machinery (hier_kernels.cuh): tiles of level-T cells + per-frame coarse levels
+// pyramid geometry of a grid as seen by the tile kernels (system buffers left null)
+HierArgs grid_hier(fbs_grid g) {
+    HierArgs h{};
+    h.L = g->L;
+    h.T = g->tileT;
+    h.F = g->F;
+    h.C = 1;
+    for (int k = 0; k < g->L; ++k) {
+        HLevel& v = h.lv[k];
+        if (k == 0) {
+            v.cellOff = g->cellOff;
+            v.ncx = g->ncx;
+            v.ncy = g->ncy;
+            v.M = g->M;
+        } else {
+            const Level& L = g->lv[k];
+            v.cellOff = L.cellOff;
+            v.ncx = L.ncx;
+            v.ncy = L.ncy;
+            v.childStart = L.childStart;
+            v.childList = L.childList;
+            v.count = L.count;
+            v.keys = L.keys;
+            v.M = L.M;
+        }
+        v.parent = (k + 1 < g->L) ? g->lv[k + 1].parent : nullptr;
+    }
+    h.ntx = h.lv[h.T].ncx;
+    h.nty = h.lv[h.T].ncy;
+    h.frameLevels = g->frameLevels;
+    h.lvFrameOff = g->lvFrameOffDev;
+    h.prog = g->tileProg;
+    h.progCap = g->tileProgCap;
+    int off = 0;
+    for (int k = 0; k <= h.T; ++k) {
+        h.soff[k] = off;
+        off += (g->tileMax[k] + 31) / 32 * 32;
+    }
+    h.soff[h.T + 1] = off;
+    return h;
+}
+
+HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     fbs_grid g = S->g;
-    const float* in = in0;
-    int64_t Min = g->M;
+    HierArgs h = grid_hier(g);
+    h.C = C;
     for (int k = 1; k < g->L; ++k) {
-        const Level& L = g->lv[k];
-        LAUNCH(k_lift, grid_for(L.M), kThreads, 0, s, in, Min, L.childStart, L.childList, L.M, C, S->lvBuf[k]);
-        in = S->lvBuf[k];
-        Min = L.M;
+        h.lv[k].mu = S->mu[k];
+        h.lv[k].buf = S->lvBuf[k];
     }
+    h.alpha = alpha;
+    h.beta = beta;
+    return h;
 }
 
-// project levels L-1 .. 1 in place (mult = μ_k if use_mu, else hier-init weights)
-void project_all(fbs_system S, int C, bool use_mu, double alpha, double beta, cudaStream_t s) {
-    fbs_grid g = S->g;
-    for (int k = g->L - 1; k >= 1; --k) {
-        const Level& L = g->lv[k];
-        const bool top = (k == g->L - 1);
-        const float* up = top ? nullptr : S->lvBuf[k + 1];
-        const int64_t Mup = top ? 0 : g->lv[k + 1].M;
-        const int* parent = top ? nullptr : g->lv[k + 1].parent;
-        LAUNCH(k_project, grid_for(L.M), kThreads, 0, s, S->lvBuf[k], L.M, up, Mup, parent, C,
-               use_mu ? S->mu[k] : nullptr, L.count, L.keys, g->frameLevels, k, alpha, beta);
-    }
+int n_tiles(const HierArgs& h) { return h.F * h.ntx * h.nty; }
+inline size_t tile_smem(const HierArgs& h, bool init) {
+    return (size_t)(h.soff[h.T + 1] + (init ? h.soff[1] : 0)) * sizeof(float);
+}
+inline size_t tile_up_smem(const HierArgs& h) { return tile_smem(h, false) + (size_t)h.progCap * 2 + 16; }
+
+// Levels T..top of every frame: shared-memory kernel when the largest frame's coarse pyramid
+// fits (grid->coarseSmem bytes), else the global-memory kernel.
+void launch_coarse(fbs_grid g, const HierArgs& h, int use_mu, int do_project, cudaStream_t s) {
+    if (g->coarseSmem > 0 && g->coarseSmem <= 200 * 1024)
+        LAUNCH(k_coarse_smem, h.F, 512, (size_t)g->coarseSmem, s, h, use_mu, do_project);
+    else
+        LAUNCH(k_coarse, h.F, 1024, 0, s, h, use_mu, do_project);
 }
 
-// s = M⁻¹ r (hier) given w0 written; finishes the ρ reduction
+// The whole pyramid application in one cooperative kernel (hier_kernels.cuh k_hier).
+template <int MODE>
+void launch_hier(fbs_system S, const HierArgs& h, const VecArgs& a, const float* in0, float* out0, int first,
+                 cudaStream_t s) {
+    // level 0 → 1 lift at full occupancy; levels 1..top in the cooperative kernel; level-0
+    // combination of the PCG preconditioner at full occupancy (k_precond_finish2)
+    const Level& L1 = S->g->lv[1];
+    LAUNCH(k_lift01, grid_for(L1.M), kThreads, 0, s, in0, S->g->M, L1.childStart, L1.childList, L1.M, h.C,
+           S->lvBuf[1]);
+    {
+        ::fbs::ProfScope _ps(MODE == HIER_PCG ? "k_hier<PCG>" : MODE == HIER_PDA ? "k_hier<PDA>"
+                             : MODE == HIER_INIT ? "k_hier<INIT>" : "k_hier<PLAIN>", s);
+        int bpf = S->bpfH;
+        unsigned* bar = S->bar;
+        int k_lift0 = 1;
+        int do_level0 = (MODE == HIER_PCG) ? 0 : 1;
+        void* args[] = {(void*)&h, (void*)&a, (void*)&in0, (void*)&out0, (void*)&first, (void*)&bpf, (void*)&bar,
+                        (void*)&k_lift0, (void*)&do_level0};
+        ck(cudaLaunchCooperativeKernel((const void*)k_hier<MODE>, dim3(S->g->F * bpf), dim3(1024), args, 0, s),
+           "k_hier cooperative launch");
+        ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (MODE == HIER_PCG) LAUNCH(k_precond_finish2, S->g->F * S->BPF, kThreads, 0, s, a, first);
+}
+
+// s = M⁻¹_hier r (Eq. hier_precond) for the PCG from w0 = mask∘r; finishes the ρ reduction.
 void hier_precond(fbs_system S, const VecArgs& a, int first, cudaStream_t s) {
-    lift_all(S, S->w0, S->K, s);
-    project_all(S, S->K, true, 0, 0, s);
-    const int nb = S->g->F * S->BPF;
-    LAUNCH(k_precond_finish, nb, kThreads, 0, s, a, first);
+    launch_hier<HIER_PCG>(S, S->hP, a, S->w0, nullptr, first, s);
 }
 
-void pcg_iteration(fbs_system S, const VecArgs& a, cudaStream_t s) {
+// One PCG iteration (Alg. 2 lines 14, 6-13): direction, SpMV + α, update (+ M⁻¹ and ρ, β).
+void pcg_iteration(fbs_system S, const VecArgs& a, int it, cudaStream_t s) {
     const int nb = S->g->F * S->BPF;
-    const bool hier = S->o.precond == FBS_PRECOND_HIER;
-    LAUNCH(k_spmv, nb, kThreads, 0, s, a);
-    if (hier) {
+    LAUNCH(k_direction2, nb, kThreads, 0, s, a, it == 0);
+    LAUNCH(k_spmv2, nb, kThreads, 0, s, a);
+    if (S->useHierP) {
         LAUNCH(k_update<true>, nb, kThreads, 0, s, a);
         hier_precond(S, a, 0, s);
     } else {
         LAUNCH(k_update<false>, nb, kThreads, 0, s, a);
     }
-    LAUNCH(k_direction, nb, kThreads, 0, s, a, 0);
 }
 
 // Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.
@@ -412,9 +552,8 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     fbs_grid g = S->g;
     const int nb = g->F * S->BPF;
     const int FK = g->F * S->K;
-    const bool hier = S->o.precond == FBS_PRECOND_HIER;
     LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK);
-    if (hier) {
+    if (S->useHierP) {
         auto k1 = k_residual0<true, true>;
         auto k2 = k_residual0<true, false>;
         if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
@@ -426,9 +565,9 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
         else LAUNCH(k2, nb, kThreads, 0, s, a);
     }
-    LAUNCH(k_direction, nb, kThreads, 0, s, a, 1);
+    // d = s (Alg. 2 line 3) is folded into the first iteration's fused direction + SpMV kernel
     if (S->o.mode == FBS_MODE_FIXED) {
-        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, s);
+        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, i, s);
         return;
     }
     // TOL: device-side per-channel stopping; the host polls the active count one chunk behind
@@ -442,7 +581,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     try {
         while (done < S->o.max_iters) {
             const int nit = std::min(chunk, S->o.max_iters - done);
-            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, s);
+            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, done + i, s);
             done += nit;
             ck(cudaMemcpyAsync(&pin[slot], a.sc_.n_active, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
             ck(cudaEventRecord(ev[slot], s), "event");
@@ -520,7 +659,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         auto& A = S->allocs;
         // launch geometry of the per-frame kernels: BPF blocks per frame
         int occ = 0;
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv, kThreads, 0), "occupancy");
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv2, kThreads, 0), "occupancy");
         const int64_t want = (g->maxFrameM + kThreads - 1) / kThreads;
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
         S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
@@ -533,10 +672,12 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->y0 = dalloc<float>(A, KM, s);
         S->xh = dalloc<float>(A, KM, s);
         S->rh = dalloc<float>(A, KM, s);
-        S->dh = dalloc<float>(A, KM, s);
+        S->dn = dalloc<float2>(A, KM, s);
         S->qh = dalloc<float>(A, KM, s);
         S->sh = dalloc<float>(A, KM, s);
-        const bool hierP = o.precond == FBS_PRECOND_HIER, hierI = o.init == FBS_INIT_HIER;
+        const bool hierP = o.precond == FBS_PRECOND_HIER && g->L > 1;  // L = 1: hier ≡ Jacobi / flat
+        const bool hierI = o.init == FBS_INIT_HIER && g->L > 1;
+        S->useHierP = hierP;
         if (hierP || hierI) {
             S->w0 = dalloc<float>(A, (size_t)S->C * M, s);
             for (int k = 1; k < g->L; ++k) {
@@ -544,7 +685,21 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
                 if (hierP) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
             }
         }
-        S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * K, s);
+        int64_t perFrameBlocks = S->BPF;
+        if (hierP || hierI) {
+            int occH = 0;
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occH, k_hier<HIER_PCG>, 1024, 0), "occupancy");
+            S->bpfH = std::max(1, (g_num_sms * std::max(occH, 1)) / F);
+            if (S->bpfH * F > g_num_sms * std::max(occH, 1)) throw Err(FBS_ELIMIT, "too many frames for one cooperative launch");
+            perFrameBlocks = std::max<int64_t>(perFrameBlocks, S->bpfH);
+            S->bar = dalloc<unsigned>(A, 2, s);
+            ck(cudaMemsetAsync(S->bar, 0, 2 * sizeof(unsigned), s), "memset");
+        }
+        if (hierP || hierI) {
+            S->hP = make_hier(S, K, o.precond_alpha, o.precond_beta);
+            perFrameBlocks = std::max<int64_t>(perFrameBlocks, (int64_t)S->hP.ntx * S->hP.nty);
+        }
+        S->partial = dalloc<double>(A, (size_t)F * perFrameBlocks * 2 * K, s);
         S->counters = dalloc<unsigned>(A, F, s);
         ck(cudaMemsetAsync(S->counters, 0, F * sizeof(unsigned), s), "memset");
         S->fwd = alloc_scalars(A, F * K, s);
@@ -556,21 +711,20 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
                S->b);
         // a5: assemble (+ flat/zero init)
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
-        LAUNCH(k_assemble, nb, kThreads, 0, s, a, S->diagA, S->mu0, hierP ? S->w0 : nullptr, o.init, S->fwd);
-        // a6/a7: hierarchical preconditioner multipliers and init
+        const int init_mode = (o.init == FBS_INIT_HIER && !hierI) ? FBS_INIT_FLAT : o.init;
+        LAUNCH(k_assemble, nb, kThreads, 0, s, a, S->diagA, S->mu0, hierP ? S->w0 : nullptr, init_mode, S->fwd);
+        // a6/a7: hierarchical preconditioner multipliers μ_k = z_w P(1) / P(diag A), and init
         if (hierP) {
-            lift_all(S, S->w0, 1, s);
-            for (int k = 1; k < g->L; ++k)
-                LAUNCH(k_mu, grid_for(g->lv[k].M), kThreads, 0, s, S->lvBuf[k], g->lv[k].count, g->lv[k].keys,
-                       g->frameLevels, g->lv[k].M, k, o.precond_alpha, o.precond_beta, S->mu[k]);
+            HierArgs h = make_hier(S, 1, o.precond_alpha, o.precond_beta);
+            launch_hier<HIER_PDA>(S, h, a, S->w0, nullptr, 0, s);
         }
         if (hierI) {
+            HierArgs h = make_hier(S, K + 1, o.init_alpha, o.init_beta);
             LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, K, S->w0);
-            lift_all(S, S->w0, K + 1, s);
-            project_all(S, K + 1, false, o.init_alpha, o.init_beta, s);
-            LAUNCH(k_init_finish, grid_for(M), kThreads, 0, s, S->w0, M, K, a.parent0, a.acc1, a.M1, S->xh);
+            launch_hier<HIER_INIT>(S, h, a, S->w0, S->xh, 0, s);
         }
         ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
+        LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, K);
         // a8: PCG
         run_pcg(S, a, false, s);
         // a9: slice
@@ -696,7 +850,7 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
         if (nbr) {
             std::vector<void*> tmp;
             int* d = dalloc<int>(tmp, (size_t)M * 10, s);
-            LAUNCH(k_export_nbr, grid_for(M), kThreads, 0, s, g->nearv, g->yoff, (int)M, d);
+            LAUNCH(k_export_nbr, grid_for(M), kThreads, 0, s, g->nbr, (int)M, d);
             ck(cudaMemcpyAsync(nbr, d, (size_t)M * 40, cudaMemcpyDeviceToHost, s), "d2h");
             free_all(tmp, s);
         }
@@ -827,7 +981,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
 int fbs_blur(fbs_grid g, const float* v, float* out, fbs_stream stream) {
     return guard("fbs_blur", [&] {
         if (!g || !v || !out) throw Err(FBS_EINVAL, "null pointer");
-        LAUNCH(k_blur, grid_for(g->M), kThreads, 0, (cudaStream_t)stream, g->nearv, g->yoff, v, g->M, out);
+        LAUNCH(k_blur, grid_for(g->M), kThreads, 0, (cudaStream_t)stream, g->nbr, v, g->M, out);
     });
 }
 
@@ -853,15 +1007,17 @@ int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_strea
         fbs_grid g = S->g;
         std::vector<void*> tmp;
         const size_t KM = (size_t)S->K * g->M;
-        float* w = (S->o.precond == FBS_PRECOND_HIER) ? S->w0 : dalloc<float>(tmp, KM, s);
+        float* w = dalloc<float>(tmp, KM, s);
         LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, r, S->mu0, g->M, S->K, w);
-        const bool hier = S->o.precond == FBS_PRECOND_HIER && g->L > 1;
-        if (hier) {
-            lift_all(S, w, S->K, s);
-            project_all(S, S->K, true, 0, 0, s);
+        if (S->useHierP) {
+            float* planar = dalloc<float>(tmp, KM, s);
+            HierArgs h = S->hP;
+            VecArgs a = make_args(S, S->fwd, S->xh, S->b);
+            launch_hier<HIER_PLAIN>(S, h, a, w, planar, 0, s);
+            LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, S->K, out);
+        } else {
+            LAUNCH(k_precond_out, grid_for(g->M), kThreads, 0, s, w, S->mu0, nullptr, nullptr, 0, g->M, S->K, out);
         }
-        LAUNCH(k_precond_out, grid_for(g->M), kThreads, 0, s, w, S->mu0, hier ? g->lv[1].parent : nullptr,
-               hier ? S->lvBuf[1] : nullptr, hier ? g->lv[1].M : 0, g->M, S->K, out);
         free_all(tmp, s);
     });
 }

@@ -17,7 +17,7 @@ constexpr int kD = 5;                // XYLUV dims
 constexpr int kBbarDiag = 2 * kD;    // B̄_diag = 2D (reading #4)
 constexpr int kCellMaxPx = 64;       // level-0 cell = one warp, ≤ 2 px per lane
 constexpr int kCellsPerBlock = 8;    // 8 warps, one cell each
-constexpr int kCoarseCap = 4096;     // children of one pyramid coarse cell (smem sort capacity)
+constexpr int kCoarseCap = 512;      // children of one pyramid coarse cell sorted in shared memory (larger: global scratch)
 constexpr int kMaxLevels = 24;
 constexpr int kThreads = 256;        // vertex-parallel kernels
 constexpr int kMaxK = 64;
@@ -115,27 +115,26 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* state
 // near: 8 signed bytes = relative offsets of the (x−, x+, l−, l+, u−, u+, v−, v+) neighbours
 // (0 = absent; |offset| ≤ 127 because a σxy cell holds ≤ 64 vertices and x-neighbours sit in
 // the adjacent cell of the same canonical row).  yoff: relative offsets of (y−, y+), 0 = absent.
-__device__ __forceinline__ int near_off(uint2 nr, int i) {
-    const unsigned w = (i < 4) ? nr.x : nr.y;
+// One int4 per vertex (16 B, a single 128-bit load): .x/.y = the 8 near offsets, .z/.w = y−, y+.
+__device__ __forceinline__ int near_off(int4 nb, int i) {
+    const unsigned w = (unsigned)((i < 4) ? nb.x : nb.y);
     return (int)(int8_t)(w >> (8 * (i & 3)));
 }
 
 // Σ_{u ∈ N(v)} x[u] in fixed slot order (x−,x+,l−,l+,u−,u+,v−,v+,y−,y+).
-__device__ __forceinline__ float nbr_sum(const float* __restrict__ x, int v, uint2 nr, int2 yo) {
+__device__ __forceinline__ float nbr_sum(const float* __restrict__ x, int v, int4 nb) {
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int o = near_off(nr, i);
+        const int o = near_off(nb, i);
         if (o) s += __ldg(x + v + o);
     }
-    if (yo.x) s += __ldg(x + v + yo.x);
-    if (yo.y) s += __ldg(x + v + yo.y);
+    if (nb.z) s += __ldg(x + v + nb.z);
+    if (nb.w) s += __ldg(x + v + nb.w);
     return s;
 }
 
-__device__ __forceinline__ bool is_isolated(uint2 nr, int2 yo) {
-    return (nr.x | nr.y | (unsigned)yo.x | (unsigned)yo.y) == 0u;
-}
+__device__ __forceinline__ bool is_isolated(int4 nb) { return (nb.x | nb.y | nb.z | nb.w) == 0; }
 
 // ------------------------------------------------------------------ handles
 struct Level {          // pyramid level k ≥ 1
@@ -163,6 +162,39 @@ struct PcgScalars {     // per (frame, channel), fk = f*K + k
     int* n_active = nullptr;  // single counter
 };
 
+// ------------------------------------------------------------------ hierarchy (hier_kernels.cuh)
+constexpr int kTileT = 4;        // largest tile level: one level-4 cell = 16 × 16 σxy-cells
+constexpr int kTileCap = 4096;   // vertices of one tile at any level (≤ its 64 × 64 pixels)
+constexpr int kTileRows = 1 << kTileT;
+
+struct HLevel {
+    const int* cellOff = nullptr;     // [ncells + 1]
+    int ncx = 0, ncy = 0;
+    const int* parent = nullptr;      // level k → k+1 (nullptr at the top level)
+    const int* childStart = nullptr;  // k ≥ 1: children (level k−1) of level-k vertices
+    const int* childList = nullptr;
+    const int* count = nullptr;       // k ≥ 1: P(1)
+    const uint64_t* keys = nullptr;   // k ≥ 1
+    const float* mu = nullptr;        // k ≥ 1: preconditioner multiplier
+    float* buf = nullptr;             // k ≥ 1: lifted values [C][M]
+    int64_t M = 0;
+};
+
+struct HierArgs {
+    HLevel lv[kMaxLevels];
+    int soff[kTileT + 2];   // shared-memory offsets (floats) of the tile's level arrays; soff[T+1] = total
+    int T;              // tile level (≤ L−1)
+    int L;              // levels incl. base (max over frames)
+    int F;
+    int C;              // channels carried through the pyramid
+    int ntx, nty;       // tiles per frame along x / y (= level-T cells)
+    const int* frameLevels;
+    const int* lvFrameOff;  // [L][F+1] per-level frame vertex offsets
+    double alpha, beta;     // z_weight parameters of the current use
+    const uint16_t* prog;   // tile programs (hier_kernels.cuh), progCap u16 per tile
+    int progCap;
+};
+
 }  // namespace fbs
 
 struct fbs_grid_s {
@@ -181,8 +213,7 @@ struct fbs_grid_s {
     uint64_t* keys = nullptr;  // [N] capacity (first M valid)
     int* m = nullptr;          // [N] capacity
     int* cellOff = nullptr;    // [ncells + 1]
-    uint2* nearv = nullptr;    // [M]
-    int2* yoff = nullptr;      // [M]
+    int4* nbr = nullptr;       // [M] packed neighbour offsets (fbs_common.cuh near_off)
     float* n = nullptr;        // [M]
     int* frameOff = nullptr;   // device [F + 1]
     std::vector<int64_t> frameOffH;
@@ -192,6 +223,12 @@ struct fbs_grid_s {
     int L = 1;  // levels incl. base (max over frames)
     fbs::Level lv[fbs::kMaxLevels];
     int64_t maxFrameM = 0;
+    int* lvFrameOffDev = nullptr;  // [L][F + 1]
+    int tileMax[8] = {};           // largest level-k vertex count of a level-3 tile (k ≤ 3)
+    int tileT = 0;                 // tile level T = min(3, L − 1)
+    int coarseSmem = 0;            // bytes of k_coarse_smem for the largest frame
+    uint16_t* tileProg = nullptr;  // per-tile programs
+    int tileProgCap = 0;
     std::vector<void*> allocs;
 };
 
@@ -213,7 +250,7 @@ struct fbs_system_s {
     float* xh = nullptr;      // [K][M] forward solution ŷ
     float* xb = nullptr;      // [K][M] backward solution ∂f/∂b
     float* rh = nullptr;
-    float* dh = nullptr;
+    float2* dn = nullptr;     // [K][M] interleaved (d, n)
     float* qh = nullptr;
     float* sh = nullptr;
     float* w0 = nullptr;                   // [C][M] level-0 pyramid input
@@ -223,6 +260,10 @@ struct fbs_system_s {
     double* partial = nullptr;  // [F][BPF][2K]
     unsigned* counters = nullptr;  // [F]
     fbs::PcgScalars fwd, bwd;
+    bool useHierP = false;
+    int bpfH = 1;              // blocks per frame of the cooperative hierarchy kernel
+    unsigned* bar = nullptr;   // its grid barrier (count, generation)
+    fbs::HierArgs hP{};
     bool has_backward = false;
     std::vector<void*> allocs;
 };

@@ -190,7 +190,7 @@ __device__ __forceinline__ int lower_bound_s(const uint32_t* a, int n, uint32_t 
 // shared memory, then each vertex binary-searches its 10 ±1 neighbours (reading #4).
 __global__ void __launch_bounds__(256) k_grid_neighbours(
     const uint64_t* __restrict__ keys, const int* __restrict__ cellOff, int ncx, int ncy,
-    int64_t ncells, uint2* __restrict__ nearv, int2* __restrict__ yoff, int* __restrict__ err) {
+    int64_t ncells, int4* __restrict__ nbr, int* __restrict__ err) {
     __shared__ uint32_t sc[kCellsPerBlock][5][kCellMaxPx];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
@@ -239,8 +239,7 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
                 const unsigned b = (unsigned)(o & 0xff);
                 if (k < 4) bx |= b << (8 * k); else by |= b << (8 * (k - 4));
             }
-            nearv[v] = make_uint2(bx, by);
-            yoff[v] = make_int2(offs[8], offs[9]);
+            nbr[v] = make_int4((int)bx, (int)by, offs[8], offs[9]);
         }
         __syncwarp();
     }
@@ -248,37 +247,35 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
 
 // ---------------------------------------------------------------- Alg. 1 bistochastization
 // n ← sqrt((n ∘ m) / (B̄ n)),  B̄ n = 2D n_v + Σ_{u∈N(v)} n_u, fp32.
-__global__ void __launch_bounds__(256) k_bistoch(const uint2* __restrict__ nearv,
-                                                 const int2* __restrict__ yoff,
+__global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
                                                  float* __restrict__ nout, int M, int first) {
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
-        const uint2 nr = nearv[v];
-        const int2 yo = yoff[v];
+        const int4 nb = nbr[v];
         float nv, bn;
         if (first) {
             int deg = 0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) deg += near_off(nr, i) != 0;
-            deg += (yo.x != 0) + (yo.y != 0);
+            for (int i = 0; i < 8; ++i) deg += near_off(nb, i) != 0;
+            deg += (nb.z != 0) + (nb.w != 0);
             nv = 1.f;
             bn = (float)kBbarDiag + (float)deg;
         } else {
             nv = nin[v];
-            bn = (float)kBbarDiag * nv + nbr_sum(nin, v, nr, yo);
+            bn = (float)kBbarDiag * nv + nbr_sum(nin, v, nb);
         }
         nout[v] = sqrtf(nv * (float)m[v] / bn);
     }
 }
 
 // max|n∘B̄n − m| and max m (order-independent max ⇒ deterministic), reporting only.
-__global__ void k_bistoch_residual(const uint2* __restrict__ nearv, const int2* __restrict__ yoff,
+__global__ void k_bistoch_residual(const int4* __restrict__ nbr,
                                    const int* __restrict__ m, const float* __restrict__ n, int M,
                                    unsigned* __restrict__ out2) {
     float e = 0.f, mm = 0.f;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
-        const float bn = (float)kBbarDiag * n[v] + nbr_sum(n, v, nearv[v], yoff[v]);
+        const float bn = (float)kBbarDiag * n[v] + nbr_sum(n, v, nbr[v]);
         e = fmaxf(e, fabsf(n[v] * bn - (float)m[v]));
         mm = fmaxf(mm, (float)m[v]);
     }
@@ -293,23 +290,22 @@ __global__ void k_bistoch_residual(const uint2* __restrict__ nearv, const int2* 
 }
 
 // ---------------------------------------------------------------- exports
-__global__ void k_export_nbr(const uint2* __restrict__ nearv, const int2* __restrict__ yoff, int M,
+__global__ void k_export_nbr(const int4* __restrict__ nbr, int M,
                              int* __restrict__ nbr10) {
     // export slot order (x−,x+,y−,y+,l−,l+,u−,u+,v−,v+); internal near order (x−,x+,l−,l+,u−,u+,v−,v+)
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
-        const uint2 nr = nearv[v];
-        const int2 yo = yoff[v];
+        const int4 q4 = nbr[v];
         int* o = nbr10 + (size_t)v * 10;
         int nb[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int d = near_off(nr, i);
+            const int d = near_off(q4, i);
             nb[i] = d ? v + d : -1;
         }
         o[0] = nb[0];
         o[1] = nb[1];
-        o[2] = yo.x ? v + yo.x : -1;
-        o[3] = yo.y ? v + yo.y : -1;
+        o[2] = q4.z ? v + q4.z : -1;
+        o[3] = q4.w ? v + q4.w : -1;
         o[4] = nb[2];
         o[5] = nb[3];
         o[6] = nb[4];

@@ -50,7 +50,7 @@ __device__ __forceinline__ int block_excl_scan(int x, int* sh /*[33]*/, int* tot
 // prefix is published first (it is known before sorting), which also places the cell's slice of
 // a global scratch array; cells with more than kCoarseCap children sort there instead of in
 // shared memory (rare: dense pixel-noise images at σl = σuv = 1).
-__global__ void __launch_bounds__(256) k_pyr_level(
+__global__ void __launch_bounds__(64) k_pyr_level(
     const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK, int ncxK, int ncyK,
     int ncxN, int ncyN, int64_t ncellsN, unsigned* __restrict__ tile_counter,
     unsigned long long* __restrict__ stateC, unsigned long long* __restrict__ stateV,

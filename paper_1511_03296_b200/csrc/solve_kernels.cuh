@@ -20,14 +20,13 @@ struct VecArgs {
     int64_t M;
     float lam;
     const int* frameOff;  // [F+1]
-    const uint2* nearv;
-    const int2* yoff;
+    const int4* nbr;
     const float* n;       // Alg. 1 result
     const float* sc;      // S c
     const float* diagA;   // diag(A) in Laplacian form; 0 ⇔ dead vertex (reading #6)
     float* x;
     float* r;
-    float* d;
+    float2* dn;           // interleaved (d, n): one 8-byte gather per neighbour in the SpMV
     float* q;
     float* s;
     const float* b;
@@ -47,23 +46,24 @@ struct VecArgs {
 // (A y)_v in Laplacian-difference form (see header): λ n_v Σ_u n_u (y_v − y_u) + Sc_v y_v,
 // neighbours in fixed slot order (x−,x+,l−,l+,u−,u+,v−,v+,y−,y+).
 __device__ __forceinline__ float apply_A_row(const float* __restrict__ y, const float* __restrict__ n, int v,
-                                            uint2 nr, int2 yo, float lam, float scv) {
-    const float yv = y[v];
+                                            int4 nb, float lam, float scv, float yv, float nv) {
     float acc = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int o = near_off(nr, i);
+        const int o = near_off(nb, i);
         if (o) acc += __ldg(n + v + o) * (yv - __ldg(y + v + o));
     }
-    if (yo.x) acc += __ldg(n + v + yo.x) * (yv - __ldg(y + v + yo.x));
-    if (yo.y) acc += __ldg(n + v + yo.y) * (yv - __ldg(y + v + yo.y));
-    return lam * n[v] * acc + scv * yv;
+    if (nb.z) acc += __ldg(n + v + nb.z) * (yv - __ldg(y + v + nb.z));
+    if (nb.w) acc += __ldg(n + v + nb.w) * (yv - __ldg(y + v + nb.w));
+    return lam * nv * acc + scv * yv;
+}
+__device__ __forceinline__ float apply_A_row(const float* __restrict__ y, const float* __restrict__ n, int v,
+                                            int4 nb, float lam, float scv) {
+    return apply_A_row(y, n, v, nb, lam, scv, y[v], n[v]);
 }
 
 // Σ_{u∈N(v)} n_u  (so that diag(A) = λ n_v Σ n_u + Sc_v)
-__device__ __forceinline__ float nbr_nsum(const float* __restrict__ n, int v, uint2 nr, int2 yo) {
-    return nbr_sum(n, v, nr, yo);
-}
+__device__ __forceinline__ float nbr_nsum(const float* __restrict__ n, int v, int4 nb) { return nbr_sum(n, v, nb); }
 
 // ---------------------------------------------------------------- splat  S p
 // One warp per σxy cell.  Pixels of a vertex all lie in its cell; the per-vertex sum is formed
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
     for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
-        const float dA = a.lam * a.n[v] * nbr_nsum(a.n, v, a.nearv[v], a.yoff[v]) + a.sc[v];
+        const float dA = a.lam * a.n[v] * nbr_nsum(a.n, v, a.nbr[v]) + a.sc[v];
         const bool live = dA > 0.f;
         diagA[v] = dA;
         mu0[v] = live ? 1.f / dA : 0.f;
@@ -232,21 +232,6 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
 }
 
 // ---------------------------------------------------------------- pyramid lift / project
-// lift: out[c][p] = Σ_{children j of p} in[c][j]   (P(y) bottom-up)
-__global__ void k_lift(const float* __restrict__ in, int64_t Min, const int* __restrict__ childStart,
-                       const int* __restrict__ childList, int64_t Mout, int C, float* __restrict__ out) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < Mout;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int s = childStart[p], e = childStart[p + 1];
-        for (int c = 0; c < C; ++c) {
-            const float* src = in + (size_t)c * Min;
-            float acc = 0.f;
-            for (int jj = s; jj < e; ++jj) acc += src[childList[jj]];
-            out[(size_t)c * Mout + p] = acc;
-        }
-    }
-}
-
 // μ_k = z_w(k) · P(1)_k / P(diag A)_k  (Eq. hier_precond); 0 where the
 // denominator is 0 (reading #10) or where the frame has fewer than k+1 levels.
 __global__ void k_mu(const float* __restrict__ PdA, const int* __restrict__ count,
@@ -258,31 +243,6 @@ __global__ void k_mu(const float* __restrict__ PdA, const int* __restrict__ coun
         const int f = (int)(keys[p] >> 56);
         const float den = PdA[p];
         mu[p] = (level < frameLevels[f] && den > 0.f) ? (float)(zw * (double)count[p] / (double)den) : 0.f;
-    }
-}
-
-// project: L_k[c][v] = mult_k(v) · L_k[c][v] + L_{k+1}[c][parent_k(v)]   (Pᵀ top-down)
-// mult_k = mu[v] (preconditioner) or z_w(k; α, β) / P(1)_k (hier init).
-__global__ void k_project(float* __restrict__ Lk, int64_t Mk, const float* __restrict__ up, int64_t Mup,
-                          const int* __restrict__ parent, int C, const float* __restrict__ mu,
-                          const int* __restrict__ count, const uint64_t* __restrict__ keys,
-                          const int* __restrict__ frameLevels, int level, double alpha, double beta) {
-    const double zw = (level == 0) ? 1.0 : pow(alpha, -(beta + (double)level));
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < Mk;
-         v += (int64_t)gridDim.x * blockDim.x) {
-        float mult;
-        if (mu) {
-            mult = mu[v];
-        } else {
-            const int f = (int)(keys[v] >> 56);
-            mult = (level < frameLevels[f]) ? (float)(zw / (double)count[v]) : 0.f;
-        }
-        const int pa = up ? parent[v] : 0;
-        for (int c = 0; c < C; ++c) {
-            float val = mult * Lk[(size_t)c * Mk + v];
-            if (up) val += up[(size_t)c * Mup + pa];
-            Lk[(size_t)c * Mk + v] = val;
-        }
     }
 }
 
@@ -338,7 +298,7 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
         double rho = 0.0, rr = 0.0;
         for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
             float r = a.b[off + v];
-            if (!X_ZERO) r -= apply_A_row(a.x + off, a.n, v, a.nearv[v], a.yoff[v], a.lam, a.sc[v]);
+            if (!X_ZERO) r -= apply_A_row(a.x + off, a.n, v, a.nbr[v], a.lam, a.sc[v]);
             a.r[off + v] = r;
             const float m0 = a.mu0[v];
             if (HIER) {
@@ -355,8 +315,98 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
     if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, true, shd);
 }
 
-// Alg. 2 lines 6-7:  q = A d;  α = ρ / dᵀq  (breakdown guard dᵀq ≤ 0, reading #11)
-__global__ void __launch_bounds__(256) k_spmv(VecArgs a) {
+// Alg. 2 lines 8-12:  x += αd;  r −= αq;  s = M⁻¹r;  ρ_new = rᵀs.
+// Jacobi: s = r/diag(A) inline, reduction finished here.  HIER: writes w0 = mask∘r.
+template <bool HIER>
+__global__ void __launch_bounds__(256) k_update(VecArgs a) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        double rho = 0.0, rr = 0.0;
+        if (a.sc_.active[fk]) {
+            const float al = (float)a.sc_.alpha[fk];
+            const size_t off = (size_t)k * a.M;
+            const int stride = a.BPF * blockDim.x;
+            for (int v0u = v0 + j * blockDim.x + threadIdx.x; v0u < v1; v0u += 4 * stride) {
+                // loads of 4 vertices first (the VecArgs pointers may alias for the compiler)
+                float xv[4], dv[4], rv[4], qv[4], mv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0u + u * stride;
+                    if (v < v1) {
+                        xv[u] = a.x[off + v];
+                        dv[u] = a.dn[off + v].x;
+                        rv[u] = a.r[off + v];
+                        qv[u] = a.q[off + v];
+                        mv[u] = a.mu0[v];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0u + u * stride;
+                    if (v >= v1) continue;
+                    a.x[off + v] = xv[u] + al * dv[u];
+                    const float r = rv[u] - al * qv[u];
+                    a.r[off + v] = r;
+                    if (HIER) {
+                        a.w0[off + v] = (mv[u] > 0.f) ? r : 0.f;
+                    } else {
+                        const float s = mv[u] * r;
+                        a.s[off + v] = s;
+                        rho += (double)r * (double)s;
+                        rr += (double)r * (double)r;
+                    }
+                }
+            }
+        }
+        if (!HIER) write_partials(a, f, j, k, rho, rr, shd);
+    }
+    if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, false, shd);
+}
+
+// ---------------------------------------------------------------- streaming PCG kernels
+// dn[k][v] = (d, n_v): the direction interleaved with n, so the SpMV's neighbour terms
+// n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
+__global__ void k_init_dn(float2* __restrict__ dn, const float* __restrict__ n, int64_t M, int K) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x)
+        dn[i] = make_float2(0.f, n[i % M]);
+}
+
+// Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
+__global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const int stride = a.BPF * blockDim.x;
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        if (!first && !a.sc_.active[fk]) continue;
+        const float be = first ? 0.f : (float)a.sc_.beta[fk];
+        const size_t off = (size_t)k * a.M;
+        for (int v0u = v0 + j * blockDim.x + threadIdx.x; v0u < v1; v0u += 4 * stride) {
+            float sv[4];
+            float2 dv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = v0u + u * stride;
+                if (v < v1) {
+                    sv[u] = a.s[off + v];
+                    dv[u] = a.dn[off + v];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = v0u + u * stride;
+                if (v < v1) a.dn[off + v] = make_float2(first ? sv[u] : sv[u] + be * dv[u].x, dv[u].y);
+            }
+        }
+    }
+}
+
+// Alg. 2 lines 6-7:  q = A d (Laplacian-difference form), α = ρ / dᵀq (breakdown: dᵀq ≤ 0).
+__global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
@@ -366,11 +416,31 @@ __global__ void __launch_bounds__(256) k_spmv(VecArgs a) {
         double dq = 0.0;
         if (a.sc_.active[fk]) {
             const size_t off = (size_t)k * a.M;
-            const float* d = a.d + off;
+            const float2* dn = a.dn + off;
             for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
-                const float q = apply_A_row(d, a.n, v, a.nearv[v], a.yoff[v], a.lam, a.sc[v]);
+                const int4 nb = a.nbr[v];
+                const float2 me = dn[v];
+                const float scv = a.sc[v];
+                float acc = 0.f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int o = near_off(nb, e);
+                    if (o) {
+                        const float2 u = __ldg(dn + v + o);
+                        acc += u.y * (me.x - u.x);
+                    }
+                }
+                if (nb.z) {
+                    const float2 u = __ldg(dn + v + nb.z);
+                    acc += u.y * (me.x - u.x);
+                }
+                if (nb.w) {
+                    const float2 u = __ldg(dn + v + nb.w);
+                    acc += u.y * (me.x - u.x);
+                }
+                const float q = a.lam * me.y * acc + scv * me.x;
                 a.q[off + v] = q;
-                dq += (double)d[v] * (double)q;
+                dq += (double)me.x * (double)q;
             }
         }
         write_partials(a, f, j, k, dq, 0.0, shd);
@@ -397,83 +467,46 @@ __global__ void __launch_bounds__(256) k_spmv(VecArgs a) {
     }
 }
 
-// Alg. 2 lines 8-12:  x += αd;  r −= αq;  s = M⁻¹r;  ρ_new = rᵀs.
-// Jacobi: s = r/diag(A) inline, reduction finished here.  HIER: writes w0 = mask∘r.
-template <bool HIER>
-__global__ void __launch_bounds__(256) k_update(VecArgs a) {
+// Hierarchical M⁻¹ at level 0 (Eq. hier_precond): s = mask∘(μ0 r + acc1[parent0]) with acc1 the
+// projected level-1 values (k_tile_project); ρ = rᵀs, ‖r‖² and the per-frame finish (Alg. 2
+// lines 11-13; first: lines 3-4).
+__global__ void __launch_bounds__(256) k_precond_finish2(VecArgs a, int first) {
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int k = 0; k < a.K; ++k) {
-        const int fk = f * a.K + k;
-        double rho = 0.0, rr = 0.0;
-        if (a.sc_.active[fk]) {
-            const float al = (float)a.sc_.alpha[fk];
-            const size_t off = (size_t)k * a.M;
-            for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
-                a.x[off + v] += al * a.d[off + v];
-                const float r = a.r[off + v] - al * a.q[off + v];
-                a.r[off + v] = r;
-                const float m0 = a.mu0[v];
-                if (HIER) {
-                    a.w0[off + v] = (m0 > 0.f) ? r : 0.f;
-                } else {
-                    const float s = m0 * r;
-                    a.s[off + v] = s;
-                    rho += (double)r * (double)s;
-                    rr += (double)r * (double)r;
-                }
-            }
-        }
-        if (!HIER) write_partials(a, f, j, k, rho, rr, shd);
-    }
-    if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, false, shd);
-}
-
-// Hierarchical M⁻¹ at level 0 (Eq. hier_precond): s = mask∘(μ0∘w + the projected coarser
-// levels); ρ = rᵀs = wᵀs (w = mask∘r), ‖r‖² (reading #6: r = 0 on dead vertices).
-__global__ void __launch_bounds__(256) k_precond_finish(VecArgs a, int first) {
-    __shared__ double shd[32];
-    __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
-    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const int stride = a.BPF * blockDim.x;
     for (int k = 0; k < a.K; ++k) {
         const int fk = f * a.K + k;
         double rho = 0.0, rr = 0.0;
         if (first || a.sc_.active[fk]) {
             const size_t off = (size_t)k * a.M;
-            for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
-                const float w = a.w0[off + v];
-                const float m0 = a.mu0[v];
-                float s = 0.f;
-                if (m0 > 0.f) {
-                    s = m0 * w;
-                    if (a.acc1) s += a.acc1[(size_t)k * a.M1 + a.parent0[v]];
+            const float* acc1 = a.acc1 + (size_t)k * a.M1;
+            for (int v0u = v0 + j * blockDim.x + threadIdx.x; v0u < v1; v0u += 4 * stride) {
+                float rv[4], mv[4], up[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0u + u * stride;
+                    if (v < v1) {
+                        rv[u] = a.r[off + v];
+                        mv[u] = a.mu0[v];
+                        up[u] = acc1[a.parent0[v]];
+                    }
                 }
-                a.s[off + v] = s;
-                const float r = a.r[off + v];
-                rho += (double)r * (double)s;
-                rr += (double)r * (double)r;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = v0u + u * stride;
+                    if (v >= v1) continue;
+                    const float sval = (mv[u] > 0.f) ? mv[u] * rv[u] + up[u] : 0.f;
+                    a.s[off + v] = sval;
+                    rho += (double)rv[u] * (double)sval;
+                    rr += (double)rv[u] * (double)rv[u];
+                }
             }
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
     if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, first != 0, shd);
-}
-
-// Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
-__global__ void __launch_bounds__(256) k_direction(VecArgs a, int first) {
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
-    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int k = 0; k < a.K; ++k) {
-        const int fk = f * a.K + k;
-        if (!first && !a.sc_.active[fk]) continue;
-        const float be = first ? 0.f : (float)a.sc_.beta[fk];
-        const size_t off = (size_t)k * a.M;
-        for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x)
-            a.d[off + v] = first ? a.s[off + v] : a.s[off + v] + be * a.d[off + v];
-    }
 }
 
 // ---------------------------------------------------------------- slice / export / backward
@@ -535,10 +568,10 @@ __global__ void k_bwd_finalize(const int* __restrict__ vid, const float* __restr
 }
 
 // B̄ v (reading #4), debug / parity operator.
-__global__ void k_blur(const uint2* __restrict__ nearv, const int2* __restrict__ yoff, const float* __restrict__ x,
+__global__ void k_blur(const int4* __restrict__ nbr, const float* __restrict__ x,
                        int64_t M, float* __restrict__ out) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x)
-        out[v] = (float)kBbarDiag * x[v] + nbr_sum(x, (int)v, nearv[v], yoff[v]);
+        out[v] = (float)kBbarDiag * x[v] + nbr_sum(x, (int)v, nbr[v]);
 }
 
 // A y for planar y, written canonical [M][K] (debug / parity operator).
@@ -546,7 +579,7 @@ __global__ void k_apply_A(VecArgs a, const float* __restrict__ ys, float* __rest
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.M; v += (int64_t)gridDim.x * blockDim.x)
         for (int k = 0; k < a.K; ++k)
             out[(size_t)v * a.K + k] =
-                apply_A_row(ys + (size_t)k * a.M, a.n, (int)v, a.nearv[v], a.yoff[v], a.lam, a.sc[v]);
+                apply_A_row(ys + (size_t)k * a.M, a.n, (int)v, a.nbr[v], a.lam, a.sc[v]);
 }
 
 // M⁻¹ r at level 0 for masked planar w, written canonical [M][K] (debug / parity operator).
