@@ -31,17 +31,26 @@ SIGMAS = (8.0, 4.0, 3.0)
 LAM = 128.0
 ITERS = 25
 
-# Algorithmic bytes per unit of each kernel: fp32 vectors, K = 1, neighbour
-# structure 16 B/vertex (8 int8 near offsets + 2 int32 y offsets).  Gathers of neighbour
-# values are cache-resident re-reads and are not counted.
-BYTES_PER_VERTEX = {
-    "k_spmv": 32,            # nbr 16 + d 4 + n 4 + Sc 4 + q write 4
-    "k_update<true>": 32,    # x rw 8 + r rw 8 + d 4 + q 4 + mu0 4 + w0 write 4
-    "k_update<false>": 32,   # x rw 8 + r rw 8 + d 4 + q 4 + mu0 4 + s write 4
-    "k_precond_finish": 24,  # w0 4 + mu0 4 + parent 4 + r 4 + s write 4 + acc1 gather (≈4)
-    "k_direction": 12,       # s 4 + d rw 8
-    "k_bistoch": 28,         # nbr 16 + m 4 + n 4 + n write 4
-}
+# Algorithmic bytes per launch of each kernel: fp32 vectors, K = 1, neighbour
+# structure 16 B/vertex (8 int8 near offsets + 2 int32 y offsets).  Gathers of neighbour values
+# are cache-resident re-reads and are not counted.  M = level-0 vertices, lv = level sizes.
+def kernel_bytes(name, M, lv, N):
+    up = sum(lv[1:])  # pyramid vertices above level 0
+    table = {
+        "k_spmv2": 32 * M,             # nbr 16 + (d,n) 8 + Sc 4 + q write 4
+        "k_update<true>": 36 * M,      # x rw 8 + r rw 8 + (d,n) 8 + q 4 + mu0 4 + w write 4
+        "k_update<false>": 36 * M,     # x rw 8 + r rw 8 + (d,n) 8 + q 4 + mu0 4 + s write 4
+        "k_direction2": 20 * M,        # s 4 + (d,n) read 8 + (d,n) write 8
+        "k_precond_finish2": 16 * M,   # r 4 + mu0 4 + parent 4 + s write 4 (acc1 gather cached)
+        "k_lift01": 8 * M + 8 * (lv[1] if len(lv) > 1 else 0),  # childList 4 + w 4 per child; start+out per parent
+        "k_hier<PCG>": 36 * up,        # per level ≥ 1: lift (start, list, value, out) + project (mu, buf rw, parent)
+        "k_bistoch": 28 * M,           # nbr 16 + m 4 + n 4 + n write 4
+        "k_grid_cells": 7 * N + 12 * M,  # rgb 3 + vid 4 per px; key 8 + m 4 per vertex
+        "k_grid_neighbours": 24 * M,   # keys 8 + nbr write 16
+        "k_splat<true>": 12 * N + 8 * M,  # vid 4 + c 4 + t 4 per px; Sc, b per vertex
+        "k_slice": 8 * N,              # vid 4 + x 4 per px
+    }
+    return table.get(name)
 
 
 def parse():
@@ -257,10 +266,12 @@ def main():
     kernels = {k: {"launches": n, "ms_per_step": tot / args.steps, "avg_us": 1e3 * tot / max(n, 1)}
                for k, (n, tot) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     roof = None
-    cand = [(k, v) for k, v in kernels.items() if k in BYTES_PER_VERTEX]
+    lv = [int(x) for x in info["level_vertices"]]
+    cand = [(k, v) for k, v in kernels.items() if kernel_bytes(k, M, lv, w.pixels) is not None]
     if cand:
+        # the dominant kernel = the largest share of the step among kernels with a byte model
         kname, kv = max(cand, key=lambda kv_: kv_[1]["ms_per_step"])
-        bytes_launch = BYTES_PER_VERTEX[kname] * M
+        bytes_launch = kernel_bytes(kname, M, lv, w.pixels)
         achieved = bytes_launch / (kv["avg_us"] * 1e-6) / 1e9
         peak, peak_src = 6545.6, "MEASURED_PEAKS.json hbm_gbs (measured copy)"
         try:
@@ -275,16 +286,21 @@ def main():
         except Exception:
             pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": kname, "bytes_per_launch": bytes_launch,
-                "bytes_per_vertex": BYTES_PER_VERTEX[kname], "vertices": M, "avg_launch_us": kv["avg_us"],
-                "share_of_step": kv["ms_per_step"] / (prof_ms / args.steps), "peak_source": peak_src}
+                "traffic": traffic, "kernel": kname, "bytes_per_launch": bytes_launch, "vertices": M,
+                "avg_launch_us": kv["avg_us"], "share_of_step": kv["ms_per_step"] / (prof_ms / args.steps),
+                "peak_source": peak_src}
+    for k, v in kernels.items():
+        b = kernel_bytes(k, M, lv, w.pixels)
+        if b is not None:
+            v["algorithmic_GBps"] = b / (v["avg_us"] * 1e-6) / 1e9
     stages = {
         "grid_build": ["k_axis_bins", "k_grid_cells", "k_frame_offsets", "k_grid_neighbours"],
         "bistochastize": ["k_bistoch", "k_bistoch_residual"],
         "pyramid": ["k_pyr_level", "k_lift_count"],
-        "splat_assemble": ["k_splat<true>", "k_assemble", "k_mu", "k_fill_init_w0", "k_init_finish"],
-        "pcg": ["k_spmv", "k_update<true>", "k_update<false>", "k_precond_finish", "k_direction", "k1", "k2",
-                "k_init_scalars", "k_lift", "k_project"],
+        "splat_assemble_init": ["k_splat<true>", "k_assemble", "k_fill_init_w0", "k_hier<PDA>", "k_hier<INIT>",
+                                "k_init_dn"],
+        "pcg": ["k_spmv2", "k_update<true>", "k_update<false>", "k_precond_finish2", "k_direction2", "k1", "k2",
+                "k_init_scalars", "k_lift01", "k_hier<PCG>"],
         "slice": ["k_slice"],
     }
     stages_ms = {s: sum(kernels[k]["ms_per_step"] for k in ks if k in kernels) for s, ks in stages.items()}

@@ -99,11 +99,6 @@ void device_setup(int* dev) {
         ck(cudaFuncSetAttribute(k_pyr_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kCoarseCap * (int)sizeof(unsigned long long)),
            "k_pyr_level smem");
-        const int big = 200 * 1024;
-        ck(cudaFuncSetAttribute(k_tile_up<UP_PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
-        ck(cudaFuncSetAttribute(k_tile_project<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
-        ck(cudaFuncSetAttribute(k_coarse_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
-        ck(cudaFuncSetAttribute(k_tile_project<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big), "smem attr");
         pool_done[*dev] = true;
     }
 }
@@ -146,11 +141,6 @@ int guard(const char* where, const std::function<void()>& body);
 
 using namespace fbs;
 
-namespace {
-HierArgs grid_hier(fbs_grid g);
-int n_tiles(const HierArgs& h);
-
-}  // namespace
 
 // ===================================================================================== grid
 static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy, double sl, double suv,
@@ -224,11 +214,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const int64_t M = g->M;
 
         g->nbr = dalloc<int4>(A, M, s);
-        // per-tile maxima (sizes the tile kernels' shared memory): [0..3] pyramid tile levels,
-        // [7] staged vertices of the fused direction + SpMV tiles
-        int* tmax = dalloc<int>(A, 8, s);
-        ck(cudaMemsetAsync(tmax, 0, 8 * sizeof(int), s), "memset");
-
         LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 8), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
                g->ncells, g->nbr, err);
 
@@ -290,24 +275,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             ncxK = L.ncx;
             ncyK = L.ncy;
         }
-        // per-level maximum vertex count of a level-T tile (T = min(3, Lmax−1)): sizes the tile
-        // kernels' shared memory (hier_kernels.cuh)
-        if (Lmax > 1) {
-            HierArgs hc{};
-            hc.T = std::min(kTileT, Lmax - 1);
-            hc.F = F;
-            for (int k = 0; k <= hc.T; ++k) {
-                hc.lv[k].cellOff = (k == 0) ? g->cellOff : g->lv[k].cellOff;
-                hc.lv[k].ncx = (k == 0) ? ncx : g->lv[k].ncx;
-                hc.lv[k].ncy = (k == 0) ? ncy : g->lv[k].ncy;
-            }
-            hc.ntx = hc.lv[hc.T].ncx;
-            hc.nty = hc.lv[hc.T].ncy;
-            const int nt = F * hc.ntx * hc.nty;
-            LAUNCH(k_tile_maxcounts, grid_for(nt), kThreads, 0, s, hc, nt, tmax);
-        }
-        int tmaxh[8] = {};
-        ck(cudaMemcpyAsync(tmaxh, tmax, sizeof(tmaxh), cudaMemcpyDeviceToHost, s), "d2h");
         // ---- sync 2: level sizes
         std::vector<std::vector<int>> lfo(Lmax);
         for (int k = 1; k < Lmax; ++k) {
@@ -346,7 +313,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
                    g->lv[k].childList, (int)g->lv[k].M, g->lv[k].count);
             countK = g->lv[k].count;
         }
-        for (int k = 0; k < 8; ++k) g->tileMax[k] = tmaxh[k];
 
         g->frameLevels = dalloc<int>(A, F, s);
         ck(cudaMemcpyAsync(g->frameLevels, g->frameLevelsH.data(), F * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
@@ -357,38 +323,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->lvFrameOffDev = dalloc<int>(A, lfoAll.size(), s);
         ck(cudaMemcpyAsync(g->lvFrameOffDev, lfoAll.data(), lfoAll.size() * sizeof(int), cudaMemcpyHostToDevice, s),
            "h2d");
-        // tile level: 4 (16×16 cells) when its shared memory fits, else 3 (maxima counted for
-        // the level-min(4, Lmax−1) tiles bound the smaller tiles too)
-        g->tileT = std::min(kTileT, L - 1);
-        if (g->tileT == 4) {
-            size_t need = 0;
-            for (int k = 0; k <= 4; ++k) need += (size_t)(g->tileMax[k] + 31) / 32 * 32 * 4;
-            need += (size_t)prog_capacity(g->tileMax, 4) * 2;
-            if (need > 96 * 1024) g->tileT = 3;
-        }
-        if (L > 1) {  // shared-memory need of k_coarse_smem: Σ_k (2c_k + c_k[k<top] + (c_k+1 + c_{k−1})[k>T]) words
-            const int T = g->tileT, top = L - 1;
-            int64_t worst = 0;
-            for (int f = 0; f < F; ++f) {
-                auto cntk = [&](int k) -> int64_t { return k == 0 ? fo[f + 1] - fo[f] : lfo[k][f + 1] - lfo[k][f]; };
-                int64_t w = 0;
-                for (int k = T; k <= top; ++k) {
-                    w += 2 * cntk(k);
-                    if (k < top) w += cntk(k);
-                    if (k > T) w += cntk(k) + 1 + cntk(k - 1);
-                }
-                worst = std::max(worst, w);
-            }
-            g->coarseSmem = (int)std::min<int64_t>(worst * 4 + 64, INT32_MAX);
-        }
-        if (L > 1) {
-            g->tileProgCap = prog_capacity(g->tileMax, g->tileT);
-            HierArgs hg = grid_hier(g);
-            const int nt = n_tiles(hg);
-            g->tileProg = dalloc<uint16_t>(A, (size_t)nt * g->tileProgCap, s);
-            hg.prog = g->tileProg;
-            LAUNCH(k_tile_program, nt, kThreads, 0, s, hg, g->tileProgCap, g->tileProg);
-        }
         ck(cudaStreamSynchronize(s), "sync");  // host vector lifetime for the H2D copy
     } catch (...) {
         free_all(g->allocs, s);
@@ -433,75 +367,32 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     return a;
 }
 
-// ---- hierarchical machinery (hier_kernels.cuh): tiles of level-T cells + per-frame coarse levels
-// pyramid geometry of a grid as seen by the tile kernels (system buffers left null)
-HierArgs grid_hier(fbs_grid g) {
+// ---- hierarchical machinery (hier_kernels.cuh)
+HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
+    fbs_grid g = S->g;
     HierArgs h{};
     h.L = g->L;
-    h.T = g->tileT;
     h.F = g->F;
-    h.C = 1;
+    h.C = C;
     for (int k = 0; k < g->L; ++k) {
         HLevel& v = h.lv[k];
-        if (k == 0) {
-            v.cellOff = g->cellOff;
-            v.ncx = g->ncx;
-            v.ncy = g->ncy;
-            v.M = g->M;
-        } else {
+        v.M = (k == 0) ? g->M : g->lv[k].M;
+        if (k > 0) {
             const Level& L = g->lv[k];
-            v.cellOff = L.cellOff;
-            v.ncx = L.ncx;
-            v.ncy = L.ncy;
             v.childStart = L.childStart;
             v.childList = L.childList;
             v.count = L.count;
             v.keys = L.keys;
-            v.M = L.M;
+            v.mu = S->mu[k];
+            v.buf = S->lvBuf[k];
         }
         v.parent = (k + 1 < g->L) ? g->lv[k + 1].parent : nullptr;
     }
-    h.ntx = h.lv[h.T].ncx;
-    h.nty = h.lv[h.T].ncy;
     h.frameLevels = g->frameLevels;
     h.lvFrameOff = g->lvFrameOffDev;
-    h.prog = g->tileProg;
-    h.progCap = g->tileProgCap;
-    int off = 0;
-    for (int k = 0; k <= h.T; ++k) {
-        h.soff[k] = off;
-        off += (g->tileMax[k] + 31) / 32 * 32;
-    }
-    h.soff[h.T + 1] = off;
-    return h;
-}
-
-HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
-    fbs_grid g = S->g;
-    HierArgs h = grid_hier(g);
-    h.C = C;
-    for (int k = 1; k < g->L; ++k) {
-        h.lv[k].mu = S->mu[k];
-        h.lv[k].buf = S->lvBuf[k];
-    }
     h.alpha = alpha;
     h.beta = beta;
     return h;
-}
-
-int n_tiles(const HierArgs& h) { return h.F * h.ntx * h.nty; }
-inline size_t tile_smem(const HierArgs& h, bool init) {
-    return (size_t)(h.soff[h.T + 1] + (init ? h.soff[1] : 0)) * sizeof(float);
-}
-inline size_t tile_up_smem(const HierArgs& h) { return tile_smem(h, false) + (size_t)h.progCap * 2 + 16; }
-
-// Levels T..top of every frame: shared-memory kernel when the largest frame's coarse pyramid
-// fits (grid->coarseSmem bytes), else the global-memory kernel.
-void launch_coarse(fbs_grid g, const HierArgs& h, int use_mu, int do_project, cudaStream_t s) {
-    if (g->coarseSmem > 0 && g->coarseSmem <= 200 * 1024)
-        LAUNCH(k_coarse_smem, h.F, 512, (size_t)g->coarseSmem, s, h, use_mu, do_project);
-    else
-        LAUNCH(k_coarse, h.F, 1024, 0, s, h, use_mu, do_project);
 }
 
 // The whole pyramid application in one cooperative kernel (hier_kernels.cuh k_hier).
@@ -697,7 +588,6 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         }
         if (hierP || hierI) {
             S->hP = make_hier(S, K, o.precond_alpha, o.precond_beta);
-            perFrameBlocks = std::max<int64_t>(perFrameBlocks, (int64_t)S->hP.ntx * S->hP.nty);
         }
         S->partial = dalloc<double>(A, (size_t)F * perFrameBlocks * 2 * K, s);
         S->counters = dalloc<unsigned>(A, F, s);

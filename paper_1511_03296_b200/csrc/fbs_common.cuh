@@ -163,36 +163,25 @@ struct PcgScalars {     // per (frame, channel), fk = f*K + k
 };
 
 // ------------------------------------------------------------------ hierarchy (hier_kernels.cuh)
-constexpr int kTileT = 4;        // largest tile level: one level-4 cell = 16 × 16 σxy-cells
-constexpr int kTileCap = 4096;   // vertices of one tile at any level (≤ its 64 × 64 pixels)
-constexpr int kTileRows = 1 << kTileT;
-
 struct HLevel {
-    const int* cellOff = nullptr;     // [ncells + 1]
-    int ncx = 0, ncy = 0;
     const int* parent = nullptr;      // level k → k+1 (nullptr at the top level)
     const int* childStart = nullptr;  // k ≥ 1: children (level k−1) of level-k vertices
     const int* childList = nullptr;
     const int* count = nullptr;       // k ≥ 1: P(1)
     const uint64_t* keys = nullptr;   // k ≥ 1
     const float* mu = nullptr;        // k ≥ 1: preconditioner multiplier
-    float* buf = nullptr;             // k ≥ 1: lifted values [C][M]
+    float* buf = nullptr;             // k ≥ 1: lifted / projected values [C][M]
     int64_t M = 0;
 };
 
 struct HierArgs {
     HLevel lv[kMaxLevels];
-    int soff[kTileT + 2];   // shared-memory offsets (floats) of the tile's level arrays; soff[T+1] = total
-    int T;              // tile level (≤ L−1)
-    int L;              // levels incl. base (max over frames)
+    int L;                  // levels incl. base (max over frames)
     int F;
-    int C;              // channels carried through the pyramid
-    int ntx, nty;       // tiles per frame along x / y (= level-T cells)
+    int C;                  // channels carried through the pyramid
     const int* frameLevels;
     const int* lvFrameOff;  // [L][F+1] per-level frame vertex offsets
     double alpha, beta;     // z_weight parameters of the current use
-    const uint16_t* prog;   // tile programs (hier_kernels.cuh), progCap u16 per tile
-    int progCap;
 };
 
 }  // namespace fbs
@@ -224,11 +213,6 @@ struct fbs_grid_s {
     fbs::Level lv[fbs::kMaxLevels];
     int64_t maxFrameM = 0;
     int* lvFrameOffDev = nullptr;  // [L][F + 1]
-    int tileMax[8] = {};           // largest level-k vertex count of a level-3 tile (k ≤ 3)
-    int tileT = 0;                 // tile level T = min(3, L − 1)
-    int coarseSmem = 0;            // bytes of k_coarse_smem for the largest frame
-    uint16_t* tileProg = nullptr;  // per-tile programs
-    int tileProgCap = 0;
     std::vector<void*> allocs;
 };
 

@@ -232,36 +232,6 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
 }
 
 // ---------------------------------------------------------------- pyramid lift / project
-// μ_k = z_w(k) · P(1)_k / P(diag A)_k  (Eq. hier_precond); 0 where the
-// denominator is 0 (reading #10) or where the frame has fewer than k+1 levels.
-__global__ void k_mu(const float* __restrict__ PdA, const int* __restrict__ count,
-                     const uint64_t* __restrict__ keys, const int* __restrict__ frameLevels, int64_t Mk,
-                     int level, double alpha, double beta, float* __restrict__ mu) {
-    const double zw = pow(alpha, -(beta + (double)level));
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < Mk;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        const int f = (int)(keys[p] >> 56);
-        const float den = PdA[p];
-        mu[p] = (level < frameLevels[f] && den > 0.f) ? (float)(zw * (double)count[p] / (double)den) : 0.f;
-    }
-}
-
-// hier init at level 0:  y_hier = Pᵀ(z∘P(b)/P(1)) / Pᵀ(z∘P(Sc)/P(1)), 0 where den = 0.
-// w0 holds [b_0..b_{K-1}, Sc]; the level-0 multiplier is z_w(0)/P(1)_0 = 1.
-__global__ void k_init_finish(const float* __restrict__ w0, int64_t M, int K, const int* __restrict__ parent0,
-                              const float* __restrict__ acc1, int64_t M1, float* __restrict__ x) {
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
-        const int pa = acc1 ? parent0[v] : 0;
-        float den = w0[(size_t)K * M + v];
-        if (acc1) den += acc1[(size_t)K * M1 + pa];
-        for (int k = 0; k < K; ++k) {
-            float num = w0[(size_t)k * M + v];
-            if (acc1) num += acc1[(size_t)k * M1 + pa];
-            x[(size_t)k * M + v] = (den > 0.f) ? num / den : 0.f;
-        }
-    }
-}
-
 __global__ void k_fill_init_w0(const float* __restrict__ b, const float* __restrict__ sc, int64_t M, int K,
                                float* __restrict__ w0) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
@@ -468,7 +438,7 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
 }
 
 // Hierarchical M⁻¹ at level 0 (Eq. hier_precond): s = mask∘(μ0 r + acc1[parent0]) with acc1 the
-// projected level-1 values (k_tile_project); ρ = rᵀs, ‖r‖² and the per-frame finish (Alg. 2
+// projected level-1 values (k_hier); ρ = rᵀs, ‖r‖² and the per-frame finish (Alg. 2
 // lines 11-13; first: lines 3-4).
 __global__ void __launch_bounds__(256) k_precond_finish2(VecArgs a, int first) {
     __shared__ double shd[32];
