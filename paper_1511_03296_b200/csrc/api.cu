@@ -214,7 +214,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const int64_t M = g->M;
 
         g->nbr = dalloc<int4>(A, M, s);
-        LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 8), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
+        LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
                g->ncells, g->nbr, err);
 
         // ---- Alg. 1 (reading #5: fixed n_bistoch iterations)
@@ -597,7 +597,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int nb = F * S->BPF;
         CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
         // a4: splat Sc, b = S(c∘t)
-        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 8), 256, 0, s, geo, g->cellOff, g->vid, c, t, K, M, S->sc,
+        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, c, t, K, M, S->sc,
                S->b);
         // a5: assemble (+ flat/zero init)
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
@@ -647,7 +647,7 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
     }
     CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
     // u = S g (∂f/∂b = A⁻¹(S ∂f/∂x̂)), solved from x0 = 0 (reading #14)
-    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 8), 256, 0, s, geo, g->cellOff, g->vid, nullptr, g_dldx, K,
+    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, nullptr, g_dldx, K,
            M, nullptr, S->u);
     VecArgs a = make_args(S, S->bwd, S->xb, S->u);
     const int nb = g->F * S->BPF;
@@ -861,7 +861,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
         const size_t KM = (size_t)K * g->M;
         float* planar = dalloc<float>(tmp, KM, s);
         CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
-        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 8), 256, 0, s, geo, g->cellOff, g->vid, nullptr, p, K,
+        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, nullptr, p, K,
                g->M, nullptr, planar);
         LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, K, out);
         free_all(tmp, s);

@@ -111,6 +111,46 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* state
     return excl;
 }
 
+
+// Warp-parallel look-back (all 32 lanes of one warp call it): each round inspects the 32 closest
+// predecessors at once, so the serial chain is ~window/32 loads instead of ~window.
+__device__ __forceinline__ unsigned long long lookback_warp(unsigned long long* state, unsigned t,
+                                                            unsigned long long agg) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(state[t]);
+        me.store((t == 0 ? kLbPre : kLbAgg) | agg, cuda::memory_order_relaxed);
+    }
+    if (t == 0) return 0ull;
+    unsigned long long excl = 0ull;
+    long long base = (long long)t - 1;
+    while (true) {
+        const long long j = base - lane;
+        unsigned long long s = kLbPre;  // before tile 0: an inclusive prefix of 0
+        if (j >= 0) {
+            cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> a(state[j]);
+            s = a.load(cuda::memory_order_relaxed);
+            while ((s & ~kLbVal) == 0ull) {
+                __nanosleep(20);
+                s = a.load(cuda::memory_order_relaxed);
+            }
+        }
+        const unsigned pre = __ballot_sync(0xffffffffu, (s & ~kLbVal) == kLbPre);
+        const int stop = pre ? (__ffs(pre) - 1) : 31;  // closest predecessor with an inclusive prefix
+        unsigned long long v = (lane <= stop) ? (s & kLbVal) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (pre) break;
+        base -= 32;
+    }
+    if (lane == 0) {
+        cuda::atomic_ref<unsigned long long, cuda::thread_scope_device> me(state[t]);
+        me.store(kLbPre | (excl + agg), cuda::memory_order_relaxed);
+    }
+    return excl;
+}
+
 // ------------------------------------------------------------------ neighbour encoding
 // near: 8 signed bytes = relative offsets of the (x−, x+, l−, l+, u−, u+, v−, v+) neighbours
 // (0 = absent; |offset| ≤ 127 because a σxy cell holds ≤ 64 vertices and x-neighbours sit in

@@ -133,10 +133,11 @@ __global__ void __launch_bounds__(256) k_grid_cells(
 
     if (lane == 0) s_cnt[warp] = (c < ncells) ? U : 0u;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         unsigned agg = 0;
         for (int i = 0; i < kCellsPerBlock; ++i) agg += s_cnt[i];
-        s_excl = lb_first(lookback(tile_state, tile, lb_pack(agg, 0u)));
+        const unsigned long long ex = lookback_warp(tile_state, tile, lb_pack(agg, 0u));
+        if (lane == 0) s_excl = lb_first(ex);
     }
     __syncthreads();
     if (c >= ncells) return;

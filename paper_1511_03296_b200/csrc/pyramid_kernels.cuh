@@ -83,7 +83,10 @@ __global__ void __launch_bounds__(64) k_pyr_level(
         }
     }
     const int nch = n0 + n1;
-    if (threadIdx.x == 0) s_cexcl = lb_first(lookback(stateC, (unsigned)C, lb_pack((unsigned)nch, 0u)));
+    if (threadIdx.x < 32) {
+        const unsigned long long ex = lookback_warp(stateC, (unsigned)C, lb_pack((unsigned)nch, 0u));
+        if (threadIdx.x == 0) s_cexcl = lb_first(ex);
+    }
     __syncthreads();
     const int cOff = (int)s_cexcl;
     int P = 1;
@@ -122,7 +125,10 @@ __global__ void __launch_bounds__(64) k_pyr_level(
     }
     int U;
     const int before = block_excl_scan(myHeads, s_scan, &U);
-    if (threadIdx.x == 0) s_vexcl = lb_first(lookback(stateV, (unsigned)C, lb_pack((unsigned)U, 0u)));
+    if (threadIdx.x < 32) {
+        const unsigned long long ex = lookback_warp(stateV, (unsigned)C, lb_pack((unsigned)U, 0u));
+        if (threadIdx.x == 0) s_vexcl = lb_first(ex);
+    }
     __syncthreads();
     const int vOff = (int)s_vexcl;
     const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)CY << 40) | ((uint64_t)CX << 24);
