@@ -194,8 +194,13 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->cellOff = dalloc<int>(A, g->ncells + 1, s);
         g->frameOff = dalloc<int>(A, F + 1, s);
         CellGeom geo{F, H, W, ncx, ncy, g->colStart, g->rowStart};
-        LAUNCH(k_grid_cells, (unsigned)ntiles, 256, 0, s, rgb, geo, 256.0 * sl, 256.0 * suv, g->ncells, counter,
-               state, keysCap, mCap, g->vid, g->cellOff, err);
+        uint8_t* lutL = dalloc<uint8_t>(A, 65536, s);
+        uint8_t* lutUV = dalloc<uint8_t>(A, 65536, s);
+        LAUNCH(k_bin_lut, 256, 256, 0, s, 256.0 * sl, lutL);
+        LAUNCH(k_bin_lut, 256, 256, 0, s, 256.0 * suv, lutUV);
+        g->perm = dalloc<uint8_t>(A, (size_t)g->ncells * kCellMaxPx, s);
+        LAUNCH(k_grid_cells, (unsigned)ntiles, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, counter, state, keysCap,
+               mCap, g->vid, g->cellOff, g->perm, err);
         LAUNCH(k_frame_offsets, 1, 288, 0, s, g->cellOff, F, (int64_t)ncx * ncy, g->frameOff);
 
         // ---- sync 1: vertex counts (sizes the vertex arrays and the pyramid capacities)
@@ -260,12 +265,12 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             L.childStart = dalloc<int>(A, M + 1, s);
             L.childList = dalloc<int>(A, M, s);
             L.count = dalloc<int>(A, M, s);
-            unsigned long long* st2 = dalloc<unsigned long long>(A, 2 * L.ncells, s);
-            unsigned* ctr2 = dalloc<unsigned>(A, 1, s);
-            ck(cudaMemsetAsync(st2, 0, 2 * L.ncells * sizeof(unsigned long long), s), "memset");
-            ck(cudaMemsetAsync(ctr2, 0, sizeof(unsigned), s), "memset");
+            unsigned long long* st2 = dalloc<unsigned long long>(A, L.ncells, s);
+            unsigned* ctr2 = dalloc<unsigned>(A, 2, s);  // tile counter, scratch bump
+            ck(cudaMemsetAsync(st2, 0, L.ncells * sizeof(unsigned long long), s), "memset");
+            ck(cudaMemsetAsync(ctr2, 0, 2 * sizeof(unsigned), s), "memset");
             LAUNCH(k_pyr_level, (unsigned)L.ncells, 64, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK,
-                   ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, st2 + L.ncells, pyrScratch, L.keys, L.parent,
+                   ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, ctr2 + 1, pyrScratch, L.keys, L.parent,
                    L.childStart, L.childList, L.cellOff);
             // P(1): upper bound M on the level size; the kernel stops at the true size via childStart
             lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
@@ -597,7 +602,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int nb = F * S->BPF;
         CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
         // a4: splat Sc, b = S(c∘t)
-        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, c, t, K, M, S->sc,
+        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t, K, M, S->sc,
                S->b);
         // a5: assemble (+ flat/zero init)
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
@@ -647,7 +652,7 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
     }
     CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
     // u = S g (∂f/∂b = A⁻¹(S ∂f/∂x̂)), solved from x0 = 0 (reading #14)
-    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, nullptr, g_dldx, K,
+    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, g_dldx, K,
            M, nullptr, S->u);
     VecArgs a = make_args(S, S->bwd, S->xb, S->u);
     const int nb = g->F * S->BPF;
@@ -861,7 +866,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
         const size_t KM = (size_t)K * g->M;
         float* planar = dalloc<float>(tmp, KM, s);
         CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
-        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, nullptr, p, K,
+        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, p, K,
                g->M, nullptr, planar);
         LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, K, out);
         free_all(tmp, s);

@@ -242,6 +242,7 @@ struct fbs_grid_s {
     uint64_t* keys = nullptr;  // [N] capacity (first M valid)
     int* m = nullptr;          // [N] capacity
     int* cellOff = nullptr;    // [ncells + 1]
+    uint8_t* perm = nullptr;   // [ncells][64] sorted position → local pixel (splat order)
     int4* nbr = nullptr;       // [M] packed neighbour offsets (fbs_common.cuh near_off)
     float* n = nullptr;        // [M]
     int* frameOff = nullptr;   // device [F + 1]

@@ -53,15 +53,22 @@ __device__ __forceinline__ void warp_bitonic64(uint32_t& a0, uint32_t& a1, int l
     }
 }
 
-// (bl, bu, bv) code of one pixel: reading #1 integer YUV numerators, reading #2 fp64 floor.
-__device__ __forceinline__ uint32_t luv_code(const uint8_t* __restrict__ px, double dl, double duv) {
+// Bin tables: lut[i] = ⌊i / d⌋ for every integer numerator i ∈ [0, 65536), one IEEE fp64 division
+// each (reading #2), d = 256σ.  Yn, Un, Vn are integers < 65536, so a table lookup reproduces the
+// fp64 division exactly while keeping the per-pixel path free of fp64 divides.
+__global__ void k_bin_lut(double d, uint8_t* __restrict__ lut) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < 65536) lut[i] = (uint8_t)min(255.0, floor((double)i / d));
+}
+
+// (bl, bu, bv) code of one pixel: reading #1 integer YUV numerators, reading #2 bins (tables).
+__device__ __forceinline__ uint32_t luv_code(const uint8_t* __restrict__ px, const uint8_t* __restrict__ lutL,
+                                            const uint8_t* __restrict__ lutUV) {
     const int R = px[0], G = px[1], B = px[2];
     const int Yn = 77 * R + 150 * G + 29 * B;
     const int Un = -43 * R - 85 * G + 128 * B + 32768;
     const int Vn = 128 * R - 107 * G - 21 * B + 32768;
-    const uint32_t bl = (uint32_t)floor((double)Yn / dl);
-    const uint32_t bu = (uint32_t)floor((double)Un / duv);
-    const uint32_t bv = (uint32_t)floor((double)Vn / duv);
+    const uint32_t bl = __ldg(lutL + Yn), bu = __ldg(lutUV + Un), bv = __ldg(lutUV + Vn);
     return (bl << 16) | (bu << 8) | bv;
 }
 
@@ -77,10 +84,10 @@ __device__ __forceinline__ void cell_of(const CellGeom& g, int64_t c, int& f, in
 // One warp per σxy cell (≤ 64 px), 8 cells per block = one look-back tile.
 // Outputs: keys[v], m[v] (= S1), vid[p], cellOff[c] (first vertex of each cell).
 __global__ void __launch_bounds__(256) k_grid_cells(
-    const uint8_t* __restrict__ rgb, CellGeom g, double dl, double duv, int64_t ncells,
-    unsigned* __restrict__ tile_counter, unsigned long long* __restrict__ tile_state,
-    uint64_t* __restrict__ keys, int* __restrict__ mcount, int* __restrict__ vid,
-    int* __restrict__ cellOff, int* __restrict__ err) {
+    const uint8_t* __restrict__ rgb, CellGeom g, const uint8_t* __restrict__ lutL,
+    const uint8_t* __restrict__ lutUV, int64_t ncells, unsigned* __restrict__ tile_counter,
+    unsigned long long* __restrict__ tile_state, uint64_t* __restrict__ keys, int* __restrict__ mcount,
+    int* __restrict__ vid, int* __restrict__ cellOff, uint8_t* __restrict__ perm, int* __restrict__ err) {
     __shared__ unsigned s_tile;
     __shared__ unsigned s_cnt[kCellsPerBlock];
     __shared__ unsigned s_excl;
@@ -106,12 +113,12 @@ __global__ void __launch_bounds__(256) k_grid_cells(
         const uint8_t* base = rgb + (size_t)f * g.H * g.W * 3;
         if (lane < npx) {
             const int px = x0 + lane % w, py = y0 + lane / w;
-            a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, dl, duv) << 6) | (uint32_t)lane;
+            a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)lane;
         }
         if (lane + 32 < npx) {
             const int i = lane + 32;
             const int px = x0 + i % w, py = y0 + i / w;
-            a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, dl, duv) << 6) | (uint32_t)i;
+            a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)i;
         }
     }
     warp_bitonic64(a0, a1, lane);
@@ -165,6 +172,7 @@ __global__ void __launch_bounds__(256) k_grid_cells(
         const int i = (int)(a & 63u);
         const int px = x0 + i % w, py = y0 + i / w;
         vbase[(size_t)py * g.W + px] = (int)v;
+        perm[(size_t)c * kCellMaxPx + e] = (uint8_t)i;  // sorted position e → local pixel i (splat order)
     }
     if (lane == 0) {
         cellOff[c] = (int)off;
@@ -173,18 +181,13 @@ __global__ void __launch_bounds__(256) k_grid_cells(
 }
 
 // ---------------------------------------------------------------- neighbours (B̄ structure)
+// lower bound in a sorted shared-memory segment of n ≤ 64 codes: 6 fixed, branch-free steps
 __device__ __forceinline__ int lower_bound_s(const uint32_t* a, int n, uint32_t q) {
-    int lo = 0;
-    while (n > 0) {
-        const int half = n >> 1;
-        if (a[lo + half] < q) {
-            lo += half + 1;
-            n -= half + 1;
-        } else {
-            n = half;
-        }
-    }
-    return lo;
+    int pos = 0;
+#pragma unroll
+    for (int step = 32; step > 0; step >>= 1)
+        if (pos + step <= n && a[pos + step - 1] < q) pos += step;
+    return pos;
 }
 
 // One warp per cell: stage the 24-bit codes of the cell and of its x∓ / y∓ neighbour cells in
@@ -252,7 +255,9 @@ __global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
                                                  float* __restrict__ nout, int M, int first) {
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
+    const int stride = gridDim.x * blockDim.x;
+#pragma unroll 2
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += stride) {
         const int4 nb = nbr[v];
         float nv, bn;
         if (first) {

@@ -46,21 +46,21 @@ __device__ __forceinline__ int block_excl_scan(int x, int* sh /*[33]*/, int* tot
     return sh[w] + incl - x;
 }
 
-// One block (T threads) per level-(k+1) coarse cell.  Two look-back chains: the children
-// prefix is published first (it is known before sorting), which also places the cell's slice of
-// a global scratch array; cells with more than kCoarseCap children sort there instead of in
-// shared memory (rare: dense pixel-noise images at σl = σuv = 1).
+// One block (T threads) per level-(k+1) coarse cell.  One look-back chain carries the packed
+// (vertex, child) counts.  Cells with more than kCoarseCap children sort in a global scratch
+// slice (rare: dense pixel-noise images at σl = σuv = 1).
 __global__ void __launch_bounds__(64) k_pyr_level(
     const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK, int ncxK, int ncyK,
     int ncxN, int ncyN, int64_t ncellsN, unsigned* __restrict__ tile_counter,
-    unsigned long long* __restrict__ stateC, unsigned long long* __restrict__ stateV,
+    unsigned long long* __restrict__ stateV, unsigned* __restrict__ bump,
     unsigned long long* __restrict__ scratch, uint64_t* __restrict__ keysN,
     int* __restrict__ parentK, int* __restrict__ childStartN, int* __restrict__ childListN,
     int* __restrict__ cellOffN) {
     extern __shared__ unsigned long long sk_smem[];  // [kCoarseCap]
     __shared__ unsigned s_tile;
     __shared__ int s_scan[33];
-    __shared__ unsigned s_cexcl, s_vexcl;
+    __shared__ unsigned s_scr;
+    __shared__ unsigned long long s_vexcl;
     if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
     const int64_t C = s_tile;
@@ -83,15 +83,13 @@ __global__ void __launch_bounds__(64) k_pyr_level(
         }
     }
     const int nch = n0 + n1;
-    if (threadIdx.x < 32) {
-        const unsigned long long ex = lookback_warp(stateC, (unsigned)C, lb_pack((unsigned)nch, 0u));
-        if (threadIdx.x == 0) s_cexcl = lb_first(ex);
-    }
-    __syncthreads();
-    const int cOff = (int)s_cexcl;
     int P = 1;
     while (P < nch) P <<= 1;
-    unsigned long long* sk = (nch <= kCoarseCap) ? sk_smem : scratch + 2 * (size_t)cOff;
+    // oversize cells sort in a global scratch slice taken from a bump allocator (its position
+    // does not affect the result); Σ P < 2·M bounds the scratch
+    if (threadIdx.x == 0) s_scr = (nch > kCoarseCap) ? atomicAdd(bump, (unsigned)P) : 0u;
+    __syncthreads();
+    unsigned long long* sk = (nch <= kCoarseCap) ? sk_smem : scratch + s_scr;
     for (int i = threadIdx.x; i < P; i += T) {
         unsigned long long key = ~0ull;
         if (i < nch) {
@@ -126,11 +124,11 @@ __global__ void __launch_bounds__(64) k_pyr_level(
     int U;
     const int before = block_excl_scan(myHeads, s_scan, &U);
     if (threadIdx.x < 32) {
-        const unsigned long long ex = lookback_warp(stateV, (unsigned)C, lb_pack((unsigned)U, 0u));
-        if (threadIdx.x == 0) s_vexcl = lb_first(ex);
+        const unsigned long long ex = lookback_warp(stateV, (unsigned)C, lb_pack((unsigned)U, (unsigned)nch));
+        if (threadIdx.x == 0) s_vexcl = ex;
     }
     __syncthreads();
-    const int vOff = (int)s_vexcl;
+    const int vOff = (int)lb_first(s_vexcl), cOff = (int)lb_second(s_vexcl);
     const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)CY << 40) | ((uint64_t)CX << 24);
     int r = before - 1;
     for (int e = 0; e < E; ++e) {

@@ -66,15 +66,15 @@ __device__ __forceinline__ float apply_A_row(const float* __restrict__ y, const 
 __device__ __forceinline__ float nbr_nsum(const float* __restrict__ n, int v, int4 nb) { return nbr_sum(n, v, nb); }
 
 // ---------------------------------------------------------------- splat  S p
-// One warp per σxy cell.  Pixels of a vertex all lie in its cell; the per-vertex sum is formed
-// deterministically: lanes holding the same vertex are grouped with match_any, each group summed
-// in lane order (fp64), and the two half-cells added in fixed order.  WEIGHTED: Sc = S c and
-// b_k = S(c∘t_k) (Eq. quad_min); otherwise out_k = S p_k.
+// One warp per σxy cell.  The grid build stored each cell's pixels in sorted (code, pixel) order
+// (perm), so the pixels of one vertex are consecutive: each vertex sum is a warp segmented scan
+// in fp64 over the two 32-pixel halves, the halves added in fixed order — deterministic.
+// WEIGHTED: Sc = S c and b_k = S(c∘t_k) (Eq. quad_min); otherwise out_k = S p_k.
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict__ cellOff,
-                                               const int* __restrict__ vid, const float* __restrict__ c,
-                                               const float* __restrict__ p, int K, int64_t M,
-                                               float* __restrict__ sc_out, float* __restrict__ out) {
+                                               const int* __restrict__ vid, const uint8_t* __restrict__ perm,
+                                               const float* __restrict__ c, const float* __restrict__ p, int K,
+                                               int64_t M, float* __restrict__ sc_out, float* __restrict__ out) {
     __shared__ double acc[kCellsPerBlock][kCellMaxPx];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ncells = (int64_t)g.F * g.ncx * g.ncy;
@@ -90,41 +90,53 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
         size_t pix[2];
         int rk[2];
         float cw[2];
+        bool tail[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            const int i = lane + 32 * j;
+            const int e = lane + 32 * j;
             rk[j] = -1;
             pix[j] = 0;
             cw[j] = 0.f;
-            if (i < npx) {
+            if (e < npx) {
+                const int i = perm[(size_t)cell * kCellMaxPx + e];
                 pix[j] = (size_t)(y0 + i / w) * g.W + (x0 + i % w);
                 rk[j] = vid[(size_t)f * HW + pix[j]] - vbeg;
                 cw[j] = WEIGHTED ? c[(size_t)f * HW + pix[j]] : 1.f;
             }
         }
-        const unsigned pe0 = __match_any_sync(0xffffffffu, rk[0]);
-        const unsigned pe1 = __match_any_sync(0xffffffffu, rk[1]);
+        // segment bounds inside each half: lane l's segment starts at the last head ≤ l
+        int sstart[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int prev = __shfl_up_sync(0xffffffffu, rk[j], 1);
+            const bool head = (lane == 0) || (rk[j] != prev);
+            const unsigned hm = __ballot_sync(0xffffffffu, head) & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
+            sstart[j] = 31 - __clz(hm);
+            const int nxt = __shfl_down_sync(0xffffffffu, rk[j], 1);
+            tail[j] = (lane == 31) || (rk[j] != nxt);
+        }
         const int nch = WEIGHTED ? K + 1 : K;
         for (int ch = 0; ch < nch; ++ch) {
-            // channel WEIGHTED&&ch==0: Sc; else b_k (k = ch - WEIGHTED)
-            const int k = WEIGHTED ? ch - 1 : ch;
+            const int k = WEIGHTED ? ch - 1 : ch;  // channel WEIGHTED&&ch==0: Sc; else b_k
             for (int i = lane; i < U; i += 32) acc[warp][i] = 0.0;
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
-                double val = 0.0;
+                double v = 0.0;
                 if (rk[j] >= 0) {
                     if (WEIGHTED && ch == 0) {
-                        val = (double)cw[j];
+                        v = (double)cw[j];
                     } else {
                         const float pv = p[((size_t)f * K + k) * HW + pix[j]];
-                        val = WEIGHTED ? (double)cw[j] * (double)pv : (double)pv;
+                        v = WEIGHTED ? (double)cw[j] * (double)pv : (double)pv;
                     }
                 }
-                const unsigned pe = j ? pe1 : pe0;
-                double sum = 0.0;
-                for (unsigned mm = pe; mm; mm &= mm - 1u) sum += __shfl_sync(pe, val, __ffs(mm) - 1);
-                if (rk[j] >= 0 && lane == __ffs(pe) - 1) acc[warp][rk[j]] += sum;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {  // segmented inclusive scan (fixed tree)
+                    const double t = __shfl_up_sync(0xffffffffu, v, d);
+                    if (lane - d >= sstart[j]) v += t;
+                }
+                if (tail[j] && rk[j] >= 0) acc[warp][rk[j]] += v;  // half 0 then half 1: fixed order
                 __syncwarp();
             }
             for (int i = lane; i < U; i += 32) {
