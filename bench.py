@@ -36,14 +36,17 @@ ITERS = 25
 # are cache-resident re-reads and are not counted.  M = level-0 vertices, lv = level sizes.
 def kernel_bytes(name, M, lv, N):
     up = sum(lv[1:])  # pyramid vertices above level 0
+    lv1 = lv[1] if len(lv) > 1 else 0
     table = {
         "k_spmv2": 32 * M,             # nbr 16 + (d,n) 8 + Sc 4 + q write 4
-        "k_update<true>": 36 * M,      # x rw 8 + r rw 8 + (d,n) 8 + q 4 + mu0 4 + w write 4
-        "k_update<false>": 36 * M,     # x rw 8 + r rw 8 + (d,n) 8 + q 4 + mu0 4 + s write 4
+        # x rw 8 + (d,n) 8 + r rw 8 + q 4 + mu0 4 + w write 4
+        "k_hier_level0<UPDATE>": 36 * M,
+        # tord0 4 + w gather 4 per level-0 vertex; csT 4 + mu1 4 + (P w)_1 write 4 + prefix write 8 per level-1 vertex
+        "k_tree_lift<PCG>": 8 * M + 20 * lv1,
+        # parent0T 4 + r 4 + mu0 4 + (d,n) rw 16 (level-1 and level-2 gathers cache-resident)
+        "k_tree_level0<PCG>": 28 * M,
+        "k_update": 36 * M,            # x rw 8 + r rw 8 + (d,n) 8 + q 4 + mu0 4 + s write 4
         "k_direction2": 20 * M,        # s 4 + (d,n) read 8 + (d,n) write 8
-        "k_precond_finish2": 16 * M,   # r 4 + mu0 4 + parent 4 + s write 4 (acc1 gather cached)
-        "k_lift01": 8 * M + 8 * (lv[1] if len(lv) > 1 else 0),  # childList 4 + w 4 per child; start+out per parent
-        "k_hier<PCG>": 36 * up,        # per level ≥ 1: lift (start, list, value, out) + project (mu, buf rw, parent)
         "k_bistoch": 28 * M,           # nbr 16 + m 4 + n 4 + n write 4
         "k_grid_cells": 7 * N + 12 * M,  # rgb 3 + vid 4 per px; key 8 + m 4 per vertex
         "k_grid_neighbours": 24 * M,   # keys 8 + nbr write 16
@@ -296,11 +299,12 @@ def main():
     stages = {
         "grid_build": ["k_axis_bins", "k_grid_cells", "k_frame_offsets", "k_grid_neighbours"],
         "bistochastize": ["k_bistoch", "k_bistoch_residual"],
-        "pyramid": ["k_pyr_level", "k_lift_count"],
-        "splat_assemble_init": ["k_splat<true>", "k_assemble", "k_fill_init_w0", "k_hier<PDA>", "k_hier<INIT>",
-                                "k_init_dn"],
-        "pcg": ["k_spmv2", "k_update<true>", "k_update<false>", "k_precond_finish2", "k_direction2", "k1", "k2",
-                "k_init_scalars", "k_lift01", "k_hier<PCG>"],
+        "pyramid": ["k_pyr_level", "k_lift_count", "k_tree_top", "k_tree_down", "k_tree_finish"],
+        "splat_assemble_init": ["k_splat<true>", "k_assemble", "k_fill_init_w0", "k_tree_lift<PDA>", "k_tree_coarse<PDA>",
+                                "k_tree_lift<INIT>", "k_tree_coarse<INIT>", "k_tree_level0<INIT>", "k_init_dn"],
+        "pcg": ["k_spmv2", "k_update", "k_direction2", "k1", "k2", "k_init_scalars", "k_hier_level0<UPDATE>",
+                "k_hier_level0<UPDATE,LAST>", "k_hier_level0<RESID>", "k_hier_level0<RESID0>", "k_tree_lift<PCG>",
+                "k_tree_coarse<PCG>", "k_tree_level0<PCG>"],
         "slice": ["k_slice"],
     }
     stages_ms = {s: sum(kernels[k]["ms_per_step"] for k in ks if k in kernels) for s, ks in stages.items()}

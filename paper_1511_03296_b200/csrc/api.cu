@@ -14,7 +14,7 @@
 #include "grid_kernels.cuh"
 #include "pyramid_kernels.cuh"
 #include "solve_kernels.cuh"
-#include "hier_kernels.cuh"
+#include "tree_kernels.cuh"
 
 namespace fbs {
 
@@ -75,9 +75,10 @@ struct ProfScope {
     }
 };
 
-#define LAUNCH(kernel, grid, block, smem, stream, ...)                                   \
+#define LAUNCH(kernel, grid, block, smem, stream, ...) LAUNCH_AS(#kernel, kernel, grid, block, smem, stream, __VA_ARGS__)
+#define LAUNCH_AS(name, kernel, grid, block, smem, stream, ...)                          \
     do {                                                                                 \
-        ::fbs::ProfScope _ps(#kernel, (stream));                                         \
+        ::fbs::ProfScope _ps((name), (stream));                                          \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                       \
         ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
         ck(cudaGetLastError(), #kernel);                                                 \
@@ -328,6 +329,55 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->lvFrameOffDev = dalloc<int>(A, lfoAll.size(), s);
         ck(cudaMemcpyAsync(g->lvFrameOffDev, lfoAll.data(), lfoAll.size() * sizeof(int), cudaMemcpyHostToDevice, s),
            "h2d");
+        // ---- tree order of the pyramid (tree_kernels.cuh): depth-first positions of the level-0 and
+        // level-1 vertices, so every coarse subtree is one contiguous level-1 range
+        std::vector<int> tfo, tframe;
+        if (L > 1) {
+            TreeOrder& T = g->tree;
+            const int64_t M1 = g->lv[1].M;
+            const int top = L - 1;
+            std::vector<int*> cnt1(L, nullptr);  // level-1 descendants of levels ≥ 2
+            for (int k = 2; k < L; ++k) {
+                cnt1[k] = dalloc<int>(A, g->lv[k].M, s);
+                LAUNCH(k_lift_count, grid_for(g->lv[k].M), kThreads, 0, s, k == 2 ? nullptr : cnt1[k - 1],
+                       g->lv[k].childStart, g->lv[k].childList, (int)g->lv[k].M, cnt1[k]);
+            }
+            std::vector<int2*> start(L, nullptr);
+            for (int k = 1; k < L; ++k) start[k] = dalloc<int2>(A, g->lv[k].M, s);
+            for (int k = 2; k < L; ++k) T.rng[k] = dalloc<int2>(A, g->lv[k].M, s);
+            T.tord0 = dalloc<int>(A, M, s);
+            T.csT = dalloc<int>(A, M1 + 1, s);
+            T.tord1 = dalloc<int>(A, M1, s);
+            T.parent0T = dalloc<int>(A, M, s);
+            LAUNCH(k_tree_top, 1, 256, 0, s, g->lvFrameOffDev, F, top, start[top], top >= 2 ? T.rng[top] : nullptr,
+                   top >= 2 ? cnt1[top] : nullptr);
+            for (int k = top; k >= 1; --k) {
+                const int km1 = k - 1;
+                LAUNCH(k_tree_down, grid_for(g->lv[k].M), kThreads, 0, s, km1, g->lv[k].childStart, g->lv[k].childList,
+                       (int)g->lv[k].M, start[k], km1 >= 1 ? g->lv[km1].count : nullptr,
+                       km1 >= 2 ? cnt1[km1] : nullptr, km1 >= 1 ? start[km1] : nullptr,
+                       km1 >= 2 ? T.rng[km1] : nullptr, T.tord0, T.tord1, T.csT);
+            }
+            LAUNCH(k_tree_finish, grid_for(M), kThreads, 0, s, g->lv[1].parent, start[1], M, M1, T.parent0T, T.csT);
+            // prefix-scan tiles: kScanTile level-1 positions, never crossing a frame
+            tfo.assign(F + 1, 0);
+            g->maxFrameM1 = 0;
+            g->maxFrameM2 = 0;
+            for (int f = 0; f < F && L > 2; ++f) g->maxFrameM2 = std::max<int64_t>(g->maxFrameM2, lfo[2][f + 1] - lfo[2][f]);
+            for (int f = 0; f < F; ++f) {
+                const int64_t m1 = lfo[1][f + 1] - lfo[1][f];
+                g->maxFrameM1 = std::max(g->maxFrameM1, m1);
+                tfo[f + 1] = tfo[f] + (int)((m1 + kScanTile - 1) / kScanTile);
+                for (int t = tfo[f]; t < tfo[f + 1]; ++t) tframe.push_back(f);
+            }
+            T.nTiles1 = tfo[F];
+            T.tileFrameOff = dalloc<int>(A, F + 1, s);
+            T.tileFrame = dalloc<int>(A, std::max<size_t>(tframe.size(), 1), s);
+            ck(cudaMemcpyAsync(T.tileFrameOff, tfo.data(), (F + 1) * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
+            if (!tframe.empty())
+                ck(cudaMemcpyAsync(T.tileFrame, tframe.data(), tframe.size() * sizeof(int), cudaMemcpyHostToDevice, s),
+                   "h2d");
+        }
         ck(cudaStreamSynchronize(s), "sync");  // host vector lifetime for the H2D copy
     } catch (...) {
         free_all(g->allocs, s);
@@ -358,11 +408,7 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     a.q = S->qh;
     a.s = S->sh;
     a.b = b;
-    a.w0 = S->w0;
     a.mu0 = S->mu0;
-    a.parent0 = (g->L > 1) ? g->lv[1].parent : nullptr;
-    a.acc1 = (g->L > 1) ? S->lvBuf[1] : nullptr;
-    a.M1 = (g->L > 1) ? g->lv[1].M : 0;
     a.partial = S->partial;
     a.counters = S->counters;
     a.sc_ = sc;
@@ -372,7 +418,7 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     return a;
 }
 
-// ---- hierarchical machinery (hier_kernels.cuh)
+// ---- hierarchical machinery (tree_kernels.cuh)
 HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     fbs_grid g = S->g;
     HierArgs h{};
@@ -387,9 +433,8 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
             v.childStart = L.childStart;
             v.childList = L.childList;
             v.count = L.count;
-            v.keys = L.keys;
-            v.mu = S->mu[k];
-            v.buf = S->lvBuf[k];
+            v.mu = (k >= 2) ? S->mu[k] : nullptr;
+            v.rng = g->tree.rng[k];
         }
         v.parent = (k + 1 < g->L) ? g->lv[k + 1].parent : nullptr;
     }
@@ -397,49 +442,92 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.lvFrameOff = g->lvFrameOffDev;
     h.alpha = alpha;
     h.beta = beta;
+    const TreeOrder& T = g->tree;
+    h.tord0 = T.tord0;
+    h.csT = T.csT;
+    h.parent0T = T.parent0T;
+    h.tileFrameOff = T.tileFrameOff;
+    h.tileFrame = T.tileFrame;
+    h.nTiles1 = T.nTiles1;
+    h.M0 = g->M;
+    h.M1 = g->lv[1].M;
+    h.mu1T = S->mu[1];
+    h.buf1T = S->buf1T;
+    h.locT = S->locT;
+    h.tileAgg = S->tileAgg;
+    h.tileBase = S->tileBase;
+    h.rhoTile = S->rhoTile;
+    h.acc1T = S->acc1T;
+    h.partial2 = S->partial2;
+    h.counters = S->counters;
+    h.bpf2 = S->bpf2;
     return h;
 }
 
-// The whole pyramid application in one cooperative kernel (hier_kernels.cuh k_hier).
+const char* mode_name(int m) {
+    static const char* n[] = {"PCG", "PDA", "INIT", "PLAIN"};
+    return n[m];
+}
+
+// P of the level-0 input in0 [C][M0] to tree-ordered level 1 + prefix scan (k_tree_lift).
 template <int MODE>
-void launch_hier(fbs_system S, const HierArgs& h, const VecArgs& a, const float* in0, float* out0, int first,
+void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s) {
+    static const std::string name = std::string("k_tree_lift<") + mode_name(MODE) + ">";
+    auto kern = k_tree_lift<MODE>;
+    LAUNCH_AS(name.c_str(), kern, S->g->tree.nTiles1, kScanTile, 0, s, h, in0);
+}
+
+// coarse values and their projection onto level 2 (k_tree_coarse)
+template <int MODE>
+void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, cudaStream_t s) {
+    static const std::string name = std::string("k_tree_coarse<") + mode_name(MODE) + ">";
+    auto kern = k_tree_coarse<MODE>;
+    LAUNCH_AS(name.c_str(), kern, S->g->F * S->bpf2, 256, 0, s, h, a, first);
+}
+
+// level-0 output (k_tree_level0)
+template <int MODE>
+void tree_level0(fbs_system S, const HierArgs& h, const VecArgs& a, const float* in0, float* out0, int first,
                  cudaStream_t s) {
-    // level 0 → 1 lift at full occupancy; levels 1..top in the cooperative kernel; level-0
-    // combination of the PCG preconditioner at full occupancy (k_precond_finish2)
-    const Level& L1 = S->g->lv[1];
-    LAUNCH(k_lift01, grid_for(L1.M), kThreads, 0, s, in0, S->g->M, L1.childStart, L1.childList, L1.M, h.C,
-           S->lvBuf[1]);
-    {
-        ::fbs::ProfScope _ps(MODE == HIER_PCG ? "k_hier<PCG>" : MODE == HIER_PDA ? "k_hier<PDA>"
-                             : MODE == HIER_INIT ? "k_hier<INIT>" : "k_hier<PLAIN>", s);
-        int bpf = S->bpfH;
-        unsigned* bar = S->bar;
-        int k_lift0 = 1;
-        int do_level0 = (MODE == HIER_PCG) ? 0 : 1;
-        void* args[] = {(void*)&h, (void*)&a, (void*)&in0, (void*)&out0, (void*)&first, (void*)&bpf, (void*)&bar,
-                        (void*)&k_lift0, (void*)&do_level0};
-        ck(cudaLaunchCooperativeKernel((const void*)k_hier<MODE>, dim3(S->g->F * bpf), dim3(1024), args, 0, s),
-           "k_hier cooperative launch");
-        ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
-    if (MODE == HIER_PCG) LAUNCH(k_precond_finish2, S->g->F * S->BPF, kThreads, 0, s, a, first);
+    static const std::string name = std::string("k_tree_level0<") + mode_name(MODE) + ">";
+    auto kern = k_tree_level0<MODE>;
+    LAUNCH_AS(name.c_str(), kern, S->g->F * S->BPF, kThreads, 0, s, h, a, in0, out0, first);
 }
 
-// s = M⁻¹_hier r (Eq. hier_precond) for the PCG from w0 = mask∘r; finishes the ρ reduction.
-void hier_precond(fbs_system S, const VecArgs& a, int first, cudaStream_t s) {
-    launch_hier<HIER_PCG>(S, S->hP, a, S->w0, nullptr, first, s);
+// level-0 PCG input w = mask∘r (+ ρ_0, ‖r‖² partials) (k_hier_level0)
+template <int SRC, bool LAST>
+void hier_level0(fbs_system S, const VecArgs& a, cudaStream_t s) {
+    static const char* src_names[] = {"UPDATE", "RESID", "RESID0"};
+    static const std::string name =
+        std::string("k_hier_level0<") + src_names[SRC] + (LAST ? ",LAST>" : ">");
+    auto kern = k_hier_level0<SRC, LAST>;
+    LAUNCH_AS(name.c_str(), kern, S->g->F * S->BPF, kThreads, 0, s, a, S->w0);
 }
 
-// One PCG iteration (Alg. 2 lines 14, 6-13): direction, SpMV + α, update (+ M⁻¹ and ρ, β).
-void pcg_iteration(fbs_system S, const VecArgs& a, int it, cudaStream_t s) {
+// s = M⁻¹_hier r and d = s + βd after the level-0 kernel (Alg. 2 lines 10-14)
+void hier_precond_direction(fbs_system S, const VecArgs& a, int first, cudaStream_t s) {
+    tree_lift<HIER_PCG>(S, S->hP, S->w0, s);
+    tree_coarse<HIER_PCG>(S, S->hP, a, first, s);
+    tree_level0<HIER_PCG>(S, S->hP, a, nullptr, nullptr, first, s);
+}
+
+// One PCG iteration (Alg. 2 lines 6-14): SpMV + α; update (+ M⁻¹ and ρ, β); direction.
+// Hierarchical: ρ = rᵀM⁻¹r comes from the lift, and Pᵀ is fused with d = s + βd
+// (tree_kernels.cuh).  last: the final FIXED-mode iteration needs no new direction.
+void pcg_iteration(fbs_system S, const VecArgs& a, int it, bool last, cudaStream_t s) {
     const int nb = S->g->F * S->BPF;
-    LAUNCH(k_direction2, nb, kThreads, 0, s, a, it == 0);
-    LAUNCH(k_spmv2, nb, kThreads, 0, s, a);
     if (S->useHierP) {
-        LAUNCH(k_update<true>, nb, kThreads, 0, s, a);
-        hier_precond(S, a, 0, s);
+        LAUNCH(k_spmv2, nb, kThreads, 0, s, a);
+        if (last) {
+            hier_level0<HSRC_UPDATE, true>(S, a, s);
+        } else {
+            hier_level0<HSRC_UPDATE, false>(S, a, s);
+            hier_precond_direction(S, a, 0, s);
+        }
     } else {
-        LAUNCH(k_update<false>, nb, kThreads, 0, s, a);
+        LAUNCH(k_direction2, nb, kThreads, 0, s, a, it == 0);
+        LAUNCH(k_spmv2, nb, kThreads, 0, s, a);
+        LAUNCH(k_update, nb, kThreads, 0, s, a);
     }
 }
 
@@ -450,20 +538,19 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     const int FK = g->F * S->K;
     LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK);
     if (S->useHierP) {
-        auto k1 = k_residual0<true, true>;
-        auto k2 = k_residual0<true, false>;
-        if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
-        else LAUNCH(k2, nb, kThreads, 0, s, a);
-        hier_precond(S, a, 1, s);
+        // Alg. 2 lines 2-4: r = b − A x, ρ = rᵀM⁻¹r (lift), d = s = M⁻¹r (project)
+        if (x_zero) hier_level0<HSRC_RESID0, false>(S, a, s);
+        else hier_level0<HSRC_RESID, false>(S, a, s);
+        hier_precond_direction(S, a, 1, s);
     } else {
-        auto k1 = k_residual0<false, true>;
-        auto k2 = k_residual0<false, false>;
+        auto k1 = k_residual0<true>;
+        auto k2 = k_residual0<false>;
         if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
         else LAUNCH(k2, nb, kThreads, 0, s, a);
+        // d = s (Alg. 2 line 3) is the first iteration's k_direction2
     }
-    // d = s (Alg. 2 line 3) is folded into the first iteration's fused direction + SpMV kernel
     if (S->o.mode == FBS_MODE_FIXED) {
-        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, i, s);
+        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, i, i == S->o.iters - 1, s);
         return;
     }
     // TOL: device-side per-channel stopping; the host polls the active count one chunk behind
@@ -477,7 +564,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     try {
         while (done < S->o.max_iters) {
             const int nit = std::min(chunk, S->o.max_iters - done);
-            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, done + i, s);
+            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, done + i, false, s);
             done += nit;
             ck(cudaMemcpyAsync(&pin[slot], a.sc_.n_active, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
             ck(cudaEventRecord(ev[slot], s), "event");
@@ -575,28 +662,27 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const bool hierI = o.init == FBS_INIT_HIER && g->L > 1;
         S->useHierP = hierP;
         if (hierP || hierI) {
-            S->w0 = dalloc<float>(A, (size_t)S->C * M, s);
-            for (int k = 1; k < g->L; ++k) {
-                S->lvBuf[k] = dalloc<float>(A, (size_t)S->C * g->lv[k].M, s);
-                if (hierP) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
-            }
+            const int C = S->C;
+            const int64_t M1 = g->lv[1].M;
+            const int nT = g->tree.nTiles1;
+            S->w0 = dalloc<float>(A, (size_t)C * M, s);
+            S->buf1T = dalloc<float>(A, (size_t)C * M1, s);
+            S->acc1T = dalloc<float>(A, (size_t)C * M1, s);
+            S->rhoTile = dalloc<double>(A, (size_t)C * nT, s);
+            S->locT = dalloc<double>(A, (size_t)C * M1, s);
+            S->tileAgg = dalloc<double>(A, (size_t)C * nT, s);
+            S->tileBase = dalloc<double>(A, (size_t)C * nT, s);
+            const int64_t want2 = ((g->L > 2 ? g->maxFrameM2 : g->maxFrameM1) + 255) / 256;
+            const int64_t cap2 = std::max<int64_t>(1, ((int64_t)g_num_sms * 8 + F - 1) / F);
+            S->bpf2 = (int)std::max<int64_t>(1, std::min(want2, cap2));
+            S->partial2 = dalloc<double>(A, (size_t)F * S->bpf2 * C, s);
+            if (hierP)
+                for (int k = 1; k < g->L; ++k) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
         }
-        int64_t perFrameBlocks = S->BPF;
-        if (hierP || hierI) {
-            int occH = 0;
-            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occH, k_hier<HIER_PCG>, 1024, 0), "occupancy");
-            S->bpfH = std::max(1, (g_num_sms * std::max(occH, 1)) / F);
-            if (S->bpfH * F > g_num_sms * std::max(occH, 1)) throw Err(FBS_ELIMIT, "too many frames for one cooperative launch");
-            perFrameBlocks = std::max<int64_t>(perFrameBlocks, S->bpfH);
-            S->bar = dalloc<unsigned>(A, 2, s);
-            ck(cudaMemsetAsync(S->bar, 0, 2 * sizeof(unsigned), s), "memset");
-        }
-        if (hierP || hierI) {
-            S->hP = make_hier(S, K, o.precond_alpha, o.precond_beta);
-        }
-        S->partial = dalloc<double>(A, (size_t)F * perFrameBlocks * 2 * K, s);
+        S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * K, s);
         S->counters = dalloc<unsigned>(A, F, s);
         ck(cudaMemsetAsync(S->counters, 0, F * sizeof(unsigned), s), "memset");
+        if (hierP || hierI) S->hP = make_hier(S, K, o.precond_alpha, o.precond_beta);
         S->fwd = alloc_scalars(A, F * K, s);
 
         const int nb = F * S->BPF;
@@ -611,12 +697,15 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         // a6/a7: hierarchical preconditioner multipliers μ_k = z_w P(1) / P(diag A), and init
         if (hierP) {
             HierArgs h = make_hier(S, 1, o.precond_alpha, o.precond_beta);
-            launch_hier<HIER_PDA>(S, h, a, S->w0, nullptr, 0, s);
+            tree_lift<HIER_PDA>(S, h, S->w0, s);
+            tree_coarse<HIER_PDA>(S, h, a, 0, s);
         }
         if (hierI) {
             HierArgs h = make_hier(S, K + 1, o.init_alpha, o.init_beta);
             LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, K, S->w0);
-            launch_hier<HIER_INIT>(S, h, a, S->w0, S->xh, 0, s);
+            tree_lift<HIER_INIT>(S, h, S->w0, s);
+            tree_coarse<HIER_INIT>(S, h, a, 0, s);
+            tree_level0<HIER_INIT>(S, h, a, S->w0, S->xh, 0, s);
         }
         ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
         LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, K);
@@ -908,7 +997,9 @@ int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_strea
             float* planar = dalloc<float>(tmp, KM, s);
             HierArgs h = S->hP;
             VecArgs a = make_args(S, S->fwd, S->xh, S->b);
-            launch_hier<HIER_PLAIN>(S, h, a, w, planar, 0, s);
+            tree_lift<HIER_PLAIN>(S, h, w, s);
+            tree_coarse<HIER_PLAIN>(S, h, a, 0, s);
+            tree_level0<HIER_PLAIN>(S, h, a, w, planar, 0, s);
             LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, S->K, out);
         } else {
             LAUNCH(k_precond_out, grid_for(g->M), kThreads, 0, s, w, S->mu0, nullptr, nullptr, 0, g->M, S->K, out);

@@ -21,6 +21,7 @@ constexpr int kCoarseCap = 512;      // children of one pyramid coarse cell sort
 constexpr int kMaxLevels = 24;
 constexpr int kThreads = 256;        // vertex-parallel kernels
 constexpr int kMaxK = 64;
+constexpr int kScanTile = 256;       // tree-ordered level-1 positions per prefix-scan tile (tree_kernels.cuh)
 
 // ------------------------------------------------------------------ launch counter
 extern std::atomic<long long> g_launches;
@@ -202,15 +203,14 @@ struct PcgScalars {     // per (frame, channel), fk = f*K + k
     int* n_active = nullptr;  // single counter
 };
 
-// ------------------------------------------------------------------ hierarchy (hier_kernels.cuh)
+// ------------------------------------------------------------------ hierarchy (tree_kernels.cuh)
 struct HLevel {
-    const int* parent = nullptr;      // level k → k+1 (nullptr at the top level)
+    const int* parent = nullptr;      // level k → k+1 (canonical ids; nullptr at the top level)
     const int* childStart = nullptr;  // k ≥ 1: children (level k−1) of level-k vertices
     const int* childList = nullptr;
     const int* count = nullptr;       // k ≥ 1: P(1)
-    const uint64_t* keys = nullptr;   // k ≥ 1
-    const float* mu = nullptr;        // k ≥ 1: preconditioner multiplier
-    float* buf = nullptr;             // k ≥ 1: lifted / projected values [C][M]
+    const float* mu = nullptr;        // k ≥ 2: preconditioner multiplier (level 1: HierArgs::mu1T)
+    const int2* rng = nullptr;        // k ≥ 2: (first tree position, count) of the level-1 descendants
     int64_t M = 0;
 };
 
@@ -220,8 +220,39 @@ struct HierArgs {
     int F;
     int C;                  // channels carried through the pyramid
     const int* frameLevels;
-    const int* lvFrameOff;  // [L][F+1] per-level frame vertex offsets
+    const int* lvFrameOff;  // [L][F+1] per-level frame vertex offsets (tree order keeps frames)
     double alpha, beta;     // z_weight parameters of the current use
+    // tree order (grid)
+    const int* tord0;       // [M0] level-0 vertex at each level-0 tree position
+    const int* csT;         // [M1+1] level-0 tree range of the level-1 vertex at tree position i
+    const int* parent0T;    // [M0] tree position of the level-1 parent of level-0 vertex v
+    const int* tileFrameOff;  // [F+1] first scan tile of each frame
+    const int* tileFrame;     // [nTiles1] frame of each scan tile
+    int nTiles1;
+    int64_t M0, M1;
+    // per use (system buffers)
+    float* mu1T;            // [M1] μ_1 in tree order
+    float* buf1T;           // [C][M1] (P y)_1 in tree order
+    double* locT;           // [C][M1] inclusive prefix within the scan tile
+    double* tileAgg;        // [C][nTiles1] tile totals
+    double* tileBase;       // [C][nTiles1] exclusive prefix of the tile totals within the frame
+    double* rhoTile;        // [C][nTiles1] ρ_1 partials per scan tile
+    float* acc1T;           // [C][M1] projection of levels ≥ 1 onto level 1, tree order
+    double* partial2;       // [F][bpf2][C] ρ partials of levels ≥ 2
+    unsigned* counters;     // [F] last-block counters (shared with VecArgs; kernels are serial)
+    int bpf2;               // blocks per frame of k_tree_coarse
+};
+
+// tree order of the pyramid (grid build)
+struct TreeOrder {
+    int* tord0 = nullptr;
+    int* csT = nullptr;
+    int* tord1 = nullptr;
+    int* parent0T = nullptr;
+    int* tileFrameOff = nullptr;
+    int* tileFrame = nullptr;
+    int nTiles1 = 0;
+    int2* rng[kMaxLevels] = {};
 };
 
 }  // namespace fbs
@@ -253,7 +284,10 @@ struct fbs_grid_s {
     int L = 1;  // levels incl. base (max over frames)
     fbs::Level lv[fbs::kMaxLevels];
     int64_t maxFrameM = 0;
+    int64_t maxFrameM1 = 0;
+    int64_t maxFrameM2 = 0;
     int* lvFrameOffDev = nullptr;  // [L][F + 1]
+    fbs::TreeOrder tree;           // tree order of the pyramid (L > 1)
     std::vector<void*> allocs;
 };
 
@@ -278,16 +312,21 @@ struct fbs_system_s {
     float2* dn = nullptr;     // [K][M] interleaved (d, n)
     float* qh = nullptr;
     float* sh = nullptr;
-    float* w0 = nullptr;                   // [C][M] level-0 pyramid input
-    float* lvBuf[fbs::kMaxLevels] = {};    // [C][M_k] level values (k ≥ 1)
-    float* mu[fbs::kMaxLevels] = {};       // [M_k] precond multipliers (k ≥ 1)
+    float* w0 = nullptr;                   // [C][M] level-0 pyramid input (init, μ_k, debug operator)
+    float* mu[fbs::kMaxLevels] = {};       // [M_k] precond multipliers (k ≥ 2 canonical; k = 1 tree order)
+    float* buf1T = nullptr;                // [C][M1] hierarchy work arrays (tree_kernels.cuh)
+    double* locT = nullptr;
+    double* tileAgg = nullptr;
+    double* tileBase = nullptr;
+    double* rhoTile = nullptr;
+    float* acc1T = nullptr;
+    double* partial2 = nullptr;
+    int bpf2 = 1;
     int C = 1;
     double* partial = nullptr;  // [F][BPF][2K]
     unsigned* counters = nullptr;  // [F]
     fbs::PcgScalars fwd, bwd;
     bool useHierP = false;
-    int bpfH = 1;              // blocks per frame of the cooperative hierarchy kernel
-    unsigned* bar = nullptr;   // its grid barrier (count, generation)
     fbs::HierArgs hP{};
     bool has_backward = false;
     std::vector<void*> allocs;

@@ -30,11 +30,7 @@ struct VecArgs {
     float* q;
     float* s;
     const float* b;
-    float* w0;            // hier: level-0 pyramid input [K][M]
-    const float* mu0;     // level-0 multiplier 1/diag(A) on live vertices
-    const int* parent0;   // hier: level 0 → 1 (nullptr if single level)
-    const float* acc1;    // hier: projected level-1 values [C][M1]
-    int64_t M1;
+    const float* mu0;     // level-0 multiplier 1/diag(A) on live vertices (0 on dead ones)
     double* partial;      // [F][BPF][2K]
     unsigned* counters;   // [F]
     PcgScalars sc_;
@@ -150,8 +146,33 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
 }
 
 // ---------------------------------------------------------------- per-frame reductions
-// finish of the ρ-reduction (Alg. 2 lines 11-13 + stopping rule, reading #11), executed by the
-// last block of frame f.  first: the reduction right after initialisation (lines 2-4).
+// Alg. 2 lines 11-13 + stopping rule (reading #11) for one (frame, channel) given its reduced
+// ρ = rᵀs and ‖r‖²; executed by one thread.  first: the reduction right after initialisation
+// (lines 2-4).
+__device__ __forceinline__ void finish_rho_one(const VecArgs& a, int fk, bool first, double R, double RR) {
+    const bool conv = a.tol_mode && RR <= a.tol2 * a.sc_.bb[fk];
+    a.sc_.rr[fk] = RR;
+    if (first) {
+        a.sc_.rho[fk] = R;
+        a.sc_.beta[fk] = 0.0;
+        a.sc_.iters[fk] = 0;
+        const bool act = !conv && R != 0.0 && a.max_iters > 0;
+        a.sc_.active[fk] = act;
+        if (!act) atomicSub(a.sc_.n_active, 1);
+    } else {
+        a.sc_.beta[fk] = R / a.sc_.rho[fk];
+        a.sc_.rho[fk] = R;
+        const int it = a.sc_.iters[fk] + 1;
+        a.sc_.iters[fk] = it;
+        if (conv || R == 0.0 || it >= a.max_iters) {
+            if (!conv && a.tol_mode && R != 0.0) atomicOr(a.sc_.status + fk, FBS_ST_NOTCONVERGED);
+            a.sc_.active[fk] = 0;
+            atomicSub(a.sc_.n_active, 1);
+        }
+    }
+}
+
+// finish of the ρ-reduction executed by the last block of frame f (partials [F][BPF][2K]).
 __device__ void finish_rho(const VecArgs& a, int f, bool first, double* shd) {
     for (int k = 0; k < a.K; ++k) {
         const int fk = f * a.K + k;
@@ -164,28 +185,7 @@ __device__ void finish_rho(const VecArgs& a, int f, bool first, double* shd) {
         }
         R = block_sum(R, shd);
         RR = block_sum(RR, shd);
-        if (threadIdx.x == 0) {
-            const bool conv = a.tol_mode && RR <= a.tol2 * a.sc_.bb[fk];
-            a.sc_.rr[fk] = RR;
-            if (first) {
-                a.sc_.rho[fk] = R;
-                a.sc_.beta[fk] = 0.0;
-                a.sc_.iters[fk] = 0;
-                const bool act = !conv && R != 0.0 && a.max_iters > 0;
-                a.sc_.active[fk] = act;
-                if (!act) atomicSub(a.sc_.n_active, 1);
-            } else {
-                a.sc_.beta[fk] = R / a.sc_.rho[fk];
-                a.sc_.rho[fk] = R;
-                const int it = a.sc_.iters[fk] + 1;
-                a.sc_.iters[fk] = it;
-                if (conv || R == 0.0 || it >= a.max_iters) {
-                    if (!conv && a.tol_mode && R != 0.0) atomicOr(a.sc_.status + fk, FBS_ST_NOTCONVERGED);
-                    a.sc_.active[fk] = 0;
-                    atomicSub(a.sc_.n_active, 1);
-                }
-            }
-        }
+        if (threadIdx.x == 0) finish_rho_one(a, fk, first, R, RR);
     }
 }
 
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
     }
 }
 
-// ---------------------------------------------------------------- pyramid lift / project
+// ---------------------------------------------------------------- hierarchical init input [b_0..b_{K−1}, Sc]
 __global__ void k_fill_init_w0(const float* __restrict__ b, const float* __restrict__ sc, int64_t M, int K,
                                float* __restrict__ w0) {
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
@@ -267,9 +267,9 @@ __global__ void k_init_scalars(PcgScalars s, int FK) {
     if (i == 0) *s.n_active = FK;
 }
 
-// Alg. 2 lines 2-4:  r = b − A x;  s = M⁻¹ r;  ρ = rᵀs   (X_ZERO: x = 0 ⇒ r = b, backward).
-// HIER: writes w0 = mask∘r for the pyramid; the reduction finishes in k_precond_finish.
-template <bool HIER, bool X_ZERO>
+// Alg. 2 lines 2-4 (Jacobi):  r = b − A x;  s = M⁻¹ r;  ρ = rᵀs   (X_ZERO: x = 0 ⇒ r = b, backward).
+// The hierarchical preconditioner has its own fused kernels (tile_kernels.cuh).
+template <bool X_ZERO>
 __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
     __shared__ double shd[32];
     __shared__ int sflag;
@@ -282,24 +282,17 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
             float r = a.b[off + v];
             if (!X_ZERO) r -= apply_A_row(a.x + off, a.n, v, a.nbr[v], a.lam, a.sc[v]);
             a.r[off + v] = r;
-            const float m0 = a.mu0[v];
-            if (HIER) {
-                a.w0[off + v] = (m0 > 0.f) ? r : 0.f;
-            } else {
-                const float s = m0 * r;
-                a.s[off + v] = s;
-                rho += (double)r * (double)s;
-                rr += (double)r * (double)r;
-            }
+            const float s = a.mu0[v] * r;
+            a.s[off + v] = s;
+            rho += (double)r * (double)s;
+            rr += (double)r * (double)r;
         }
-        if (!HIER) write_partials(a, f, j, k, rho, rr, shd);
+        write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, true, shd);
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, true, shd);
 }
 
-// Alg. 2 lines 8-12:  x += αd;  r −= αq;  s = M⁻¹r;  ρ_new = rᵀs.
-// Jacobi: s = r/diag(A) inline, reduction finished here.  HIER: writes w0 = mask∘r.
-template <bool HIER>
+// Alg. 2 lines 8-12 (Jacobi):  x += αd;  r −= αq;  s = M⁻¹r = r/diag(A);  ρ_new = rᵀs.
 __global__ void __launch_bounds__(256) k_update(VecArgs a) {
     __shared__ double shd[32];
     __shared__ int sflag;
@@ -333,20 +326,16 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
                     a.x[off + v] = xv[u] + al * dv[u];
                     const float r = rv[u] - al * qv[u];
                     a.r[off + v] = r;
-                    if (HIER) {
-                        a.w0[off + v] = (mv[u] > 0.f) ? r : 0.f;
-                    } else {
-                        const float s = mv[u] * r;
-                        a.s[off + v] = s;
-                        rho += (double)r * (double)s;
-                        rr += (double)r * (double)r;
-                    }
+                    const float s = mv[u] * r;
+                    a.s[off + v] = s;
+                    rho += (double)r * (double)s;
+                    rr += (double)r * (double)r;
                 }
             }
         }
-        if (!HIER) write_partials(a, f, j, k, rho, rr, shd);
+        write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (!HIER && last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, false, shd);
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, false, shd);
 }
 
 // ---------------------------------------------------------------- streaming PCG kernels
@@ -447,48 +436,6 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
             }
         }
     }
-}
-
-// Hierarchical M⁻¹ at level 0 (Eq. hier_precond): s = mask∘(μ0 r + acc1[parent0]) with acc1 the
-// projected level-1 values (k_hier); ρ = rᵀs, ‖r‖² and the per-frame finish (Alg. 2
-// lines 11-13; first: lines 3-4).
-__global__ void __launch_bounds__(256) k_precond_finish2(VecArgs a, int first) {
-    __shared__ double shd[32];
-    __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
-    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    const int stride = a.BPF * blockDim.x;
-    for (int k = 0; k < a.K; ++k) {
-        const int fk = f * a.K + k;
-        double rho = 0.0, rr = 0.0;
-        if (first || a.sc_.active[fk]) {
-            const size_t off = (size_t)k * a.M;
-            const float* acc1 = a.acc1 + (size_t)k * a.M1;
-            for (int v0u = v0 + j * blockDim.x + threadIdx.x; v0u < v1; v0u += 4 * stride) {
-                float rv[4], mv[4], up[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int v = v0u + u * stride;
-                    if (v < v1) {
-                        rv[u] = a.r[off + v];
-                        mv[u] = a.mu0[v];
-                        up[u] = acc1[a.parent0[v]];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int v = v0u + u * stride;
-                    if (v >= v1) continue;
-                    const float sval = (mv[u] > 0.f) ? mv[u] * rv[u] + up[u] : 0.f;
-                    a.s[off + v] = sval;
-                    rho += (double)rv[u] * (double)sval;
-                    rr += (double)rv[u] * (double)rv[u];
-                }
-            }
-        }
-        write_partials(a, f, j, k, rho, rr, shd);
-    }
-    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, first != 0, shd);
 }
 
 // ---------------------------------------------------------------- slice / export / backward

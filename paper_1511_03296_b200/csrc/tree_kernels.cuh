@@ -1,0 +1,428 @@
+// tree_kernels.cuh — the hierarchical preconditioner and initialisation in tree order
+// (Eq. hier_precond, hier init PAPER.md:287-293, pyramid PAPER.md:745-766).
+//
+// P lifts y through the pyramid, Pᵀ projects back (:763), and both hierarchical
+// operators are  out = Pᵀ(mult ∘ P(in))  with per-level multipliers (reading #8: level 0 = y).
+// TREE ORDER.  At grid build the level-1 vertices (and the level-0 vertices) are numbered in
+// depth-first order of the pyramid (siblings in canonical child order), so the level-1
+// descendants of ANY coarse vertex a (level ≥ 2) are one contiguous range rng(a) of the
+// tree-ordered level-1 vector.  Hence, per (frame, channel):
+//   (P y)_a = Π(end_a) − Π(start_a − 1),   Π = fp64 inclusive prefix of the tree-ordered (P y)_1,
+// and the projection of the levels ≥ 2 onto a level-2 vertex a is one ancestor-chain walk
+//   acc2_a = Σ_{k≥2} mult_k(anc_k(a))·(P y)_{anc_k(a)},
+// handed to its children (one contiguous tree range): acc1_i = mult_1(i)·(P y)_1,i + acc2_{parent(i)}.
+// No level-by-level synchronisation remains: one lift+scan pass over level 1, one pass over
+// level 2 for all coarse values, one pass over level 0.  Every sum has a fixed order (child
+// order, fixed scan trees), so results are bitwise reproducible.
+//
+// PCG (Alg. 2) uses M⁻¹ = mask∘Pᵀ(μ∘P(mask∘·)), so ρ = rᵀM⁻¹r = Σ_k Σ_a μ_k,a (P w)²_a with
+// w = mask∘r: ρ is complete after the lift, and the projection is fused with d = s + βd.
+#pragma once
+#include "fbs_common.cuh"
+#include "solve_kernels.cuh"
+
+namespace fbs {
+
+enum { HIER_PCG = 0, HIER_PDA = 1, HIER_INIT = 2, HIER_PLAIN = 3 };
+enum { HSRC_UPDATE = 0, HSRC_RESID = 1, HSRC_RESID0 = 2 };
+
+// ================================================================ grid build: tree order
+// start positions of the top vertex of each frame: its frame's first level-0 / level-1 positions
+// (top ≥ 2: also its level-1 range)
+__global__ void k_tree_top(const int* __restrict__ lvFrameOff, int F, int top, int2* __restrict__ startTop,
+                           int2* __restrict__ rngTop, const int* __restrict__ cnt1Top) {
+    for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
+        const int F1 = F + 1;
+        const int a = lvFrameOff[top * F1 + f];
+        if (a < lvFrameOff[top * F1 + f + 1]) {
+            startTop[a] = make_int2(lvFrameOff[f], lvFrameOff[F1 + f]);
+            if (rngTop) rngTop[a] = make_int2(lvFrameOff[F1 + f], cnt1Top[a]);
+        }
+    }
+}
+
+// level k → k−1: each level-k vertex hands consecutive sub-ranges (in canonical child order) of
+// its level-0 / level-1 tree ranges to its children.  cnt0 = P(1) of level k−1, cnt1 = level-1
+// descendants of level k−1 (k−1 ≥ 2).  k−1 = 1: writes tord1, csT; k−1 = 0: writes tord0;
+// k−1 ≥ 2: writes rng = (level-1 start, level-1 count).
+__global__ void k_tree_down(int km1, const int* __restrict__ childStart, const int* __restrict__ childList, int Mk,
+                            const int2* __restrict__ startK, const int* __restrict__ cnt0, const int* __restrict__ cnt1,
+                            int2* __restrict__ startKm1, int2* __restrict__ rngKm1, int* __restrict__ tord0,
+                            int* __restrict__ tord1, int* __restrict__ csT) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < Mk; a += gridDim.x * blockDim.x) {
+        int2 r = startK[a];
+        for (int q = childStart[a]; q < childStart[a + 1]; ++q) {
+            const int c = childList[q];
+            if (km1 == 0) {
+                tord0[r.x] = c;
+                r.x += 1;
+            } else {
+                startKm1[c] = r;
+                if (km1 == 1) {
+                    tord1[r.y] = c;
+                    csT[r.y] = r.x;
+                    r.y += 1;
+                } else {
+                    rngKm1[c] = make_int2(r.y, cnt1[c]);
+                    r.y += cnt1[c];
+                }
+                r.x += cnt0[c];
+            }
+        }
+    }
+}
+
+// parent0T[v] = tree position of v's level-1 parent; csT[M1] = M0.
+__global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __restrict__ start1, int64_t M0,
+                              int64_t M1, int* __restrict__ parent0T, int* __restrict__ csT) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t v = t0; v < M0; v += stride) parent0T[v] = start1[parent0[v]].y;
+    if (t0 == 0) csT[M1] = (int)M0;
+}
+
+// ================================================================ level 0 → PCG input
+// w = mask∘r with r from the PCG update (Alg. 2 lines 8-9), the initial residual r = b − A x
+// (lines 2), or r = b (x = 0, backward); partials ρ_0 = Σ μ0 w² and ‖r‖².  FINISH_LAST: the
+// final FIXED-mode iteration needs no new direction: its last block per frame records ‖r‖² and
+// the iteration count and retires the channel.
+template <int SRC, bool FINISH_LAST>
+__global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restrict__ w0) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const int stride = a.BPF * blockDim.x;
+    for (int k = 0; k < a.K; ++k) {
+        const int fk = f * a.K + k;
+        double rho = 0.0, rr = 0.0;
+        if (SRC != HSRC_UPDATE || a.sc_.active[fk]) {
+            const size_t off = (size_t)k * a.M;
+            const float al = (SRC == HSRC_UPDATE) ? (float)a.sc_.alpha[fk] : 0.f;
+            for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += 4 * stride) {
+                float rv[4], mv[4];
+                if (SRC == HSRC_UPDATE) {
+                    float xv[4], dv[4], qv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int v = vb + u * stride;
+                        if (v < v1) {
+                            xv[u] = a.x[off + v];
+                            dv[u] = a.dn[off + v].x;
+                            rv[u] = a.r[off + v];
+                            qv[u] = a.q[off + v];
+                            mv[u] = a.mu0[v];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int v = vb + u * stride;
+                        if (v < v1) {
+                            a.x[off + v] = xv[u] + al * dv[u];
+                            rv[u] -= al * qv[u];
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int v = vb + u * stride;
+                        if (v < v1) {
+                            rv[u] = a.b[off + v];
+                            if (SRC == HSRC_RESID) rv[u] -= apply_A_row(a.x + off, a.n, v, a.nbr[v], a.lam, a.sc[v]);
+                            mv[u] = a.mu0[v];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int v = vb + u * stride;
+                    if (v >= v1) continue;
+                    a.r[off + v] = rv[u];
+                    const float w = (mv[u] > 0.f) ? rv[u] : 0.f;
+                    if (!FINISH_LAST) w0[off + v] = w;
+                    rr += (double)rv[u] * (double)rv[u];
+                    rho += (double)mv[u] * (double)w * (double)w;
+                }
+            }
+        }
+        write_partials(a, f, j, k, rho, rr, shd);
+    }
+    if (FINISH_LAST && last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
+        for (int k = 0; k < a.K; ++k) {
+            const int fk = f * a.K + k;
+            if (!a.sc_.active[fk]) continue;
+            double RR = 0.0;
+            for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
+                RR += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k + 1);
+            RR = block_sum(RR, shd);
+            if (threadIdx.x == 0) {
+                a.sc_.rr[fk] = RR;
+                a.sc_.iters[fk] += 1;
+                a.sc_.active[fk] = 0;
+                atomicSub(a.sc_.n_active, 1);
+            }
+        }
+    }
+}
+
+// ================================================================ lift 0 → 1 and the prefix scan
+// One block = one scan tile of kScanTile consecutive tree positions of one frame; warp w lifts
+// positions [32w, 32w + 32): the children of its 32 level-1 vertices are one contiguous range of
+// level-0 tree positions, staged (coalesced index load + gather) in shared memory and summed by
+// each lane over its own children in canonical child order.  Then a fixed-tree fp64 block scan
+// gives the within-tile inclusive prefix; the last tile of the frame scans the tile totals.
+constexpr int kLiftStage = 256;
+
+// INIT multiplier z_w(k)/P(1)_k; 0 above the frame's top level (reading #8)
+__device__ __forceinline__ float init_mult1(const HierArgs& h, int k, int fl, int count) {
+    return (k < fl) ? (float)(pow(h.alpha, -(h.beta + (double)k)) / (double)count) : 0.f;
+}
+
+__device__ __forceinline__ float zw_count(double alpha, double beta, int k, int count, double den) {
+    return (float)(pow(alpha, -(beta + (double)k)) * (double)count / den);
+}
+
+
+__device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*/, double* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) sh[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        double s = (lane < nw) ? sh[lane] : 0.0;
+        double si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, si, o);
+            if (lane >= o) si += y;
+        }
+        if (lane < nw) sh[lane] = si - s;
+        if (lane == nw - 1) sh[31] = si;
+    }
+    __syncthreads();
+    *total = sh[31];
+    return sh[w] + incl;
+}
+
+// PCG: also the ρ terms of level 1, μ_1 (P w)²_1 (tile partials); PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
+template <int MODE>
+__global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0) {
+    __shared__ float stage[kScanTile / 32][kLiftStage];
+    __shared__ double shs[32];
+    __shared__ int sflag;
+    const int t = blockIdx.x;
+    const int f = h.tileFrame[t];
+    const int F1 = h.F + 1;
+    const int fb = h.lvFrameOff[F1 + f], fe = h.lvFrameOff[F1 + f + 1];
+    const int i0 = fb + (t - h.tileFrameOff[f]) * kScanTile;
+    const int i1 = min(i0 + kScanTile, fe);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = i0 + (int)threadIdx.x;
+    const bool valid = i < i1;
+    const int wa = min(i0 + 32 * w, i1), wb = min(i0 + 32 * w + 32, i1);
+    const int qa = h.csT[wa], qb = h.csT[wb];
+    const int myLo = valid ? h.csT[i] : 0, myHi = valid ? h.csT[i + 1] : 0;
+    for (int c = 0; c < h.C; ++c) {
+        const float* src = in0 + (size_t)c * h.M0;
+        float acc = 0.f;
+        for (int qc = qa; qc < qb; qc += kLiftStage) {
+            const int n = min(kLiftStage, qb - qc);
+#pragma unroll
+            for (int e = 0; e < kLiftStage / 32; ++e) {
+                const int q = lane + 32 * e;
+                if (q < n) stage[w][q] = src[h.tord0[qc + q]];
+            }
+            __syncwarp();
+            const int lo = max(myLo, qc), hi = min(myHi, qc + n);
+            for (int q = lo; q < hi; ++q) acc += stage[w][q - qc];
+            __syncwarp();
+        }
+        if (valid) h.buf1T[(size_t)c * h.M1 + i] = acc;
+        if (MODE == HIER_PDA && valid)
+            h.mu1T[i] = (1 < h.frameLevels[f] && acc > 0.f) ? zw_count(h.alpha, h.beta, 1, myHi - myLo, (double)acc) : 0.f;
+        if (MODE == HIER_PCG) {
+            const float m1 = valid ? h.mu1T[i] : 0.f;
+            double r1 = (double)m1 * (double)acc * (double)acc;
+            r1 = block_sum(r1, shs);
+            if (threadIdx.x == 0) h.rhoTile[(size_t)c * h.nTiles1 + t] = r1;
+        }
+        double tot;
+        const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
+        if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
+        if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + t] = tot;
+        __syncthreads();
+    }
+    // last tile of the frame: exclusive prefix of the frame's tile totals (fixed order)
+    const int nt = h.tileFrameOff[f + 1] - h.tileFrameOff[f];
+    if (last_block_of_frame(h.counters + f, nt, &sflag) && w == 0) {
+        for (int c = 0; c < h.C; ++c) {
+            const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + h.tileFrameOff[f];
+            double* base = h.tileBase + (size_t)c * h.nTiles1 + h.tileFrameOff[f];
+            double carry = 0.0;
+            for (int b = 0; b < nt; b += 32) {
+                const double x = (b + lane < nt) ? __ldcg(agg + b + lane) : 0.0;
+                double incl = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                if (b + lane < nt) base[b + lane] = carry + incl - x;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+    }
+}
+
+// ================================================================ coarse values and their projection onto level 2
+// Π(j) = fp64 inclusive prefix of tree-ordered (P y)_1 of frame f up to position j
+__device__ __forceinline__ double tree_prefix(const HierArgs& h, int c, int f, int fb, int j) {
+    if (j < fb) return 0.0;
+    const int t = h.tileFrameOff[f] + (j - fb) / kScanTile;
+    return __ldg(h.tileBase + (size_t)c * h.nTiles1 + t) + __ldg(h.locT + (size_t)c * h.M1 + j);
+}
+
+// One thread per level-2 vertex a (blocks per frame: h.bpf2), walking its ancestor chain, then
+// writing acc1 for its children (L = 2: one thread per level-1 position, acc2 = 0):
+//   PCG/PLAIN: acc2_a = Σ_{k≥2} μ_k (P w)_anc;  PCG also ρ_{≥2} = Σ μ (P w)² (each coarse vertex
+//              counted once, by its first level-2 descendant) and, in the last block of the
+//              frame, the ρ finish (with the ρ_0, ‖r‖² partials of k_hier_level0 and the ρ_1 tile
+//              partials of k_tree_lift): β and the stopping rule (Alg. 2 lines 11-13).
+//   INIT:      mult_k = z_w(k)/P(1)_k.
+//   PDA:       μ_k = z_w(k; α, β) P(1)_k / P(diag A)_k, 0 where the
+//              denominator is 0 (reading #10) or above the frame's top level.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / h.bpf2, j = blockIdx.x % h.bpf2;
+    const int F1 = h.F + 1;
+    const int fb = h.lvFrameOff[F1 + f];
+    const int top = h.L - 1;
+    const int fl = h.frameLevels[f];
+    const int stride = h.bpf2 * blockDim.x;
+    const int lv = (top >= 2) ? 2 : 1;  // level of the threads' vertices
+    const int a0 = h.lvFrameOff[lv * F1 + f], a1 = h.lvFrameOff[lv * F1 + f + 1];
+    for (int c = 0; c < h.C; ++c) {
+        const int fk = f * a.K + c;
+        const bool act = (MODE != HIER_PCG) || first || a.sc_.active[fk];
+        double rho = 0.0;
+        if (act) {
+            for (int v = a0 + j * blockDim.x + threadIdx.x; v < a1; v += stride) {
+                // level-1 children of v: one contiguous tree range (L = 2: v itself)
+                const int2 kids = (lv == 2) ? h.lv[2].rng[v] : make_int2(v, 1);
+                const int first1 = kids.x;
+                float acc = 0.f;
+                int an = (lv == 2) ? v : -1;
+                for (int k = 2; k <= top && an >= 0; ++k) {
+                    const HLevel& L = h.lv[k];
+                    const int2 rg = L.rng[an];
+                    const int nxt = (k < top) ? L.parent[an] : -1;
+                    const double S = tree_prefix(h, c, f, fb, rg.x + rg.y - 1) - tree_prefix(h, c, f, fb, rg.x - 1);
+                    if (MODE == HIER_PDA) {
+                        if (rg.x == first1)
+                            const_cast<float*>(L.mu)[an] =
+                                (k < fl && S > 0.0) ? zw_count(h.alpha, h.beta, k, L.count[an], S) : 0.f;
+                    } else {
+                        const float mk = (MODE == HIER_INIT) ? init_mult1(h, k, fl, L.count[an]) : L.mu[an];
+                        acc += mk * (float)S;
+                        if (MODE == HIER_PCG && rg.x == first1) rho += (double)mk * S * S;
+                    }
+                    an = nxt;
+                }
+                if (MODE != HIER_PDA) {
+                    for (int i = kids.x; i < kids.x + kids.y; ++i) {
+                        const float m1 =
+                            (MODE == HIER_INIT) ? init_mult1(h, 1, fl, h.csT[i + 1] - h.csT[i]) : h.mu1T[i];
+                        h.acc1T[(size_t)c * h.M1 + i] = m1 * h.buf1T[(size_t)c * h.M1 + i] + acc;
+                    }
+                }
+            }
+        }
+        if (MODE == HIER_PCG) {
+            rho = block_sum(rho, shd);
+            if (threadIdx.x == 0) h.partial2[((size_t)f * h.bpf2 + j) * h.C + c] = rho;
+        }
+    }
+    if (MODE == HIER_PCG && last_block_of_frame(h.counters + f, h.bpf2, &sflag)) {
+        const int t0 = h.tileFrameOff[f], t1 = h.tileFrameOff[f + 1];
+        for (int c = 0; c < a.K; ++c) {
+            const int fk = f * a.K + c;
+            if (!first && !a.sc_.active[fk]) continue;
+            double R = 0.0, RR = 0.0;
+            for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x) {
+                const double* pp = a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * c;
+                R += __ldcg(pp);
+                RR += __ldcg(pp + 1);
+            }
+            for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) R += __ldcg(h.rhoTile + (size_t)c * h.nTiles1 + t);
+            for (int jj = threadIdx.x; jj < h.bpf2; jj += blockDim.x)
+                R += __ldcg(h.partial2 + ((size_t)f * h.bpf2 + jj) * h.C + c);
+            R = block_sum(R, shd);
+            RR = block_sum(RR, shd);
+            if (threadIdx.x == 0) finish_rho_one(a, fk, first != 0, R, RR);
+            __syncthreads();
+        }
+    }
+}
+
+// ================================================================ level 0
+// acc1 = acc1T at the tree position pT of the level-1 parent, then
+// PCG:   d = s + βd with s = mask∘(μ0 r + acc1) (Alg. 2 line 14; first: d = s, line 3)
+// PLAIN: out0 = mask∘(μ0 in0 + acc1[parent])
+// INIT:  out0_k = (in0_k + acc1_k[parent]) / (in0_K + acc1_K[parent]), 0 where the denominator is 0
+template <int MODE>
+__global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, const float* __restrict__ in0,
+                                                   float* __restrict__ out0, int first) {
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const int stride = a.BPF * blockDim.x;
+    const int K = (MODE == HIER_INIT) ? h.C - 1 : a.K;
+    auto acc1 = [&](int c, int pT) { return h.acc1T[(size_t)c * h.M1 + pT]; };
+    for (int k = 0; k < K; ++k) {
+        const int fk = f * a.K + k;
+        if (MODE == HIER_PCG && !first && !a.sc_.active[fk]) continue;
+        const float be = (MODE == HIER_PCG && !first) ? (float)a.sc_.beta[fk] : 0.f;
+        const size_t off = (size_t)k * a.M;
+        for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += 4 * stride) {
+            float sv[4], mv[4], up[4];
+            float2 dv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = vb + u * stride;
+                if (v < v1) {
+                    const int pT = h.parent0T[v];
+                    up[u] = acc1(k, pT);
+                    if (MODE == HIER_INIT) {
+                        sv[u] = in0[off + v];
+                        mv[u] = in0[(size_t)K * a.M + v] + acc1(K, pT);
+                    } else {
+                        sv[u] = (MODE == HIER_PCG) ? a.r[off + v] : in0[off + v];
+                        mv[u] = a.mu0[v];
+                        if (MODE == HIER_PCG) dv[u] = a.dn[off + v];
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = vb + u * stride;
+                if (v >= v1) continue;
+                if (MODE == HIER_INIT) {
+                    out0[off + v] = (mv[u] > 0.f) ? (sv[u] + up[u]) / mv[u] : 0.f;
+                } else {
+                    const float s = (mv[u] > 0.f) ? mv[u] * sv[u] + up[u] : 0.f;
+                    if (MODE == HIER_PCG) a.dn[off + v] = make_float2(first ? s : s + be * dv[u].x, dv[u].y);
+                    else out0[off + v] = s;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace fbs
