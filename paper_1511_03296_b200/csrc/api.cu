@@ -332,6 +332,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // ---- tree order of the pyramid (tree_kernels.cuh): depth-first positions of the level-0 and
         // level-1 vertices, so every coarse subtree is one contiguous level-1 range
         std::vector<int> tfo, tframe;
+        std::vector<int2> trange;
         if (L > 1) {
             TreeOrder& T = g->tree;
             const int64_t M1 = g->lv[1].M;
@@ -368,11 +369,22 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
                 const int64_t m1 = lfo[1][f + 1] - lfo[1][f];
                 g->maxFrameM1 = std::max(g->maxFrameM1, m1);
                 tfo[f + 1] = tfo[f] + (int)((m1 + kScanTile - 1) / kScanTile);
-                for (int t = tfo[f]; t < tfo[f + 1]; ++t) tframe.push_back(f);
+                T.maxFrameTiles = std::max(T.maxFrameTiles, tfo[f + 1] - tfo[f]);
+                for (int t = tfo[f]; t < tfo[f + 1]; ++t) {
+                    tframe.push_back(f);
+                    const int a0 = lfo[1][f] + (t - tfo[f]) * kScanTile;
+                    trange.push_back(make_int2(a0, (int)std::min<int64_t>(a0 + kScanTile, lfo[1][f + 1])));
+                }
             }
+            if ((size_t)T.maxFrameTiles * sizeof(double) > 200 * 1024)
+                throw Err(FBS_ELIMIT, "frame too large for the shared-memory tile scan of the hierarchy");
             T.nTiles1 = tfo[F];
             T.tileFrameOff = dalloc<int>(A, F + 1, s);
             T.tileFrame = dalloc<int>(A, std::max<size_t>(tframe.size(), 1), s);
+            T.tileRange = dalloc<int2>(A, std::max<size_t>(trange.size(), 1), s);
+            if (!trange.empty())
+                ck(cudaMemcpyAsync(T.tileRange, trange.data(), trange.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
+                   "h2d");
             ck(cudaMemcpyAsync(T.tileFrameOff, tfo.data(), (F + 1) * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
             if (!tframe.empty())
                 ck(cudaMemcpyAsync(T.tileFrame, tframe.data(), tframe.size() * sizeof(int), cudaMemcpyHostToDevice, s),
@@ -448,6 +460,7 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.parent0T = T.parent0T;
     h.tileFrameOff = T.tileFrameOff;
     h.tileFrame = T.tileFrame;
+    h.tileRange = T.tileRange;
     h.nTiles1 = T.nTiles1;
     h.M0 = g->M;
     h.M1 = g->lv[1].M;
@@ -455,8 +468,6 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.buf1T = S->buf1T;
     h.locT = S->locT;
     h.tileAgg = S->tileAgg;
-    h.tileBase = S->tileBase;
-    h.rhoTile = S->rhoTile;
     h.acc1T = S->acc1T;
     h.partial2 = S->partial2;
     h.counters = S->counters;
@@ -482,7 +493,10 @@ template <int MODE>
 void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, cudaStream_t s) {
     static const std::string name = std::string("k_tree_coarse<") + mode_name(MODE) + ">";
     auto kern = k_tree_coarse<MODE>;
-    LAUNCH_AS(name.c_str(), kern, S->g->F * S->bpf2, 256, 0, s, h, a, first);
+    const size_t sm = (size_t)S->g->tree.maxFrameTiles * sizeof(double);
+    if (sm > 48 * 1024)
+        ck(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "smem attr");
+    LAUNCH_AS(name.c_str(), kern, S->g->F * S->bpf2, 256, sm, s, h, a, first);
 }
 
 // level-0 output (k_tree_level0)
@@ -668,10 +682,8 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             S->w0 = dalloc<float>(A, (size_t)C * M, s);
             S->buf1T = dalloc<float>(A, (size_t)C * M1, s);
             S->acc1T = dalloc<float>(A, (size_t)C * M1, s);
-            S->rhoTile = dalloc<double>(A, (size_t)C * nT, s);
             S->locT = dalloc<double>(A, (size_t)C * M1, s);
             S->tileAgg = dalloc<double>(A, (size_t)C * nT, s);
-            S->tileBase = dalloc<double>(A, (size_t)C * nT, s);
             const int64_t want2 = ((g->L > 2 ? g->maxFrameM2 : g->maxFrameM1) + 255) / 256;
             const int64_t cap2 = std::max<int64_t>(1, ((int64_t)g_num_sms * 8 + F - 1) / F);
             S->bpf2 = (int)std::max<int64_t>(1, std::min(want2, cap2));

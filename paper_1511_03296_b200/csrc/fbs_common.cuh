@@ -228,6 +228,7 @@ struct HierArgs {
     const int* parent0T;    // [M0] tree position of the level-1 parent of level-0 vertex v
     const int* tileFrameOff;  // [F+1] first scan tile of each frame
     const int* tileFrame;     // [nTiles1] frame of each scan tile
+    const int2* tileRange;    // [nTiles1] tree positions [i0, i1) of each scan tile
     int nTiles1;
     int64_t M0, M1;
     // per use (system buffers)
@@ -235,10 +236,8 @@ struct HierArgs {
     float* buf1T;           // [C][M1] (P y)_1 in tree order
     double* locT;           // [C][M1] inclusive prefix within the scan tile
     double* tileAgg;        // [C][nTiles1] tile totals
-    double* tileBase;       // [C][nTiles1] exclusive prefix of the tile totals within the frame
-    double* rhoTile;        // [C][nTiles1] ρ_1 partials per scan tile
     float* acc1T;           // [C][M1] projection of levels ≥ 1 onto level 1, tree order
-    double* partial2;       // [F][bpf2][C] ρ partials of levels ≥ 2
+    double* partial2;       // [F][bpf2][C] ρ partials of levels ≥ 1
     unsigned* counters;     // [F] last-block counters (shared with VecArgs; kernels are serial)
     int bpf2;               // blocks per frame of k_tree_coarse
 };
@@ -251,6 +250,8 @@ struct TreeOrder {
     int* parent0T = nullptr;
     int* tileFrameOff = nullptr;
     int* tileFrame = nullptr;
+    int2* tileRange = nullptr;
+    int maxFrameTiles = 0;
     int nTiles1 = 0;
     int2* rng[kMaxLevels] = {};
 };
@@ -317,8 +318,6 @@ struct fbs_system_s {
     float* buf1T = nullptr;                // [C][M1] hierarchy work arrays (tree_kernels.cuh)
     double* locT = nullptr;
     double* tileAgg = nullptr;
-    double* tileBase = nullptr;
-    double* rhoTile = nullptr;
     float* acc1T = nullptr;
     double* partial2 = nullptr;
     int bpf2 = 1;

@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
 // positions [32w, 32w + 32): the children of its 32 level-1 vertices are one contiguous range of
 // level-0 tree positions, staged (coalesced index load + gather) in shared memory and summed by
 // each lane over its own children in canonical child order.  Then a fixed-tree fp64 block scan
-// gives the within-tile inclusive prefix; the last tile of the frame scans the tile totals.
+// gives the within-tile inclusive prefix and the tile total; the coarse pass scans the frame's
+// tile totals in shared memory (no inter-block signalling here).
 constexpr int kLiftStage = 256;
 
 // INIT multiplier z_w(k)/P(1)_k; 0 above the frame's top level (reading #8)
@@ -210,18 +211,14 @@ __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*
     return sh[w] + incl;
 }
 
-// PCG: also the ρ terms of level 1, μ_1 (P w)²_1 (tile partials); PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
+// PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
 template <int MODE>
 __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0) {
     __shared__ float stage[kScanTile / 32][kLiftStage];
     __shared__ double shs[32];
-    __shared__ int sflag;
     const int t = blockIdx.x;
-    const int f = h.tileFrame[t];
-    const int F1 = h.F + 1;
-    const int fb = h.lvFrameOff[F1 + f], fe = h.lvFrameOff[F1 + f + 1];
-    const int i0 = fb + (t - h.tileFrameOff[f]) * kScanTile;
-    const int i1 = min(i0 + kScanTile, fe);
+    const int2 tr = h.tileRange[t];  // tree positions [i0, i1) of this tile (one frame)
+    const int i0 = tr.x, i1 = tr.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i = i0 + (int)threadIdx.x;
     const bool valid = i < i1;
@@ -233,11 +230,16 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
         float acc = 0.f;
         for (int qc = qa; qc < qb; qc += kLiftStage) {
             const int n = min(kLiftStage, qb - qc);
+            constexpr int E = kLiftStage / 32;
+            int id[E];
+            float val[E];
 #pragma unroll
-            for (int e = 0; e < kLiftStage / 32; ++e) {
-                const int q = lane + 32 * e;
-                if (q < n) stage[w][q] = src[h.tord0[qc + q]];
-            }
+            for (int e = 0; e < E; ++e) id[e] = (lane + 32 * e < n) ? __ldg(h.tord0 + qc + lane + 32 * e) : -1;
+#pragma unroll
+            for (int e = 0; e < E; ++e) val[e] = (id[e] >= 0) ? src[id[e]] : 0.f;
+#pragma unroll
+            for (int e = 0; e < E; ++e)
+                if (lane + 32 * e < n) stage[w][lane + 32 * e] = val[e];
             __syncwarp();
             const int lo = max(myLo, qc), hi = min(myHi, qc + n);
             for (int q = lo; q < hi; ++q) acc += stage[w][q - qc];
@@ -245,60 +247,52 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
         }
         if (valid) h.buf1T[(size_t)c * h.M1 + i] = acc;
         if (MODE == HIER_PDA && valid)
-            h.mu1T[i] = (1 < h.frameLevels[f] && acc > 0.f) ? zw_count(h.alpha, h.beta, 1, myHi - myLo, (double)acc) : 0.f;
-        if (MODE == HIER_PCG) {
-            const float m1 = valid ? h.mu1T[i] : 0.f;
-            double r1 = (double)m1 * (double)acc * (double)acc;
-            r1 = block_sum(r1, shs);
-            if (threadIdx.x == 0) h.rhoTile[(size_t)c * h.nTiles1 + t] = r1;
-        }
+            h.mu1T[i] = (1 < h.frameLevels[h.tileFrame[t]] && acc > 0.f)
+                            ? zw_count(h.alpha, h.beta, 1, myHi - myLo, (double)acc) : 0.f;
         double tot;
         const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
         if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
         if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + t] = tot;
         __syncthreads();
     }
-    // last tile of the frame: exclusive prefix of the frame's tile totals (fixed order)
-    const int nt = h.tileFrameOff[f + 1] - h.tileFrameOff[f];
-    if (last_block_of_frame(h.counters + f, nt, &sflag) && w == 0) {
-        for (int c = 0; c < h.C; ++c) {
-            const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + h.tileFrameOff[f];
-            double* base = h.tileBase + (size_t)c * h.nTiles1 + h.tileFrameOff[f];
-            double carry = 0.0;
-            for (int b = 0; b < nt; b += 32) {
-                const double x = (b + lane < nt) ? __ldcg(agg + b + lane) : 0.0;
-                double incl = x;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const double y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                if (b + lane < nt) base[b + lane] = carry + incl - x;
-                carry += __shfl_sync(0xffffffffu, incl, 31);
-            }
-        }
-    }
 }
 
 // ================================================================ coarse values and their projection onto level 2
-// Π(j) = fp64 inclusive prefix of tree-ordered (P y)_1 of frame f up to position j
-__device__ __forceinline__ double tree_prefix(const HierArgs& h, int c, int f, int fb, int j) {
+// Π(j) = fp64 inclusive prefix of tree-ordered (P y)_1 of frame f up to position j; tb = the
+// frame's exclusive tile prefixes (shared memory)
+__device__ __forceinline__ double tree_prefix(const HierArgs& h, const double* tb, int c, int fb, int j) {
     if (j < fb) return 0.0;
-    const int t = h.tileFrameOff[f] + (j - fb) / kScanTile;
-    return __ldg(h.tileBase + (size_t)c * h.nTiles1 + t) + __ldg(h.locT + (size_t)c * h.M1 + j);
+    return tb[(j - fb) / kScanTile] + __ldg(h.locT + (size_t)c * h.M1 + j);
+}
+
+// exclusive prefix of frame f's tile totals of channel c into shared memory (fixed order)
+__device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int f, double* tb, double* sh) {
+    const int t0 = h.tileFrameOff[f], nt = h.tileFrameOff[f + 1] - t0;
+    const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + t0;
+    double carry = 0.0;
+    for (int b = 0; b < nt; b += blockDim.x) {
+        const int tt = b + threadIdx.x;
+        const double x = (tt < nt) ? agg[tt] : 0.0;
+        double tot;
+        const double incl = block_incl_scan_d(x, sh, &tot);
+        if (tt < nt) tb[tt] = carry + incl - x;
+        carry += tot;
+    }
+    __syncthreads();
 }
 
 // One thread per level-2 vertex a (blocks per frame: h.bpf2), walking its ancestor chain, then
 // writing acc1 for its children (L = 2: one thread per level-1 position, acc2 = 0):
-//   PCG/PLAIN: acc2_a = Σ_{k≥2} μ_k (P w)_anc;  PCG also ρ_{≥2} = Σ μ (P w)² (each coarse vertex
-//              counted once, by its first level-2 descendant) and, in the last block of the
-//              frame, the ρ finish (with the ρ_0, ‖r‖² partials of k_hier_level0 and the ρ_1 tile
-//              partials of k_tree_lift): β and the stopping rule (Alg. 2 lines 11-13).
+//   PCG/PLAIN: acc2_a = Σ_{k≥2} μ_k (P w)_anc;  PCG also ρ_{≥1} = Σ μ (P w)² (each coarse vertex
+//              counted once, by its first level-2 descendant; level 1 by its parent) and, in the
+//              last block of the frame, the ρ finish (with the ρ_0, ‖r‖² partials of
+//              k_hier_level0): β and the stopping rule (Alg. 2 lines 11-13).
 //   INIT:      mult_k = z_w(k)/P(1)_k.
 //   PDA:       μ_k = z_w(k; α, β) P(1)_k / P(diag A)_k, 0 where the
 //              denominator is 0 (reading #10) or above the frame's top level.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
+    extern __shared__ double tb[];  // [tiles of the frame]
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / h.bpf2, j = blockIdx.x % h.bpf2;
@@ -314,6 +308,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
         const bool act = (MODE != HIER_PCG) || first || a.sc_.active[fk];
         double rho = 0.0;
         if (act) {
+            tile_bases(h, c, f, tb, shd);
             for (int v = a0 + j * blockDim.x + threadIdx.x; v < a1; v += stride) {
                 // level-1 children of v: one contiguous tree range (L = 2: v itself)
                 const int2 kids = (lv == 2) ? h.lv[2].rng[v] : make_int2(v, 1);
@@ -324,7 +319,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                     const HLevel& L = h.lv[k];
                     const int2 rg = L.rng[an];
                     const int nxt = (k < top) ? L.parent[an] : -1;
-                    const double S = tree_prefix(h, c, f, fb, rg.x + rg.y - 1) - tree_prefix(h, c, f, fb, rg.x - 1);
+                    const double S = tree_prefix(h, tb, c, fb, rg.x + rg.y - 1) - tree_prefix(h, tb, c, fb, rg.x - 1);
                     if (MODE == HIER_PDA) {
                         if (rg.x == first1)
                             const_cast<float*>(L.mu)[an] =
@@ -337,10 +332,26 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                     an = nxt;
                 }
                 if (MODE != HIER_PDA) {
-                    for (int i = kids.x; i < kids.x + kids.y; ++i) {
-                        const float m1 =
-                            (MODE == HIER_INIT) ? init_mult1(h, 1, fl, h.csT[i + 1] - h.csT[i]) : h.mu1T[i];
-                        h.acc1T[(size_t)c * h.M1 + i] = m1 * h.buf1T[(size_t)c * h.M1 + i] + acc;
+                    // acc1 for the children (+ PCG: their ρ_1 terms μ_1 (P w)²_1), 4 loads in flight
+                    const float* b1 = h.buf1T + (size_t)c * h.M1;
+                    for (int ib = kids.x; ib < kids.x + kids.y; ib += 4) {
+                        float m1[4], bv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = ib + u;
+                            if (i < kids.x + kids.y) {
+                                m1[u] = (MODE == HIER_INIT) ? init_mult1(h, 1, fl, h.csT[i + 1] - h.csT[i]) : h.mu1T[i];
+                                bv[u] = b1[i];
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = ib + u;
+                            if (i < kids.x + kids.y) {
+                                h.acc1T[(size_t)c * h.M1 + i] = m1[u] * bv[u] + acc;
+                                if (MODE == HIER_PCG) rho += (double)m1[u] * (double)bv[u] * (double)bv[u];
+                            }
+                        }
                     }
                 }
             }
@@ -351,7 +362,6 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
         }
     }
     if (MODE == HIER_PCG && last_block_of_frame(h.counters + f, h.bpf2, &sflag)) {
-        const int t0 = h.tileFrameOff[f], t1 = h.tileFrameOff[f + 1];
         for (int c = 0; c < a.K; ++c) {
             const int fk = f * a.K + c;
             if (!first && !a.sc_.active[fk]) continue;
@@ -361,7 +371,6 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                 R += __ldcg(pp);
                 RR += __ldcg(pp + 1);
             }
-            for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) R += __ldcg(h.rhoTile + (size_t)c * h.nTiles1 + t);
             for (int jj = threadIdx.x; jj < h.bpf2; jj += blockDim.x)
                 R += __ldcg(h.partial2 + ((size_t)f * h.bpf2 + jj) * h.C + c);
             R = block_sum(R, shd);

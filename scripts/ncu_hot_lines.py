@@ -3,9 +3,11 @@
 import csv, subprocess, sys
 
 
-def hot(path, n=25):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                         capture_output=True, text=True).stdout
+def hot(path, n=25, kernel=None):
+    cmd = ["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if kernel:
+        cmd += ["--kernel-name", "regex:" + kernel]
+    raw = subprocess.run(cmd, capture_output=True, text=True).stdout
     fname, cur = "", ""
     by_line, by_inst, total = {}, [], 0.0
     for r in csv.reader(raw.splitlines()):
@@ -46,6 +48,8 @@ def hot(path, n=25):
 
 
 if __name__ == "__main__":
-    for p in sys.argv[1:]:
-        print("==", p)
-        hot(p)
+    # ncu_hot_lines.py REPORT [KERNEL_REGEX ...]
+    path, kernels = sys.argv[1], sys.argv[2:] or [None]
+    for k in kernels:
+        print("==", path, k or "")
+        hot(path, n=12, kernel=k)
