@@ -360,6 +360,19 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
                        km1 >= 2 ? T.rng[km1] : nullptr, T.tord0, T.tord1, T.csT);
             }
             LAUNCH(k_tree_finish, grid_for(M), kThreads, 0, s, g->lv[1].parent, start[1], M, M1, T.parent0T, T.csT);
+            if (top >= 3) {  // ancestor tables of the level-2 vertices
+                const int64_t M2 = g->lv[2].M;
+                T.ancId = dalloc<int>(A, (size_t)(top - 2) * M2, s);
+                T.ancRng = dalloc<int2>(A, (size_t)(top - 2) * M2, s);
+                HierArgs hb{};
+                hb.L = L;
+                for (int k = 2; k < L; ++k) {
+                    hb.lv[k].M = g->lv[k].M;
+                    hb.lv[k].parent = (k + 1 < L) ? g->lv[k + 1].parent : nullptr;
+                    hb.lv[k].rng = T.rng[k];
+                }
+                LAUNCH(k_tree_anc, grid_for(M2), kThreads, 0, s, hb, T.ancId, T.ancRng);
+            }
             // prefix-scan tiles: kScanTile level-1 positions, never crossing a frame
             tfo.assign(F + 1, 0);
             g->maxFrameM1 = 0;
@@ -456,6 +469,9 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.beta = beta;
     const TreeOrder& T = g->tree;
     h.tord0 = T.tord0;
+    h.ancRng = T.ancRng;
+    h.ancMu = S->ancMu;
+    h.M2 = (g->L > 2) ? g->lv[2].M : 0;
     h.csT = T.csT;
     h.parent0T = T.parent0T;
     h.tileFrameOff = T.tileFrameOff;
@@ -688,8 +704,10 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             const int64_t cap2 = std::max<int64_t>(1, ((int64_t)g_num_sms * 8 + F - 1) / F);
             S->bpf2 = (int)std::max<int64_t>(1, std::min(want2, cap2));
             S->partial2 = dalloc<double>(A, (size_t)F * S->bpf2 * C, s);
-            if (hierP)
+            if (hierP) {
                 for (int k = 1; k < g->L; ++k) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
+                if (g->L > 3) S->ancMu = dalloc<float>(A, (size_t)(g->L - 3) * g->lv[2].M, s);
+            }
         }
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * K, s);
         S->counters = dalloc<unsigned>(A, F, s);
@@ -711,6 +729,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             HierArgs h = make_hier(S, 1, o.precond_alpha, o.precond_beta);
             tree_lift<HIER_PDA>(S, h, S->w0, s);
             tree_coarse<HIER_PDA>(S, h, a, 0, s);
+            if (g->L > 3) LAUNCH(k_tree_anc_mu, grid_for(g->lv[2].M), kThreads, 0, s, h, g->tree.ancId, S->ancMu);
         }
         if (hierI) {
             HierArgs h = make_hier(S, K + 1, o.init_alpha, o.init_beta);

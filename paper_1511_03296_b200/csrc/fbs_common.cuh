@@ -224,13 +224,15 @@ struct HierArgs {
     double alpha, beta;     // z_weight parameters of the current use
     // tree order (grid)
     const int* tord0;       // [M0] level-0 vertex at each level-0 tree position
+    const int2* ancRng;     // [top−2][M2] level-1 ranges of the level-k ancestors (k = 3..top) of level-2 vertices
+    const float* ancMu;     // [top−2][M2] their μ_k (per solve)
     const int* csT;         // [M1+1] level-0 tree range of the level-1 vertex at tree position i
     const int* parent0T;    // [M0] tree position of the level-1 parent of level-0 vertex v
     const int* tileFrameOff;  // [F+1] first scan tile of each frame
     const int* tileFrame;     // [nTiles1] frame of each scan tile
     const int2* tileRange;    // [nTiles1] tree positions [i0, i1) of each scan tile
     int nTiles1;
-    int64_t M0, M1;
+    int64_t M0, M1, M2;
     // per use (system buffers)
     float* mu1T;            // [M1] μ_1 in tree order
     float* buf1T;           // [C][M1] (P y)_1 in tree order
@@ -245,6 +247,8 @@ struct HierArgs {
 // tree order of the pyramid (grid build)
 struct TreeOrder {
     int* tord0 = nullptr;
+    int* ancId = nullptr;    // [top−2][M2]
+    int2* ancRng = nullptr;  // [top−2][M2]
     int* csT = nullptr;
     int* tord1 = nullptr;
     int* parent0T = nullptr;
@@ -315,6 +319,7 @@ struct fbs_system_s {
     float* sh = nullptr;
     float* w0 = nullptr;                   // [C][M] level-0 pyramid input (init, μ_k, debug operator)
     float* mu[fbs::kMaxLevels] = {};       // [M_k] precond multipliers (k ≥ 2 canonical; k = 1 tree order)
+    float* ancMu = nullptr;                // [top−2][M2] μ of the level-2 vertices' ancestors
     float* buf1T = nullptr;                // [C][M1] hierarchy work arrays (tree_kernels.cuh)
     double* locT = nullptr;
     double* tileAgg = nullptr;

@@ -81,6 +81,31 @@ __global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __res
     if (t0 == 0) csT[M1] = (int)M0;
 }
 
+// Ancestor tables of the level-2 vertices (k = 3..top, row k−3): ancId = the level-k ancestor,
+// ancRng = its level-1 range.  The PCG coarse pass then reads a whole ancestor chain in one
+// coalesced round instead of top−2 dependent (and, after each iteration's streams, DRAM) loads.
+__global__ void k_tree_anc(HierArgs h, int* __restrict__ ancId, int2* __restrict__ ancRng) {
+    const int top = h.L - 1;
+    const int64_t M2 = h.lv[2].M;
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < M2; a += (int64_t)gridDim.x * blockDim.x) {
+        int an = (int)a;
+        for (int k = 3; k <= top; ++k) {
+            an = h.lv[k - 1].parent[an];
+            ancId[(size_t)(k - 3) * M2 + a] = an;
+            ancRng[(size_t)(k - 3) * M2 + a] = h.lv[k].rng[an];
+        }
+    }
+}
+
+// per solve: ancMu[k−3][a] = μ_k of the level-k ancestor of level-2 vertex a
+__global__ void k_tree_anc_mu(HierArgs h, const int* __restrict__ ancId, float* __restrict__ ancMu) {
+    const int top = h.L - 1;
+    const int64_t M2 = h.lv[2].M;
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < M2; a += (int64_t)gridDim.x * blockDim.x)
+        for (int k = 3; k <= top; ++k)
+            ancMu[(size_t)(k - 3) * M2 + a] = h.lv[k].mu[ancId[(size_t)(k - 3) * M2 + a]];
+}
+
 // ================================================================ level 0 → PCG input
 // w = mask∘r with r from the PCG update (Alg. 2 lines 8-9), the initial residual r = b − A x
 // (lines 2), or r = b (x = 0, backward); partials ρ_0 = Σ μ0 w² and ‖r‖².  FINISH_LAST: the
@@ -315,6 +340,38 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                 const int first1 = kids.x;
                 float acc = 0.f;
                 int an = (lv == 2) ? v : -1;
+                if ((MODE == HIER_PCG || MODE == HIER_PLAIN) && lv == 2) {
+                    // v itself, then its ancestors from the tables, four per load round
+                    {
+                        const double S = tree_prefix(h, tb, c, fb, kids.x + kids.y - 1) - tree_prefix(h, tb, c, fb, kids.x - 1);
+                        const float m = h.lv[2].mu[v];
+                        acc = m * (float)S;
+                        if (MODE == HIER_PCG) rho += (double)m * S * S;
+                    }
+                    for (int kb = 3; kb <= top; kb += 4) {
+                        int2 r[4];
+                        float m[4];
+                        double S[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (kb + u > top) continue;
+                            const size_t o = (size_t)(kb + u - 3) * h.M2 + v;
+                            r[u] = __ldg(h.ancRng + o);
+                            m[u] = __ldg(h.ancMu + o);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (kb + u <= top)
+                                S[u] = tree_prefix(h, tb, c, fb, r[u].x + r[u].y - 1) - tree_prefix(h, tb, c, fb, r[u].x - 1);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            if (kb + u > top) continue;
+                            acc += m[u] * (float)S[u];
+                            if (MODE == HIER_PCG && r[u].x == first1) rho += (double)m[u] * S[u] * S[u];
+                        }
+                    }
+                    an = -1;
+                }
                 for (int k = 2; k <= top && an >= 0; ++k) {
                     const HLevel& L = h.lv[k];
                     const int2 rg = L.rng[an];
