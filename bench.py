@@ -48,7 +48,8 @@ def kernel_bytes(name, M, lv, N):
         "k_update": 36 * M,            # x rw 8 + r rw 8 + (d,n) 8 + q 4 + mu0 4 + s write 4
         "k_direction2": 20 * M,        # s 4 + (d,n) read 8 + (d,n) write 8
         "k_bistoch": 28 * M,           # nbr 16 + m 4 + n 4 + n write 4
-        "k_grid_cells": 7 * N + 12 * M,  # rgb 3 + vid 4 per px; key 8 + m 4 per vertex
+        "k_grid_sort": 4 * N,          # rgb 3 + perm 1 per px (+ 12 B per cell)
+        "k_grid_write": 8 * N + 12 * M,  # perm 1 + rgb 3 (heads) + vid 4 per px; key 8 + m 4 per vertex
         "k_grid_neighbours": 24 * M,   # keys 8 + nbr write 16
         "k_splat<true>": 12 * N + 8 * M,  # vid 4 + c 4 + t 4 per px; Sc, b per vertex
         "k_slice": 8 * N,              # vid 4 + x 4 per px
@@ -296,18 +297,31 @@ def main():
         b = kernel_bytes(k, M, lv, w.pixels)
         if b is not None:
             v["algorithmic_GBps"] = b / (v["avg_us"] * 1e-6) / 1e9
-    stages = {
-        "grid_build": ["k_axis_bins", "k_grid_cells", "k_frame_offsets", "k_grid_neighbours"],
-        "bistochastize": ["k_bistoch", "k_bistoch_residual"],
-        "pyramid": ["k_pyr_level", "k_lift_count", "k_tree_top", "k_tree_down", "k_tree_finish"],
-        "splat_assemble_init": ["k_splat<true>", "k_assemble", "k_fill_init_w0", "k_tree_lift<PDA>", "k_tree_coarse<PDA>",
-                                "k_tree_lift<INIT>", "k_tree_coarse<INIT>", "k_tree_level0<INIT>", "k_init_dn"],
-        "pcg": ["k_spmv2", "k_update", "k_direction2", "k1", "k2", "k_init_scalars", "k_hier_level0<UPDATE>",
-                "k_hier_level0<UPDATE,LAST>", "k_hier_level0<RESID>", "k_hier_level0<RESID0>", "k_tree_lift<PCG>",
-                "k_tree_coarse<PCG>", "k_tree_level0<PCG>"],
-        "slice": ["k_slice"],
-    }
-    stages_ms = {s: sum(kernels[k]["ms_per_step"] for k in ks if k in kernels) for s, ks in stages.items()}
+    def stage_of(name):
+        for prefix, st in (("k_axis_bins", "grid_build"), ("k_bin_lut", "grid_build"), ("k_grid_", "grid_build"),
+                           ("k_scan_excl", "grid_build"), ("k_frame_offsets", "grid_build"),
+                           ("k_bistoch", "bistochastize"),
+                           ("k_pyr_", "pyramid"), ("k_lift_count", "pyramid"), ("k_tree_top", "pyramid"),
+                           ("k_tree_down", "pyramid"), ("k_tree_finish", "pyramid"),
+                           ("k_tree_anc_mu", "splat_assemble_init"), ("k_tree_anc", "pyramid"),
+                           ("k_splat", "splat_assemble_init"), ("k_assemble", "splat_assemble_init"),
+                           ("k_fill_init_w0", "splat_assemble_init"), ("k_init_dn", "splat_assemble_init"),
+                           ("k_tree_anc_mu", "splat_assemble_init"), ("k_tree_lift<PDA>", "splat_assemble_init"),
+                           ("k_tree_coarse<PDA>", "splat_assemble_init"), ("k_tree_lift<INIT>", "splat_assemble_init"),
+                           ("k_tree_coarse<INIT>", "splat_assemble_init"), ("k_tree_level0<INIT>", "splat_assemble_init"),
+                           ("k_spmv2", "pcg"), ("k_update", "pcg"), ("k_direction2", "pcg"), ("k_residual0", "pcg"),
+                           ("k_init_scalars", "pcg"), ("k_hier_level0", "pcg"), ("k_tree_", "pcg"),
+                           ("k_slice", "slice")):
+            if name.startswith(prefix):
+                return st
+        return "other"
+
+    stages_ms = {}
+    for k, v in kernels.items():
+        st = stage_of(k)
+        stages_ms[st] = stages_ms.get(st, 0.0) + v["ms_per_step"]
+    for st in ("grid_build", "bistochastize", "pyramid", "splat_assemble_init", "pcg", "slice"):
+        stages_ms.setdefault(st, 0.0)
     stages_ms["pcg_per_iteration"] = stages_ms["pcg"] / ITERS
 
     # ---- end to end through the public API with host buffers (H2D + D2H inside the timed region)

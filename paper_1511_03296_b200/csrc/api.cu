@@ -97,9 +97,9 @@ void device_setup(int* dev) {
         int sms = 0;
         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, *dev), "sm count");
         g_num_sms = sms;
-        ck(cudaFuncSetAttribute(k_pyr_level, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        ck(cudaFuncSetAttribute(k_pyr_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kCoarseCap * (int)sizeof(unsigned long long)),
-           "k_pyr_level smem");
+           "k_pyr_sort smem");
         pool_done[*dev] = true;
     }
 }
@@ -180,15 +180,14 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         LAUNCH(k_axis_bins, grid_for(W), kThreads, 0, s, W, sxy, ncx, g->colStart);
         LAUNCH(k_axis_bins, grid_for(H), kThreads, 0, s, H, sxy, ncy, g->rowStart);
 
-        const int64_t ntiles = (g->ncells + kCellsPerBlock - 1) / kCellsPerBlock;
-        const int64_t maxTiles = std::max<int64_t>(ntiles, 1);
-        // scratch: tile counter + look-back state (+ error flag, + residual words)
+        // scratch: scan tile counter + look-back state (+ error flag, + residual words)
+        const int64_t scanTiles = (g->ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems);
         unsigned* counter = dalloc<unsigned>(A, 1, s);
         int* err = dalloc<int>(A, 4, s);
-        unsigned long long* state = dalloc<unsigned long long>(A, maxTiles, s);
+        unsigned long long* state = dalloc<unsigned long long>(A, std::max<int64_t>(scanTiles, 1), s);
         ck(cudaMemsetAsync(counter, 0, sizeof(unsigned), s), "memset");
         ck(cudaMemsetAsync(err, 0, 4 * sizeof(int), s), "memset");
-        ck(cudaMemsetAsync(state, 0, maxTiles * sizeof(unsigned long long), s), "memset");
+        ck(cudaMemsetAsync(state, 0, std::max<int64_t>(scanTiles, 1) * sizeof(unsigned long long), s), "memset");
         g->vid = dalloc<int>(A, N, s);
         uint64_t* keysCap = dalloc<uint64_t>(A, N, s);
         int* mCap = dalloc<int>(A, N, s);
@@ -200,8 +199,14 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         LAUNCH(k_bin_lut, 256, 256, 0, s, 256.0 * sl, lutL);
         LAUNCH(k_bin_lut, 256, 256, 0, s, 256.0 * suv, lutUV);
         g->perm = dalloc<uint8_t>(A, (size_t)g->ncells * kCellMaxPx, s);
-        LAUNCH(k_grid_cells, (unsigned)ntiles, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, counter, state, keysCap,
-               mCap, g->vid, g->cellOff, g->perm, err);
+        int* cellCnt = dalloc<int>(A, g->ncells, s);
+        unsigned long long* heads = dalloc<unsigned long long>(A, g->ncells, s);
+        const int cellBlocks = grid_for(g->ncells * 32, 256, 1 << 20);
+        LAUNCH(k_grid_sort, cellBlocks, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, cellCnt, heads, g->perm, err);
+        LAUNCH(k_scan_excl, (unsigned)std::max<int64_t>(scanTiles, 1), kScanBlock, 0, s, cellCnt, g->ncells, g->cellOff,
+               counter, state);
+        LAUNCH(k_grid_write, cellBlocks, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, g->cellOff, heads, g->perm,
+               keysCap, mCap, g->vid);
         LAUNCH(k_frame_offsets, 1, 288, 0, s, g->cellOff, F, (int64_t)ncx * ncy, g->frameOff);
 
         // ---- sync 1: vertex counts (sizes the vertex arrays and the pyramid capacities)
@@ -255,6 +260,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const int* countK = nullptr;  // level 0: P(1) = 1
         std::vector<int*> lvFrameOffDev(Lmax, nullptr);
         unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
+        int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, s) : nullptr;  // parent rank of each sorted child
         for (int k = 1; k < Lmax; ++k) {
             Level& L = g->lv[k];
             L.ncx = ((ncx - 1) >> k) + 1;
@@ -266,13 +272,17 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             L.childStart = dalloc<int>(A, M + 1, s);
             L.childList = dalloc<int>(A, M, s);
             L.count = dalloc<int>(A, M, s);
-            unsigned long long* st2 = dalloc<unsigned long long>(A, L.ncells, s);
-            unsigned* ctr2 = dalloc<unsigned>(A, 2, s);  // tile counter, scratch bump
-            ck(cudaMemsetAsync(st2, 0, L.ncells * sizeof(unsigned long long), s), "memset");
+            int* cnt2 = dalloc<int>(A, L.ncells, s);
+            const int64_t st2n = std::max<int64_t>(1, (L.ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems));
+            unsigned long long* st2 = dalloc<unsigned long long>(A, st2n, s);
+            unsigned* ctr2 = dalloc<unsigned>(A, 2, s);  // scan tile counter, scratch bump
+            ck(cudaMemsetAsync(st2, 0, st2n * sizeof(unsigned long long), s), "memset");
             ck(cudaMemsetAsync(ctr2, 0, 2 * sizeof(unsigned), s), "memset");
-            LAUNCH(k_pyr_level, (unsigned)L.ncells, 64, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK,
-                   ncxK, ncyK, L.ncx, L.ncy, L.ncells, ctr2, st2, ctr2 + 1, pyrScratch, L.keys, L.parent,
-                   L.childStart, L.childList, L.cellOff);
+            LAUNCH(k_pyr_sort, (unsigned)L.ncells, 64, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK, ncxK,
+                   ncyK, L.ncx, L.ncy, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
+            LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2);
+            LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
+                   L.ncy, L.ncells, L.cellOff, L.childList, pyrRank, L.keys, L.parent, L.childStart);
             // P(1): upper bound M on the level size; the kernel stops at the true size via childStart
             lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
             LAUNCH(k_frame_offsets, 1, 288, 0, s, L.cellOff, F, (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);

@@ -81,36 +81,32 @@ __device__ __forceinline__ void cell_of(const CellGeom& g, int64_t c, int& f, in
 }
 
 // ---------------------------------------------------------------- level-0 grid build
-// One warp per σxy cell (≤ 64 px), 8 cells per block = one look-back tile.
-// Outputs: keys[v], m[v] (= S1), vid[p], cellOff[c] (first vertex of each cell).
-__global__ void __launch_bounds__(256) k_grid_cells(
+// Three passes (count → scan → write), so no pass waits on a serial inter-block chain:
+//   k_grid_sort   one warp per σxy cell (≤ 64 px): 24-bit (l,u,v) codes of the pixels, a
+//                 64-element warp bitonic sort of (code‖pixel), run heads → the cell's unique
+//                 count, its head bitmask and its sorted pixel permutation (1 B/px).
+//   k_scan_excl   exclusive scan of the per-cell counts → cellOff (global canonical vertex ids).
+//   k_grid_write  per cell: vid[p] = cellOff + rank of p's run, keys/m of every run head.
+// Outputs: keys[v], m[v] (= S1), vid[p], cellOff[c] (first vertex of each cell), perm.
+__global__ void __launch_bounds__(256) k_grid_sort(
     const uint8_t* __restrict__ rgb, CellGeom g, const uint8_t* __restrict__ lutL,
-    const uint8_t* __restrict__ lutUV, int64_t ncells, unsigned* __restrict__ tile_counter,
-    unsigned long long* __restrict__ tile_state, uint64_t* __restrict__ keys, int* __restrict__ mcount,
-    int* __restrict__ vid, int* __restrict__ cellOff, uint8_t* __restrict__ perm, int* __restrict__ err) {
-    __shared__ unsigned s_tile;
-    __shared__ unsigned s_cnt[kCellsPerBlock];
-    __shared__ unsigned s_excl;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
+    const uint8_t* __restrict__ lutUV, int64_t ncells, int* __restrict__ cnt,
+    unsigned long long* __restrict__ heads, uint8_t* __restrict__ perm, int* __restrict__ err) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t c = (int64_t)tile * kCellsPerBlock + warp;
-
-    uint32_t a0 = 0xffffffffu, a1 = 0xffffffffu;
-    int f = 0, cy = 0, cx = 0, x0 = 0, y0 = 0, w = 1, npx = 0;
-    if (c < ncells) {
+    for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
+         c += (int64_t)gridDim.x * kCellsPerBlock) {
+        int f, cy, cx;
         cell_of(g, c, f, cy, cx);
-        x0 = g.colStart[cx];
-        y0 = g.rowStart[cy];
-        w = g.colStart[cx + 1] - x0;
+        const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
+        const int w = g.colStart[cx + 1] - x0;
         const int h = g.rowStart[cy + 1] - y0;
-        npx = w * h;
+        int npx = w * h;
         if (npx > kCellMaxPx) {  // host validated σxy ≤ 8; keep the kernel safe anyway
             if (lane == 0) atomicOr(err, 1);
             npx = kCellMaxPx;
         }
         const uint8_t* base = rgb + (size_t)f * g.H * g.W * 3;
+        uint32_t a0 = 0xffffffffu, a1 = 0xffffffffu;
         if (lane < npx) {
             const int px = x0 + lane % w, py = y0 + lane / w;
             a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)lane;
@@ -120,63 +116,109 @@ __global__ void __launch_bounds__(256) k_grid_cells(
             const int px = x0 + i % w, py = y0 + i / w;
             a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)i;
         }
+        warp_bitonic64(a0, a1, lane);
+        // run heads in sorted order (same code ⇒ same vertex)
+        const uint32_t up0 = __shfl_up_sync(0xffffffffu, a0, 1);
+        const uint32_t up1 = __shfl_up_sync(0xffffffffu, a1, 1);
+        const uint32_t last0 = __shfl_sync(0xffffffffu, a0, 31);
+        const uint32_t prev1 = lane ? up1 : last0;
+        const bool v0 = a0 != 0xffffffffu, v1 = a1 != 0xffffffffu;
+        const bool h0 = v0 && (lane == 0 || (up0 >> 6) != (a0 >> 6));
+        const bool h1 = v1 && ((prev1 >> 6) != (a1 >> 6));
+        const unsigned hb0 = __ballot_sync(0xffffffffu, h0);
+        const unsigned hb1 = __ballot_sync(0xffffffffu, h1);
+        if (v0) perm[(size_t)c * kCellMaxPx + lane] = (uint8_t)(a0 & 63u);  // sorted position → local pixel
+        if (v1) perm[(size_t)c * kCellMaxPx + lane + 32] = (uint8_t)(a1 & 63u);
+        if (lane == 0) {
+            cnt[c] = __popc(hb0) + __popc(hb1);
+            heads[c] = (unsigned long long)hb0 | ((unsigned long long)hb1 << 32);
+        }
     }
-    warp_bitonic64(a0, a1, lane);
+}
 
-    // run heads in sorted order (same code ⇒ same vertex)
-    const uint32_t up0 = __shfl_up_sync(0xffffffffu, a0, 1);
-    const uint32_t up1 = __shfl_up_sync(0xffffffffu, a1, 1);
-    const uint32_t last0 = __shfl_sync(0xffffffffu, a0, 31);
-    const uint32_t prev1 = lane ? up1 : last0;
-    const bool v0 = a0 != 0xffffffffu, v1 = a1 != 0xffffffffu;
-    const bool h0 = v0 && (lane == 0 || (up0 >> 6) != (a0 >> 6));
-    const bool h1 = v1 && ((prev1 >> 6) != (a1 >> 6));
-    const unsigned hb0 = __ballot_sync(0xffffffffu, h0);
-    const unsigned hb1 = __ballot_sync(0xffffffffu, h1);
-    const unsigned le = (lane == 31) ? 0xffffffffu : ((2u << lane) - 1u);
-    const int r0 = __popc(hb0 & le) - 1;
-    const int r1 = __popc(hb0) + __popc(hb1 & le) - 1;
-    const unsigned U = (unsigned)(__popc(hb0) + __popc(hb1));
-
-    if (lane == 0) s_cnt[warp] = (c < ncells) ? U : 0u;
+// Exclusive scan of n ints → out[0..n] (out[n] = total), one pass: tiles of kScanBlock·kScanItems
+// values with a warp-parallel decoupled look-back (few tiles ⇒ a short chain).
+constexpr int kScanBlock = 256, kScanItems = 16;
+__global__ void __launch_bounds__(kScanBlock) k_scan_excl(const int* __restrict__ in, int64_t n, int* __restrict__ out,
+                                                        unsigned* __restrict__ tile_counter,
+                                                        unsigned long long* __restrict__ tile_state) {
+    __shared__ unsigned s_tile;
+    __shared__ int s_warp[kScanBlock / 32];
+    __shared__ unsigned s_excl;
+    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
     __syncthreads();
-    if (warp == 0) {
-        unsigned agg = 0;
-        for (int i = 0; i < kCellsPerBlock; ++i) agg += s_cnt[i];
-        const unsigned long long ex = lookback_warp(tile_state, tile, lb_pack(agg, 0u));
+    const unsigned tile = s_tile;
+    const int64_t base = (int64_t)tile * kScanBlock * kScanItems + (int64_t)threadIdx.x * kScanItems;
+    int v[kScanItems];
+    int sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        v[i] = (base + i < n) ? in[base + i] : 0;
+        sum += v[i];
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[w] = incl;
+    __syncthreads();
+    int wex = 0, agg = 0;
+    for (int i = 0; i < kScanBlock / 32; ++i) {
+        if (i < w) wex += s_warp[i];
+        agg += s_warp[i];
+    }
+    if (w == 0) {
+        const unsigned long long ex = lookback_warp(tile_state, tile, lb_pack((unsigned)agg, 0u));
         if (lane == 0) s_excl = lb_first(ex);
     }
     __syncthreads();
-    if (c >= ncells) return;
-    unsigned off = s_excl;
-    for (int i = 0; i < warp; ++i) off += s_cnt[i];
-
-    const unsigned long long H64 = (unsigned long long)hb0 | ((unsigned long long)hb1 << 32);
-    const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)cy << 40) | ((uint64_t)cx << 24);
-    int* vbase = vid + (size_t)f * g.H * g.W;
+    int run = (int)s_excl + wex + incl - sum;
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const uint32_t a = j ? a1 : a0;
-        const bool valid = j ? v1 : v0;
-        const bool head = j ? h1 : h0;
-        const int r = j ? r1 : r0;
-        const int e = lane + 32 * j;
-        if (!valid) continue;
-        const unsigned v = off + (unsigned)r;
-        if (head) {
-            const unsigned long long rest = H64 & ~((2ull << e) - 1ull);
-            const int nxt = rest ? (__ffsll((long long)rest) - 1) : npx;
-            keys[v] = khi | (uint64_t)(a >> 6);
-            mcount[v] = nxt - e;
-        }
-        const int i = (int)(a & 63u);
-        const int px = x0 + i % w, py = y0 + i / w;
-        vbase[(size_t)py * g.W + px] = (int)v;
-        perm[(size_t)c * kCellMaxPx + e] = (uint8_t)i;  // sorted position e → local pixel i (splat order)
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) out[base + i] = run;
+        if (base + i == n - 1) out[n] = run + v[i];
+        run += v[i];
     }
-    if (lane == 0) {
-        cellOff[c] = (int)off;
-        if (c == ncells - 1) cellOff[ncells] = (int)(off + U);
+    if (n == 0 && tile == 0 && threadIdx.x == 0) out[0] = 0;
+}
+
+__global__ void __launch_bounds__(256) k_grid_write(
+    const uint8_t* __restrict__ rgb, CellGeom g, const uint8_t* __restrict__ lutL,
+    const uint8_t* __restrict__ lutUV, int64_t ncells, const int* __restrict__ cellOff,
+    const unsigned long long* __restrict__ heads, const uint8_t* __restrict__ perm, uint64_t* __restrict__ keys,
+    int* __restrict__ mcount, int* __restrict__ vid) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
+         c += (int64_t)gridDim.x * kCellsPerBlock) {
+        int f, cy, cx;
+        cell_of(g, c, f, cy, cx);
+        const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
+        const int w = g.colStart[cx + 1] - x0;
+        const int npx = min(w * (g.rowStart[cy + 1] - y0), kCellMaxPx);
+        const unsigned long long H64 = heads[c];
+        const unsigned off = (unsigned)cellOff[c];
+        const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)cy << 40) | ((uint64_t)cx << 24);
+        const uint8_t* base = rgb + (size_t)f * g.H * g.W * 3;
+        int* vbase = vid + (size_t)f * g.H * g.W;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int e = lane + 32 * j;
+            if (e >= npx) continue;
+            const int i = perm[(size_t)c * kCellMaxPx + e];
+            const int px = x0 + i % w, py = y0 + i / w;
+            const unsigned long long upto = (e == 63) ? ~0ull : ((2ull << e) - 1ull);
+            const unsigned v = off + (unsigned)__popcll(H64 & upto) - 1u;
+            vbase[(size_t)py * g.W + px] = (int)v;
+            if ((H64 >> e) & 1ull) {
+                const unsigned long long rest = H64 & ~upto;
+                const int nxt = rest ? (__ffsll((long long)rest) - 1) : npx;
+                keys[v] = khi | (uint64_t)luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV);
+                mcount[v] = nxt - e;
+            }
+        }
     }
 }
 

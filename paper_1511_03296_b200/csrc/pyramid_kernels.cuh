@@ -2,10 +2,11 @@
 //
 // Level k+1 = unique(⌊V_k / 2⌋) with the frame field kept.  A level-(k+1) vertex lies in the
 // coarse cell (⌊by/2⌋, ⌊bx/2⌋); its children are the level-k vertices of the ≤ 2×2 level-k cells
-// below it, i.e. two contiguous ranges of the canonical level-k order.  One block per coarse
-// cell sorts (halved code, child id) pairs in shared memory, takes unique runs as parents, and a
-// decoupled look-back over coarse cells assigns global parent and child-list offsets — the
-// level is canonical (ascending key) by construction.
+// below it, i.e. two contiguous ranges of the canonical level-k order.  Per level: one block per
+// coarse cell sorts (halved code, child id) pairs and takes unique runs as parents (k_pyr_sort),
+// an exclusive scan of the parent counts gives the global parent offsets (k_scan_excl), and
+// k_pyr_write assigns the canonical parent ids — the level is canonical (ascending key) by
+// construction.
 #pragma once
 #include "fbs_common.cuh"
 
@@ -46,54 +47,60 @@ __device__ __forceinline__ int block_excl_scan(int x, int* sh /*[33]*/, int* tot
     return sh[w] + incl - x;
 }
 
-// One block (T threads) per level-(k+1) coarse cell.  One look-back chain carries the packed
-// (vertex, child) counts.  Cells with more than kCoarseCap children sort in a global scratch
-// slice (rare: dense pixel-noise images at σl = σuv = 1).
-__global__ void __launch_bounds__(64) k_pyr_level(
-    const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK, int ncxK, int ncyK,
-    int ncxN, int ncyN, int64_t ncellsN, unsigned* __restrict__ tile_counter,
-    unsigned long long* __restrict__ stateV, unsigned* __restrict__ bump,
-    unsigned long long* __restrict__ scratch, uint64_t* __restrict__ keysN,
-    int* __restrict__ parentK, int* __restrict__ childStartN, int* __restrict__ childListN,
-    int* __restrict__ cellOffN) {
+// Coarse cell C = (f, CY, CX) of level k+1 covers the level-k cells (2CY..2CY+1, 2CX..2CX+1): its
+// children are two contiguous ranges [s0, s0+n0) (row 2CY) and [s1, s1+n1) (row 2CY+1), and its
+// child-list offset has a closed form — the children of all earlier coarse cells are the level-k
+// vertices of earlier level-k rows plus those left of column 2CX in rows 2CY and 2CY+1.
+struct CoarseCell {
+    int f, CY, CX, s0, n0, s1, n1, cOff;
+};
+__device__ __forceinline__ CoarseCell coarse_cell(int64_t C, const int* __restrict__ cellOffK, int ncxK, int ncyK,
+                                                  int ncxN, int ncyN) {
+    CoarseCell cc{};
+    const int64_t per = (int64_t)ncxN * ncyN;
+    cc.f = (int)(C / per);
+    const int64_t r = C - (int64_t)cc.f * per;
+    cc.CY = (int)(r / ncxN);
+    cc.CX = (int)(r - (int64_t)cc.CY * ncxN);
+    const int cx0 = 2 * cc.CX, cx1 = min(2 * cc.CX + 1, ncxK - 1);
+    const int64_t ck0 = ((int64_t)cc.f * ncyK + 2 * cc.CY) * ncxK;
+    cc.s0 = cellOffK[ck0 + cx0];
+    cc.n0 = cellOffK[ck0 + cx1 + 1] - cc.s0;
+    cc.cOff = cc.s0;
+    if (2 * cc.CY + 1 < ncyK) {
+        const int64_t ck1 = ck0 + ncxK;
+        cc.s1 = cellOffK[ck1 + cx0];
+        cc.n1 = cellOffK[ck1 + cx1 + 1] - cc.s1;
+        cc.cOff += cc.s1 - cellOffK[ck1];
+    }
+    return cc;
+}
+
+// Pass 1: one block (T threads) per coarse cell sorts its (halved code, child id) pairs in shared
+// memory (cells with more than kCoarseCap children in a global scratch slice from a bump
+// allocator; rare: dense pixel-noise images at σl = σuv = 1), writes the children grouped by
+// parent in canonical order to the child list, each sorted position's parent rank (rankS) and
+// the cell's parent count.  Blocks are independent (no inter-block chain).
+__global__ void __launch_bounds__(64) k_pyr_sort(const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK,
+                                                 int ncxK, int ncyK, int ncxN, int ncyN, unsigned* __restrict__ bump,
+                                                 unsigned long long* __restrict__ scratch, int* __restrict__ childListN,
+                                                 int* __restrict__ rankS, int* __restrict__ cnt) {
     extern __shared__ unsigned long long sk_smem[];  // [kCoarseCap]
-    __shared__ unsigned s_tile;
     __shared__ int s_scan[33];
     __shared__ unsigned s_scr;
-    __shared__ unsigned long long s_vexcl;
-    if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
-    __syncthreads();
-    const int64_t C = s_tile;
+    const int64_t C = blockIdx.x;
     const int T = blockDim.x;
-
-    int f = 0, CY = 0, CX = 0, n0 = 0, n1 = 0, s0 = 0, s1 = 0;
-    {
-        const int64_t per = (int64_t)ncxN * ncyN;
-        f = (int)(C / per);
-        const int64_t r = C - (int64_t)f * per;
-        CY = (int)(r / ncxN);
-        CX = (int)(r - (int64_t)CY * ncxN);
-        const int cx0 = 2 * CX, cx1 = min(2 * CX + 1, ncxK - 1);
-        for (int a = 0; a < 2; ++a) {
-            const int cy = 2 * CY + a;
-            if (cy >= ncyK) continue;
-            const int64_t ck = ((int64_t)f * ncyK + cy) * ncxK + cx0;
-            const int st = cellOffK[ck], en = cellOffK[ck + (cx1 - cx0) + 1];
-            if (a == 0) { s0 = st; n0 = en - st; } else { s1 = st; n1 = en - st; }
-        }
-    }
-    const int nch = n0 + n1;
+    const CoarseCell cc = coarse_cell(C, cellOffK, ncxK, ncyK, ncxN, ncyN);
+    const int nch = cc.n0 + cc.n1;
     int P = 1;
     while (P < nch) P <<= 1;
-    // oversize cells sort in a global scratch slice taken from a bump allocator (its position
-    // does not affect the result); Σ P < 2·M bounds the scratch
     if (threadIdx.x == 0) s_scr = (nch > kCoarseCap) ? atomicAdd(bump, (unsigned)P) : 0u;
     __syncthreads();
     unsigned long long* sk = (nch <= kCoarseCap) ? sk_smem : scratch + s_scr;
     for (int i = threadIdx.x; i < P; i += T) {
         unsigned long long key = ~0ull;
         if (i < nch) {
-            const int gch = (i < n0) ? s0 + i : s1 + (i - n0);
+            const int gch = (i < cc.n0) ? cc.s0 + i : cc.s1 + (i - cc.n0);
             key = ((unsigned long long)halve_code((uint32_t)(keysK[gch] & 0xffffffu)) << 32) | (unsigned)gch;
         }
         sk[i] = key;
@@ -101,9 +108,9 @@ __global__ void __launch_bounds__(64) k_pyr_level(
     __syncthreads();
     // bitonic sort of P (power of two) keys
     for (int k = 2; k <= P; k <<= 1) {
-        for (int s = k >> 1; s > 0; s >>= 1) {
+        for (int sd = k >> 1; sd > 0; sd >>= 1) {
             for (int i = threadIdx.x; i < P; i += T) {
-                const int j = i ^ s;
+                const int j = i ^ sd;
                 if (j > i) {
                     const bool asc = (i & k) == 0;
                     const unsigned long long a = sk[i], b = sk[j];
@@ -123,33 +130,41 @@ __global__ void __launch_bounds__(64) k_pyr_level(
     }
     int U;
     const int before = block_excl_scan(myHeads, s_scan, &U);
-    if (threadIdx.x < 32) {
-        const unsigned long long ex = lookback_warp(stateV, (unsigned)C, lb_pack((unsigned)U, (unsigned)nch));
-        if (threadIdx.x == 0) s_vexcl = ex;
-    }
-    __syncthreads();
-    const int vOff = (int)lb_first(s_vexcl), cOff = (int)lb_second(s_vexcl);
-    const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)CY << 40) | ((uint64_t)CX << 24);
     int r = before - 1;
     for (int e = 0; e < E; ++e) {
         const int i = i0 + e;
         if (i >= nch) break;
-        const bool head = (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32));
-        if (head) ++r;
-        const int gch = (int)(sk[i] & 0xffffffffull);
-        parentK[gch] = vOff + r;
-        childListN[cOff + i] = gch;
-        if (head) {
-            keysN[vOff + r] = khi | (sk[i] >> 32);
-            childStartN[vOff + r] = cOff + i;
-        }
+        if (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) ++r;
+        childListN[cc.cOff + i] = (int)(sk[i] & 0xffffffffull);
+        rankS[cc.cOff + i] = r;
     }
-    if (threadIdx.x == 0) {
-        cellOffN[C] = vOff;
-        if (C == ncellsN - 1) {
-            cellOffN[ncellsN] = vOff + U;
-            childStartN[vOff + U] = cOff + nch;
+    if (threadIdx.x == 0) cnt[C] = U;
+}
+
+// Pass 3 (after the exclusive scan of the parent counts → cellOffN): parents get their canonical
+// ids vOff + rank: parent map, parent keys and child-list starts.  One warp per coarse cell.
+__global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK,
+                                                   int ncxK, int ncyK, int ncxN, int ncyN, int64_t ncellsN,
+                                                   const int* __restrict__ cellOffN, const int* __restrict__ childListN,
+                                                   const int* __restrict__ rankS, uint64_t* __restrict__ keysN,
+                                                   int* __restrict__ parentK, int* __restrict__ childStartN) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t C = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; C < ncellsN;
+         C += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const CoarseCell cc = coarse_cell(C, cellOffK, ncxK, ncyK, ncxN, ncyN);
+        const int nch = cc.n0 + cc.n1;
+        const int vOff = cellOffN[C];
+        const uint64_t khi = ((uint64_t)cc.f << 56) | ((uint64_t)cc.CY << 40) | ((uint64_t)cc.CX << 24);
+        for (int i = lane; i < nch; i += 32) {
+            const int gch = childListN[cc.cOff + i];
+            const int r = rankS[cc.cOff + i];
+            parentK[gch] = vOff + r;
+            if (i == 0 || rankS[cc.cOff + i - 1] != r) {
+                keysN[vOff + r] = khi | (uint64_t)halve_code((uint32_t)(keysK[gch] & 0xffffffu));
+                childStartN[vOff + r] = cc.cOff + i;
+            }
         }
+        if (C == ncellsN - 1 && lane == 0) childStartN[cellOffN[ncellsN]] = cc.cOff + nch;
     }
 }
 

@@ -259,5 +259,5 @@ def test_launch_counter_and_profile():
     fbs.profile_enable(False)
     rep = fbs.profile_report()
     assert fbs.launch_count() > n0
-    assert rep["k_spmv2"][0] == 3 and rep["k_direction2"][0] == 3 and rep["k_grid_cells"][0] == 1
+    assert rep["k_spmv2"][0] == 3 and rep["k_direction2"][0] == 3 and rep["k_grid_sort"][0] == 1
     assert sum(v[0] for v in rep.values()) == fbs.launch_count() - n0
