@@ -1,6 +1,8 @@
 // api.cu — C ABI (include/fbs.h) and host orchestration of the sm_100a bilateral solver.
 // Unity build: this translation unit includes every kernel header of csrc/.
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 #include <cmath>
 #include <functional>
 #include <map>
@@ -75,13 +77,37 @@ struct ProfScope {
     }
 };
 
+// Every launch uses programmatic stream serialization (fbs_common.cuh pdl_entry); FBS_NO_PDL=1
+// in the environment turns it off (A/B measurement).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("FBS_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 #define LAUNCH(kernel, grid, block, smem, stream, ...) LAUNCH_AS(#kernel, kernel, grid, block, smem, stream, __VA_ARGS__)
 #define LAUNCH_AS(name, kernel, grid, block, smem, stream, ...)                          \
     do {                                                                                 \
         ::fbs::ProfScope _ps((name), (stream));                                          \
-        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                       \
+        ck(::fbs::launch_pdl(kernel, dim3(grid), dim3(block), (smem), (stream), __VA_ARGS__), #kernel); \
         ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
-        ck(cudaGetLastError(), #kernel);                                                 \
     } while (0)
 
 int g_num_sms = 0;

@@ -26,6 +26,17 @@ constexpr int kScanTile = 256;       // tree-ordered level-1 positions per prefi
 // ------------------------------------------------------------------ launch counter
 extern std::atomic<long long> g_launches;
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every kernel is launched with programmatic stream serialization (api.cu launch_pdl) and starts
+// here: it lets the next kernel of the stream be scheduled once all of this grid's blocks are
+// resident (its blocks then fill SMs as ours retire), and waits until the previous grid has
+// completed and its memory is visible.  Data dependencies stay fully serial; only the launch
+// latency and the ramp between kernels overlap.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ------------------------------------------------------------------ small device helpers
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -14,6 +14,7 @@ namespace fbs {
 // ---------------------------------------------------------------- axis bins (reading #2)
 // start[b] = first coordinate i with ⌊i/σ⌋ = b; start[nb] = len.  σ ≥ 1, so bins are dense.
 __global__ void k_axis_bins(int len, double sigma, int nb, int* __restrict__ start) {
+    pdl_entry();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < len; i += gridDim.x * blockDim.x) {
         const int b = (int)floor((double)i / sigma);
         const int bp = (i == 0) ? -1 : (int)floor((double)(i - 1) / sigma);
@@ -57,6 +58,7 @@ __device__ __forceinline__ void warp_bitonic64(uint32_t& a0, uint32_t& a1, int l
 // each (reading #2), d = 256σ.  Yn, Un, Vn are integers < 65536, so a table lookup reproduces the
 // fp64 division exactly while keeping the per-pixel path free of fp64 divides.
 __global__ void k_bin_lut(double d, uint8_t* __restrict__ lut) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < 65536) lut[i] = (uint8_t)min(255.0, floor((double)i / d));
 }
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256) k_grid_sort(
     const uint8_t* __restrict__ rgb, CellGeom g, const uint8_t* __restrict__ lutL,
     const uint8_t* __restrict__ lutUV, int64_t ncells, int* __restrict__ cnt,
     unsigned long long* __restrict__ heads, uint8_t* __restrict__ perm, int* __restrict__ err) {
+    pdl_entry();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
          c += (int64_t)gridDim.x * kCellsPerBlock) {
@@ -142,6 +145,7 @@ constexpr int kScanBlock = 256, kScanItems = 16;
 __global__ void __launch_bounds__(kScanBlock) k_scan_excl(const int* __restrict__ in, int64_t n, int* __restrict__ out,
                                                         unsigned* __restrict__ tile_counter,
                                                         unsigned long long* __restrict__ tile_state) {
+    pdl_entry();
     __shared__ unsigned s_tile;
     __shared__ int s_warp[kScanBlock / 32];
     __shared__ unsigned s_excl;
@@ -190,6 +194,7 @@ __global__ void __launch_bounds__(256) k_grid_write(
     const uint8_t* __restrict__ lutUV, int64_t ncells, const int* __restrict__ cellOff,
     const unsigned long long* __restrict__ heads, const uint8_t* __restrict__ perm, uint64_t* __restrict__ keys,
     int* __restrict__ mcount, int* __restrict__ vid) {
+    pdl_entry();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
          c += (int64_t)gridDim.x * kCellsPerBlock) {
@@ -237,6 +242,7 @@ __device__ __forceinline__ int lower_bound_s(const uint32_t* a, int n, uint32_t 
 __global__ void __launch_bounds__(256) k_grid_neighbours(
     const uint64_t* __restrict__ keys, const int* __restrict__ cellOff, int ncx, int ncy,
     int64_t ncells, int4* __restrict__ nbr, int* __restrict__ err) {
+    pdl_entry();
     __shared__ uint32_t sc[kCellsPerBlock][5][kCellMaxPx];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
@@ -297,6 +303,7 @@ __global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
                                                  float* __restrict__ nout, int M, int first) {
+    pdl_entry();
     const int stride = gridDim.x * blockDim.x;
 #pragma unroll 2
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += stride) {
@@ -321,6 +328,7 @@ __global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
 __global__ void k_bistoch_residual(const int4* __restrict__ nbr,
                                    const int* __restrict__ m, const float* __restrict__ n, int M,
                                    unsigned* __restrict__ out2) {
+    pdl_entry();
     float e = 0.f, mm = 0.f;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
         const float bn = (float)kBbarDiag * n[v] + nbr_sum(n, v, nbr[v]);
@@ -340,6 +348,7 @@ __global__ void k_bistoch_residual(const int4* __restrict__ nbr,
 // ---------------------------------------------------------------- exports
 __global__ void k_export_nbr(const int4* __restrict__ nbr, int M,
                              int* __restrict__ nbr10) {
+    pdl_entry();
     // export slot order (x−,x+,y−,y+,l−,l+,u−,u+,v−,v+); internal near order (x−,x+,l−,l+,u−,u+,v−,v+)
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
         const int4 q4 = nbr[v];

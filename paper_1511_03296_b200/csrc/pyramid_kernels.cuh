@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(64) k_pyr_sort(const uint64_t* __restrict__ ke
                                                  int ncxK, int ncyK, int ncxN, int ncyN, unsigned* __restrict__ bump,
                                                  unsigned long long* __restrict__ scratch, int* __restrict__ childListN,
                                                  int* __restrict__ rankS, int* __restrict__ cnt) {
+    pdl_entry();
     extern __shared__ unsigned long long sk_smem[];  // [kCoarseCap]
     __shared__ int s_scan[33];
     __shared__ unsigned s_scr;
@@ -148,6 +149,7 @@ __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ 
                                                    const int* __restrict__ cellOffN, const int* __restrict__ childListN,
                                                    const int* __restrict__ rankS, uint64_t* __restrict__ keysN,
                                                    int* __restrict__ parentK, int* __restrict__ childStartN) {
+    pdl_entry();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t C = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; C < ncellsN;
          C += (int64_t)gridDim.x * (blockDim.x >> 5)) {
@@ -171,6 +173,7 @@ __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ 
 // P(1) at level k+1 from level k (segment sums over the child lists; integers, exact).
 __global__ void k_lift_count(const int* __restrict__ countK, const int* __restrict__ childStart,
                              const int* __restrict__ childList, int Mn, int* __restrict__ countN) {
+    pdl_entry();
     for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < Mn; p += gridDim.x * blockDim.x) {
         int s = 0;
         for (int j = childStart[p]; j < childStart[p + 1]; ++j) s += countK ? countK[childList[j]] : 1;
@@ -181,6 +184,7 @@ __global__ void k_lift_count(const int* __restrict__ countK, const int* __restri
 // frame offsets of a level from its cell offsets: frameOff[f] = cellOff[f * ncx * ncy]
 __global__ void k_frame_offsets(const int* __restrict__ cellOff, int F, int64_t cellsPerFrame,
                                 int* __restrict__ frameOff) {
+    pdl_entry();
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f <= F) frameOff[f] = cellOff[(int64_t)f * cellsPerFrame];
 }

@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
                                                const int* __restrict__ vid, const uint8_t* __restrict__ perm,
                                                const float* __restrict__ c, const float* __restrict__ p, int K,
                                                int64_t M, float* __restrict__ sc_out, float* __restrict__ out) {
+    pdl_entry();
     __shared__ double acc[kCellsPerBlock][kCellMaxPx];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ncells = (int64_t)g.F * g.ncx * g.ncy;
@@ -206,6 +207,7 @@ __device__ __forceinline__ void write_partials(const VecArgs& a, int f, int j, i
 // flat init y_flat = b/Sc (reading #9) or zero init.  Per-frame blocks.
 __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__ diagA, float* __restrict__ mu0,
                                                   float* __restrict__ w0diag, int init_mode, PcgScalars scal) {
+    pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
 // ---------------------------------------------------------------- hierarchical init input [b_0..b_{K−1}, Sc]
 __global__ void k_fill_init_w0(const float* __restrict__ b, const float* __restrict__ sc, int64_t M, int K,
                                float* __restrict__ w0) {
+    pdl_entry();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
         for (int k = 0; k < K; ++k) w0[(size_t)k * M + v] = b[(size_t)k * M + v];
         w0[(size_t)K * M + v] = sc[v];
@@ -254,6 +257,7 @@ __global__ void k_fill_init_w0(const float* __restrict__ b, const float* __restr
 
 // ---------------------------------------------------------------- PCG (Alg. 2)
 __global__ void k_init_scalars(PcgScalars s, int FK) {
+    pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < FK) {
         s.rho[i] = 0.0;
@@ -271,6 +275,7 @@ __global__ void k_init_scalars(PcgScalars s, int FK) {
 // The hierarchical preconditioner has its own fused kernels (tile_kernels.cuh).
 template <bool X_ZERO>
 __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
+    pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
 
 // Alg. 2 lines 8-12 (Jacobi):  x += αd;  r −= αq;  s = M⁻¹r = r/diag(A);  ρ_new = rᵀs.
 __global__ void __launch_bounds__(256) k_update(VecArgs a) {
+    pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
@@ -342,12 +348,14 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
 // dn[k][v] = (d, n_v): the direction interleaved with n, so the SpMV's neighbour terms
 // n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
 __global__ void k_init_dn(float2* __restrict__ dn, const float* __restrict__ n, int64_t M, int K) {
+    pdl_entry();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x)
         dn[i] = make_float2(0.f, n[i % M]);
 }
 
 // Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
 __global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
+    pdl_entry();
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
     const int stride = a.BPF * blockDim.x;
@@ -378,6 +386,7 @@ __global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
 
 // Alg. 2 lines 6-7:  q = A d (Laplacian-difference form), α = ρ / dᵀq (breakdown: dᵀq ≤ 0).
 __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
+    pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
@@ -442,6 +451,7 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
 // x̂ = Sᵀŷ.  ys planar [K][M] (planar = 1) or canonical [M][K].
 __global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ ys, int64_t M, int K, int F,
                         int64_t HW, int planar, float* __restrict__ out) {
+    pdl_entry();
     const int64_t N = (int64_t)F * HW;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
         const int v = vid[p];
@@ -456,6 +466,7 @@ __global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ y
 
 // planar [K][M] → canonical [M][K]
 __global__ void k_export_vk(const float* __restrict__ src, int64_t M, int K, float* __restrict__ dst) {
+    pdl_entry();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / K;
         const int k = (int)(i - v * K);
@@ -466,6 +477,7 @@ __global__ void k_export_vk(const float* __restrict__ src, int64_t M, int K, flo
 // canonical [M][K] → planar [K][M], optionally masked to live vertices (mu0 > 0)
 __global__ void k_import_vk(const float* __restrict__ src, const float* __restrict__ mask, int64_t M, int K,
                             float* __restrict__ dst) {
+    pdl_entry();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / K;
         const int k = (int)(i - v * K);
@@ -478,6 +490,7 @@ __global__ void k_import_vk(const float* __restrict__ src, const float* __restri
 __global__ void k_bwd_finalize(const int* __restrict__ vid, const float* __restrict__ db,
                                const float* __restrict__ y, const float* __restrict__ c, const float* __restrict__ t,
                                int64_t M, int K, int F, int64_t HW, float* __restrict__ dt, float* __restrict__ dc) {
+    pdl_entry();
     const int64_t N = (int64_t)F * HW;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
         const int v = vid[p];
@@ -499,12 +512,14 @@ __global__ void k_bwd_finalize(const int* __restrict__ vid, const float* __restr
 // B̄ v (reading #4), debug / parity operator.
 __global__ void k_blur(const int4* __restrict__ nbr, const float* __restrict__ x,
                        int64_t M, float* __restrict__ out) {
+    pdl_entry();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x)
         out[v] = (float)kBbarDiag * x[v] + nbr_sum(x, (int)v, nbr[v]);
 }
 
 // A y for planar y, written canonical [M][K] (debug / parity operator).
 __global__ void k_apply_A(VecArgs a, const float* __restrict__ ys, float* __restrict__ out) {
+    pdl_entry();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.M; v += (int64_t)gridDim.x * blockDim.x)
         for (int k = 0; k < a.K; ++k)
             out[(size_t)v * a.K + k] =
@@ -515,6 +530,7 @@ __global__ void k_apply_A(VecArgs a, const float* __restrict__ ys, float* __rest
 __global__ void k_precond_out(const float* __restrict__ w0, const float* __restrict__ mu0,
                               const int* __restrict__ parent0, const float* __restrict__ acc1, int64_t M1,
                               int64_t M, int K, float* __restrict__ out) {
+    pdl_entry();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
         for (int k = 0; k < K; ++k) {
             float s = 0.f;

@@ -31,6 +31,7 @@ enum { HSRC_UPDATE = 0, HSRC_RESID = 1, HSRC_RESID0 = 2 };
 // (top ≥ 2: also its level-1 range)
 __global__ void k_tree_top(const int* __restrict__ lvFrameOff, int F, int top, int2* __restrict__ startTop,
                            int2* __restrict__ rngTop, const int* __restrict__ cnt1Top) {
+    pdl_entry();
     for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < F; f += gridDim.x * blockDim.x) {
         const int F1 = F + 1;
         const int a = lvFrameOff[top * F1 + f];
@@ -49,6 +50,7 @@ __global__ void k_tree_down(int km1, const int* __restrict__ childStart, const i
                             const int2* __restrict__ startK, const int* __restrict__ cnt0, const int* __restrict__ cnt1,
                             int2* __restrict__ startKm1, int2* __restrict__ rngKm1, int* __restrict__ tord0,
                             int* __restrict__ tord1, int* __restrict__ csT) {
+    pdl_entry();
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < Mk; a += gridDim.x * blockDim.x) {
         int2 r = startK[a];
         for (int q = childStart[a]; q < childStart[a + 1]; ++q) {
@@ -75,6 +77,7 @@ __global__ void k_tree_down(int km1, const int* __restrict__ childStart, const i
 // parent0T[v] = tree position of v's level-1 parent; csT[M1] = M0.
 __global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __restrict__ start1, int64_t M0,
                               int64_t M1, int* __restrict__ parent0T, int* __restrict__ csT) {
+    pdl_entry();
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t v = t0; v < M0; v += stride) parent0T[v] = start1[parent0[v]].y;
@@ -85,6 +88,7 @@ __global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __res
 // ancRng = its level-1 range.  The PCG coarse pass then reads a whole ancestor chain in one
 // coalesced round instead of top−2 dependent (and, after each iteration's streams, DRAM) loads.
 __global__ void k_tree_anc(HierArgs h, int* __restrict__ ancId, int2* __restrict__ ancRng) {
+    pdl_entry();
     const int top = h.L - 1;
     const int64_t M2 = h.lv[2].M;
     for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < M2; a += (int64_t)gridDim.x * blockDim.x) {
@@ -99,6 +103,7 @@ __global__ void k_tree_anc(HierArgs h, int* __restrict__ ancId, int2* __restrict
 
 // per solve: ancMu[k−3][a] = μ_k of the level-k ancestor of level-2 vertex a
 __global__ void k_tree_anc_mu(HierArgs h, const int* __restrict__ ancId, float* __restrict__ ancMu) {
+    pdl_entry();
     const int top = h.L - 1;
     const int64_t M2 = h.lv[2].M;
     for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < M2; a += (int64_t)gridDim.x * blockDim.x)
@@ -113,6 +118,7 @@ __global__ void k_tree_anc_mu(HierArgs h, const int* __restrict__ ancId, float* 
 // the iteration count and retires the channel.
 template <int SRC, bool FINISH_LAST>
 __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restrict__ w0) {
+    pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
@@ -239,6 +245,7 @@ __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*
 // PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
 template <int MODE>
 __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0) {
+    pdl_entry();
     __shared__ float stage[kScanTile / 32][kLiftStage];
     __shared__ double shs[32];
     const int t = blockIdx.x;
@@ -317,6 +324,7 @@ __device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int f, doub
 //              denominator is 0 (reading #10) or above the frame's top level.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
+    pdl_entry();
     extern __shared__ double tb[];  // [tiles of the frame]
     __shared__ double shd[32];
     __shared__ int sflag;
@@ -446,6 +454,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, const float* __restrict__ in0,
                                                    float* __restrict__ out0, int first) {
+    pdl_entry();
     const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
     const int stride = a.BPF * blockDim.x;
