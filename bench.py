@@ -303,10 +303,10 @@ def main():
                            ("k_bistoch", "bistochastize"),
                            ("k_pyr_", "pyramid"), ("k_lift_count", "pyramid"), ("k_tree_top", "pyramid"),
                            ("k_tree_down", "pyramid"), ("k_tree_finish", "pyramid"),
-                           ("k_tree_anc_mu", "splat_assemble_init"), ("k_tree_anc", "pyramid"),
+                           ("k_tree_anc_mult", "splat_assemble_init"), ("k_tree_anc", "pyramid"),
                            ("k_splat", "splat_assemble_init"), ("k_assemble", "splat_assemble_init"),
                            ("k_fill_init_w0", "splat_assemble_init"), ("k_init_dn", "splat_assemble_init"),
-                           ("k_tree_anc_mu", "splat_assemble_init"), ("k_tree_lift<PDA>", "splat_assemble_init"),
+                           ("k_tree_lift<PDA>", "splat_assemble_init"),
                            ("k_tree_coarse<PDA>", "splat_assemble_init"), ("k_tree_lift<INIT>", "splat_assemble_init"),
                            ("k_tree_coarse<INIT>", "splat_assemble_init"), ("k_tree_level0<INIT>", "splat_assemble_init"),
                            ("k_spmv2", "pcg"), ("k_update", "pcg"), ("k_direction2", "pcg"), ("k_residual0", "pcg"),

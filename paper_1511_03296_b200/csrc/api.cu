@@ -230,10 +230,9 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const int cellBlocks = grid_for(g->ncells * 32, 256, 1 << 20);
         LAUNCH(k_grid_sort, cellBlocks, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, cellCnt, heads, g->perm, err);
         LAUNCH(k_scan_excl, (unsigned)std::max<int64_t>(scanTiles, 1), kScanBlock, 0, s, cellCnt, g->ncells, g->cellOff,
-               counter, state);
+               counter, state, (int64_t)ncx * ncy, g->frameOff);
         LAUNCH(k_grid_write, cellBlocks, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, g->cellOff, heads, g->perm,
                keysCap, mCap, g->vid);
-        LAUNCH(k_frame_offsets, 1, 288, 0, s, g->cellOff, F, (int64_t)ncx * ncy, g->frameOff);
 
         // ---- sync 1: vertex counts (sizes the vertex arrays and the pyramid capacities)
         std::vector<int> fo(F + 1);
@@ -269,8 +268,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             ck(cudaMemcpyAsync(g->n, ones.data(), M * sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
             ck(cudaStreamSynchronize(s), "sync");
         }
-        unsigned* res2 = reinterpret_cast<unsigned*>(err + 2);
-        LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, res2);
 
         // ---- pyramid (Supp. Sec. 2), levels 1 .. Lmax-1
         int Lmax = 1;
@@ -283,7 +280,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const uint64_t* keysK = g->keys;
         const int* cellOffK = g->cellOff;
         int ncxK = ncx, ncyK = ncy;
-        const int* countK = nullptr;  // level 0: P(1) = 1
         std::vector<int*> lvFrameOffDev(Lmax, nullptr);
         unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
         int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, s) : nullptr;  // parent rank of each sorted child
@@ -298,6 +294,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             L.childStart = dalloc<int>(A, M + 1, s);
             L.childList = dalloc<int>(A, M, s);
             L.count = dalloc<int>(A, M, s);
+            if (k >= 2) L.cnt1 = dalloc<int>(A, M, s);
             int* cnt2 = dalloc<int>(A, L.ncells, s);
             const int64_t st2n = std::max<int64_t>(1, (L.ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems));
             unsigned long long* st2 = dalloc<unsigned long long>(A, st2n, s);
@@ -306,12 +303,13 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             ck(cudaMemsetAsync(ctr2, 0, 2 * sizeof(unsigned), s), "memset");
             LAUNCH(k_pyr_sort, (unsigned)L.ncells, 64, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK, ncxK,
                    ncyK, L.ncx, L.ncy, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
-            LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2);
-            LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
-                   L.ncy, L.ncells, L.cellOff, L.childList, pyrRank, L.keys, L.parent, L.childStart);
-            // P(1): upper bound M on the level size; the kernel stops at the true size via childStart
             lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
-            LAUNCH(k_frame_offsets, 1, 288, 0, s, L.cellOff, F, (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
+            LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2,
+                   (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
+            LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
+                   L.ncy, L.ncells, L.cellOff, L.childList, pyrRank, L.keys, L.parent, L.childStart,
+                   k >= 2 ? g->lv[k - 1].count : nullptr, L.count, k >= 3 ? g->lv[k - 1].cnt1 : nullptr,
+                   k >= 2 ? L.cnt1 : nullptr);
             keysK = L.keys;
             cellOffK = L.cellOff;
             ncxK = L.ncx;
@@ -327,12 +325,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         ck(cudaMemcpyAsync(errh, err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaStreamSynchronize(s), "sync");
         if (errh[0] & ~8) throw Err(FBS_ECUDA, "internal grid-build check failed (code " + std::to_string(errh[0]) + ")");
-        {
-            float e, mm;
-            std::memcpy(&e, &errh[2], 4);
-            std::memcpy(&mm, &errh[3], 4);
-            g->bistoch_residual = (mm > 0.f) ? e / mm : 0.f;
-        }
+        g->bistoch_residual = -1.f;  // computed on request (fbs_grid_export)
         // per-frame level counts: first level with a single vertex (reading #8)
         g->frameLevelsH.assign(F, Lmax);
         for (int f = 0; f < F; ++f) {
@@ -351,9 +344,6 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         for (int k = 1; k < L; ++k) {
             g->lv[k].M = lfo[k][F];
             g->lv[k].frameOff.assign(lfo[k].begin(), lfo[k].end());
-            LAUNCH(k_lift_count, grid_for(g->lv[k].M), kThreads, 0, s, countK, g->lv[k].childStart,
-                   g->lv[k].childList, (int)g->lv[k].M, g->lv[k].count);
-            countK = g->lv[k].count;
         }
 
         g->frameLevels = dalloc<int>(A, F, s);
@@ -374,11 +364,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             const int64_t M1 = g->lv[1].M;
             const int top = L - 1;
             std::vector<int*> cnt1(L, nullptr);  // level-1 descendants of levels ≥ 2
-            for (int k = 2; k < L; ++k) {
-                cnt1[k] = dalloc<int>(A, g->lv[k].M, s);
-                LAUNCH(k_lift_count, grid_for(g->lv[k].M), kThreads, 0, s, k == 2 ? nullptr : cnt1[k - 1],
-                       g->lv[k].childStart, g->lv[k].childList, (int)g->lv[k].M, cnt1[k]);
-            }
+            for (int k = 2; k < L; ++k) cnt1[k] = g->lv[k].cnt1;
             std::vector<int2*> start(L, nullptr);
             for (int k = 1; k < L; ++k) start[k] = dalloc<int2>(A, g->lv[k].M, s);
             for (int k = 2; k < L; ++k) T.rng[k] = dalloc<int2>(A, g->lv[k].M, s);
@@ -503,10 +489,11 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.lvFrameOff = g->lvFrameOffDev;
     h.alpha = alpha;
     h.beta = beta;
+    for (int k = 0; k < kMaxLevels; ++k) h.zw[k] = std::pow(alpha, -(beta + (double)k));
     const TreeOrder& T = g->tree;
     h.tord0 = T.tord0;
     h.ancRng = T.ancRng;
-    h.ancMu = S->ancMu;
+    h.ancMult = S->ancMult;
     h.M2 = (g->L > 2) ? g->lv[2].M : 0;
     h.csT = T.csT;
     h.parent0T = T.parent0T;
@@ -742,8 +729,8 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             S->partial2 = dalloc<double>(A, (size_t)F * S->bpf2 * C, s);
             if (hierP) {
                 for (int k = 1; k < g->L; ++k) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
-                if (g->L > 3) S->ancMu = dalloc<float>(A, (size_t)(g->L - 3) * g->lv[2].M, s);
             }
+            if (g->L > 3) S->ancMult = dalloc<float>(A, (size_t)(g->L - 3) * g->lv[2].M, s);
         }
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * K, s);
         S->counters = dalloc<unsigned>(A, F, s);
@@ -765,14 +752,22 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             HierArgs h = make_hier(S, 1, o.precond_alpha, o.precond_beta);
             tree_lift<HIER_PDA>(S, h, S->w0, s);
             tree_coarse<HIER_PDA>(S, h, a, 0, s);
-            if (g->L > 3) LAUNCH(k_tree_anc_mu, grid_for(g->lv[2].M), kThreads, 0, s, h, g->tree.ancId, S->ancMu);
+
         }
         if (hierI) {
             HierArgs h = make_hier(S, K + 1, o.init_alpha, o.init_beta);
             LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, K, S->w0);
+            if (g->L > 3) {
+                auto km = k_tree_anc_mult<HIER_INIT>;
+                LAUNCH_AS("k_tree_anc_mult<INIT>", km, F * S->bpf2, kThreads, 0, s, h, g->tree.ancId, S->ancMult);
+            }
             tree_lift<HIER_INIT>(S, h, S->w0, s);
             tree_coarse<HIER_INIT>(S, h, a, 0, s);
             tree_level0<HIER_INIT>(S, h, a, S->w0, S->xh, 0, s);
+        }
+        if (hierP && g->L > 3) {
+            auto km = k_tree_anc_mult<HIER_PCG>;
+            LAUNCH_AS("k_tree_anc_mult<PCG>", km, F * S->bpf2, kThreads, 0, s, S->hP, g->tree.ancId, S->ancMult);
         }
         ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
         LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, K);
@@ -905,7 +900,23 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
             ck(cudaMemcpyAsync(nbr, d, (size_t)M * 40, cudaMemcpyDeviceToHost, s), "d2h");
             free_all(tmp, s);
         }
-        if (res) *res = g->bistoch_residual;
+        if (res) {
+            if (g->bistoch_residual < 0.f) {  // reporting only: max|n∘B̄n − m| / max m, on request
+                std::vector<void*> tmp;
+                unsigned* d = dalloc<unsigned>(tmp, 2, s);
+                ck(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned), s), "memset");
+                LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, d);
+                unsigned h2[2];
+                ck(cudaMemcpyAsync(h2, d, sizeof(h2), cudaMemcpyDeviceToHost, s), "d2h");
+                ck(cudaStreamSynchronize(s), "sync");
+                free_all(tmp, s);
+                float e, mm;
+                std::memcpy(&e, &h2[0], 4);
+                std::memcpy(&mm, &h2[1], 4);
+                g->bistoch_residual = (mm > 0.f) ? e / mm : 0.f;
+            }
+            *res = g->bistoch_residual;
+        }
         ck(cudaStreamSynchronize(s), "sync");
     });
 }

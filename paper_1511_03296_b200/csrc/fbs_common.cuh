@@ -199,6 +199,7 @@ struct Level {          // pyramid level k ≥ 1
     int* childStart = nullptr;      // [M + 1]
     int* childList = nullptr;       // [M_{k-1}]  children grouped by parent, fixed order
     int* count = nullptr;           // [M] P(1)
+    int* cnt1 = nullptr;            // [M] level-1 descendants (k ≥ 2)
     std::vector<int64_t> frameOff;  // host copy [F + 1]
 };
 
@@ -233,10 +234,11 @@ struct HierArgs {
     const int* frameLevels;
     const int* lvFrameOff;  // [L][F+1] per-level frame vertex offsets (tree order keeps frames)
     double alpha, beta;     // z_weight parameters of the current use
+    double zw[kMaxLevels];  // z_w(k) = α^−(β+k), k ≥ 1
     // tree order (grid)
     const int* tord0;       // [M0] level-0 vertex at each level-0 tree position
     const int2* ancRng;     // [top−2][M2] level-1 ranges of the level-k ancestors (k = 3..top) of level-2 vertices
-    const float* ancMu;     // [top−2][M2] their μ_k (per solve)
+    const float* ancMult;   // [top−2][M2] their multipliers of the current use (k_tree_anc_mult)
     const int* csT;         // [M1+1] level-0 tree range of the level-1 vertex at tree position i
     const int* parent0T;    // [M0] tree position of the level-1 parent of level-0 vertex v
     const int* tileFrameOff;  // [F+1] first scan tile of each frame
@@ -330,7 +332,7 @@ struct fbs_system_s {
     float* sh = nullptr;
     float* w0 = nullptr;                   // [C][M] level-0 pyramid input (init, μ_k, debug operator)
     float* mu[fbs::kMaxLevels] = {};       // [M_k] precond multipliers (k ≥ 2 canonical; k = 1 tree order)
-    float* ancMu = nullptr;                // [top−2][M2] μ of the level-2 vertices' ancestors
+    float* ancMult = nullptr;              // [top−2][M2] multipliers of the level-2 vertices' ancestors
     float* buf1T = nullptr;                // [C][M1] hierarchy work arrays (tree_kernels.cuh)
     double* locT = nullptr;
     double* tileAgg = nullptr;

@@ -140,11 +140,14 @@ __global__ void __launch_bounds__(256) k_grid_sort(
 }
 
 // Exclusive scan of n ints → out[0..n] (out[n] = total), one pass: tiles of kScanBlock·kScanItems
-// values with a warp-parallel decoupled look-back (few tiles ⇒ a short chain).
+// values with a warp-parallel decoupled look-back (few tiles ⇒ a short chain).  frameOff (if not
+// null): frameOff[i / per] = out[i] for i a multiple of per (per-frame offsets of cell-ordered
+// counts).
 constexpr int kScanBlock = 256, kScanItems = 16;
 __global__ void __launch_bounds__(kScanBlock) k_scan_excl(const int* __restrict__ in, int64_t n, int* __restrict__ out,
                                                         unsigned* __restrict__ tile_counter,
-                                                        unsigned long long* __restrict__ tile_state) {
+                                                        unsigned long long* __restrict__ tile_state, int64_t per,
+                                                        int* __restrict__ frameOff) {
     pdl_entry();
     __shared__ unsigned s_tile;
     __shared__ int s_warp[kScanBlock / 32];
@@ -182,11 +185,20 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(const int* __restrict_
     int run = (int)s_excl + wex + incl - sum;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-        if (base + i < n) out[base + i] = run;
-        if (base + i == n - 1) out[n] = run + v[i];
+        if (base + i < n) {
+            out[base + i] = run;
+            if (frameOff && (base + i) % per == 0) frameOff[(base + i) / per] = run;
+        }
+        if (base + i == n - 1) {
+            out[n] = run + v[i];
+            if (frameOff) frameOff[n / per] = run + v[i];
+        }
         run += v[i];
     }
-    if (n == 0 && tile == 0 && threadIdx.x == 0) out[0] = 0;
+    if (n == 0 && tile == 0 && threadIdx.x == 0) {
+        out[0] = 0;
+        if (frameOff) frameOff[0] = 0;
+    }
 }
 
 __global__ void __launch_bounds__(256) k_grid_write(

@@ -143,12 +143,17 @@ __global__ void __launch_bounds__(64) k_pyr_sort(const uint64_t* __restrict__ ke
 }
 
 // Pass 3 (after the exclusive scan of the parent counts → cellOffN): parents get their canonical
-// ids vOff + rank: parent map, parent keys and child-list starts.  One warp per coarse cell.
+// ids vOff + rank: parent map, parent keys and child-list starts, and (summed by the run head over
+// its children in child order, integers) P(1) = level-0 descendants (countK = nullptr: level 0,
+// one each) and the level-1 descendant counts cnt1 (cnt1K = nullptr: the children are level-1
+// vertices, one each; cnt1N = nullptr: not needed at level 1).  One warp per coarse cell.
 __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK,
                                                    int ncxK, int ncyK, int ncxN, int ncyN, int64_t ncellsN,
                                                    const int* __restrict__ cellOffN, const int* __restrict__ childListN,
                                                    const int* __restrict__ rankS, uint64_t* __restrict__ keysN,
-                                                   int* __restrict__ parentK, int* __restrict__ childStartN) {
+                                                   int* __restrict__ parentK, int* __restrict__ childStartN,
+                                                   const int* __restrict__ countK, int* __restrict__ countN,
+                                                   const int* __restrict__ cnt1K, int* __restrict__ cnt1N) {
     pdl_entry();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t C = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp; C < ncellsN;
@@ -164,6 +169,16 @@ __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ 
             if (i == 0 || rankS[cc.cOff + i - 1] != r) {
                 keysN[vOff + r] = khi | (uint64_t)halve_code((uint32_t)(keysK[gch] & 0xffffffu));
                 childStartN[vOff + r] = cc.cOff + i;
+                int e = i + 1;
+                while (e < nch && rankS[cc.cOff + e] == r) ++e;  // this parent's children: [i, e)
+                int c0 = 0, c1 = 0;
+                for (int q = i; q < e; ++q) {
+                    const int ch = childListN[cc.cOff + q];
+                    c0 += countK ? countK[ch] : 1;
+                    if (cnt1N) c1 += cnt1K ? cnt1K[ch] : 1;
+                }
+                countN[vOff + r] = c0;
+                if (cnt1N) cnt1N[vOff + r] = c1;
             }
         }
         if (C == ncellsN - 1 && lane == 0) childStartN[cellOffN[ncellsN]] = cc.cOff + nch;

@@ -26,6 +26,17 @@ namespace fbs {
 enum { HIER_PCG = 0, HIER_PDA = 1, HIER_INIT = 2, HIER_PLAIN = 3 };
 enum { HSRC_UPDATE = 0, HSRC_RESID = 1, HSRC_RESID0 = 2 };
 
+// INIT multiplier z_w(k)/P(1)_k; 0 above the frame's top level (reading #8).
+// h.zw[k] = α^−(β+k) of the current use (host-computed).
+__device__ __forceinline__ float init_mult1(const HierArgs& h, int k, int fl, int count) {
+    return (k < fl) ? (float)(h.zw[k] / (double)count) : 0.f;
+}
+
+// μ_k = z_w(k) P(1) / den (Eq. hier_precond)
+__device__ __forceinline__ float zw_count(const HierArgs& h, int k, int count, double den) {
+    return (float)(h.zw[k] * (double)count / den);
+}
+
 // ================================================================ grid build: tree order
 // start positions of the top vertex of each frame: its frame's first level-0 / level-1 positions
 // (top ≥ 2: also its level-1 range)
@@ -101,14 +112,23 @@ __global__ void k_tree_anc(HierArgs h, int* __restrict__ ancId, int2* __restrict
     }
 }
 
-// per solve: ancMu[k−3][a] = μ_k of the level-k ancestor of level-2 vertex a
-__global__ void k_tree_anc_mu(HierArgs h, const int* __restrict__ ancId, float* __restrict__ ancMu) {
+// per use: ancMult[k−3][a] = the multiplier of the level-k ancestor of level-2 vertex a:
+// μ_k (PCG/PLAIN) or z_w(k)/P(1)_k (INIT).  Blocks per frame (h.bpf2).
+template <int MODE>
+__global__ void k_tree_anc_mult(HierArgs h, const int* __restrict__ ancId, float* __restrict__ ancMult) {
     pdl_entry();
+    const int f = blockIdx.x / h.bpf2, j = blockIdx.x % h.bpf2;
+    const int F1 = h.F + 1;
     const int top = h.L - 1;
+    const int fl = h.frameLevels[f];
     const int64_t M2 = h.lv[2].M;
-    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < M2; a += (int64_t)gridDim.x * blockDim.x)
-        for (int k = 3; k <= top; ++k)
-            ancMu[(size_t)(k - 3) * M2 + a] = h.lv[k].mu[ancId[(size_t)(k - 3) * M2 + a]];
+    const int a0 = h.lvFrameOff[2 * F1 + f], a1 = h.lvFrameOff[2 * F1 + f + 1];
+    for (int a = a0 + j * blockDim.x + threadIdx.x; a < a1; a += h.bpf2 * blockDim.x)
+        for (int k = 3; k <= top; ++k) {
+            const int id = ancId[(size_t)(k - 3) * M2 + a];
+            ancMult[(size_t)(k - 3) * M2 + a] =
+                (MODE == HIER_INIT) ? init_mult1(h, k, fl, h.lv[k].count[id]) : h.lv[k].mu[id];
+        }
 }
 
 // ================================================================ level 0 → PCG input
@@ -205,16 +225,6 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
 // tile totals in shared memory (no inter-block signalling here).
 constexpr int kLiftStage = 256;
 
-// INIT multiplier z_w(k)/P(1)_k; 0 above the frame's top level (reading #8)
-__device__ __forceinline__ float init_mult1(const HierArgs& h, int k, int fl, int count) {
-    return (k < fl) ? (float)(pow(h.alpha, -(h.beta + (double)k)) / (double)count) : 0.f;
-}
-
-__device__ __forceinline__ float zw_count(double alpha, double beta, int k, int count, double den) {
-    return (float)(pow(alpha, -(beta + (double)k)) * (double)count / den);
-}
-
-
 __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*/, double* total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double incl = x;
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
         if (valid) h.buf1T[(size_t)c * h.M1 + i] = acc;
         if (MODE == HIER_PDA && valid)
             h.mu1T[i] = (1 < h.frameLevels[h.tileFrame[t]] && acc > 0.f)
-                            ? zw_count(h.alpha, h.beta, 1, myHi - myLo, (double)acc) : 0.f;
+                            ? zw_count(h, 1, myHi - myLo, (double)acc) : 0.f;
         double tot;
         const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
         if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
@@ -313,15 +323,17 @@ __device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int f, doub
     __syncthreads();
 }
 
-// One thread per level-2 vertex a (blocks per frame: h.bpf2), walking its ancestor chain, then
-// writing acc1 for its children (L = 2: one thread per level-1 position, acc2 = 0):
+// One thread per level-2 vertex a (blocks per frame: h.bpf2): (P y)_a and those of its ancestors
+// (level-1 ranges and multipliers from the ancestor tables, four per load round), then acc1 for
+// its children (L = 2: one thread per level-1 position, acc2 = 0):
 //   PCG/PLAIN: acc2_a = Σ_{k≥2} μ_k (P w)_anc;  PCG also ρ_{≥1} = Σ μ (P w)² (each coarse vertex
 //              counted once, by its first level-2 descendant; level 1 by its parent) and, in the
 //              last block of the frame, the ρ finish (with the ρ_0, ‖r‖² partials of
 //              k_hier_level0): β and the stopping rule (Alg. 2 lines 11-13).
 //   INIT:      mult_k = z_w(k)/P(1)_k.
-//   PDA:       μ_k = z_w(k; α, β) P(1)_k / P(diag A)_k, 0 where the
-//              denominator is 0 (reading #10) or above the frame's top level.
+// PDA (one thread per coarse vertex of every level ≥ 1... levels ≥ 2 here, level 1 in the lift):
+//   μ_k = z_w(k; α, β) P(1)_k / P(diag A)_k, 0 where the denominator is 0
+//   (reading #10) or above the frame's top level.
 template <int MODE>
 __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
     pdl_entry();
@@ -342,21 +354,32 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
         double rho = 0.0;
         if (act) {
             tile_bases(h, c, f, tb, shd);
+            if (MODE == HIER_PDA) {
+                for (int k = 2; k <= top; ++k) {
+                    const HLevel& L = h.lv[k];
+                    float* mu = const_cast<float*>(L.mu);
+                    const int b0 = h.lvFrameOff[k * F1 + f], b1 = h.lvFrameOff[k * F1 + f + 1];
+                    for (int v = b0 + j * blockDim.x + threadIdx.x; v < b1; v += stride) {
+                        const int2 rg = L.rng[v];
+                        const double S = tree_prefix(h, tb, c, fb, rg.x + rg.y - 1) - tree_prefix(h, tb, c, fb, rg.x - 1);
+                        mu[v] = (k < fl && S > 0.0) ? zw_count(h, k, L.count[v], S) : 0.f;
+                    }
+                }
+                continue;
+            }
             for (int v = a0 + j * blockDim.x + threadIdx.x; v < a1; v += stride) {
                 // level-1 children of v: one contiguous tree range (L = 2: v itself)
                 const int2 kids = (lv == 2) ? h.lv[2].rng[v] : make_int2(v, 1);
                 const int first1 = kids.x;
                 float acc = 0.f;
-                int an = (lv == 2) ? v : -1;
-                if ((MODE == HIER_PCG || MODE == HIER_PLAIN) && lv == 2) {
-                    // v itself, then its ancestors from the tables, four per load round
-                    {
+                if (lv == 2) {
+                    {   // v itself
                         const double S = tree_prefix(h, tb, c, fb, kids.x + kids.y - 1) - tree_prefix(h, tb, c, fb, kids.x - 1);
-                        const float m = h.lv[2].mu[v];
+                        const float m = (MODE == HIER_INIT) ? init_mult1(h, 2, fl, h.lv[2].count[v]) : h.lv[2].mu[v];
                         acc = m * (float)S;
                         if (MODE == HIER_PCG) rho += (double)m * S * S;
                     }
-                    for (int kb = 3; kb <= top; kb += 4) {
+                    for (int kb = 3; kb <= top; kb += 4) {  // its ancestors, four per load round
                         int2 r[4];
                         float m[4];
                         double S[4];
@@ -365,7 +388,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                             if (kb + u > top) continue;
                             const size_t o = (size_t)(kb + u - 3) * h.M2 + v;
                             r[u] = __ldg(h.ancRng + o);
-                            m[u] = __ldg(h.ancMu + o);
+                            m[u] = __ldg(h.ancMult + o);
                         }
 #pragma unroll
                         for (int u = 0; u < 4; ++u)
@@ -378,44 +401,25 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                             if (MODE == HIER_PCG && r[u].x == first1) rho += (double)m[u] * S[u] * S[u];
                         }
                     }
-                    an = -1;
                 }
-                for (int k = 2; k <= top && an >= 0; ++k) {
-                    const HLevel& L = h.lv[k];
-                    const int2 rg = L.rng[an];
-                    const int nxt = (k < top) ? L.parent[an] : -1;
-                    const double S = tree_prefix(h, tb, c, fb, rg.x + rg.y - 1) - tree_prefix(h, tb, c, fb, rg.x - 1);
-                    if (MODE == HIER_PDA) {
-                        if (rg.x == first1)
-                            const_cast<float*>(L.mu)[an] =
-                                (k < fl && S > 0.0) ? zw_count(h.alpha, h.beta, k, L.count[an], S) : 0.f;
-                    } else {
-                        const float mk = (MODE == HIER_INIT) ? init_mult1(h, k, fl, L.count[an]) : L.mu[an];
-                        acc += mk * (float)S;
-                        if (MODE == HIER_PCG && rg.x == first1) rho += (double)mk * S * S;
-                    }
-                    an = nxt;
-                }
-                if (MODE != HIER_PDA) {
-                    // acc1 for the children (+ PCG: their ρ_1 terms μ_1 (P w)²_1), 4 loads in flight
-                    const float* b1 = h.buf1T + (size_t)c * h.M1;
-                    for (int ib = kids.x; ib < kids.x + kids.y; ib += 4) {
-                        float m1[4], bv[4];
+                // acc1 for the children (+ PCG: their ρ_1 terms μ_1 (P w)²_1), 4 loads in flight
+                const float* b1 = h.buf1T + (size_t)c * h.M1;
+                for (int ib = kids.x; ib < kids.x + kids.y; ib += 4) {
+                    float m1[4], bv[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = ib + u;
-                            if (i < kids.x + kids.y) {
-                                m1[u] = (MODE == HIER_INIT) ? init_mult1(h, 1, fl, h.csT[i + 1] - h.csT[i]) : h.mu1T[i];
-                                bv[u] = b1[i];
-                            }
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = ib + u;
+                        if (i < kids.x + kids.y) {
+                            m1[u] = (MODE == HIER_INIT) ? init_mult1(h, 1, fl, h.csT[i + 1] - h.csT[i]) : h.mu1T[i];
+                            bv[u] = b1[i];
                         }
+                    }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int i = ib + u;
-                            if (i < kids.x + kids.y) {
-                                h.acc1T[(size_t)c * h.M1 + i] = m1[u] * bv[u] + acc;
-                                if (MODE == HIER_PCG) rho += (double)m1[u] * (double)bv[u] * (double)bv[u];
-                            }
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = ib + u;
+                        if (i < kids.x + kids.y) {
+                            h.acc1T[(size_t)c * h.M1 + i] = m1[u] * bv[u] + acc;
+                            if (MODE == HIER_PCG) rho += (double)m1[u] * (double)bv[u] * (double)bv[u];
                         }
                     }
                 }
