@@ -123,6 +123,7 @@ void device_setup(int* dev) {
         int sms = 0;
         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, *dev), "sm count");
         g_num_sms = sms;
+        ck(cudaFuncSetAttribute(k_bistoch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsSmem), "k_bistoch smem");
         ck(cudaFuncSetAttribute(k_pyr_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kCoarseCap * (int)sizeof(unsigned long long)),
            "k_pyr_sort smem");
@@ -216,7 +217,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         ck(cudaMemsetAsync(state, 0, std::max<int64_t>(scanTiles, 1) * sizeof(unsigned long long), s), "memset");
         g->vid = dalloc<int>(A, N, s);
         uint64_t* keysCap = dalloc<uint64_t>(A, N, s);
-        int* mCap = dalloc<int>(A, N, s);
+        int* mCap = dalloc<int>(A, N + kVecPad, s);
         g->cellOff = dalloc<int>(A, g->ncells + 1, s);
         g->frameOff = dalloc<int>(A, F + 1, s);
         CellGeom geo{F, H, W, ncx, ncy, g->colStart, g->rowStart};
@@ -249,18 +250,20 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->m = mCap;
         const int64_t M = g->M;
 
-        g->nbr = dalloc<int4>(A, M, s);
+        g->nbr = dalloc<int4>(A, M + kVecPad, s);
         LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
                g->ncells, g->nbr, err);
 
         // ---- Alg. 1 (reading #5: fixed n_bistoch iterations)
-        g->n = dalloc<float>(A, M, s);
-        float* ntmp = dalloc<float>(A, M, s);
+        g->n = dalloc<float>(A, M + kVecPad, s);
+        float* ntmp = dalloc<float>(A, M + kVecPad, s);
         float* cur = ntmp;
         float* nxt = g->n;
         if (g->n_bistoch % 2 == 0) std::swap(cur, nxt);  // make the last write land in g->n
         for (int it = 0; it < g->n_bistoch; ++it) {
-            LAUNCH(k_bistoch, grid_for(M), kThreads, 0, s, g->nbr, g->m, cur, nxt, (int)M, it == 0);
+            const int nch = (int)((M + kBsChunk - 1) / kBsChunk);
+            LAUNCH(k_bistoch, std::max(1, std::min(nch, 3 * (g_num_sms > 0 ? g_num_sms : 148))), kThreads, kBsSmem, s,
+                   g->nbr, g->m, cur, nxt, (int)M, it == 0);
             std::swap(cur, nxt);
         }
         if (g->n_bistoch == 0) {

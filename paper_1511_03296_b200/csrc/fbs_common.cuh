@@ -21,6 +21,7 @@ constexpr int kCoarseCap = 512;      // children of one pyramid coarse cell sort
 constexpr int kMaxLevels = 24;
 constexpr int kThreads = 256;        // vertex-parallel kernels
 constexpr int kMaxK = 64;
+constexpr int kVecPad = 512;         // vertex arrays streamed by bulk copies are allocated with this slack
 constexpr int kScanTile = 256;       // tree-ordered level-1 positions per prefix-scan tile (tree_kernels.cuh)
 
 // ------------------------------------------------------------------ launch counter
@@ -35,6 +36,38 @@ extern std::atomic<long long> g_launches;
 __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// ------------------------------------------------------------------ bulk async copies (TMA engine)
+// 1-D cp.async.bulk global → shared with mbarrier completion (sm_90+): one elected thread arms
+// the barrier with the byte count and issues the copies; consumers wait on the phase parity.
+// Addresses and sizes must be multiples of 16 bytes.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 // ------------------------------------------------------------------ small device helpers

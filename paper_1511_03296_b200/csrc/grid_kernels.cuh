@@ -311,28 +311,95 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
 
 // ---------------------------------------------------------------- Alg. 1 bistochastization
 // n ← sqrt((n ∘ m) / (B̄ n)),  B̄ n = 2D n_v + Σ_{u∈N(v)} n_u, fp32.
+// Persistent blocks take chunks of kBsChunk consecutive vertices through a two-stage bulk-copy
+// pipeline: while a chunk is computed, the TMA engine copies the next chunk's neighbour structure,
+// m and the n window [c0 − 128, c0 + chunk + 128) into shared memory.  The 8 near neighbours
+// (|offset| ≤ 127 by construction) are read from the window; only y∓ are global gathers.
+// Vertex arrays carry kVecPad slack, so whole 16-byte-multiple copies never leave allocations.
+constexpr int kBsChunk = 1024;
+constexpr int kBsWin = kBsChunk + 256;
+struct BsStage {
+    int4 nb[kBsChunk];
+    int m[kBsChunk];
+    float n[kBsWin];
+};
+constexpr size_t kBsSmem = 2 * sizeof(BsStage) + 64;
+
 __global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
                                                  float* __restrict__ nout, int M, int first) {
     pdl_entry();
-    const int stride = gridDim.x * blockDim.x;
-#pragma unroll 2
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += stride) {
-        const int4 nb = nbr[v];
-        float nv, bn;
-        if (first) {
-            int deg = 0;
+    extern __shared__ __align__(128) unsigned char bs_smem[];
+    BsStage* st = reinterpret_cast<BsStage*>(bs_smem);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(bs_smem + 2 * sizeof(BsStage));
+    const int nChunks = (M + kBsChunk - 1) / kBsChunk;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    auto issue = [&](int slot, int ci) {  // thread 0
+        const int c0 = ci * kBsChunk;
+        const int n = min(kBsChunk, M - c0);
+        const int n4 = (n + 3) & ~3;
+        const int w0 = max(c0 - 128, 0);                 // 16-byte aligned (c0 is a multiple of 1024)
+        const int w1 = min(c0 + kBsChunk + 128, (M + 3) & ~3);
+        const uint32_t bytes = (uint32_t)(n * 16 + n4 * 4 + (first ? 0 : (w1 - w0) * 4));
+        mbar_expect_tx(&bar[slot], bytes);
+        bulk_g2s(st[slot].nb, nbr + c0, n * 16, &bar[slot]);
+        bulk_g2s(st[slot].m, m + c0, n4 * 4, &bar[slot]);
+        if (!first) bulk_g2s(st[slot].n + (w0 - (c0 - 128)), nin + w0, (w1 - w0) * 4, &bar[slot]);
+    };
+    int ci = blockIdx.x;
+    if (threadIdx.x == 0) {
+        if (ci < nChunks) issue(0, ci);
+        if (ci + (int)gridDim.x < nChunks) issue(1, ci + gridDim.x);
+    }
+    for (int it = 0; ci < nChunks; ++it, ci += gridDim.x) {
+        const int slot = it & 1;
+        mbar_wait(&bar[slot], (it >> 1) & 1);
+        const BsStage& S = st[slot];
+        const int c0 = ci * kBsChunk;
+        float ny[kBsChunk / 256][2];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) deg += near_off(nb, i) != 0;
-            deg += (nb.z != 0) + (nb.w != 0);
-            nv = 1.f;
-            bn = (float)kBbarDiag + (float)deg;
-        } else {
-            nv = nin[v];
-            bn = (float)kBbarDiag * nv + nbr_sum(nin, v, nb);
+        for (int u = 0; u < kBsChunk / 256; ++u) {
+            const int l = threadIdx.x + 256 * u, v = c0 + l;
+            const int4 nb = S.nb[l];
+            ny[u][0] = (!first && v < M && nb.z) ? __ldg(nin + v + nb.z) : 0.f;
+            ny[u][1] = (!first && v < M && nb.w) ? __ldg(nin + v + nb.w) : 0.f;
         }
-        nout[v] = sqrtf(nv * (float)m[v] / bn);
+#pragma unroll
+        for (int u = 0; u < kBsChunk / 256; ++u) {
+            const int l = threadIdx.x + 256 * u, v = c0 + l;
+            if (v >= M) continue;
+            const int4 nb = S.nb[l];
+            float nv, bn;
+            if (first) {
+                int deg = 0;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) deg += near_off(nb, i) != 0;
+                deg += (nb.z != 0) + (nb.w != 0);
+                nv = 1.f;
+                bn = (float)kBbarDiag + (float)deg;
+            } else {
+                const int lv = l + 128;
+                nv = S.n[lv];
+                float sn = 0.f;  // Σ_{u ∈ N(v)} n_u in the fixed slot order of nbr_sum
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int o = near_off(nb, i);
+                    if (o) sn += S.n[lv + o];
+                }
+                if (nb.z) sn += ny[u][0];
+                if (nb.w) sn += ny[u][1];
+                bn = (float)kBbarDiag * nv + sn;
+            }
+            nout[v] = sqrtf(nv * (float)S.m[l] / bn);
+        }
+        __syncthreads();  // stage `slot` fully consumed
+        if (threadIdx.x == 0 && ci + 2 * (int)gridDim.x < nChunks) issue(slot, ci + 2 * gridDim.x);
     }
 }
 
