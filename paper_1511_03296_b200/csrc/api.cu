@@ -262,7 +262,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         if (g->n_bistoch % 2 == 0) std::swap(cur, nxt);  // make the last write land in g->n
         for (int it = 0; it < g->n_bistoch; ++it) {
             const int nch = (int)((M + kBsChunk - 1) / kBsChunk);
-            LAUNCH(k_bistoch, std::max(1, std::min(nch, 3 * (g_num_sms > 0 ? g_num_sms : 148))), kThreads, kBsSmem, s,
+            LAUNCH(k_bistoch, std::max(1, std::min(nch, 3 * (g_num_sms > 0 ? g_num_sms : 148))), kBsThreads, kBsSmem, s,
                    g->nbr, g->m, cur, nxt, (int)M, it == 0);
             std::swap(cur, nxt);
         }
@@ -455,6 +455,7 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     a.x = x;
     a.r = S->rh;
     a.dn = S->dn;
+    a.ldn = (g->M + 3) & ~3ll;
     a.q = S->qh;
     a.s = S->sh;
     a.b = b;
@@ -567,13 +568,18 @@ void hier_precond_direction(fbs_system S, const VecArgs& a, int first, cudaStrea
     tree_level0<HIER_PCG>(S, S->hP, a, nullptr, nullptr, first, s);
 }
 
+// q = A d and α (k_spmv2)
+void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
+    LAUNCH(k_spmv2, S->g->F * S->BPF, kThreads, 0, s, a);
+}
+
 // One PCG iteration (Alg. 2 lines 6-14): SpMV + α; update (+ M⁻¹ and ρ, β); direction.
 // Hierarchical: ρ = rᵀM⁻¹r comes from the lift, and Pᵀ is fused with d = s + βd
 // (tree_kernels.cuh).  last: the final FIXED-mode iteration needs no new direction.
 void pcg_iteration(fbs_system S, const VecArgs& a, int it, bool last, cudaStream_t s) {
     const int nb = S->g->F * S->BPF;
     if (S->useHierP) {
-        LAUNCH(k_spmv2, nb, kThreads, 0, s, a);
+        spmv(S, a, s);
         if (last) {
             hier_level0<HSRC_UPDATE, true>(S, a, s);
         } else {
@@ -582,7 +588,7 @@ void pcg_iteration(fbs_system S, const VecArgs& a, int it, bool last, cudaStream
         }
     } else {
         LAUNCH(k_direction2, nb, kThreads, 0, s, a, it == 0);
-        LAUNCH(k_spmv2, nb, kThreads, 0, s, a);
+        spmv(S, a, s);
         LAUNCH(k_update, nb, kThreads, 0, s, a);
     }
 }
@@ -697,21 +703,20 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int F = g->F;
         auto& A = S->allocs;
         // launch geometry of the per-frame kernels: BPF blocks per frame
-        int occ = 0;
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_spmv2, kThreads, 0), "occupancy");
+        const int occ = 8;  // a full SM of 256-thread blocks (2048 threads)
         const int64_t want = (g->maxFrameM + kThreads - 1) / kThreads;
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
         S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
         S->C = K + 1;
         const size_t KM = (size_t)K * M;
-        S->sc = dalloc<float>(A, M, s);
+        S->sc = dalloc<float>(A, M + kVecPad, s);
         S->b = dalloc<float>(A, KM, s);
         S->diagA = dalloc<float>(A, M, s);
         S->mu0 = dalloc<float>(A, M, s);
         S->y0 = dalloc<float>(A, KM, s);
         S->xh = dalloc<float>(A, KM, s);
         S->rh = dalloc<float>(A, KM, s);
-        S->dn = dalloc<float2>(A, KM, s);
+        S->dn = dalloc<float2>(A, (size_t)K * ((M + 3) & ~3ll) + kVecPad, s);
         S->qh = dalloc<float>(A, KM, s);
         S->sh = dalloc<float>(A, KM, s);
         const bool hierP = o.precond == FBS_PRECOND_HIER && g->L > 1;  // L = 1: hier ≡ Jacobi / flat
@@ -773,7 +778,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             LAUNCH_AS("k_tree_anc_mult<PCG>", km, F * S->bpf2, kThreads, 0, s, S->hP, g->tree.ancId, S->ancMult);
         }
         ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
-        LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, K);
+        LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, (int64_t)((M + 3) & ~3ll), K);
         // a8: PCG
         run_pcg(S, a, false, s);
         // a9: slice

@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
 // (|offset| ≤ 127 by construction) are read from the window; only y∓ are global gathers.
 // Vertex arrays carry kVecPad slack, so whole 16-byte-multiple copies never leave allocations.
 constexpr int kBsChunk = 1024;
+constexpr int kBsThreads = 512;
 constexpr int kBsWin = kBsChunk + 256;
 struct BsStage {
     int4 nb[kBsChunk];
@@ -325,7 +326,7 @@ struct BsStage {
 };
 constexpr size_t kBsSmem = 2 * sizeof(BsStage) + 64;
 
-__global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
+__global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
                                                  float* __restrict__ nout, int M, int first) {
@@ -362,17 +363,17 @@ __global__ void __launch_bounds__(256) k_bistoch(const int4* __restrict__ nbr,
         mbar_wait(&bar[slot], (it >> 1) & 1);
         const BsStage& S = st[slot];
         const int c0 = ci * kBsChunk;
-        float ny[kBsChunk / 256][2];
+        float ny[kBsChunk / kBsThreads][2];
 #pragma unroll
-        for (int u = 0; u < kBsChunk / 256; ++u) {
-            const int l = threadIdx.x + 256 * u, v = c0 + l;
+        for (int u = 0; u < kBsChunk / kBsThreads; ++u) {
+            const int l = threadIdx.x + kBsThreads * u, v = c0 + l;
             const int4 nb = S.nb[l];
             ny[u][0] = (!first && v < M && nb.z) ? __ldg(nin + v + nb.z) : 0.f;
             ny[u][1] = (!first && v < M && nb.w) ? __ldg(nin + v + nb.w) : 0.f;
         }
 #pragma unroll
-        for (int u = 0; u < kBsChunk / 256; ++u) {
-            const int l = threadIdx.x + 256 * u, v = c0 + l;
+        for (int u = 0; u < kBsChunk / kBsThreads; ++u) {
+            const int l = threadIdx.x + kBsThreads * u, v = c0 + l;
             if (v >= M) continue;
             const int4 nb = S.nb[l];
             float nv, bn;

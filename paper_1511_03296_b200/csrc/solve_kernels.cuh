@@ -26,7 +26,8 @@ struct VecArgs {
     const float* diagA;   // diag(A) in Laplacian form; 0 ⇔ dead vertex (reading #6)
     float* x;
     float* r;
-    float2* dn;           // interleaved (d, n): one 8-byte gather per neighbour in the SpMV
+    float2* dn;           // interleaved (d, n) [K][ldn]: one 8-byte gather per neighbour in the SpMV
+    int64_t ldn;          // channel stride of dn: M rounded up to 4 (16-byte aligned bulk copies)
     float* q;
     float* s;
     const float* b;
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
                     const int v = v0u + u * stride;
                     if (v < v1) {
                         xv[u] = a.x[off + v];
-                        dv[u] = a.dn[off + v].x;
+                        dv[u] = a.dn[(size_t)k * a.ldn + v].x;
                         rv[u] = a.r[off + v];
                         qv[u] = a.q[off + v];
                         mv[u] = a.mu0[v];
@@ -347,10 +348,10 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
 // ---------------------------------------------------------------- streaming PCG kernels
 // dn[k][v] = (d, n_v): the direction interleaved with n, so the SpMV's neighbour terms
 // n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
-__global__ void k_init_dn(float2* __restrict__ dn, const float* __restrict__ n, int64_t M, int K) {
+__global__ void k_init_dn(float2* __restrict__ dn, const float* __restrict__ n, int64_t M, int64_t ldn, int K) {
     pdl_entry();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x)
-        dn[i] = make_float2(0.f, n[i % M]);
+        dn[(i / M) * ldn + i % M] = make_float2(0.f, n[i % M]);
 }
 
 // Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
@@ -372,13 +373,13 @@ __global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
                 const int v = v0u + u * stride;
                 if (v < v1) {
                     sv[u] = a.s[off + v];
-                    dv[u] = a.dn[off + v];
+                    dv[u] = a.dn[(size_t)k * a.ldn + v];
                 }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int v = v0u + u * stride;
-                if (v < v1) a.dn[off + v] = make_float2(first ? sv[u] : sv[u] + be * dv[u].x, dv[u].y);
+                if (v < v1) a.dn[(size_t)k * a.ldn + v] = make_float2(first ? sv[u] : sv[u] + be * dv[u].x, dv[u].y);
             }
         }
     }
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
         double dq = 0.0;
         if (a.sc_.active[fk]) {
             const size_t off = (size_t)k * a.M;
-            const float2* dn = a.dn + off;
+            const float2* dn = a.dn + (size_t)k * a.ldn;
             for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
                 const int4 nb = a.nbr[v];
                 const float2 me = dn[v];

@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                         const int v = vb + u * stride;
                         if (v < v1) {
                             xv[u] = a.x[off + v];
-                            dv[u] = a.dn[off + v].x;
+                            dv[u] = a.dn[(size_t)k * a.ldn + v].x;
                             rv[u] = a.r[off + v];
                             qv[u] = a.q[off + v];
                             mv[u] = a.mu0[v];
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
                     } else {
                         sv[u] = (MODE == HIER_PCG) ? a.r[off + v] : in0[off + v];
                         mv[u] = a.mu0[v];
-                        if (MODE == HIER_PCG) dv[u] = a.dn[off + v];
+                        if (MODE == HIER_PCG) dv[u] = a.dn[(size_t)k * a.ldn + v];
                     }
                 }
             }
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
                     out0[off + v] = (mv[u] > 0.f) ? (sv[u] + up[u]) / mv[u] : 0.f;
                 } else {
                     const float s = (mv[u] > 0.f) ? mv[u] * sv[u] + up[u] : 0.f;
-                    if (MODE == HIER_PCG) a.dn[off + v] = make_float2(first ? s : s + be * dv[u].x, dv[u].y);
+                    if (MODE == HIER_PCG) a.dn[(size_t)k * a.ldn + v] = make_float2(first ? s : s + be * dv[u].x, dv[u].y);
                     else out0[off + v] = s;
                 }
             }
