@@ -399,9 +399,9 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
             const size_t off = (size_t)k * a.M;
             const float2* dn = a.dn + (size_t)k * a.ldn;
             for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
-                const int4 nb = a.nbr[v];
+                const int4 nb = __ldcs(a.nbr + v);  // streamed once per iteration: evict-first
                 const float2 me = dn[v];
-                const float scv = a.sc[v];
+                const float scv = __ldcs(a.sc + v);
                 float acc = 0.f;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {

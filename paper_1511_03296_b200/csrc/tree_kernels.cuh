@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
             int id[E];
             float val[E];
 #pragma unroll
-            for (int e = 0; e < E; ++e) id[e] = (lane + 32 * e < n) ? __ldg(h.tord0 + qc + lane + 32 * e) : -1;
+            for (int e = 0; e < E; ++e) id[e] = (lane + 32 * e < n) ? __ldcs(h.tord0 + qc + lane + 32 * e) : -1;
 #pragma unroll
             for (int e = 0; e < E; ++e) val[e] = (id[e] >= 0) ? src[id[e]] : 0.f;
 #pragma unroll
@@ -476,14 +476,14 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
             for (int u = 0; u < 4; ++u) {
                 const int v = vb + u * stride;
                 if (v < v1) {
-                    const int pT = h.parent0T[v];
+                    const int pT = __ldcs(h.parent0T + v);
                     up[u] = acc1(k, pT);
                     if (MODE == HIER_INIT) {
                         sv[u] = in0[off + v];
                         mv[u] = in0[(size_t)K * a.M + v] + acc1(K, pT);
                     } else {
-                        sv[u] = (MODE == HIER_PCG) ? a.r[off + v] : in0[off + v];
-                        mv[u] = a.mu0[v];
+                        sv[u] = (MODE == HIER_PCG) ? __ldcs(a.r + off + v) : in0[off + v];
+                        mv[u] = __ldcs(a.mu0 + v);
                         if (MODE == HIER_PCG) dv[u] = a.dn[(size_t)k * a.ldn + v];
                     }
                 }
