@@ -493,6 +493,68 @@ def solve_backward(sol: FrameSolution, g: np.ndarray, t: np.ndarray, c: np.ndarr
     return dt, dc, db, iters
 
 
+# ----------------------------------------------------------------------------- robust (Supp. §3)
+def gm_rho(e, sigma_gm: float):
+    """Geman–McClure estimator ρ(e) = e² / (σ_gm² + e²)  (Supp. §3)."""
+    e = np.asarray(e, dtype=np.float64)
+    return e * e / (sigma_gm * sigma_gm + e * e)
+
+
+def gm_weight(e, sigma_gm: float):
+    """Its IRLS weight w(e) = 2σ_gm² / (σ_gm² + e²)²  (Alg. 3 line 5)."""
+    e = np.asarray(e, dtype=np.float64)
+    s2 = sigma_gm * sigma_gm
+    return 2.0 * s2 / (s2 + e * e) ** 2
+
+
+def smoothness(sol: FrameSolution) -> float:
+    """λ/2 Σ_ij Ŵ_ij (x_i − x_j)² at x = Sᵀŷ, evaluated in bilateral space as ŷᵀ(A − diag(Sc))ŷ
+    (reading #17: Eq.1(Sᵀy) = yᵀAy − 2bᵀy + (c∘t)ᵀt)."""
+    y = sol.y[:, 0]
+    return float(y @ (sol.sys.A @ y) - y @ (sol.sys.Sc * y))
+
+
+@dataclass
+class RobustSolution:
+    sol: FrameSolution  # the last inner solve (its x is x̂)
+    weights: np.ndarray  # c after the last update (Alg. 3 line 5), [H*W]
+    losses: List[float]  # Eq. robust_loss after each inner solve
+    mm_losses: List[float]  # λ/2 Σ Ŵ (x_i − x_j)² + 2 Σ ρ(e_i): what c ← w minimises exactly (reading #25)
+
+
+def robust_solve_frame(grid: Grid, f: int, t: np.ndarray, c_init: np.ndarray, lam: float, opts: SolveOptions,
+                       sigma_gm: float, n_irls: int) -> RobustSolution:
+    """Alg. 3 "The Geman-McClure Robust Bilateral Solver", verbatim:
+        c ← c_init;  repeat n times:  x̂ ← solve(t, c);  e ← x̂ − t;  c ← 2σ²/(σ² + e∘e)².
+    Scalar targets only (t: [1][H*W]; reading #25).  The grid, n and the smoothness part of A
+    are the same for every inner solve; only diag(S c) and b change."""
+    assert t.shape[0] == 1 and n_irls >= 1 and sigma_gm > 0
+    c = np.asarray(c_init, dtype=np.float64).copy()
+    losses, mm = [], []
+    sol = None
+    for _ in range(n_irls):
+        sol = solve_frame(grid, f, t, c, lam, opts)  # line 3
+        e = sol.x[0] - t[0]  # line 4
+        sm = smoothness(sol)
+        losses.append(sm + float(gm_rho(e, sigma_gm).sum()))
+        mm.append(sm + 2.0 * float(gm_rho(e, sigma_gm).sum()))
+        c = gm_weight(e, sigma_gm)  # line 5
+    return RobustSolution(sol=sol, weights=c, losses=losses, mm_losses=mm)
+
+
+def robust_solve(rgb, t, c_init, sigma_xy, sigma_l, sigma_uv, lam, opts: SolveOptions, sigma_gm: float,
+                 n_irls: int, frames=None):
+    """Batch entry of Alg. 3: rgb [F][H][W][3], t [F][1][H][W], c_init [F][H][W]."""
+    F, H, W, _ = rgb.shape
+    grid = build_grid(rgb, sigma_xy, sigma_l, sigma_uv)
+    out = []
+    for f in (range(F) if frames is None else frames):
+        tf = t[f].reshape(1, H * W).astype(np.float64)
+        cf = c_init[f].reshape(H * W).astype(np.float64)
+        out.append(robust_solve_frame(grid, f, tf, cf, lam, opts, sigma_gm, n_irls))
+    return grid, out
+
+
 # ----------------------------------------------------------------------------- brute force helpers
 def dense_W_hat(S: sp.csr_matrix, Bbar: sp.csr_matrix, m, n) -> np.ndarray:
     """Ŵ = Sᵀ Dm⁻¹ Dn B̄ Dn Dm⁻¹ S  (PAPER.md:114-117 Eq. equiv / :650-652 Eq. What). Tiny inputs only."""

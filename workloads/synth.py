@@ -56,6 +56,9 @@ class Workload:
     n_bistoch: int = 20
     g: Optional[np.ndarray] = None
     labels: Optional[np.ndarray] = field(default=None, repr=False)
+    truth: Optional[np.ndarray] = field(default=None, repr=False)  # clean target (robust configs)
+    sigma_gm: float = 0.0  # robust configs: Geman–McClure scale
+    n_irls: int = 0  # robust configs: IRLS iterations
 
     @property
     def frames(self) -> int:
@@ -197,12 +200,34 @@ def c5_batch(frames=8, W=1920, H=1080, first_frame=0, n_cells=300):
                     labels=np.stack(labs))
 
 
+def rbs_depth(W=640, H=480, seed=1006, n_cells=120, frac=0.10, frames=1, n_irls=8):
+    """Robust bilateral solver workload (Supp. §3): piecewise-planar depth
+    with a fraction of uniform outliers that the confidence does NOT flag (c_init = 1), so the
+    IRLS weights must find them; `truth` is the clean depth.  Stand-in for the Middlebury stereo
+    post-processing experiment, whose MC-CNN depth maps are not available."""
+    rgbs, ts, cs, tr = [], [], [], []
+    for f in range(frames):
+        rng = np.random.default_rng(seed + 100 * f)
+        rgb, lab, seeds = voronoi_reference(rng, W, H, n_cells, "gradient", 3.0)
+        d = planar_depth(rng, lab, seeds)
+        out = rng.uniform(0, 1, (H, W)) < frac
+        t = np.where(out, rng.uniform(0, 255, (H, W)), d)
+        rgbs.append(rgb)
+        ts.append(t[None].astype(np.float32))
+        cs.append(np.ones((H, W), np.float32))
+        tr.append(d.astype(np.float32))
+    return Workload("rbs_depth", np.stack(rgbs), np.stack(ts), np.stack(cs), 8.0, 4.0, 3.0, 128.0,
+                    precond="hier", init="hier", mode="fixed", iters=25, tol=1e-6,
+                    truth=np.stack(tr), sigma_gm=10.0, n_irls=n_irls)
+
+
 CONFIGS = {
     "c1": c1_tiny,
     "c2": c2_depth_refine,
     "c3": c3_depth_sr,
     "c4": c4_multichannel,
     "c5": c5_batch,
+    "rbs": rbs_depth,
 }
 
 
