@@ -150,6 +150,21 @@ int fbs_solve(fbs_grid g, const float* t_dev, int K, const float* c_dev, double 
               const fbs_solve_opts* opts, float* x_dev, float* y_dev, fbs_system* sys_out,
               fbs_stream stream);
 
+/* Robust bilateral solver (Supp. §3, Alg. 3 "The Geman-McClure Robust Bilateral Solver",
+ * PAPER.md:798-813):  c ← c_init;  n_irls times:  x̂ ← solve(t, c);  e ← x̂ − t;
+ * c ← 2σ_gm² / (σ_gm² + e∘e)².  Every inner solve is fbs_solve with `opts` on the same grid
+ * (n, pyramid and the smoothness part of A are reused; only diag(S c) and b change).
+ *   t_dev       float [frames][1][H][W]   scalar targets (K = 1, reading #25)
+ *   c_init_dev  float [frames][H][W]      initial confidences, ≥ 0 (read only)
+ *   sigma_gm    > 0                        Geman–McClure scale
+ *   n_irls      ≥ 1                        IRLS iterations (the paper uses 32)
+ *   x_dev       float [frames][1][H][W]   output: x̂ of the last inner solve
+ *   c_out_dev   float [frames][H][W] or NULL   the weights after the last update (line 5)
+ * Errors: as fbs_solve, plus FBS_EINVAL for K ≠ 1, σ_gm ≤ 0 or n_irls < 1. */
+int fbs_solve_robust(fbs_grid g, const float* t_dev, int K, const float* c_init_dev, double lambda,
+                     const fbs_solve_opts* opts, double sigma_gm, int n_irls, float* x_dev,
+                     float* c_out_dev, fbs_stream stream);
+
 /* Backward pass: given g = ∂f/∂x̂ [frames][K][H][W], solve A d = S g
  * with the forward's preconditioner and stopping rule from d = 0 (reading #14), then
  *   ∂f/∂t = c ∘ Sᵀd              → dt_dev float [frames][K][H][W]

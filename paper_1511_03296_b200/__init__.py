@@ -16,6 +16,7 @@ from .fbs import (  # noqa: F401
     profile_reset,
     slice_,
     solve,
+    solve_robust,
     splat,
     version,
 )

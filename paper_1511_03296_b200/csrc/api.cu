@@ -797,6 +797,32 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
     }
 }
 
+// Alg. 3: IRLS around the solver with Geman–McClure weights.
+static void robust_impl(fbs_grid g, const float* t, int K, const float* c_init, double lam, const fbs_solve_opts* opts,
+                        double sigma_gm, int n_irls, float* x, float* c_out, cudaStream_t s) {
+    if (!g || !t || !c_init || !x) throw Err(FBS_EINVAL, "null pointer");
+    if (K != 1) throw Err(FBS_EINVAL, "the robust solver takes scalar targets (K = 1)");
+    if (!(sigma_gm > 0.0) || !std::isfinite(sigma_gm)) throw Err(FBS_EINVAL, "sigma_gm must be finite and > 0");
+    if (n_irls < 1) throw Err(FBS_EINVAL, "n_irls must be >= 1");
+    std::vector<void*> tmp;
+    float* c = (n_irls > 1 || c_out) ? (c_out ? c_out : dalloc<float>(tmp, g->N, s)) : nullptr;
+    try {
+        const float* cur = c_init;
+        const float s2 = (float)(sigma_gm * sigma_gm);
+        for (int i = 0; i < n_irls; ++i) {
+            solve_impl(g, t, 1, cur, lam, opts, x, nullptr, nullptr, s);  // line 3
+            if (i + 1 < n_irls || c_out) {                                // lines 4-5
+                LAUNCH(k_gm_weight, grid_for(g->N), kThreads, 0, s, x, t, g->N, s2, c);
+                cur = c;
+            }
+        }
+    } catch (...) {
+        free_all(tmp, s);
+        throw;
+    }
+    free_all(tmp, s);
+}
+
 static void backward_impl(fbs_system S, const float* g_dldx, const float* t, const float* c, float* dt, float* dc,
                           cudaStream_t s) {
     if (!S || !g_dldx || !t || !c || !dt || !dc) throw Err(FBS_EINVAL, "null pointer");
@@ -952,6 +978,13 @@ void fbs_grid_destroy(fbs_grid g) {
 int fbs_solve(fbs_grid g, const float* t, int K, const float* c, double lam, const fbs_solve_opts* opts, float* x,
               float* y, fbs_system* sys_out, fbs_stream stream) {
     return guard("fbs_solve", [&] { solve_impl(g, t, K, c, lam, opts, x, y, sys_out, (cudaStream_t)stream); });
+}
+
+int fbs_solve_robust(fbs_grid g, const float* t, int K, const float* c_init, double lam, const fbs_solve_opts* opts,
+                     double sigma_gm, int n_irls, float* x, float* c_out, fbs_stream stream) {
+    return guard("fbs_solve_robust", [&] {
+        robust_impl(g, t, K, c_init, lam, opts, sigma_gm, n_irls, x, c_out, (cudaStream_t)stream);
+    });
 }
 
 int fbs_solve_backward(fbs_system S, const float* dldx, const float* t, const float* c, float* dt, float* dc,

@@ -465,6 +465,17 @@ __global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ y
     }
 }
 
+// Alg. 3 line 4-5: e = x̂ − t, c = 2σ² / (σ² + e²)² per pixel (K = 1).
+__global__ void k_gm_weight(const float* __restrict__ x, const float* __restrict__ t, int64_t N, float s2,
+                            float* __restrict__ c) {
+    pdl_entry();
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
+        const float e = x[p] - t[p];
+        const float d = s2 + e * e;
+        c[p] = 2.f * s2 / (d * d);
+    }
+}
+
 // planar [K][M] → canonical [M][K]
 __global__ void k_export_vk(const float* __restrict__ src, int64_t M, int K, float* __restrict__ dst) {
     pdl_entry();

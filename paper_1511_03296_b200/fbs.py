@@ -48,6 +48,7 @@ _SIGS = {
     "fbs_pyramid_export": (_i, [_vp, _i, _vp, _vp, _vp]),
     "fbs_grid_destroy": (None, [_vp]),
     "fbs_solve": (_i, [_vp, _vp, _i, _vp, _d, C.POINTER(SolveOpts), _vp, _vp, C.POINTER(_vp), _vp]),
+    "fbs_solve_robust": (_i, [_vp, _vp, _i, _vp, _d, C.POINTER(SolveOpts), _d, _i, _vp, _vp, _vp]),
     "fbs_solve_backward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fbs_system_stats": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "fbs_system_export": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -296,6 +297,23 @@ def solve(grid: Grid, t: torch.Tensor, c: torch.Tensor, lam: float, want_y: bool
     if keep_system:
         res.append(System(h, grid, K))
     return res[0] if len(res) == 1 else tuple(res)
+
+
+def solve_robust(grid: Grid, t: torch.Tensor, c_init: torch.Tensor, lam: float, sigma_gm: float, n_irls: int,
+                 want_weights: bool = False, stream=None, out: Optional[torch.Tensor] = None, **opts):
+    """fbs_solve_robust (Supp. Alg. 3): t float32 [F][1][H][W], c_init float32 [F][H][W] →
+    x [F][1][H][W] (+ the final IRLS weights [F][H][W] if want_weights)."""
+    t = _dev_tensor(t, torch.float32, "t", 4)
+    c_init = _dev_tensor(c_init, torch.float32, "c_init", 3)
+    F, K, H, W = t.shape
+    if (F, H, W) != (grid.frames, grid.H, grid.W) or tuple(c_init.shape) != (F, H, W):
+        raise ValueError("t/c_init shapes do not match the grid")
+    x = torch.empty_like(t) if out is None else out
+    w = torch.empty_like(c_init) if want_weights else None
+    o = make_opts(**opts)
+    _check(_lib.fbs_solve_robust(grid.handle, _ptr(t), K, _ptr(c_init), float(lam), C.byref(o), float(sigma_gm),
+                                 int(n_irls), _ptr(x), _ptr(w), _stream(stream)))
+    return (x, w) if want_weights else x
 
 
 # ----------------------------------------------------------------------------- operators
