@@ -555,6 +555,67 @@ def robust_solve(rgb, t, c_init, sigma_xy, sigma_l, sigma_uv, lam, opts: SolveOp
     return grid, out
 
 
+# ----------------------------------------------------------------------------- low-rank RHS (Supp. §4)
+@dataclass
+class ReducedRHS:
+    Q: np.ndarray  # [M][t] orthonormal columns  (Q̃ = Q'[:, :t])
+    R: np.ndarray  # [t][K]                     (R̃ = (R' Pᵀ)[:t, :])
+    t: int
+    masses: np.ndarray  # m_i of the rows of R', non-increasing
+
+
+def reduce_rhs(B: np.ndarray, eps: float) -> ReducedRHS:
+    """Rank reduction of the right-hand sides B [M][K] (Supp. §4):
+    B P = Q R (column-pivoted QR; scipy.linalg.qr as the library step), R' = rows of R Pᵀ
+    sorted by non-increasing squared norm m_i with Q' = the columns of Q in the same order,
+    t = the smallest count with Σ_{i<t} m_i ≥ (1 − ε) Σ_i m_i (reading #26: the displayed
+    inequality is inverted relative to the prose), Q̃ = Q'[:, :t], R̃ = R'[:t, :]."""
+    import scipy.linalg as sla
+    assert 0.0 <= eps < 1.0
+    M, K = B.shape
+    Q, R, piv = sla.qr(B, mode="economic", pivoting=True)  # B[:, piv] = Q R
+    RPt = np.zeros_like(R)
+    RPt[:, piv] = R  # R Pᵀ: columns back in channel order
+    m = np.sum(RPt * RPt, axis=1)
+    order = np.argsort(-m, kind="stable")
+    m = m[order]
+    total = float(m.sum())
+    if total == 0.0:
+        return ReducedRHS(Q=np.zeros((M, 0)), R=np.zeros((0, K)), t=0, masses=m)
+    cum = np.cumsum(m)
+    t = int(np.searchsorted(cum, (1.0 - eps) * total - 1e-12 * total) + 1)
+    t = min(t, K)
+    return ReducedRHS(Q=Q[:, order[:t]], R=RPt[order[:t], :], t=t, masses=m)
+
+
+def solve_frame_lowrank(grid: Grid, f: int, t: np.ndarray, c: np.ndarray, lam: float, opts: SolveOptions,
+                        eps: float):
+    """Y = (A⁻¹ Q̃) R̃ (Supp. §4): solve the t reduced systems A ỹ_i = Q̃_i (initialised and
+    preconditioned as the full solve would be, with Q̃ in place of b) and expand by R̃;
+    x̂ = Sᵀ Y.  Returns (x [K][H*W], Y [M][K], ReducedRHS)."""
+    full = solve_frame(grid, f, t, c, lam, SolveOptions(**{**opts.__dict__, "mode": "fixed", "iters": 0}))
+    red = reduce_rhs(full.sys.b, eps)
+    sysr = System(A=full.sys.A, b=red.Q, Sc=full.sys.Sc, diagA=full.sys.diagA, live=full.sys.live,
+                  c0=np.zeros(red.t))
+    if opts.init == "hier":
+        y0 = hier_init(full.pyr, sysr, opts.init_alpha, opts.init_beta)
+    elif opts.init == "flat":
+        y0 = flat_init(sysr)
+    else:
+        y0 = np.zeros_like(red.Q)
+    Aop = lambda v: full.sys.A @ v  # noqa: E731
+    Yr = np.zeros((full.sys.A.shape[0], red.t))
+    for i in range(red.t):
+        if opts.mode == "fixed":
+            r = pcg(Aop, red.Q[:, i], y0[:, i], full.Minv, opts.iters, None)
+        else:
+            r = pcg(Aop, red.Q[:, i], y0[:, i], full.Minv, opts.max_iters, opts.tol)
+        Yr[:, i] = r.x
+    Y = Yr @ red.R
+    x = np.stack([full.S.T @ Y[:, k] for k in range(Y.shape[1])])
+    return x, Y, red
+
+
 # ----------------------------------------------------------------------------- brute force helpers
 def dense_W_hat(S: sp.csr_matrix, Bbar: sp.csr_matrix, m, n) -> np.ndarray:
     """Ŵ = Sᵀ Dm⁻¹ Dn B̄ Dn Dm⁻¹ S  (PAPER.md:114-117 Eq. equiv / :650-652 Eq. What). Tiny inputs only."""
