@@ -86,6 +86,9 @@ typedef struct {
     double precond_beta;
     double init_alpha;    /* z_weight α, β of the initialisation; default 4, 0    */
     double init_beta;
+    double lowrank_eps;   /* > 0 (K > 1): low-rank reduction of the right-hand sides (Supp. §4,  */
+                          /* PAPER.md:867-900): solve only the rows of R' holding ≥ (1 − ε) of  */
+                          /* the mass, Y = (A⁻¹Q̃)R̃ (reading #26); 0 = off (default)            */
 } fbs_solve_opts;
 
 void fbs_default_grid_opts(fbs_grid_opts* o);
@@ -144,6 +147,8 @@ void fbs_grid_destroy(fbs_grid g);
  *   sys_out    receives the system handle (A-state, M⁻¹, ŷ) for fbs_solve_backward and
  *              the stats/export calls; NULL = destroy it after the solve.
  * Each (frame, channel) runs its own PCG scalars and stopping rule (reading #13).
+ * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4); the reduced solve
+ * runs max_f t_f channels (one extra host synchronisation), and sys_out must then be NULL.
  * Errors: FBS_EINVAL (NULL pointer, K ∉ [1, 64], λ ≤ 0 or not finite, HIER precond/init
  * on a grid built without pyramid, bad opts); FBS_ENOMEM; FBS_ECUDA. */
 int fbs_solve(fbs_grid g, const float* t_dev, int K, const float* c_dev, double lambda,

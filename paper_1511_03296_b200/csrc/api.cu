@@ -17,6 +17,7 @@
 #include "pyramid_kernels.cuh"
 #include "solve_kernels.cuh"
 #include "tree_kernels.cuh"
+#include "lowrank_kernels.cuh"
 
 namespace fbs {
 
@@ -677,6 +678,7 @@ void validate_opts(const fbs_solve_opts& o, fbs_grid g) {
         throw Err(FBS_EINVAL, "hierarchical precond/init need a grid built with build_pyramid = 1");
     if (o.precond == FBS_PRECOND_HIER && !(o.precond_alpha > 0.0)) throw Err(FBS_EINVAL, "precond_alpha must be > 0");
     if (o.init == FBS_INIT_HIER && !(o.init_alpha > 0.0)) throw Err(FBS_EINVAL, "init_alpha must be > 0");
+    if (!(o.lowrank_eps >= 0.0 && o.lowrank_eps < 1.0)) throw Err(FBS_EINVAL, "lowrank_eps must be in [0, 1)");
 }
 
 }  // namespace
@@ -692,10 +694,12 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
     int dev = 0;
     device_setup(&dev);
 
+    const bool lowrank = o.lowrank_eps > 0.0 && K > 1;
+    if (lowrank && sys_out) throw Err(FBS_EINVAL, "a low-rank solve keeps no system (sys_out must be NULL)");
+
     fbs_system S = new fbs_system_s();
     try {
         S->g = g;
-        S->K = K;
         S->lam = lam;
         S->o = o;
         S->stream = s;
@@ -707,16 +711,47 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int64_t want = (g->maxFrameM + kThreads - 1) / kThreads;
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
         S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
-        S->C = K + 1;
-        const size_t KM = (size_t)K * M;
         S->sc = dalloc<float>(A, M + kVecPad, s);
-        S->b = dalloc<float>(A, KM, s);
+        float* bIn = dalloc<float>(A, (size_t)K * M, s);
+        CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
+        // a4: splat Sc, b = S(c∘t)
+        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t,
+               K, M, S->sc, bIn);
+        // optional low-rank reduction of B (Supp. §4): Kc reduced channels
+        int Kc = K;
+        double* lrRt = nullptr;
+        if (lowrank) {
+            const int P = K * (K + 1) / 2;
+            const int bpfG = std::min(S->BPF, 64);
+            double* part = dalloc<double>(A, (size_t)F * bpfG * P, s);
+            unsigned* ctr = dalloc<unsigned>(A, F, s);
+            double* G = dalloc<double>(A, (size_t)F * K * K, s);
+            double* T = dalloc<double>(A, (size_t)F * K * K, s);
+            lrRt = dalloc<double>(A, (size_t)F * K * K, s);
+            int* tF = dalloc<int>(A, F, s);
+            ck(cudaMemsetAsync(ctr, 0, F * sizeof(unsigned), s), "memset");
+            LAUNCH(k_gram, F * bpfG, 256, 0, s, bIn, M, K, g->frameOff, bpfG, part, ctr, G);
+            LAUNCH(k_pchol, F, 64, 0, s, G, K, o.lowrank_eps, tF, lrRt, T);
+            std::vector<int> tH(F);
+            ck(cudaMemcpyAsync(tH.data(), tF, F * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+            ck(cudaStreamSynchronize(s), "sync");
+            Kc = 1;
+            for (int f = 0; f < F; ++f) Kc = std::max(Kc, tH[f]);
+            S->lr_rank.assign(tH.begin(), tH.end());
+            S->b = dalloc<float>(A, (size_t)Kc * M, s);
+            LAUNCH(k_reduce_rhs, F * S->BPF, kThreads, 0, s, bIn, M, K, Kc, g->frameOff, S->BPF, T, S->b);
+        } else {
+            S->b = bIn;
+        }
+        S->K = Kc;
+        S->C = Kc + 1;
+        const size_t KM = (size_t)Kc * M;
         S->diagA = dalloc<float>(A, M, s);
         S->mu0 = dalloc<float>(A, M, s);
         S->y0 = dalloc<float>(A, KM, s);
         S->xh = dalloc<float>(A, KM, s);
         S->rh = dalloc<float>(A, KM, s);
-        S->dn = dalloc<float2>(A, (size_t)K * ((M + 3) & ~3ll) + kVecPad, s);
+        S->dn = dalloc<float2>(A, (size_t)Kc * ((M + 3) & ~3ll) + kVecPad, s);
         S->qh = dalloc<float>(A, KM, s);
         S->sh = dalloc<float>(A, KM, s);
         const bool hierP = o.precond == FBS_PRECOND_HIER && g->L > 1;  // L = 1: hier ≡ Jacobi / flat
@@ -740,17 +775,13 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             }
             if (g->L > 3) S->ancMult = dalloc<float>(A, (size_t)(g->L - 3) * g->lv[2].M, s);
         }
-        S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * K, s);
+        S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
         S->counters = dalloc<unsigned>(A, F, s);
         ck(cudaMemsetAsync(S->counters, 0, F * sizeof(unsigned), s), "memset");
-        if (hierP || hierI) S->hP = make_hier(S, K, o.precond_alpha, o.precond_beta);
-        S->fwd = alloc_scalars(A, F * K, s);
+        if (hierP || hierI) S->hP = make_hier(S, Kc, o.precond_alpha, o.precond_beta);
+        S->fwd = alloc_scalars(A, F * Kc, s);
 
         const int nb = F * S->BPF;
-        CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
-        // a4: splat Sc, b = S(c∘t)
-        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t, K, M, S->sc,
-               S->b);
         // a5: assemble (+ flat/zero init)
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
         const int init_mode = (o.init == FBS_INIT_HIER && !hierI) ? FBS_INIT_FLAT : o.init;
@@ -763,8 +794,8 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
 
         }
         if (hierI) {
-            HierArgs h = make_hier(S, K + 1, o.init_alpha, o.init_beta);
-            LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, K, S->w0);
+            HierArgs h = make_hier(S, Kc + 1, o.init_alpha, o.init_beta);
+            LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, Kc, S->w0);
             if (g->L > 3) {
                 auto km = k_tree_anc_mult<HIER_INIT>;
                 LAUNCH_AS("k_tree_anc_mult<INIT>", km, F * S->bpf2, kThreads, 0, s, h, g->tree.ancId, S->ancMult);
@@ -778,12 +809,19 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             LAUNCH_AS("k_tree_anc_mult<PCG>", km, F * S->bpf2, kThreads, 0, s, S->hP, g->tree.ancId, S->ancMult);
         }
         ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
-        LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, (int64_t)((M + 3) & ~3ll), K);
+        LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, (int64_t)((M + 3) & ~3ll), Kc);
         // a8: PCG
         run_pcg(S, a, false, s);
+        // low rank: Y = Ỹ R̃ (Supp. §4)
+        const float* ysol = S->xh;
+        if (lowrank) {
+            float* yfull = dalloc<float>(A, (size_t)K * M, s);
+            LAUNCH(k_expand, F * S->BPF, kThreads, 0, s, S->xh, M, K, Kc, g->frameOff, S->BPF, lrRt, yfull);
+            ysol = yfull;
+        }
         // a9: slice
-        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, S->xh, M, K, F, (int64_t)g->H * g->W, 1, x);
-        if (y) LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, S->xh, M, K, y);
+        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, ysol, M, K, F, (int64_t)g->H * g->W, 1, x);
+        if (y) LAUNCH(k_export_vk, grid_for((size_t)K * M), kThreads, 0, s, ysol, M, K, y);
     } catch (...) {
         free_all(S->allocs, s);
         delete S;
@@ -891,6 +929,7 @@ void fbs_default_solve_opts(fbs_solve_opts* o) {
     o->precond_beta = 5.0;
     o->init_alpha = 4.0;
     o->init_beta = 0.0;
+    o->lowrank_eps = 0.0;
 }
 
 int fbs_grid_build(const uint8_t* rgb, int frames, int height, int width, double sxy, double sl, double suv,

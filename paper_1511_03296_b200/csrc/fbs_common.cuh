@@ -379,5 +379,6 @@ struct fbs_system_s {
     bool useHierP = false;
     fbs::HierArgs hP{};
     bool has_backward = false;
+    std::vector<int> lr_rank;  // low-rank solves: kept rank t_f per frame
     std::vector<void*> allocs;
 };

@@ -35,7 +35,8 @@ class GridOpts(C.Structure):
 class SolveOpts(C.Structure):
     _fields_ = [("precond", C.c_int), ("init", C.c_int), ("mode", C.c_int), ("iters", C.c_int),
                 ("tol", C.c_double), ("max_iters", C.c_int), ("precond_alpha", C.c_double),
-                ("precond_beta", C.c_double), ("init_alpha", C.c_double), ("init_beta", C.c_double)]
+                ("precond_beta", C.c_double), ("init_alpha", C.c_double), ("init_beta", C.c_double),
+                ("lowrank_eps", C.c_double)]
 
 
 _vp, _i, _d, _i64 = C.c_void_p, C.c_int, C.c_double, C.c_int64
@@ -206,9 +207,10 @@ def grid_build(rgb: torch.Tensor, sigma_xy: float, sigma_l: float, sigma_uv: flo
 
 # ----------------------------------------------------------------------------- solve
 def make_opts(precond="hier", init="hier", mode="fixed", iters=25, tol=1e-6, max_iters=2000,
-              precond_alpha=2.0, precond_beta=5.0, init_alpha=4.0, init_beta=0.0) -> SolveOpts:
+              precond_alpha=2.0, precond_beta=5.0, init_alpha=4.0, init_beta=0.0, lowrank_eps=0.0) -> SolveOpts:
     return SolveOpts(PRECOND[precond], INIT[init], MODE[mode], int(iters), float(tol), int(max_iters),
-                     float(precond_alpha), float(precond_beta), float(init_alpha), float(init_beta))
+                     float(precond_alpha), float(precond_beta), float(init_alpha), float(init_beta),
+                     float(lowrank_eps))
 
 
 class System:

@@ -77,11 +77,16 @@ def test_default_opts(lib):
     class SolveOpts(ctypes.Structure):
         _fields_ = [("precond", ctypes.c_int), ("init", ctypes.c_int), ("mode", ctypes.c_int), ("iters", ctypes.c_int),
                     ("tol", ctypes.c_double), ("max_iters", ctypes.c_int), ("precond_alpha", ctypes.c_double),
-                    ("precond_beta", ctypes.c_double), ("init_alpha", ctypes.c_double), ("init_beta", ctypes.c_double)]
+                    ("precond_beta", ctypes.c_double), ("init_alpha", ctypes.c_double), ("init_beta", ctypes.c_double),
+                    ("lowrank_eps", ctypes.c_double)]
     o = SolveOpts()
     lib.fbs_default_solve_opts(ctypes.byref(o))
-    # PAPER.md:285 (α=2, β=5), :293 (α=4, β=0), :334 (25 iterations)
+    # PAPER.md:285 (α=2, β=5), :293 (α=4, β=0), :334 (25 iterations); low-rank reduction off
     assert (o.precond_alpha, o.precond_beta, o.init_alpha, o.init_beta, o.iters) == (2.0, 5.0, 4.0, 0.0, 25)
+    assert o.lowrank_eps == 0.0
+    # the binding's struct has the same layout as the header's
+    import paper_1511_03296_b200.fbs as F
+    assert ctypes.sizeof(F.SolveOpts) == ctypes.sizeof(SolveOpts)
 
 
 def test_oracle_is_not_imported_by_product():
