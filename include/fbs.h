@@ -67,6 +67,8 @@ typedef struct fbs_system_s* fbs_system;
 typedef struct {
     int n_bistoch;     /* Alg. 1 iterations, fixed count (reading #5); default 20          */
     int build_pyramid; /* 1: build the Supp. Sec. 2 pyramid (needed by HIER precond/init) */
+    int dims;          /* D: 5 = XYLUV grid (default); 3 = XYL grid of a grayscale reference */
+                       /* (chroma not used, B̄ = 2·3·I + Adj, reading #27)     */
 } fbs_grid_opts;
 
 enum { FBS_PRECOND_JACOBI = 0, FBS_PRECOND_HIER = 1 };

@@ -89,6 +89,7 @@ class Grid:
     nbr: np.ndarray  # int64 [M][10] ±1 neighbours per dim, −1 if absent
     frames: int
     frame_start: np.ndarray  # int64 [F+1] first vertex of each frame
+    dims: int = 5  # D: 5 = XYLUV (colour), 3 = XYL (grayscale reference, reading #27)
 
     @property
     def M(self) -> int:
@@ -140,18 +141,24 @@ def find_neighbours(V: np.ndarray) -> np.ndarray:
     return nbr
 
 
-def build_grid(rgb: np.ndarray, sigma_xy: float, sigma_l: float, sigma_uv: float) -> Grid:
+def build_grid(rgb: np.ndarray, sigma_xy: float, sigma_l: float, sigma_uv: float, dims: int = 5) -> Grid:
     """Simplified bilateral grid: unique occupied coordinates, hard splat map, counts,
-    neighbours (PAPER.md:114-116 Eq. equiv, :664 m ← S1; readings #2, #3)."""
+    neighbours (PAPER.md:114-116 Eq. equiv, :664 m ← S1; readings #2, #3).
+    dims = 3: the XYL grid of a grayscale reference (reading #27): the chroma
+    coordinates are not used (held at 0)."""
+    assert dims in (3, 5)
     F = rgb.shape[0]
     P = pixel_coords(rgb, sigma_xy, sigma_l, sigma_uv)
+    if dims == 3:
+        P[:, COL["u"]] = 0
+        P[:, COL["v"]] = 0
     # np.unique(axis=0) sorts rows lexicographically by (frame, by, bx, bl, bu, bv)
     # = ascending packed key (reading #3 canonical order).
     V, vid, m = np.unique(P, axis=0, return_inverse=True, return_counts=True)
     vid = vid.reshape(-1)
     frame_start = np.searchsorted(V[:, 0], np.arange(F + 1))
     return Grid(V=V, vid=vid.astype(np.int64), m=m.astype(np.int64), nbr=find_neighbours(V),
-                frames=F, frame_start=frame_start.astype(np.int64))
+                frames=F, frame_start=frame_start.astype(np.int64), dims=dims)
 
 
 def splat_matrix(vid: np.ndarray, M: int) -> sp.csr_matrix:
@@ -160,12 +167,13 @@ def splat_matrix(vid: np.ndarray, M: int) -> sp.csr_matrix:
     return sp.csr_matrix((np.ones(N), (vid, np.arange(N))), shape=(M, N))
 
 
-def blur_matrix(nbr: np.ndarray) -> sp.csr_matrix:
-    """B̄ = 2D·I + Σ_d (E_d⁺ + E_d⁻): sum of 1-D [1 2 1] blurs (reading #4)."""
+def blur_matrix(nbr: np.ndarray, dims: int = D) -> sp.csr_matrix:
+    """B̄ = 2D·I + Σ_d (E_d⁺ + E_d⁻): sum of 1-D [1 2 1] blurs over the D grid dimensions
+    (PAPER.md:233, reading #4; D = 3 for a grayscale reference, reading #27)."""
     M = nbr.shape[0]
     rows, cols = np.nonzero(nbr >= 0)
     adj = sp.csr_matrix((np.ones(rows.size), (rows, nbr[rows, cols])), shape=(M, M))
-    return (BBAR_DIAG * sp.identity(M, format="csr") + adj).tocsr()
+    return (2 * dims * sp.identity(M, format="csr") + adj).tocsr()
 
 
 def bistochastize(m: np.ndarray, Bbar: sp.csr_matrix, n_iters: int = 20):
@@ -208,7 +216,8 @@ def assemble(S: sp.csr_matrix, Bbar: sp.csr_matrix, m, n, nbr, t: np.ndarray, c:
     fix = np.where(isolated, -A_smooth.diagonal(), 0.0)
     A = (A_smooth + sp.diags(fix) + sp.diags(Sc)).tocsr()
     # diag(A) per PAPER.md:230: λ(diag Dm − diag Dn · B̄_diag · diag Dn) + S c
-    diagA = lam * (m - n * BBAR_DIAG * n) + Sc
+    bdiag = Bbar.diagonal()  # the constant 2D (reading #4)
+    diagA = lam * (m - n * bdiag * n) + Sc
     diagA = np.where(isolated, Sc, diagA)
     live = ~(isolated & (Sc == 0))
     c0 = 0.5 * np.array([np.dot(c * tk, tk) for tk in t])
@@ -418,7 +427,7 @@ def solve_frame(grid: Grid, f: int, t: np.ndarray, c: np.ndarray, lam: float,
     nbr = np.where(grid.nbr[v0:v1] >= 0, grid.nbr[v0:v1] - v0, -1)
     M = v1 - v0
     S = splat_matrix(vid, M)
-    Bbar = blur_matrix(nbr)
+    Bbar = blur_matrix(nbr, grid.dims)
     n, res = bistochastize(m, Bbar, opts.n_bistoch)
     sysm = assemble(S, Bbar, m, n, nbr, t, c, lam)
     pyr = build_pyramid(V) if (opts.precond == "hier" or opts.init == "hier") else None
@@ -451,10 +460,10 @@ def solve_frame(grid: Grid, f: int, t: np.ndarray, c: np.ndarray, lam: float,
                          y0=y0, y=y, x=x, iterations=iters, relres=rel, Minv=Minv, S=S, vid=vid)
 
 
-def solve(rgb, t, c, sigma_xy, sigma_l, sigma_uv, lam, opts: SolveOptions, frames=None):
+def solve(rgb, t, c, sigma_xy, sigma_l, sigma_uv, lam, opts: SolveOptions, frames=None, dims: int = 5):
     """Batch entry: rgb [F][H][W][3], t [F][K][H][W], c [F][H][W] → (grid, [FrameSolution])."""
     F, H, W, _ = rgb.shape
-    grid = build_grid(rgb, sigma_xy, sigma_l, sigma_uv)
+    grid = build_grid(rgb, sigma_xy, sigma_l, sigma_uv, dims)
     sols = []
     for f in (range(F) if frames is None else frames):
         tf = t[f].reshape(t.shape[1], H * W).astype(np.float64)

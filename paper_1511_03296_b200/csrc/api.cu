@@ -197,6 +197,8 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->F = F; g->H = H; g->W = W; g->sxy = sxy; g->sl = sl; g->suv = suv;
         g->ncx = ncx; g->ncy = ncy; g->ncells = (int64_t)F * ncx * ncy; g->N = N;
         g->n_bistoch = opts ? opts->n_bistoch : 20;
+        g->dims = opts ? opts->dims : 5;
+        if (g->dims != 5 && g->dims != 3) throw Err(FBS_EINVAL, "dims must be 5 or 3");
         if (g->n_bistoch < 0) throw Err(FBS_EINVAL, "n_bistoch must be >= 0");
         const bool want_pyr = opts ? opts->build_pyramid != 0 : true;
         g->stream = s;
@@ -225,7 +227,8 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         uint8_t* lutL = dalloc<uint8_t>(A, 65536, s);
         uint8_t* lutUV = dalloc<uint8_t>(A, 65536, s);
         LAUNCH(k_bin_lut, 256, 256, 0, s, 256.0 * sl, lutL);
-        LAUNCH(k_bin_lut, 256, 256, 0, s, 256.0 * suv, lutUV);
+        // D = 3: the chroma bins are held at 0 (reading #27)
+        LAUNCH(k_bin_lut, 256, 256, 0, s, g->dims == 3 ? 1e300 : 256.0 * suv, lutUV);
         g->perm = dalloc<uint8_t>(A, (size_t)g->ncells * kCellMaxPx, s);
         int* cellCnt = dalloc<int>(A, g->ncells, s);
         unsigned long long* heads = dalloc<unsigned long long>(A, g->ncells, s);
@@ -264,7 +267,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         for (int it = 0; it < g->n_bistoch; ++it) {
             const int nch = (int)((M + kBsChunk - 1) / kBsChunk);
             LAUNCH(k_bistoch, std::max(1, std::min(nch, 3 * (g_num_sms > 0 ? g_num_sms : 148))), kBsThreads, kBsSmem, s,
-                   g->nbr, g->m, cur, nxt, (int)M, it == 0);
+                   g->nbr, g->m, cur, nxt, (int)M, it == 0, (float)(2 * g->dims));
             std::swap(cur, nxt);
         }
         if (g->n_bistoch == 0) {
@@ -915,6 +918,7 @@ void fbs_default_grid_opts(fbs_grid_opts* o) {
     if (!o) return;
     o->n_bistoch = 20;
     o->build_pyramid = 1;
+    o->dims = 5;
 }
 
 void fbs_default_solve_opts(fbs_solve_opts* o) {
@@ -978,7 +982,8 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
                 std::vector<void*> tmp;
                 unsigned* d = dalloc<unsigned>(tmp, 2, s);
                 ck(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned), s), "memset");
-                LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, d);
+                LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, d,
+                       (float)(2 * g->dims));
                 unsigned h2[2];
                 ck(cudaMemcpyAsync(h2, d, sizeof(h2), cudaMemcpyDeviceToHost, s), "d2h");
                 ck(cudaStreamSynchronize(s), "sync");
@@ -1123,7 +1128,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
 int fbs_blur(fbs_grid g, const float* v, float* out, fbs_stream stream) {
     return guard("fbs_blur", [&] {
         if (!g || !v || !out) throw Err(FBS_EINVAL, "null pointer");
-        LAUNCH(k_blur, grid_for(g->M), kThreads, 0, (cudaStream_t)stream, g->nbr, v, g->M, out);
+        LAUNCH(k_blur, grid_for(g->M), kThreads, 0, (cudaStream_t)stream, g->nbr, v, g->M, (float)(2 * g->dims), out);
     });
 }
 

@@ -14,7 +14,6 @@
 namespace fbs {
 
 constexpr int kD = 5;                // XYLUV dims
-constexpr int kBbarDiag = 2 * kD;    // B̄_diag = 2D (reading #4)
 constexpr int kCellMaxPx = 64;       // level-0 cell = one warp, ≤ 2 px per lane
 constexpr int kCellsPerBlock = 8;    // 8 warps, one cell each
 constexpr int kCoarseCap = 512;      // children of one pyramid coarse cell sorted in shared memory (larger: global scratch)
@@ -314,6 +313,7 @@ struct fbs_grid_s {
     int ncx = 0, ncy = 0;
     int64_t ncells = 0, N = 0, M = 0;
     int n_bistoch = 20;
+    int dims = 5;               // D (5: XYLUV; 3: XYL of a grayscale reference)
     bool has_pyramid = false;
     cudaStream_t stream = nullptr;
     int device = 0;

@@ -329,7 +329,7 @@ constexpr size_t kBsSmem = 2 * sizeof(BsStage) + 64;
 __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
-                                                 float* __restrict__ nout, int M, int first) {
+                                                 float* __restrict__ nout, int M, int first, float bdiag) {
     pdl_entry();
     extern __shared__ __align__(128) unsigned char bs_smem[];
     BsStage* st = reinterpret_cast<BsStage*>(bs_smem);
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
                 for (int i = 0; i < 8; ++i) deg += near_off(nb, i) != 0;
                 deg += (nb.z != 0) + (nb.w != 0);
                 nv = 1.f;
-                bn = (float)kBbarDiag + (float)deg;
+                bn = bdiag + (float)deg;
             } else {
                 const int lv = l + 128;
                 nv = S.n[lv];
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
                 }
                 if (nb.z) sn += ny[u][0];
                 if (nb.w) sn += ny[u][1];
-                bn = (float)kBbarDiag * nv + sn;
+                bn = bdiag * nv + sn;
             }
             nout[v] = sqrtf(nv * (float)S.m[l] / bn);
         }
@@ -407,11 +407,11 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
 // max|n∘B̄n − m| and max m (order-independent max ⇒ deterministic), reporting only.
 __global__ void k_bistoch_residual(const int4* __restrict__ nbr,
                                    const int* __restrict__ m, const float* __restrict__ n, int M,
-                                   unsigned* __restrict__ out2) {
+                                   unsigned* __restrict__ out2, float bdiag) {
     pdl_entry();
     float e = 0.f, mm = 0.f;
     for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < M; v += gridDim.x * blockDim.x) {
-        const float bn = (float)kBbarDiag * n[v] + nbr_sum(n, v, nbr[v]);
+        const float bn = bdiag * n[v] + nbr_sum(n, v, nbr[v]);
         e = fmaxf(e, fabsf(n[v] * bn - (float)m[v]));
         mm = fmaxf(mm, (float)m[v]);
     }

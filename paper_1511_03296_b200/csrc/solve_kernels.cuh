@@ -523,10 +523,10 @@ __global__ void k_bwd_finalize(const int* __restrict__ vid, const float* __restr
 
 // B̄ v (reading #4), debug / parity operator.
 __global__ void k_blur(const int4* __restrict__ nbr, const float* __restrict__ x,
-                       int64_t M, float* __restrict__ out) {
+                       int64_t M, float bdiag, float* __restrict__ out) {
     pdl_entry();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x)
-        out[v] = (float)kBbarDiag * x[v] + nbr_sum(x, (int)v, nbr[v]);
+        out[v] = bdiag * x[v] + nbr_sum(x, (int)v, nbr[v]);
 }
 
 // A y for planar y, written canonical [M][K] (debug / parity operator).

@@ -29,7 +29,7 @@ MODE = {"fixed": 0, "tol": 1}
 
 
 class GridOpts(C.Structure):
-    _fields_ = [("n_bistoch", C.c_int), ("build_pyramid", C.c_int)]
+    _fields_ = [("n_bistoch", C.c_int), ("build_pyramid", C.c_int), ("dims", C.c_int)]
 
 
 class SolveOpts(C.Structure):
@@ -190,15 +190,16 @@ class Grid:
 
 
 def grid_build(rgb: torch.Tensor, sigma_xy: float, sigma_l: float, sigma_uv: float, n_bistoch: int = 20,
-               build_pyramid: bool = True, stream=None) -> Grid:
-    """fbs_grid_build: rgb uint8 CUDA [F][H][W][3] (or [H][W][3])."""
+               build_pyramid: bool = True, stream=None, dims: int = 5) -> Grid:
+    """fbs_grid_build: rgb uint8 CUDA [F][H][W][3] (or [H][W][3]); dims = 3 builds the XYL grid
+    of a grayscale reference."""
     if isinstance(rgb, torch.Tensor) and rgb.dim() == 3:
         rgb = rgb.unsqueeze(0)
     rgb = _dev_tensor(rgb, torch.uint8, "rgb", 4)
     F, H, W, ch = rgb.shape
     if ch != 3:
         raise ValueError("rgb must be [F][H][W][3]")
-    o = GridOpts(int(n_bistoch), int(bool(build_pyramid)))
+    o = GridOpts(int(n_bistoch), int(bool(build_pyramid)), int(dims))
     h = C.c_void_p()
     _check(_lib.fbs_grid_build(_ptr(rgb), F, H, W, float(sigma_xy), float(sigma_l), float(sigma_uv),
                                C.byref(o), _stream(stream), C.byref(h)))

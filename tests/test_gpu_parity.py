@@ -118,3 +118,27 @@ def test_solve_parity(name, mode, pc):
         if mode == "fixed":
             assert np.all(st["iterations"][f] == np.minimum(w.iters, sol.iterations))
     assert st["status"] & ~2 == 0
+
+
+@pytest.mark.parametrize("gray_ref", [True, False])
+def test_d3_grid_bit_exact_and_colorization_parity(gray_ref):
+    """D = 3 (XYL) grid of PAPER.md:511's colorization (reading #27): bit-exact grid against the
+    oracle (on a gray and on a colour reference, whose chroma is then ignored), and a
+    colorization-style solve — 2 chroma channels, confidence 1 on ~3% scribbled pixels —
+    within north_star's bounds."""
+    w = make("c2", W=190, H=150, n_cells=25)
+    rgb = np.repeat(w.rgb[..., :1], 3, axis=3) if gray_ref else w.rgb
+    H, W = w.H, w.W
+    rng = np.random.default_rng(11)
+    scrib = (rng.uniform(size=(1, H, W)) < 0.03).astype(np.float32)
+    t = np.stack([w.t[:, 0] / 255.0 * 100.0 + 28.0, 200.0 - w.t[:, 0] / 2.0], axis=1).astype(np.float32) * scrib[:, None]
+    g = fbs.grid_build(dev(rgb), 4.0, 4.0, 4.0, dims=3)
+    og = O.build_grid(rgb, 4.0, 4.0, 4.0, dims=3)
+    assert_grid_equal(g, og)
+    x = fbs.solve(g, dev(t), dev(scrib), 0.5, precond="hier", init="hier", mode="tol", tol=1e-6).cpu().numpy()
+    _, sols = O.solve(rgb, t, scrib, 4.0, 4.0, 4.0, 0.5,
+                      O.SolveOptions(precond="hier", init="hier", mode="tol", tol=1e-6), dims=3)
+    HW = H * W
+    ex = zero_conf_pixels(sols[0])
+    mx, rms = compare_x(x[0].reshape(2, HW), sols[0].x, t[0].reshape(2, HW).astype(float), scrib[0].ravel(), exclude=ex)
+    assert mx <= MAX_TOL and rms <= RMS_TOL, (mx, rms)
