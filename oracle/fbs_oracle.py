@@ -625,6 +625,44 @@ def solve_frame_lowrank(grid: Grid, f: int, t: np.ndarray, c: np.ndarray, lam: f
     return x, Y, red
 
 
+# ----------------------------------------------------------------------------- domain transform (post-filter)
+def dt_filter(signal: np.ndarray, rgb: np.ndarray, sigma_s: float, sigma_r: float, n_iters: int = 3) -> np.ndarray:
+    """Edge-aware post-filter of the solver output: the recursive-filter (RF) domain transform of
+    Gastal & Oliveira 2011, which the paper cites and applies to every result (PAPER.md:329,
+    :333 σ'_xy, σ'_rgb; Supp. §3 "the recursive formulation of the domain transform"), restated
+    from that publication (reading #28):
+        d_x(p) = 1 + σ_s/σ_r Σ_c |I_c(p) − I_c(p − x̂)|   (L1 over RGB in [0, 255]; 1 at x = 0)
+        pass i = 1..N:  σ_i = σ_s √3 2^(N−i) / √(4^N − 1),  a_i = exp(−√2 / σ_i),  w = a_i^d
+          rows:    J[n] += w[n] (J[n−1] − J[n])  for n = 1 … W−1,  then
+                   J[n] += w[n+1] (J[n+1] − J[n]) for n = W−2 … 0
+          columns: the same with d_y.
+    signal: [K][H][W], rgb: uint8 [H][W][3].  Returns float64 [K][H][W]."""
+    F = np.array(signal, dtype=np.float64, copy=True)
+    K, H, W = F.shape
+    I = rgb.astype(np.float64)
+    dx = np.zeros((H, W))
+    dy = np.zeros((H, W))
+    dx[:, 1:] = np.abs(np.diff(I, axis=1)).sum(axis=2)
+    dy[1:, :] = np.abs(np.diff(I, axis=0)).sum(axis=2)
+    Dx = 1.0 + sigma_s / sigma_r * dx
+    Dy = 1.0 + sigma_s / sigma_r * dy
+    N = n_iters
+    for i in range(1, N + 1):
+        sig = sigma_s * np.sqrt(3.0) * 2.0 ** (N - i) / np.sqrt(4.0 ** N - 1.0)
+        a = np.exp(-np.sqrt(2.0) / sig)
+        V = a ** Dx
+        for x in range(1, W):
+            F[:, :, x] += V[:, x] * (F[:, :, x - 1] - F[:, :, x])
+        for x in range(W - 2, -1, -1):
+            F[:, :, x] += V[:, x + 1] * (F[:, :, x + 1] - F[:, :, x])
+        V = a ** Dy
+        for y in range(1, H):
+            F[:, y, :] += V[y, :] * (F[:, y - 1, :] - F[:, y, :])
+        for y in range(H - 2, -1, -1):
+            F[:, y, :] += V[y + 1, :] * (F[:, y + 1, :] - F[:, y, :])
+    return F
+
+
 # ----------------------------------------------------------------------------- brute force helpers
 def dense_W_hat(S: sp.csr_matrix, Bbar: sp.csr_matrix, m, n) -> np.ndarray:
     """Ŵ = Sᵀ Dm⁻¹ Dn B̄ Dn Dm⁻¹ S  (PAPER.md:114-117 Eq. equiv / :650-652 Eq. What). Tiny inputs only."""
