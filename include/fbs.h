@@ -172,6 +172,18 @@ int fbs_solve_robust(fbs_grid g, const float* t_dev, int K, const float* c_init_
                      const fbs_solve_opts* opts, double sigma_gm, int n_irls, float* x_dev,
                      float* c_out_dev, fbs_stream stream);
 
+/* Domain-transform post-filter of solver output ("post-processed by the domain
+ * transform … included in all runtimes", :333 σ'_xy, σ'_rgb): the recursive-filter variant of
+ * Gastal & Oliveira 2011, restated in reading #28 — n_iters (default 3) row + column passes with
+ * per-pass σ_i = σ_s √3 2^(N−i)/√(4^N − 1), weights a_i^(1 + σ_s/σ_r Σ_c|ΔI_c|) from the RGB guide.
+ *   rgb_dev  uint8 [frames][H][W][3]   guide (the reference image)
+ *   in_dev   float [frames][K][H][W]   signal (e.g. fbs_solve's x)
+ *   out_dev  float [frames][K][H][W]   output; may equal in_dev (in place)
+ * Errors: FBS_EINVAL (NULL pointer, K ∉ [1, 64], σ ≤ 0, n_iters < 1, H or W > 16384); FBS_ENOMEM;
+ * FBS_ECUDA. */
+int fbs_dt_filter(const uint8_t* rgb_dev, int frames, int height, int width, const float* in_dev, int K,
+                  double sigma_s, double sigma_r, int n_iters, float* out_dev, fbs_stream stream);
+
 /* Backward pass: given g = ∂f/∂x̂ [frames][K][H][W], solve A d = S g
  * with the forward's preconditioner and stopping rule from d = 0 (reading #14), then
  *   ∂f/∂t = c ∘ Sᵀd              → dt_dev float [frames][K][H][W]

@@ -8,6 +8,7 @@ from .fbs import (  # noqa: F401
     Grid,
     System,
     blur,
+    dt_filter,
     grid_build,
     launch_count,
     make_opts,

@@ -18,6 +18,7 @@
 #include "solve_kernels.cuh"
 #include "tree_kernels.cuh"
 #include "lowrank_kernels.cuh"
+#include "dt_kernels.cuh"
 
 namespace fbs {
 
@@ -864,6 +865,54 @@ static void robust_impl(fbs_grid g, const float* t, int K, const float* c_init, 
     free_all(tmp, s);
 }
 
+// Domain-transform post-filter (reading #28): N iterations of a row pass and a column pass.
+static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, int K, double sigma_s, double sigma_r,
+                    int n_iters, float* out, cudaStream_t s) {
+    if (!rgb || !in || !out) throw Err(FBS_EINVAL, "null pointer");
+    if (F < 1 || H < 1 || W < 1 || K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "bad sizes");
+    if (H > 16384 || W > 16384) throw Err(FBS_EINVAL, "lines longer than 16384 pixels are not supported");
+    if (!(sigma_s > 0.0) || !(sigma_r > 0.0) || n_iters < 1) throw Err(FBS_EINVAL, "sigma_s, sigma_r > 0, n_iters >= 1");
+    int dev = 0;
+    device_setup(&dev);
+    std::vector<void*> tmp;
+    try {
+        const size_t NP = (size_t)F * H * W, NS = NP * K;
+        float* Dx = dalloc<float>(tmp, NP, s);
+        float* Dy = dalloc<float>(tmp, NP, s);
+        float* DyT = dalloc<float>(tmp, NP, s);
+        float* bufT = dalloc<float>(tmp, NS, s);
+        LAUNCH(k_dt_dist, grid_for((int64_t)NP), kThreads, 0, s, rgb, F, H, W, (float)(sigma_s / sigma_r), Dx, Dy);
+        const int tgrid = (int)std::min<int64_t>(((int64_t)F * ((H + 31) / 32) * ((W + 31) / 32)), 148 * 64);
+        LAUNCH(k_transpose, tgrid, dim3(32, 8), 0, s, Dy, F, H, W, DyT);
+        if (out != in) ck(cudaMemcpyAsync(out, in, NS * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
+        auto rows = [&](float* sig, const float* D, int Hr, int L, float lna) {
+            const int lpad = L + 32;
+            const size_t perWarp = 2 * (size_t)lpad * sizeof(float);
+            const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / perWarp));
+            const size_t smem = perWarp * nw;
+            if (smem > 48 * 1024)
+                ck(cudaFuncSetAttribute((const void*)k_dt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+                   "smem attr");
+            const int64_t lines = (int64_t)F * K * Hr;
+            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((lines + nw - 1) / nw, 148 * 32));
+            LAUNCH(k_dt_rows, blocks, 32 * nw, smem, s, sig, D, F, K, Hr, L, lna);
+        };
+        const int tgridS = (int)std::min<int64_t>(((int64_t)F * K * ((H + 31) / 32) * ((W + 31) / 32)), 148 * 64);
+        for (int i = 1; i <= n_iters; ++i) {
+            const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, n_iters - i) / std::sqrt(std::pow(4.0, n_iters) - 1.0);
+            const float lna = (float)(-std::sqrt(2.0) / sig);  // ln a_i
+            rows(out, Dx, H, W, lna);
+            LAUNCH(k_transpose, tgridS, dim3(32, 8), 0, s, out, F * K, H, W, bufT);
+            rows(bufT, DyT, W, H, lna);
+            LAUNCH(k_transpose, tgridS, dim3(32, 8), 0, s, bufT, F * K, W, H, out);
+        }
+    } catch (...) {
+        free_all(tmp, s);
+        throw;
+    }
+    free_all(tmp, s);
+}
+
 static void backward_impl(fbs_system S, const float* g_dldx, const float* t, const float* c, float* dt, float* dc,
                           cudaStream_t s) {
     if (!S || !g_dldx || !t || !c || !dt || !dc) throw Err(FBS_EINVAL, "null pointer");
@@ -1028,6 +1077,13 @@ int fbs_solve_robust(fbs_grid g, const float* t, int K, const float* c_init, dou
                      double sigma_gm, int n_irls, float* x, float* c_out, fbs_stream stream) {
     return guard("fbs_solve_robust", [&] {
         robust_impl(g, t, K, c_init, lam, opts, sigma_gm, n_irls, x, c_out, (cudaStream_t)stream);
+    });
+}
+
+int fbs_dt_filter(const uint8_t* rgb, int frames, int height, int width, const float* in, int K, double sigma_s,
+                  double sigma_r, int n_iters, float* out, fbs_stream stream) {
+    return guard("fbs_dt_filter", [&] {
+        dt_impl(rgb, frames, height, width, in, K, sigma_s, sigma_r, n_iters, out, (cudaStream_t)stream);
     });
 }
 

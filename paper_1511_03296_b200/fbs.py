@@ -51,6 +51,7 @@ _SIGS = {
     "fbs_solve": (_i, [_vp, _vp, _i, _vp, _d, C.POINTER(SolveOpts), _vp, _vp, C.POINTER(_vp), _vp]),
     "fbs_solve_robust": (_i, [_vp, _vp, _i, _vp, _d, C.POINTER(SolveOpts), _d, _i, _vp, _vp, _vp]),
     "fbs_solve_backward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fbs_dt_filter": (_i, [_vp, _i, _i, _i, _vp, _i, _d, _d, _i, _vp, _vp]),
     "fbs_system_stats": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "fbs_system_export": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fbs_system_destroy": (None, [_vp]),
@@ -317,6 +318,23 @@ def solve_robust(grid: Grid, t: torch.Tensor, c_init: torch.Tensor, lam: float, 
     _check(_lib.fbs_solve_robust(grid.handle, _ptr(t), K, _ptr(c_init), float(lam), C.byref(o), float(sigma_gm),
                                  int(n_irls), _ptr(x), _ptr(w), _stream(stream)))
     return (x, w) if want_weights else x
+
+
+def dt_filter(rgb: torch.Tensor, x: torch.Tensor, sigma_s: float, sigma_r: float, n_iters: int = 3,
+              out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """fbs_dt_filter: domain-transform post-filter of x float32 [F][K][H][W] guided by rgb uint8
+    [F][H][W][3] (reading #28)."""
+    if isinstance(rgb, torch.Tensor) and rgb.dim() == 3:
+        rgb = rgb.unsqueeze(0)
+    rgb = _dev_tensor(rgb, torch.uint8, "rgb", 4)
+    x = _dev_tensor(x, torch.float32, "x", 4)
+    F, K, H, W = x.shape
+    if tuple(rgb.shape) != (F, H, W, 3):
+        raise ValueError("rgb must be [F][H][W][3] matching x")
+    y = torch.empty_like(x) if out is None else out
+    _check(_lib.fbs_dt_filter(_ptr(rgb), F, H, W, _ptr(x), K, float(sigma_s), float(sigma_r), int(n_iters), _ptr(y),
+                              _stream(stream)))
+    return y
 
 
 # ----------------------------------------------------------------------------- operators
