@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     return ap.parse_args()
 
 
@@ -382,6 +383,42 @@ def main():
                "ms_per_step": ems / args.steps,
                "pipelining": "double-buffered: H2D of step i+1 and D2H of step i on separate streams overlap step i"}
 
+    # ---- §8(f) rows on the same GPU (device time, not part of `value`): the domain-transform
+    # post-filter of this workload's output, the robust solver per IRLS round on it, and
+    # configs[3] (21 channels, 500×375) solved in full vs with the low-rank reduction (ε = 0.01)
+    extras = None
+    if not args.no_extras and rank == 0:
+        def dev_ms(fn, reps=3):
+            fn()
+            torch.cuda.synchronize()
+            a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_.record(stream)
+            for _ in range(reps):
+                fn()
+            b_.record(stream)
+            torch.cuda.synchronize()
+            return a_.elapsed_time(b_) / reps
+
+        g_x = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=20)
+        fbs.solve(g_x, t_d, c_d, LAM, precond="hier", init="hier", mode="fixed", iters=ITERS, out=x_d)
+        dt_ms = dev_ms(lambda: fbs.dt_filter(rgb_d, x_d, 16.0, 16.0))
+        rb_ms = dev_ms(lambda: fbs.solve_robust(g_x, t_d, c_d, LAM, 10.0, 2, precond="hier", init="hier",
+                                                mode="fixed", iters=ITERS, out=x_d), reps=2) / 2
+        g_x.close()
+        w4 = make("c4")
+        rgb4, t4, c4 = (torch.from_numpy(a_).to(dev) for a_ in (w4.rgb, w4.t, w4.c))
+        g4 = fbs.grid_build(rgb4, w4.sigma_xy, w4.sigma_l, w4.sigma_uv)
+        full_ms = dev_ms(lambda: fbs.solve(g4, t4, c4, w4.lam, precond="hier", init="hier", mode="tol", tol=1e-6))
+        lr_ms = dev_ms(lambda: fbs.solve(g4, t4, c4, w4.lam, precond="hier", init="hier", mode="tol", tol=1e-6,
+                                         lowrank_eps=0.01))
+        g4.close()
+        extras = {"dt_post_filter_ms": dt_ms,
+                  "dt_post_filter": f"{F} frames x1, sigma'_xy = sigma'_rgb = 16, 3 iterations (PAPER.md:329)",
+                  "robust_ms_per_irls_round": rb_ms,
+                  "robust": f"{F} frames, sigma_gm = 10, hier+hier, {ITERS} PCG iters per round (Supp. Alg. 3)",
+                  "configs3_full_solve_ms": full_ms, "configs3_lowrank_solve_ms": lr_ms,
+                  "lowrank": "configs[3] 500x375, K = 21, hier+hier to tol 1e-6: full vs eps = 0.01 (Supp. §4)"}
+
     # ---- CPU baseline: the oracle as it stands, one frame, host cores (rank 0, N = 1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -401,7 +438,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": workload_config(args) | {"vertices_per_gpu": M,
                                                    "levels": int(info["levels"])},
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "extras": extras,
                 "clocks": clk, "stages_ms_per_step": stages_ms, "kernels": kernels,
                 "profiled_ms_per_step": prof_ms / args.steps}
         print(json.dumps(line), flush=True)
