@@ -879,32 +879,24 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
         const size_t NP = (size_t)F * H * W, NS = NP * K;
         float* Dx = dalloc<float>(tmp, NP, s);
         float* Dy = dalloc<float>(tmp, NP, s);
-        float* DyT = dalloc<float>(tmp, NP, s);
-        float* bufT = dalloc<float>(tmp, NS, s);
         LAUNCH(k_dt_dist, grid_for((int64_t)NP), kThreads, 0, s, rgb, F, H, W, (float)(sigma_s / sigma_r), Dx, Dy);
-        const int tgrid = (int)std::min<int64_t>(((int64_t)F * ((H + 31) / 32) * ((W + 31) / 32)), 148 * 64);
-        LAUNCH(k_transpose, tgrid, dim3(32, 8), 0, s, Dy, F, H, W, DyT);
         if (out != in) ck(cudaMemcpyAsync(out, in, NS * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
-        auto rows = [&](float* sig, const float* D, int Hr, int L, float lna) {
-            const int lpad = L + 32;
-            const size_t perWarp = 2 * (size_t)lpad * sizeof(float);
-            const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / perWarp));
-            const size_t smem = perWarp * nw;
-            if (smem > 48 * 1024)
-                ck(cudaFuncSetAttribute((const void*)k_dt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
-                   "smem attr");
-            const int64_t lines = (int64_t)F * K * Hr;
-            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((lines + nw - 1) / nw, 148 * 32));
-            LAUNCH(k_dt_rows, blocks, 32 * nw, smem, s, sig, D, F, K, Hr, L, lna);
-        };
-        const int tgridS = (int)std::min<int64_t>(((int64_t)F * K * ((H + 31) / 32) * ((W + 31) / 32)), 148 * 64);
+        const size_t perWarp = 2 * (size_t)(W + 32) * sizeof(float);
+        const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / perWarp));
+        const size_t smem = perWarp * nw;
+        if (smem > 48 * 1024)
+            ck(cudaFuncSetAttribute((const void*)k_dt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+               "smem attr");
+        const int64_t lines = (int64_t)F * K * H;
+        const int rowBlocks = (int)std::max<int64_t>(1, std::min<int64_t>((lines + nw - 1) / nw, 148 * 32));
+        const int colThreads = 32 * std::max(1, std::min(32, H));  // ≥ 1 row per warp chunk
+        const int64_t colTiles = (int64_t)F * K * ((W + 31) / 32);
+        const int colBlocks = (int)std::max<int64_t>(1, std::min<int64_t>(colTiles, 148 * 8));
         for (int i = 1; i <= n_iters; ++i) {
             const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, n_iters - i) / std::sqrt(std::pow(4.0, n_iters) - 1.0);
             const float lna = (float)(-std::sqrt(2.0) / sig);  // ln a_i
-            rows(out, Dx, H, W, lna);
-            LAUNCH(k_transpose, tgridS, dim3(32, 8), 0, s, out, F * K, H, W, bufT);
-            rows(bufT, DyT, W, H, lna);
-            LAUNCH(k_transpose, tgridS, dim3(32, 8), 0, s, bufT, F * K, W, H, out);
+            LAUNCH(k_dt_rows, rowBlocks, 32 * nw, smem, s, out, Dx, F, K, H, W, lna);
+            LAUNCH(k_dt_cols, colBlocks, colThreads, 0, s, out, Dy, F, K, H, W, lna);
         }
     } catch (...) {
         free_all(tmp, s);

@@ -34,65 +34,56 @@ __global__ void k_dt_dist(const uint8_t* __restrict__ rgb, int F, int H, int W, 
     }
 }
 
-// out[b][c][r] = in[b][r][c]: 32×32 shared-memory tiles (coalesced both ways)
-__global__ void k_transpose(const float* __restrict__ in, int B, int R, int C, float* __restrict__ out) {
-    pdl_entry();
-    __shared__ float tile[32][33];
-    const int64_t tilesC = (C + 31) / 32, tilesR = (R + 31) / 32;
-    for (int64_t t = blockIdx.x; t < (int64_t)B * tilesR * tilesC; t += gridDim.x) {
-        const int b = (int)(t / (tilesR * tilesC));
-        const int tr = (int)((t / tilesC) % tilesR), tc = (int)(t % tilesC);
-        const float* src = in + (size_t)b * R * C;
-        float* dst = out + (size_t)b * R * C;
-        for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-            const int r = tr * 32 + i, c = tc * 32 + threadIdx.x;
-            if (r < R && c < C) tile[i][threadIdx.x] = src[(size_t)r * C + c];
-        }
-        __syncthreads();
-        for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-            const int c = tc * 32 + i, r = tr * 32 + threadIdx.x;
-            if (r < R && c < C) dst[(size_t)c * R + r] = tile[threadIdx.x][i];
-        }
-        __syncthreads();
-    }
-}
+constexpr int kDtB = 8;  // loads issued together before their dependent steps
 
 // composition of affine maps J ↦ A J + B: (later ∘ earlier)
 __device__ __forceinline__ float2 amap_compose(float2 later, float2 earlier) {
     return make_float2(later.x * earlier.x, later.x * earlier.y + later.y);
 }
 
-// One causal + anticausal pass over every line of sig [F][K][Hr][L] (in place), weights
-// w = exp(lna · D) with D [F][Hr][L].  Warps per block = blockDim.x / 32; dynamic shared memory:
-// 2 · lpad floats per warp, lpad = L + 32 (one pad slot per lane's chunk against bank conflicts).
-__global__ void k_dt_rows(float* __restrict__ sig, const float* __restrict__ D, int F, int K, int Hr, int L, float lna) {
+// Row pass: one causal + anticausal pass along every row of sig [F][K][H][W] (in place),
+// w = exp(lna · Dx) with Dx [F][H][W].  One warp per row; the row's values and weights are staged
+// in shared memory with coalesced loads (2 · (W + 32) floats per warp: element n at n + n/C, one
+// pad slot per lane chunk against bank conflicts).
+__global__ void k_dt_rows(float* __restrict__ sig, const float* __restrict__ Dx, int F, int K, int H, int W, float lna) {
     pdl_entry();
     extern __shared__ float dt_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int C = (L + 31) / 32;           // chunk length
-    const int lpad = L + 32;               // padded line: element n at n + n / C (lane = n / C ≤ 31)
+    const int C = (W + 31) / 32;           // chunk length
+    const float invC = 1.f / (float)C;     // ⌊n/C⌋ = ⌊(n + ½)/C⌋ in fp32: exact for n < 2^14·C
+    const int lpad = W + 32;
     float* val = dt_smem + (size_t)warp * 2 * lpad;
     float* wgt = val + lpad;
-    const int64_t lines = (int64_t)F * K * Hr;
+    const int64_t lines = (int64_t)F * K * H;
     for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < lines; r += (int64_t)gridDim.x * nw) {
-        const int f = (int)(r / ((int64_t)K * Hr));
-        const int y = (int)(r % Hr);
-        float* line = sig + (size_t)r * L;
-        const float* dl = D + ((size_t)f * Hr + y) * L;
-        for (int n = lane; n < L; n += 32) {
-            const int pn = n + n / C;
-            val[pn] = line[n];
-            wgt[pn] = __expf(lna * dl[n]);
+        const int f = (int)(r / ((int64_t)K * H));
+        const int y = (int)(r % H);
+        float* line = sig + (size_t)r * W;
+        const float* dl = Dx + ((size_t)f * H + y) * W;
+        for (int nb = lane; nb < W; nb += 32 * kDtB) {  // kDtB loads of each array in flight
+            float lv[kDtB], dv[kDtB];
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u) {
+                const int n = nb + 32 * u;
+                lv[u] = (n < W) ? line[n] : 0.f;
+                dv[u] = (n < W) ? __ldg(dl + n) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u) {
+                const int n = nb + 32 * u;
+                if (n < W) {
+                    const int pn = n + __float2int_rz(((float)n + 0.5f) * invC);
+                    val[pn] = lv[u];
+                    wgt[pn] = (n == 0) ? 0.f : __expf(lna * dv[u]);  // w[0] = 0: the first element keeps its value
+                }
+            }
         }
         __syncwarp();
-        const int n0 = lane * C, n1 = min(n0 + C, L);
+        const int n0 = lane * C, n1 = min(n0 + C, W);
         const int base = lane * (C + 1);  // padded index of n0
-        // causal: map_n = (w[n], (1 − w[n]) I[n]); element 0 has w = 0
+        // causal: map_n = (w[n], (1 − w[n]) I[n])
         float2 m = make_float2(1.f, 0.f);
-        for (int n = n0, q = base; n < n1; ++n, ++q) {
-            const float w = (n == 0) ? 0.f : wgt[q];
-            m = amap_compose(make_float2(w, (1.f - w) * val[q]), m);
-        }
+        for (int q = base; q < base + (n1 - n0); ++q) m = amap_compose(make_float2(wgt[q], (1.f - wgt[q]) * val[q]), m);
         float2 incl = m;  // inclusive warp scan (lanes in increasing order)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -100,17 +91,17 @@ __global__ void k_dt_rows(float* __restrict__ sig, const float* __restrict__ D, 
             if (lane >= o) incl = amap_compose(incl, make_float2(ax, ay));
         }
         float J = __shfl_up_sync(0xffffffffu, incl.y, 1);  // value entering the chunk (maps chain from A = 0)
-        for (int n = n0, q = base; n < n1; ++n, ++q) {
-            const float w = (n == 0) ? 0.f : wgt[q];
-            J = w * J + (1.f - w) * val[q];
+        for (int q = base; q < base + (n1 - n0); ++q) {
+            J = wgt[q] * J + (1.f - wgt[q]) * val[q];
             val[q] = J;
         }
         __syncwarp();
-        // anticausal: element n uses w[n+1]; the last element keeps its value
+        // anticausal: element n uses w[n+1] (0 for the last element); the padded position of n+1
+        // is q+1 inside the chunk and q+2 across the next chunk's pad slot
+        auto wnext = [&](int n, int q) { return (n + 1 < W) ? wgt[(n + 1 == n1) ? q + 2 : q + 1] : 0.f; };
         m = make_float2(1.f, 0.f);
-        for (int n = n1 - 1; n >= n0; --n) {
-            const int q = base + (n - n0);
-            const float w = (n == L - 1) ? 0.f : wgt[(n + 1) + (n + 1) / C];
+        for (int n = n1 - 1, q = base + (n1 - 1 - n0); n >= n0; --n, --q) {
+            const float w = wnext(n, q);
             m = amap_compose(make_float2(w, (1.f - w) * val[q]), m);
         }
         incl = m;  // inclusive scan in decreasing lane order
@@ -120,15 +111,112 @@ __global__ void k_dt_rows(float* __restrict__ sig, const float* __restrict__ D, 
             if (lane + o < 32) incl = amap_compose(incl, make_float2(ax, ay));
         }
         J = __shfl_down_sync(0xffffffffu, incl.y, 1);
-        for (int n = n1 - 1; n >= n0; --n) {
-            const int q = base + (n - n0);
-            const float w = (n == L - 1) ? 0.f : wgt[(n + 1) + (n + 1) / C];
+        for (int n = n1 - 1, q = base + (n1 - 1 - n0); n >= n0; --n, --q) {
+            const float w = wnext(n, q);
             J = w * J + (1.f - w) * val[q];
             val[q] = J;
         }
         __syncwarp();
-        for (int n = lane; n < L; n += 32) line[n] = val[n + n / C];
+        for (int n = lane; n < W; n += 32) line[n] = val[n + __float2int_rz(((float)n + 0.5f) * invC)];
         __syncwarp();
+    }
+}
+
+// Column pass, in place on the row-major sig [F][K][H][W], w = exp(lna · Dy) with Dy [F][H][W]:
+// one block per 32 adjacent columns of one (frame, channel) plane; lane = column (coalesced
+// 128-byte row segments), warp = a chunk of rows.  Each lane composes its chunk's maps, the
+// chunk maps of a column are scanned across warps in shared memory, and the chunk is re-run
+// from its incoming value (values re-read from L2).  Rows are processed in batches of kDtB with
+// every load of the batch issued before its dependent compose/apply steps.
+__global__ void __launch_bounds__(1024) k_dt_cols(float* __restrict__ sig, const float* __restrict__ Dy, int F, int K,
+                                                  int H, int W, float lna) {
+    pdl_entry();
+    __shared__ float2 cm[32][33];  // [warp][lane] chunk maps
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int tilesX = (W + 31) / 32;
+    const int64_t planes = (int64_t)F * K;
+    const int R = (H + nw - 1) / nw;  // rows per chunk
+    for (int64_t b = blockIdx.x; b < planes * tilesX; b += gridDim.x) {
+        const int64_t pl = b / tilesX;
+        const int x = (int)(b % tilesX) * 32 + lane;
+        const int f = (int)(pl / K);
+        const bool ok = x < W;
+        float* col = sig + (size_t)pl * H * W + (ok ? x : 0);
+        const float* dcol = Dy + (size_t)f * H * W + (ok ? x : 0);
+        const int y0 = warp * R, y1 = ok ? min(y0 + R, H) : y0;
+        float wv[kDtB], iv[kDtB];
+        // causal: row y uses w[y] (w = 0 at y = 0)
+        float2 m = make_float2(1.f, 0.f);
+        for (int yb = y0; yb < y1; yb += kDtB) {
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u) {
+                const int y = yb + u;
+                wv[u] = (y < y1 && y > 0) ? __ldg(dcol + (size_t)y * W) : 0.f;
+                iv[u] = (y < y1) ? col[(size_t)y * W] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u)
+                if (yb + u < y1) {
+                    const float w = (yb + u > 0) ? __expf(lna * wv[u]) : 0.f;
+                    m = amap_compose(make_float2(w, (1.f - w) * iv[u]), m);
+                }
+        }
+        cm[warp][lane] = m;
+        __syncthreads();
+        float J = 0.f;  // value entering this chunk: maps of the earlier chunks (chained from A = 0)
+        for (int q = 0; q < warp; ++q) J = cm[q][lane].x * J + cm[q][lane].y;
+        for (int yb = y0; yb < y1; yb += kDtB) {
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u) {
+                const int y = yb + u;
+                wv[u] = (y < y1 && y > 0) ? __ldg(dcol + (size_t)y * W) : 0.f;
+                iv[u] = (y < y1) ? col[(size_t)y * W] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u)
+                if (yb + u < y1) {
+                    const float w = (yb + u > 0) ? __expf(lna * wv[u]) : 0.f;
+                    J = w * J + (1.f - w) * iv[u];
+                    col[(size_t)(yb + u) * W] = J;
+                }
+        }
+        __syncthreads();
+        // anticausal: row y uses w[y+1]; the last row keeps its value
+        m = make_float2(1.f, 0.f);
+        for (int yb = y1 - 1; yb >= y0; yb -= kDtB) {
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u) {
+                const int y = yb - u;
+                wv[u] = (y >= y0 && y < H - 1) ? __ldg(dcol + (size_t)(y + 1) * W) : 0.f;
+                iv[u] = (y >= y0) ? col[(size_t)y * W] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u)
+                if (yb - u >= y0) {
+                    const float w = (yb - u < H - 1) ? __expf(lna * wv[u]) : 0.f;
+                    m = amap_compose(make_float2(w, (1.f - w) * iv[u]), m);
+                }
+        }
+        cm[warp][lane] = m;
+        __syncthreads();
+        J = 0.f;
+        for (int q = nw - 1; q > warp; --q) J = cm[q][lane].x * J + cm[q][lane].y;
+        for (int yb = y1 - 1; yb >= y0; yb -= kDtB) {
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u) {
+                const int y = yb - u;
+                wv[u] = (y >= y0 && y < H - 1) ? __ldg(dcol + (size_t)(y + 1) * W) : 0.f;
+                iv[u] = (y >= y0) ? col[(size_t)y * W] : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < kDtB; ++u)
+                if (yb - u >= y0) {
+                    const float w = (yb - u < H - 1) ? __expf(lna * wv[u]) : 0.f;
+                    J = w * J + (1.f - w) * iv[u];
+                    col[(size_t)(yb - u) * W] = J;
+                }
+        }
+        __syncthreads();
     }
 }
 
