@@ -46,20 +46,25 @@ def stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = None) -> str:
+    """Compile csrc/api.cu into `out` (default libfbs.so)."""
+    target = out or LIB
+    if not force and out is None and not stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, os.path.join(CSRC, "api.cu"), "-o", LIB + ".tmp"]
+    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, os.path.join(CSRC, "api.cu"), "-o", target + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(res.stderr)
+    os.replace(target + ".tmp", target)
+    if out is None:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
+            fh.write(res.stderr)
     if verbose:
         print(res.stderr, file=sys.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # build.py [--force] [-v] [--out PATH]   (--out: an alternative build for FBS_LIB A/B runs)
+    o = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, out=o))

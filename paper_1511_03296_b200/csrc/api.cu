@@ -422,6 +422,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             if ((size_t)T.maxFrameTiles * sizeof(double) > 200 * 1024)
                 throw Err(FBS_ELIMIT, "frame too large for the shared-memory tile scan of the hierarchy");
             T.nTiles1 = tfo[F];
+            T.tileFrameOffH = tfo;
             T.tileFrameOff = dalloc<int>(A, F + 1, s);
             T.tileFrame = dalloc<int>(A, std::max<size_t>(tframe.size(), 1), s);
             T.tileRange = dalloc<int2>(A, std::max<size_t>(trange.size(), 1), s);
@@ -450,6 +451,7 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     VecArgs a{};
     a.K = S->K;
     a.BPF = S->BPF;
+    a.nf = g->F;
     a.M = g->M;
     a.lam = (float)S->lam;
     a.frameOff = g->frameOff;
@@ -481,6 +483,7 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.L = g->L;
     h.F = g->F;
     h.C = C;
+    h.nt = g->tree.nTiles1;
     for (int k = 0; k < g->L; ++k) {
         HLevel& v = h.lv[k];
         v.M = (k == 0) ? g->M : g->lv[k].M;
@@ -533,7 +536,7 @@ template <int MODE>
 void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s) {
     static const std::string name = std::string("k_tree_lift<") + mode_name(MODE) + ">";
     auto kern = k_tree_lift<MODE>;
-    LAUNCH_AS(name.c_str(), kern, S->g->tree.nTiles1, kScanTile, 0, s, h, in0);
+    LAUNCH_AS(name.c_str(), kern, h.nt, kScanTile, 0, s, h, in0);
 }
 
 // coarse values and their projection onto level 2 (k_tree_coarse)
@@ -544,7 +547,7 @@ void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, c
     const size_t sm = (size_t)S->g->tree.maxFrameTiles * sizeof(double);
     if (sm > 48 * 1024)
         ck(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "smem attr");
-    LAUNCH_AS(name.c_str(), kern, S->g->F * S->bpf2, 256, sm, s, h, a, first);
+    LAUNCH_AS(name.c_str(), kern, a.nf * S->bpf2, 256, sm, s, h, a, first);
 }
 
 // level-0 output (k_tree_level0)
@@ -553,7 +556,7 @@ void tree_level0(fbs_system S, const HierArgs& h, const VecArgs& a, const float*
                  cudaStream_t s) {
     static const std::string name = std::string("k_tree_level0<") + mode_name(MODE) + ">";
     auto kern = k_tree_level0<MODE>;
-    LAUNCH_AS(name.c_str(), kern, S->g->F * S->BPF, kThreads, 0, s, h, a, in0, out0, first);
+    LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, h, a, in0, out0, first);
 }
 
 // level-0 PCG input w = mask∘r (+ ρ_0, ‖r‖² partials) (k_hier_level0)
@@ -563,33 +566,62 @@ void hier_level0(fbs_system S, const VecArgs& a, cudaStream_t s) {
     static const std::string name =
         std::string("k_hier_level0<") + src_names[SRC] + (LAST ? ",LAST>" : ">");
     auto kern = k_hier_level0<SRC, LAST>;
-    LAUNCH_AS(name.c_str(), kern, S->g->F * S->BPF, kThreads, 0, s, a, S->w0);
+    LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, a, S->w0);
 }
 
 // s = M⁻¹_hier r and d = s + βd after the level-0 kernel (Alg. 2 lines 10-14)
-void hier_precond_direction(fbs_system S, const VecArgs& a, int first, cudaStream_t s) {
-    tree_lift<HIER_PCG>(S, S->hP, S->w0, s);
-    tree_coarse<HIER_PCG>(S, S->hP, a, first, s);
-    tree_level0<HIER_PCG>(S, S->hP, a, nullptr, nullptr, first, s);
+void hier_precond_direction(fbs_system S, const VecArgs& a, const HierArgs& h, int first, cudaStream_t s) {
+    tree_lift<HIER_PCG>(S, h, S->w0, s);
+    tree_coarse<HIER_PCG>(S, h, a, first, s);
+    tree_level0<HIER_PCG>(S, h, a, nullptr, nullptr, first, s);
+}
+
+// The launch arguments of frames [f0, f0 + nf): per-frame and per-tile pointers shifted so that
+// the kernels (which index frames from blockIdx) see the group as frames 0 … nf − 1.
+void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
+    fbs_grid g = S->g;
+    const int K = S->K;
+    a.nf = nf;
+    a.frameOff += f0;
+    a.counters += f0;
+    a.partial += (size_t)f0 * S->BPF * 2 * K;
+    PcgScalars& q = a.sc_;
+    q.rho += f0 * K;
+    q.alpha += f0 * K;
+    q.beta += f0 * K;
+    q.bb += f0 * K;
+    q.rr += f0 * K;
+    q.active += f0 * K;
+    q.iters += f0 * K;
+    q.status += f0 * K;
+    const int t0 = g->tree.tileFrameOffH.empty() ? 0 : g->tree.tileFrameOffH[f0];
+    h.nt = g->tree.tileFrameOffH.empty() ? 0 : g->tree.tileFrameOffH[f0 + nf] - t0;
+    h.lvFrameOff += f0;  // [L][F+1] row-major: k·(F+1) + f0 + f
+    h.frameLevels += f0;
+    h.tileFrameOff += f0;  // tile ids stay global (tileFrameOff[f] − tileFrameOff[0] is group-local)
+    h.tileRange += t0;
+    h.tileFrame += t0;
+    h.partial2 += (size_t)f0 * S->bpf2 * h.C;
+    h.counters += f0;
 }
 
 // q = A d and α (k_spmv2)
 void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
-    LAUNCH(k_spmv2, S->g->F * S->BPF, kThreads, 0, s, a);
+    LAUNCH(k_spmv2, a.nf * S->BPF, kThreads, 0, s, a);
 }
 
 // One PCG iteration (Alg. 2 lines 6-14): SpMV + α; update (+ M⁻¹ and ρ, β); direction.
 // Hierarchical: ρ = rᵀM⁻¹r comes from the lift, and Pᵀ is fused with d = s + βd
 // (tree_kernels.cuh).  last: the final FIXED-mode iteration needs no new direction.
-void pcg_iteration(fbs_system S, const VecArgs& a, int it, bool last, cudaStream_t s) {
-    const int nb = S->g->F * S->BPF;
+void pcg_iteration(fbs_system S, const VecArgs& a, const HierArgs& h, int it, bool last, cudaStream_t s) {
+    const int nb = a.nf * S->BPF;
     if (S->useHierP) {
         spmv(S, a, s);
         if (last) {
             hier_level0<HSRC_UPDATE, true>(S, a, s);
         } else {
             hier_level0<HSRC_UPDATE, false>(S, a, s);
-            hier_precond_direction(S, a, 0, s);
+            hier_precond_direction(S, a, h, 0, s);
         }
     } else {
         LAUNCH(k_direction2, nb, kThreads, 0, s, a, it == 0);
@@ -598,17 +630,16 @@ void pcg_iteration(fbs_system S, const VecArgs& a, int it, bool last, cudaStream
     }
 }
 
-// Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.
-void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
-    fbs_grid g = S->g;
-    const int nb = g->F * S->BPF;
-    const int FK = g->F * S->K;
-    LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK);
+// Alg. 2 lines 1-4 for the frames of `a`.
+void pcg_start(fbs_system S, const VecArgs& a, const HierArgs& h, bool x_zero, cudaStream_t s) {
+    const int nb = a.nf * S->BPF;
+    const int FKg = a.nf * S->K;  // a group's scalars start at its first frame (restrict_frames)
+    LAUNCH(k_init_scalars, (FKg + 255) / 256, 256, 0, s, a.sc_, FKg, a.nf == S->g->F ? 1 : 0);
     if (S->useHierP) {
         // Alg. 2 lines 2-4: r = b − A x, ρ = rᵀM⁻¹r (lift), d = s = M⁻¹r (project)
         if (x_zero) hier_level0<HSRC_RESID0, false>(S, a, s);
         else hier_level0<HSRC_RESID, false>(S, a, s);
-        hier_precond_direction(S, a, 1, s);
+        hier_precond_direction(S, a, h, 1, s);
     } else {
         auto k1 = k_residual0<true>;
         auto k2 = k_residual0<false>;
@@ -616,8 +647,58 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         else LAUNCH(k2, nb, kThreads, 0, s, a);
         // d = s (Alg. 2 line 3) is the first iteration's k_direction2
     }
+}
+
+// Side streams of the frame-group split (one pair per device, created once).
+cudaStream_t group_stream(int dev, int i) {
+    static std::mutex mu;
+    static std::map<int, std::vector<cudaStream_t>> streams;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& v = streams[dev];
+    while ((int)v.size() <= i) {
+        cudaStream_t st;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+        v.push_back(st);
+    }
+    return v[i];
+}
+
+// Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.
+// FIXED mode with several frames: the frames are split into two groups whose PCGs run on two
+// streams (forked from and joined back to `s`): the frames are independent systems, so one
+// group's latency-bound kernels overlap the other's bandwidth-bound ones.
+void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
+    fbs_grid g = S->g;
+    const int G = std::min(S->nGroups, g->F);
+    if (S->o.mode == FBS_MODE_FIXED && G > 1) {
+        int dev = 0;
+        ck(cudaGetDevice(&dev), "cudaGetDevice");
+        cudaEvent_t fork;
+        std::vector<cudaEvent_t> join(G);
+        ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
+        ck(cudaEventRecord(fork, s), "event");
+        for (int gi = 0; gi < G; ++gi) {
+            const int f0 = (int)((int64_t)g->F * gi / G), f1 = (int)((int64_t)g->F * (gi + 1) / G);
+            cudaStream_t sg = group_stream(dev, gi);
+            ck(cudaStreamWaitEvent(sg, fork, 0), "wait");
+            VecArgs ag = a;
+            HierArgs hg = S->hP;
+            restrict_frames(S, f0, f1 - f0, ag, hg);
+            pcg_start(S, ag, hg, x_zero, sg);
+            for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, ag, hg, i, i == S->o.iters - 1, sg);
+            ck(cudaEventCreateWithFlags(&join[gi], cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(join[gi], sg), "event");
+        }
+        for (int gi = 0; gi < G; ++gi) {
+            ck(cudaStreamWaitEvent(s, join[gi], 0), "wait");
+            cudaEventDestroy(join[gi]);
+        }
+        cudaEventDestroy(fork);
+        return;
+    }
+    pcg_start(S, a, S->hP, x_zero, s);
     if (S->o.mode == FBS_MODE_FIXED) {
-        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, i, i == S->o.iters - 1, s);
+        for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, S->hP, i, i == S->o.iters - 1, s);
         return;
     }
     // TOL: device-side per-channel stopping; the host polls the active count one chunk behind
@@ -631,7 +712,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     try {
         while (done < S->o.max_iters) {
             const int nit = std::min(chunk, S->o.max_iters - done);
-            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, done + i, false, s);
+            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, S->hP, done + i, false, s);
             done += nit;
             ck(cudaMemcpyAsync(&pin[slot], a.sc_.n_active, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
             ck(cudaEventRecord(ev[slot], s), "event");
@@ -715,6 +796,10 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int64_t want = (g->maxFrameM + kThreads - 1) / kThreads;
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
         S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
+        {
+            const char* e = std::getenv("FBS_PCG_GROUPS");  // A/B measurement: 1 disables the split
+            S->nGroups = (e && e[0]) ? std::max(1, std::min(8, std::atoi(e))) : 2;
+        }
         S->sc = dalloc<float>(A, M + kVecPad, s);
         float* bIn = dalloc<float>(A, (size_t)K * M, s);
         CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};

@@ -260,6 +260,8 @@ struct HLevel {
 
 struct HierArgs {
     HLevel lv[kMaxLevels];
+    int nt;                 // scan tiles of this launch (a frame group's HierArgs has its per-frame
+                            // and per-tile pointers shifted to the group, api.cu)
     int L;                  // levels incl. base (max over frames)
     int F;
     int C;                  // channels carried through the pyramid
@@ -302,6 +304,7 @@ struct TreeOrder {
     int2* tileRange = nullptr;
     int maxFrameTiles = 0;
     int nTiles1 = 0;
+    std::vector<int> tileFrameOffH;  // host copy [F+1]
     int2* rng[kMaxLevels] = {};
 };
 
@@ -350,6 +353,7 @@ struct fbs_system_s {
     cudaStream_t stream = nullptr;
     cudaStream_t capture = nullptr;
     int BPF = 1;
+    int nGroups = 2;          // frame groups of the FIXED-mode PCG (run_pcg); FBS_PCG_GROUPS=1 disables
     // vertex arrays
     float* sc = nullptr;      // [M]
     float* b = nullptr;       // [K][M] S(c∘t)

@@ -17,6 +17,8 @@ namespace fbs {
 
 struct VecArgs {
     int K, BPF;
+    int nf;               // frames of this launch (blocks: nf · BPF); a frame group's VecArgs has
+                          // its per-frame pointers shifted to the group's first frame (api.cu)
     int64_t M;
     float lam;
     const int* frameOff;  // [F+1]
@@ -257,10 +259,12 @@ __global__ void k_fill_init_w0(const float* __restrict__ b, const float* __restr
 }
 
 // ---------------------------------------------------------------- PCG (Alg. 2)
-__global__ void k_init_scalars(PcgScalars s, int FK) {
+// scalars of n (frame, channel) pairs (a frame group's arrays are pointer-shifted); set_count:
+// also the global active count of the TOL-mode host poll
+__global__ void k_init_scalars(PcgScalars s, int n, int set_count) {
     pdl_entry();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < FK) {
+    if (i < n) {
         s.rho[i] = 0.0;
         s.alpha[i] = 0.0;
         s.beta[i] = 0.0;
@@ -269,7 +273,7 @@ __global__ void k_init_scalars(PcgScalars s, int FK) {
         s.iters[i] = 0;
         s.status[i] = 0;
     }
-    if (i == 0) *s.n_active = FK;
+    if (i == 0 && set_count) *s.n_active = n;
 }
 
 // Alg. 2 lines 2-4 (Jacobi):  r = b − A x;  s = M⁻¹ r;  ρ = rᵀs   (X_ZERO: x = 0 ⇒ r = b, backward).

@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
         double tot;
         const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
         if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
-        if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + t] = tot;
+        if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + h.tileFrameOff[0] + t] = tot;  // global tile id
         __syncthreads();
     }
 }

@@ -15,7 +15,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfbs.so")
+# FBS_LIB: an alternative in-tree build of the same library (same-box A/B measurements)
+LIB_PATH = os.environ.get("FBS_LIB") or os.path.join(_HERE, "libfbs.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing — build it with `python paper_1511_03296_b200/build.py` "
                       "(the product path has no CPU fallback)")
