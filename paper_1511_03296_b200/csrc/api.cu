@@ -588,6 +588,7 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     PcgScalars& q = a.sc_;
     q.rho += f0 * K;
     q.alpha += f0 * K;
+    q.xalpha += f0 * K;
     q.beta += f0 * K;
     q.bb += f0 * K;
     q.rr += f0 * K;
@@ -739,6 +740,7 @@ PcgScalars alloc_scalars(std::vector<void*>& A, int FK, cudaStream_t s) {
     PcgScalars p;
     p.rho = dalloc<double>(A, FK, s);
     p.alpha = dalloc<double>(A, FK, s);
+    p.xalpha = dalloc<double>(A, FK, s);
     p.beta = dalloc<double>(A, FK, s);
     p.bb = dalloc<double>(A, FK, s);
     p.rr = dalloc<double>(A, FK, s);

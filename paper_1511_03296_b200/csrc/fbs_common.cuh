@@ -238,6 +238,8 @@ struct Level {          // pyramid level k ≥ 1
 struct PcgScalars {     // per (frame, channel), fk = f*K + k
     double* rho = nullptr;
     double* alpha = nullptr;
+    double* xalpha = nullptr; // hierarchical PCG: α of the x update (Alg. 2 line 8) the next direction
+                              // pass applies (0: none); set by the SpMV's finish for every channel
     double* beta = nullptr;
     double* bb = nullptr;   // ‖b‖²
     double* rr = nullptr;   // last ‖r‖² (TOL)

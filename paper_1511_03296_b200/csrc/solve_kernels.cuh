@@ -267,6 +267,7 @@ __global__ void k_init_scalars(PcgScalars s, int n, int set_count) {
     if (i < n) {
         s.rho[i] = 0.0;
         s.alpha[i] = 0.0;
+        s.xalpha[i] = 0.0;
         s.beta[i] = 0.0;
         s.rr[i] = 0.0;
         s.active[i] = 1;
@@ -433,7 +434,10 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
     if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
         for (int k = 0; k < a.K; ++k) {
             const int fk = f * a.K + k;
-            if (!a.sc_.active[fk]) continue;
+            if (!a.sc_.active[fk]) {
+                if (threadIdx.x == 0) a.sc_.xalpha[fk] = 0.0;
+                continue;
+            }
             double DQ = 0.0;
             for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
                 DQ += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k);
@@ -442,10 +446,12 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
                 if (DQ <= 0.0) {
                     a.sc_.active[fk] = 0;
                     a.sc_.alpha[fk] = 0.0;
+                    a.sc_.xalpha[fk] = 0.0;
                     atomicOr(a.sc_.status + fk, FBS_ST_BREAKDOWN);
                     atomicSub(a.sc_.n_active, 1);
                 } else {
                     a.sc_.alpha[fk] = a.sc_.rho[fk] / DQ;
+                    a.sc_.xalpha[fk] = a.sc_.alpha[fk];
                 }
             }
         }

@@ -132,8 +132,10 @@ __global__ void k_tree_anc_mult(HierArgs h, const int* __restrict__ ancId, float
 }
 
 // ================================================================ level 0 → PCG input
-// w = mask∘r with r from the PCG update (Alg. 2 lines 8-9), the initial residual r = b − A x
-// (lines 2), or r = b (x = 0, backward); partials ρ_0 = Σ μ0 w² and ‖r‖².  FINISH_LAST: the
+// w = mask∘r with r from the PCG update r −= αq (Alg. 2 line 9), the initial residual r = b − A x
+// (line 2), or r = b (x = 0, backward); partials ρ_0 = Σ μ0 w² and ‖r‖².  The x update x += αd
+// (line 8) is done by the next direction pass (k_tree_level0, which streams d anyway), except in
+// the FINISH_LAST kernel of the final FIXED-mode iteration.  FINISH_LAST: the
 // final FIXED-mode iteration needs no new direction: its last block per frame records ‖r‖² and
 // the iteration count and retires the channel.
 template <int SRC, bool FINISH_LAST>
@@ -158,8 +160,10 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     for (int u = 0; u < 4; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
-                            xv[u] = a.x[off + v];
-                            dv[u] = a.dn[(size_t)k * a.ldn + v].x;
+                            if (FINISH_LAST) {
+                                xv[u] = a.x[off + v];
+                                dv[u] = a.dn[(size_t)k * a.ldn + v].x;
+                            }
                             rv[u] = a.r[off + v];
                             qv[u] = a.q[off + v];
                             mv[u] = a.mu0[v];
@@ -169,7 +173,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     for (int u = 0; u < 4; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
-                            a.x[off + v] = xv[u] + al * dv[u];
+                            if (FINISH_LAST) a.x[off + v] = xv[u] + al * dv[u];
                             rv[u] -= al * qv[u];
                         }
                     }
@@ -466,11 +470,15 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
     auto acc1 = [&](int c, int pT) { return h.acc1T[(size_t)c * h.M1 + pT]; };
     for (int k = 0; k < K; ++k) {
         const int fk = f * a.K + k;
-        if (MODE == HIER_PCG && !first && !a.sc_.active[fk]) continue;
+        // PCG: this iteration's x += αd (Alg. 2 line 8, deferred from the update kernel) for every
+        // channel the SpMV advanced, even one that stopped since; the new direction for active ones
+        const float xa = (MODE == HIER_PCG && !first) ? (float)a.sc_.xalpha[fk] : 0.f;
+        const bool dir = MODE != HIER_PCG || first || a.sc_.active[fk];
+        if (!dir && xa == 0.f) continue;
         const float be = (MODE == HIER_PCG && !first) ? (float)a.sc_.beta[fk] : 0.f;
         const size_t off = (size_t)k * a.M;
         for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += 4 * stride) {
-            float sv[4], mv[4], up[4];
+            float sv[4], mv[4], up[4], xv[4];
             float2 dv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -484,7 +492,10 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
                     } else {
                         sv[u] = (MODE == HIER_PCG) ? __ldcs(a.r + off + v) : in0[off + v];
                         mv[u] = __ldcs(a.mu0 + v);
-                        if (MODE == HIER_PCG) dv[u] = a.dn[(size_t)k * a.ldn + v];
+                        if (MODE == HIER_PCG) {
+                            dv[u] = a.dn[(size_t)k * a.ldn + v];
+                            if (xa != 0.f) xv[u] = a.x[off + v];
+                        }
                     }
                 }
             }
@@ -496,8 +507,12 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
                     out0[off + v] = (mv[u] > 0.f) ? (sv[u] + up[u]) / mv[u] : 0.f;
                 } else {
                     const float s = (mv[u] > 0.f) ? mv[u] * sv[u] + up[u] : 0.f;
-                    if (MODE == HIER_PCG) a.dn[(size_t)k * a.ldn + v] = make_float2(first ? s : s + be * dv[u].x, dv[u].y);
-                    else out0[off + v] = s;
+                    if (MODE == HIER_PCG) {
+                        if (xa != 0.f) a.x[off + v] = xv[u] + xa * dv[u].x;
+                        if (dir) a.dn[(size_t)k * a.ldn + v] = make_float2(first ? s : s + be * dv[u].x, dv[u].y);
+                    } else {
+                        out0[off + v] = s;
+                    }
                 }
             }
         }
