@@ -469,6 +469,7 @@ VecArgs make_args(fbs_system S, PcgScalars sc, float* x, const float* b) {
     a.mu0 = S->mu0;
     a.partial = S->partial;
     a.counters = S->counters;
+    a.ksplit = 0;
     a.sc_ = sc;
     a.tol_mode = S->o.mode == FBS_MODE_TOL;
     a.tol2 = S->o.tol * S->o.tol;
@@ -521,7 +522,7 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.tileAgg = S->tileAgg;
     h.acc1T = S->acc1T;
     h.partial2 = S->partial2;
-    h.counters = S->counters;
+    h.counters = S->counters2;
     h.bpf2 = S->bpf2;
     return h;
 }
@@ -583,7 +584,7 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     const int K = S->K;
     a.nf = nf;
     a.frameOff += f0;
-    a.counters += f0;
+    a.counters += (size_t)f0 * K;
     a.partial += (size_t)f0 * S->BPF * 2 * K;
     PcgScalars& q = a.sc_;
     q.rho += f0 * K;
@@ -606,16 +607,29 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     h.counters += f0;
 }
 
-// q = A d and α (k_spmv2)
+// The channel-split view of `a` (block_unit): K > 1 right-hand sides get BPFs blocks each.
+VecArgs split_args(fbs_system S, const VecArgs& a) {
+    VecArgs as = a;
+    if (a.K > 1) {
+        as.ksplit = 1;
+        as.BPF = S->BPFs;
+    }
+    return as;
+}
+int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
+
+// q = A d and α (k_spmv2), channel-split
 void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
-    LAUNCH(k_spmv2, a.nf * S->BPF, kThreads, 0, s, a);
+    const VecArgs as = split_args(S, a);
+    LAUNCH(k_spmv2, vec_blocks(as), kThreads, 0, s, as);
 }
 
 // One PCG iteration (Alg. 2 lines 6-14): SpMV + α; update (+ M⁻¹ and ρ, β); direction.
 // Hierarchical: ρ = rᵀM⁻¹r comes from the lift, and Pᵀ is fused with d = s + βd
 // (tree_kernels.cuh).  last: the final FIXED-mode iteration needs no new direction.
 void pcg_iteration(fbs_system S, const VecArgs& a, const HierArgs& h, int it, bool last, cudaStream_t s) {
-    const int nb = a.nf * S->BPF;
+    const VecArgs as = split_args(S, a);
+    const int nb = vec_blocks(as);
     if (S->useHierP) {
         spmv(S, a, s);
         if (last) {
@@ -625,15 +639,16 @@ void pcg_iteration(fbs_system S, const VecArgs& a, const HierArgs& h, int it, bo
             hier_precond_direction(S, a, h, 0, s);
         }
     } else {
-        LAUNCH(k_direction2, nb, kThreads, 0, s, a, it == 0);
+        LAUNCH(k_direction2, nb, kThreads, 0, s, as, it == 0);
         spmv(S, a, s);
-        LAUNCH(k_update, nb, kThreads, 0, s, a);
+        LAUNCH(k_update, nb, kThreads, 0, s, as);
     }
 }
 
 // Alg. 2 lines 1-4 for the frames of `a`.
 void pcg_start(fbs_system S, const VecArgs& a, const HierArgs& h, bool x_zero, cudaStream_t s) {
-    const int nb = a.nf * S->BPF;
+    const VecArgs as = split_args(S, a);
+    const int nb = vec_blocks(as);
     const int FKg = a.nf * S->K;  // a group's scalars start at its first frame (restrict_frames)
     LAUNCH(k_init_scalars, (FKg + 255) / 256, 256, 0, s, a.sc_, FKg, a.nf == S->g->F ? 1 : 0);
     if (S->useHierP) {
@@ -644,8 +659,8 @@ void pcg_start(fbs_system S, const VecArgs& a, const HierArgs& h, bool x_zero, c
     } else {
         auto k1 = k_residual0<true>;
         auto k2 = k_residual0<false>;
-        if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, a);
-        else LAUNCH(k2, nb, kThreads, 0, s, a);
+        if (x_zero) LAUNCH(k1, nb, kThreads, 0, s, as);
+        else LAUNCH(k2, nb, kThreads, 0, s, as);
         // d = s (Alg. 2 line 3) is the first iteration's k_direction2
     }
 }
@@ -866,17 +881,21 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             }
             if (g->L > 3) S->ancMult = dalloc<float>(A, (size_t)(g->L - 3) * g->lv[2].M, s);
         }
+        S->BPFs = (int)std::max<int64_t>(
+            1, std::min<int64_t>(S->BPF, ((int64_t)g_num_sms * occ + (int64_t)F * Kc - 1) / ((int64_t)F * Kc)));
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
-        S->counters = dalloc<unsigned>(A, F, s);
-        ck(cudaMemsetAsync(S->counters, 0, F * sizeof(unsigned), s), "memset");
+        S->counters = dalloc<unsigned>(A, (size_t)F * Kc, s);
+        S->counters2 = dalloc<unsigned>(A, F, s);
+        ck(cudaMemsetAsync(S->counters, 0, (size_t)F * Kc * sizeof(unsigned), s), "memset");
+        ck(cudaMemsetAsync(S->counters2, 0, F * sizeof(unsigned), s), "memset");
         if (hierP || hierI) S->hP = make_hier(S, Kc, o.precond_alpha, o.precond_beta);
         S->fwd = alloc_scalars(A, F * Kc, s);
 
-        const int nb = F * S->BPF;
         // a5: assemble (+ flat/zero init)
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
         const int init_mode = (o.init == FBS_INIT_HIER && !hierI) ? FBS_INIT_FLAT : o.init;
-        LAUNCH(k_assemble, nb, kThreads, 0, s, a, S->diagA, S->mu0, hierP ? S->w0 : nullptr, init_mode, S->fwd);
+        const VecArgs as = split_args(S, a);
+        LAUNCH(k_assemble, vec_blocks(as), kThreads, 0, s, as, S->diagA, S->mu0, hierP ? S->w0 : nullptr, init_mode, S->fwd);
         // a6/a7: hierarchical preconditioner multipliers μ_k = z_w P(1) / P(diag A), and init
         if (hierP) {
             HierArgs h = make_hier(S, 1, o.precond_alpha, o.precond_beta);
@@ -1009,9 +1028,9 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
     LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, g_dldx, K,
            M, nullptr, S->u);
     VecArgs a = make_args(S, S->bwd, S->xb, S->u);
-    const int nb = g->F * S->BPF;
+    const VecArgs as = split_args(S, a);
     // k_assemble here only zeroes x and forms ‖u‖² (diag(A), μ0 are recomputed from the same inputs)
-    LAUNCH(k_assemble, nb, kThreads, 0, s, a, S->diagA, S->mu0, nullptr, FBS_INIT_ZERO, S->bwd);
+    LAUNCH(k_assemble, vec_blocks(as), kThreads, 0, s, as, S->diagA, S->mu0, nullptr, FBS_INIT_ZERO, S->bwd);
     run_pcg(S, a, true, s);
     LAUNCH(k_bwd_finalize, grid_for(g->N), kThreads, 0, s, g->vid, S->xb, S->xh, c, t, M, K, g->F,
            (int64_t)g->H * g->W, dt, dc);

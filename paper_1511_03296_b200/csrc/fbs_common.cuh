@@ -289,7 +289,7 @@ struct HierArgs {
     double* tileAgg;        // [C][nTiles1] tile totals
     float* acc1T;           // [C][M1] projection of levels ≥ 1 onto level 1, tree order
     double* partial2;       // [F][bpf2][C] ρ partials of levels ≥ 1
-    unsigned* counters;     // [F] last-block counters (shared with VecArgs; kernels are serial)
+    unsigned* counters;     // [F] last-block counters of the level-≥1 reductions
     int bpf2;               // blocks per frame of k_tree_coarse
 };
 
@@ -355,6 +355,7 @@ struct fbs_system_s {
     cudaStream_t stream = nullptr;
     cudaStream_t capture = nullptr;
     int BPF = 1;
+    int BPFs = 1;             // blocks per (frame, channel) of the channel-split kernels (K > 1)
     int nGroups = 2;          // frame groups of the FIXED-mode PCG (run_pcg); FBS_PCG_GROUPS=1 disables
     // vertex arrays
     float* sc = nullptr;      // [M]
@@ -380,7 +381,8 @@ struct fbs_system_s {
     int bpf2 = 1;
     int C = 1;
     double* partial = nullptr;  // [F][BPF][2K]
-    unsigned* counters = nullptr;  // [F]
+    unsigned* counters = nullptr;  // [F][K] (VecArgs kernels)
+    unsigned* counters2 = nullptr; // [F] (HierArgs kernels)
     fbs::PcgScalars fwd, bwd;
     bool useHierP = false;
     fbs::HierArgs hP{};

@@ -35,12 +35,38 @@ struct VecArgs {
     const float* b;
     const float* mu0;     // level-0 multiplier 1/diag(A) on live vertices (0 on dead ones)
     double* partial;      // [F][BPF][2K]
-    unsigned* counters;   // [F]
+    unsigned* counters;   // [F][K] last-block counters (block_unit)
+    int ksplit;           // 1: one channel per block group (F·K·BPF blocks), else F·BPF blocks
     PcgScalars sc_;
     int tol_mode;
     double tol2;
     int max_iters;
 };
+
+// Block → (frame f, part j of BPF, channels [k0, k1)) and its last-block counter.  Channel split
+// (ksplit): the K right-hand sides of one frame are independent PCGs sharing A, so each gets its
+// own BPF blocks — K-fold more parallelism for the multi-channel solves (configs[3]) instead of
+// looping the channels inside every block.
+struct BlockUnit {
+    int f, j, k0, k1;
+    unsigned* ctr;
+};
+__device__ __forceinline__ BlockUnit block_unit(const VecArgs& a) {
+    BlockUnit u;
+    const int g = blockIdx.x / a.BPF;
+    u.j = blockIdx.x - g * a.BPF;
+    if (a.ksplit) {
+        u.f = g / a.K;
+        u.k0 = g - u.f * a.K;
+        u.k1 = u.k0 + 1;
+    } else {
+        u.f = g;
+        u.k0 = 0;
+        u.k1 = a.K;
+    }
+    u.ctr = a.counters + (size_t)u.f * a.K + u.k0;
+    return u;
+}
 
 // (A y)_v in Laplacian-difference form (see header): λ n_v Σ_u n_u (y_v − y_u) + Sc_v y_v,
 // neighbours in fixed slot order (x−,x+,l−,l+,u−,u+,v−,v+,y−,y+).
@@ -177,8 +203,8 @@ __device__ __forceinline__ void finish_rho_one(const VecArgs& a, int fk, bool fi
 }
 
 // finish of the ρ-reduction executed by the last block of frame f (partials [F][BPF][2K]).
-__device__ void finish_rho(const VecArgs& a, int f, bool first, double* shd) {
-    for (int k = 0; k < a.K; ++k) {
+__device__ void finish_rho(const VecArgs& a, int f, int k0, int k1, bool first, double* shd) {
+    for (int k = k0; k < k1; ++k) {
         const int fk = f * a.K + k;
         if (!first && !a.sc_.active[fk]) continue;
         double R = 0.0, RR = 0.0;
@@ -213,16 +239,17 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const BlockUnit bu = block_unit(a);
+    const int f = bu.f, j = bu.j;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+    for (int v = v0 + j * blockDim.x + threadIdx.x; bu.k0 == 0 && v < v1; v += a.BPF * blockDim.x) {
         const float dA = a.lam * a.n[v] * nbr_nsum(a.n, v, a.nbr[v]) + a.sc[v];
         const bool live = dA > 0.f;
         diagA[v] = dA;
         mu0[v] = live ? 1.f / dA : 0.f;
         if (w0diag) w0diag[v] = dA;
     }
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = bu.k0; k < bu.k1; ++k) {
         double bb = 0.0;
         const size_t off = (size_t)k * a.M;
         for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
@@ -237,8 +264,8 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
         }
         write_partials(a, f, j, k, bb, 0.0, shd);
     }
-    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
-        for (int k = 0; k < a.K; ++k) {
+    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) {
+        for (int k = bu.k0; k < bu.k1; ++k) {
             double R = 0.0;
             for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
                 R += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k);
@@ -284,9 +311,10 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const BlockUnit bu = block_unit(a);
+    const int f = bu.f, j = bu.j;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = bu.k0; k < bu.k1; ++k) {
         const size_t off = (size_t)k * a.M;
         double rho = 0.0, rr = 0.0;
         for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
@@ -300,7 +328,7 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, true, shd);
+    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, true, shd);
 }
 
 // Alg. 2 lines 8-12 (Jacobi):  x += αd;  r −= αq;  s = M⁻¹r = r/diag(A);  ρ_new = rᵀs.
@@ -308,9 +336,10 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const BlockUnit bu = block_unit(a);
+    const int f = bu.f, j = bu.j;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = bu.k0; k < bu.k1; ++k) {
         const int fk = f * a.K + k;
         double rho = 0.0, rr = 0.0;
         if (a.sc_.active[fk]) {
@@ -347,7 +376,7 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) finish_rho(a, f, false, shd);
+    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, false, shd);
 }
 
 // ---------------------------------------------------------------- streaming PCG kernels
@@ -362,10 +391,11 @@ __global__ void k_init_dn(float2* __restrict__ dn, const float* __restrict__ n, 
 // Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
 __global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
     pdl_entry();
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const BlockUnit bu = block_unit(a);
+    const int f = bu.f, j = bu.j;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
     const int stride = a.BPF * blockDim.x;
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = bu.k0; k < bu.k1; ++k) {
         const int fk = f * a.K + k;
         if (!first && !a.sc_.active[fk]) continue;
         const float be = first ? 0.f : (float)a.sc_.beta[fk];
@@ -395,9 +425,10 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const BlockUnit bu = block_unit(a);
+    const int f = bu.f, j = bu.j;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = bu.k0; k < bu.k1; ++k) {
         const int fk = f * a.K + k;
         double dq = 0.0;
         if (a.sc_.active[fk]) {
@@ -431,8 +462,8 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
         }
         write_partials(a, f, j, k, dq, 0.0, shd);
     }
-    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
-        for (int k = 0; k < a.K; ++k) {
+    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) {
+        for (int k = bu.k0; k < bu.k1; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) {
                 if (threadIdx.x == 0) a.sc_.xalpha[fk] = 0.0;
