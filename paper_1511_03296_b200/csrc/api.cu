@@ -621,7 +621,8 @@ int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
 // q = A d and α (k_spmv2), channel-split
 void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
     const VecArgs as = split_args(S, a);
-    LAUNCH(k_spmv2, vec_blocks(as), kThreads, 0, s, as);
+    auto kern = as.ksplit ? k_spmv2_split : k_spmv2;
+    LAUNCH_AS("k_spmv2", kern, vec_blocks(as), kThreads, 0, s, as);
 }
 
 // One PCG iteration (Alg. 2 lines 6-14): SpMV + α; update (+ M⁻¹ and ρ, β); direction.
@@ -884,10 +885,9 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->BPFs = (int)std::max<int64_t>(
             1, std::min<int64_t>(S->BPF, ((int64_t)g_num_sms * occ + (int64_t)F * Kc - 1) / ((int64_t)F * Kc)));
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
-        S->counters = dalloc<unsigned>(A, (size_t)F * Kc, s);
-        S->counters2 = dalloc<unsigned>(A, F, s);
-        ck(cudaMemsetAsync(S->counters, 0, (size_t)F * Kc * sizeof(unsigned), s), "memset");
-        ck(cudaMemsetAsync(S->counters2, 0, F * sizeof(unsigned), s), "memset");
+        S->counters = dalloc<unsigned>(A, (size_t)F * Kc + F, s);
+        S->counters2 = S->counters + (size_t)F * Kc;
+        ck(cudaMemsetAsync(S->counters, 0, ((size_t)F * Kc + F) * sizeof(unsigned), s), "memset");
         if (hierP || hierI) S->hP = make_hier(S, Kc, o.precond_alpha, o.precond_beta);
         S->fwd = alloc_scalars(A, F * Kc, s);
 

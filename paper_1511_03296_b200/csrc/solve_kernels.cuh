@@ -19,6 +19,7 @@ struct VecArgs {
     int K, BPF;
     int nf;               // frames of this launch (blocks: nf · BPF); a frame group's VecArgs has
                           // its per-frame pointers shifted to the group's first frame (api.cu)
+    int ksplit;           // 1: one channel per block group (F·K·BPF blocks), else F·BPF blocks
     int64_t M;
     float lam;
     const int* frameOff;  // [F+1]
@@ -36,7 +37,6 @@ struct VecArgs {
     const float* mu0;     // level-0 multiplier 1/diag(A) on live vertices (0 on dead ones)
     double* partial;      // [F][BPF][2K]
     unsigned* counters;   // [F][K] last-block counters (block_unit)
-    int ksplit;           // 1: one channel per block group (F·K·BPF blocks), else F·BPF blocks
     PcgScalars sc_;
     int tol_mode;
     double tol2;
@@ -49,13 +49,14 @@ struct VecArgs {
 // looping the channels inside every block.
 struct BlockUnit {
     int f, j, k0, k1;
-    unsigned* ctr;
+    int g;  // last-block counter index: f·K + k (split) or f
 };
+template <int KS>  // 1: split, 0: not split, -1: a.ksplit decides
 __device__ __forceinline__ BlockUnit block_unit(const VecArgs& a) {
     BlockUnit u;
     const int g = blockIdx.x / a.BPF;
     u.j = blockIdx.x - g * a.BPF;
-    if (a.ksplit) {
+    if (KS == 1 || (KS < 0 && a.ksplit)) {
         u.f = g / a.K;
         u.k0 = g - u.f * a.K;
         u.k1 = u.k0 + 1;
@@ -64,9 +65,10 @@ __device__ __forceinline__ BlockUnit block_unit(const VecArgs& a) {
         u.k0 = 0;
         u.k1 = a.K;
     }
-    u.ctr = a.counters + (size_t)u.f * a.K + u.k0;
+    u.g = g;  // non-split: f, unique within a frame group's [f0·K, (f0 + nf)·K)
     return u;
 }
+__device__ __forceinline__ BlockUnit block_unit(const VecArgs& a) { return block_unit<-1>(a); }
 
 // (A y)_v in Laplacian-difference form (see header): λ n_v Σ_u n_u (y_v − y_u) + Sc_v y_v,
 // neighbours in fixed slot order (x−,x+,l−,l+,u−,u+,v−,v+,y−,y+).
@@ -264,7 +266,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
         }
         write_partials(a, f, j, k, bb, 0.0, shd);
     }
-    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) {
+    if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) {
         for (int k = bu.k0; k < bu.k1; ++k) {
             double R = 0.0;
             for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
@@ -328,7 +330,7 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, true, shd);
+    if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, true, shd);
 }
 
 // Alg. 2 lines 8-12 (Jacobi):  x += αd;  r −= αq;  s = M⁻¹r = r/diag(A);  ρ_new = rᵀs.
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, false, shd);
+    if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, false, shd);
 }
 
 // ---------------------------------------------------------------- streaming PCG kernels
@@ -421,14 +423,16 @@ __global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
 }
 
 // Alg. 2 lines 6-7:  q = A d (Laplacian-difference form), α = ρ / dᵀq (breakdown: dᵀq ≤ 0).
+// Latency-bound gathers: 8 resident blocks per SM (≤ 32 registers) matter (40 registers: 6 blocks,
+// 45 → 68 µs on the bench workload with one frame group), and ptxas's allocation for this loop is
+// fragile, so the unsplit kernel keeps its own body and the channel-split one (K > 1) has its own.
 __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
-    const BlockUnit bu = block_unit(a);
-    const int f = bu.f, j = bu.j;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
-    for (int k = bu.k0; k < bu.k1; ++k) {
+    for (int k = 0; k < a.K; ++k) {
         const int fk = f * a.K + k;
         double dq = 0.0;
         if (a.sc_.active[fk]) {
@@ -462,8 +466,77 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
         }
         write_partials(a, f, j, k, dq, 0.0, shd);
     }
-    if (last_block_of_frame(bu.ctr, a.BPF, &sflag)) {
-        for (int k = bu.k0; k < bu.k1; ++k) {
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
+        for (int k = 0; k < a.K; ++k) {
+            const int fk = f * a.K + k;
+            if (!a.sc_.active[fk]) {
+                if (threadIdx.x == 0) a.sc_.xalpha[fk] = 0.0;
+                continue;
+            }
+            double DQ = 0.0;
+            for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
+                DQ += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k);
+            DQ = block_sum(DQ, shd);
+            if (threadIdx.x == 0) {
+                if (DQ <= 0.0) {
+                    a.sc_.active[fk] = 0;
+                    a.sc_.alpha[fk] = 0.0;
+                    a.sc_.xalpha[fk] = 0.0;
+                    atomicOr(a.sc_.status + fk, FBS_ST_BREAKDOWN);
+                    atomicSub(a.sc_.n_active, 1);
+                } else {
+                    a.sc_.alpha[fk] = a.sc_.rho[fk] / DQ;
+                    a.sc_.xalpha[fk] = a.sc_.alpha[fk];
+                }
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_spmv2_split(VecArgs a) {
+    pdl_entry();
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int g = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int f = g / a.K;  // block_unit, inline
+    const int kb = g - f * a.K, ke = kb + 1;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    for (int k = kb; k < ke; ++k) {
+        const int fk = f * a.K + k;
+        double dq = 0.0;
+        if (a.sc_.active[fk]) {
+            const size_t off = (size_t)k * a.M;
+            const float2* dn = a.dn + (size_t)k * a.ldn;
+            for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
+                const int4 nb = __ldcs(a.nbr + v);  // streamed once per iteration: evict-first
+                const float2 me = dn[v];
+                const float scv = __ldcs(a.sc + v);
+                float acc = 0.f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int o = near_off(nb, e);
+                    if (o) {
+                        const float2 u = __ldg(dn + v + o);
+                        acc += u.y * (me.x - u.x);
+                    }
+                }
+                if (nb.z) {
+                    const float2 u = __ldg(dn + v + nb.z);
+                    acc += u.y * (me.x - u.x);
+                }
+                if (nb.w) {
+                    const float2 u = __ldg(dn + v + nb.w);
+                    acc += u.y * (me.x - u.x);
+                }
+                const float q = a.lam * me.y * acc + scv * me.x;
+                a.q[off + v] = q;
+                dq += (double)me.x * (double)q;
+            }
+        }
+        write_partials(a, f, j, k, dq, 0.0, shd);
+    }
+    if (last_block_of_frame(a.counters + g, a.BPF, &sflag)) {
+        for (int k = kb; k < ke; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) {
                 if (threadIdx.x == 0) a.sc_.xalpha[fk] = 0.0;

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (FINISH_LAST && last_block_of_frame(a.counters + (size_t)f * a.K, a.BPF, &sflag)) {
+    if (FINISH_LAST && last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
         for (int k = 0; k < a.K; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) continue;

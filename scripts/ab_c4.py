@@ -13,14 +13,17 @@ dev = torch.device('cuda:0')
 w = make('c4')
 rgb, t, c, gg = (torch.from_numpy(a).to(dev) for a in (w.rgb, w.t, w.c, w.g))
 g = fbs.grid_build(rgb, w.sigma_xy, w.sigma_l, w.sigma_uv, n_bistoch=w.n_bistoch)
-def ms(fn, n=5):
+def ms(fn, n=7):
     for _ in range(2): fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(n): fn()
-    e1.record(); torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / n
+    best = 1e30
+    for _ in range(n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record(); torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    return best
 def jac():
     x, S = fbs.solve(g, t, c, w.lam, precond='jacobi', init='flat', mode='tol', tol=1e-6, keep_system=True)
     S.backward(gg, t, c)
@@ -34,7 +37,7 @@ print(json.dumps(out))
 """
 
 libs = sys.argv[1:] or [""]
-for rep in range(2):
+for rep in range(3):
     for lib in libs:
         env = dict(os.environ)
         if lib:
