@@ -126,9 +126,6 @@ void device_setup(int* dev) {
         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, *dev), "sm count");
         g_num_sms = sms;
         ck(cudaFuncSetAttribute(k_bistoch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBsSmem), "k_bistoch smem");
-        ck(cudaFuncSetAttribute(k_pyr_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                kCoarseCap * (int)sizeof(unsigned long long)),
-           "k_pyr_sort smem");
         pool_done[*dev] = true;
     }
 }
@@ -309,8 +306,8 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             unsigned* ctr2 = dalloc<unsigned>(A, 2, s);  // scan tile counter, scratch bump
             ck(cudaMemsetAsync(st2, 0, st2n * sizeof(unsigned long long), s), "memset");
             ck(cudaMemsetAsync(ctr2, 0, 2 * sizeof(unsigned), s), "memset");
-            LAUNCH(k_pyr_sort, (unsigned)L.ncells, 64, kCoarseCap * sizeof(unsigned long long), s, keysK, cellOffK, ncxK,
-                   ncyK, L.ncx, L.ncy, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
+            LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
+                   L.ncy, L.ncells, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
             lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
             LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2,
                    (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
@@ -878,7 +875,9 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             S->locT = dalloc<double>(A, (size_t)C * M1, s);
             S->tileAgg = dalloc<double>(A, (size_t)C * nT, s);
             const int64_t want2 = ((g->L > 2 ? g->maxFrameM2 : g->maxFrameM1) + 255) / 256;
-            const int64_t cap2 = std::max<int64_t>(1, ((int64_t)g_num_sms * 8 + F - 1) / F);
+            int occ2 = 8;
+            if (const char* e = std::getenv("FBS_BPF2_OCC")) occ2 = std::max(1, std::min(64, std::atoi(e)));  // A/B
+            const int64_t cap2 = std::max<int64_t>(1, ((int64_t)g_num_sms * occ2 + F - 1) / F);
             S->bpf2 = (int)std::max<int64_t>(1, std::min(want2, cap2));
             S->partial2 = dalloc<double>(A, (size_t)F * S->bpf2 * C, s);
             if (hierP) {

@@ -76,70 +76,147 @@ __device__ __forceinline__ CoarseCell coarse_cell(int64_t C, const int* __restri
     return cc;
 }
 
-// Pass 1: one block (T threads) per coarse cell sorts its (halved code, child id) pairs in shared
-// memory (cells with more than kCoarseCap children in a global scratch slice from a bump
-// allocator; rare: dense pixel-noise images at σl = σuv = 1), writes the children grouped by
-// parent in canonical order to the child list, each sorted position's parent rank (rankS) and
-// the cell's parent count.  Blocks are independent (no inter-block chain).
-__global__ void __launch_bounds__(64) k_pyr_sort(const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK,
-                                                 int ncxK, int ncyK, int ncxN, int ncyN, unsigned* __restrict__ bump,
-                                                 unsigned long long* __restrict__ scratch, int* __restrict__ childListN,
-                                                 int* __restrict__ rankS, int* __restrict__ cnt) {
-    pdl_entry();
-    extern __shared__ unsigned long long sk_smem[];  // [kCoarseCap]
-    __shared__ int s_scan[33];
-    __shared__ unsigned s_scr;
-    const int64_t C = blockIdx.x;
-    const int T = blockDim.x;
-    const CoarseCell cc = coarse_cell(C, cellOffK, ncxK, ncyK, ncxN, ncyN);
-    const int nch = cc.n0 + cc.n1;
-    int P = 1;
-    while (P < nch) P <<= 1;
-    if (threadIdx.x == 0) s_scr = (nch > kCoarseCap) ? atomicAdd(bump, (unsigned)P) : 0u;
-    __syncthreads();
-    unsigned long long* sk = (nch <= kCoarseCap) ? sk_smem : scratch + s_scr;
-    for (int i = threadIdx.x; i < P; i += T) {
-        unsigned long long key = ~0ull;
-        if (i < nch) {
-            const int gch = (i < cc.n0) ? cc.s0 + i : cc.s1 + (i - cc.n0);
-            key = ((unsigned long long)halve_code((uint32_t)(keysK[gch] & 0xffffffu)) << 32) | (unsigned)gch;
-        }
-        sk[i] = key;
-    }
-    __syncthreads();
-    // bitonic sort of P (power of two) keys
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int sd = k >> 1; sd > 0; sd >>= 1) {
-            for (int i = threadIdx.x; i < P; i += T) {
-                const int j = i ^ sd;
-                if (j > i) {
-                    const bool asc = (i & k) == 0;
-                    const unsigned long long a = sk[i], b = sk[j];
-                    if ((a > b) == asc) { sk[i] = b; sk[j] = a; }
+// Bitonic sort of 32·E keys held in a warp's registers, blocked layout (lane l holds elements
+// l·E .. l·E + E − 1): strides ≥ E exchange across lanes with shuffles, smaller ones inside a lane.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(unsigned long long (&key)[E]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int kk = 2; kk <= 32 * E; kk <<= 1) {
+#pragma unroll
+        for (int sd = kk >> 1; sd > 0; sd >>= 1) {
+            if (sd >= E) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = lane * E + e;
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key[e], sd / E);
+                    const bool keepMin = ((i & sd) == 0) == ((i & kk) == 0);
+                    key[e] = keepMin ? (key[e] < o ? key[e] : o) : (key[e] < o ? o : key[e]);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int pe = e ^ sd;
+                    if (pe > e) {
+                        const bool asc = ((lane * E + e) & kk) == 0;
+                        const unsigned long long a = key[e], b = key[pe];
+                        const bool sw = (a > b) == asc;
+                        key[e] = sw ? b : a;
+                        key[pe] = sw ? a : b;
+                    }
                 }
             }
-            __syncthreads();
         }
     }
-    // heads and ranks: thread t owns elements [t*E, t*E + E)
-    const int E = (nch + T - 1) / T;
-    const int i0 = threadIdx.x * E;
-    int myHeads = 0;
+}
+
+__device__ __forceinline__ unsigned long long child_key(const uint64_t* __restrict__ keysK, const CoarseCell& cc,
+                                                        int i) {
+    const int gch = (i < cc.n0) ? cc.s0 + i : cc.s1 + (i - cc.n0);
+    return ((unsigned long long)halve_code((uint32_t)(keysK[gch] & 0xffffffu)) << 32) | (unsigned)gch;
+}
+
+// ≤ 32·E children sorted in registers; heads (first child of each parent code) → parent ranks.
+template <int E>
+__device__ __forceinline__ int pyr_sort_regs(const uint64_t* __restrict__ keysK, const CoarseCell& cc, int nch,
+                                             int* __restrict__ childListN, int* __restrict__ rankS) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long key[E];
+#pragma unroll
     for (int e = 0; e < E; ++e) {
-        const int i = i0 + e;
-        if (i < nch && (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32))) ++myHeads;
+        const int i = lane * E + e;
+        key[e] = (i < nch) ? child_key(keysK, cc, i) : ~0ull;
     }
-    int U;
-    const int before = block_excl_scan(myHeads, s_scan, &U);
-    int r = before - 1;
+    warp_bitonic<E>(key);
+    const uint32_t hiPrevLane = __shfl_up_sync(0xffffffffu, (uint32_t)(key[E - 1] >> 32), 1);
+    int heads = 0;
+    unsigned hm = 0;
+#pragma unroll
     for (int e = 0; e < E; ++e) {
-        const int i = i0 + e;
-        if (i >= nch) break;
-        if (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) ++r;
-        childListN[cc.cOff + i] = (int)(sk[i] & 0xffffffffull);
-        rankS[cc.cOff + i] = r;
+        const int i = lane * E + e;
+        const uint32_t prev = (e == 0) ? hiPrevLane : (uint32_t)(key[e - 1] >> 32);
+        const bool head = i < nch && (i == 0 || (uint32_t)(key[e] >> 32) != prev);
+        hm |= (unsigned)head << e;
+        heads += head;
     }
-    if (threadIdx.x == 0) cnt[C] = U;
+    int incl = heads;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    int r = incl - heads - 1;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        if (i < nch) {
+            r += (hm >> e) & 1u;
+            childListN[cc.cOff + i] = (int)(key[e] & 0xffffffffull);
+            rankS[cc.cOff + i] = r;
+        }
+    }
+    return __shfl_sync(0xffffffffu, incl, 31);
+}
+
+// Pass 1: one warp per coarse cell sorts its (halved code, child id) pairs — in registers for
+// ≤ 256 children (every level-1 cell: 4 level-0 cells of ≤ 64 vertices), else in a global scratch
+// slice from a bump allocator — writes the children grouped by parent in canonical order to the
+// child list, each sorted position's parent rank (rankS) and the cell's parent count.  Warps are
+// independent (no inter-block chain, no shared memory).
+__global__ void __launch_bounds__(256) k_pyr_sort(const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK,
+                                                  int ncxK, int ncyK, int ncxN, int ncyN, int64_t ncellsN,
+                                                  unsigned* __restrict__ bump, unsigned long long* __restrict__ scratch,
+                                                  int* __restrict__ childListN, int* __restrict__ rankS,
+                                                  int* __restrict__ cnt) {
+    pdl_entry();
+    const int lane = threadIdx.x & 31;
+    for (int64_t C = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; C < ncellsN;
+         C += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const CoarseCell cc = coarse_cell(C, cellOffK, ncxK, ncyK, ncxN, ncyN);
+        const int nch = cc.n0 + cc.n1;
+        int U;
+        if (nch <= 32) U = pyr_sort_regs<1>(keysK, cc, nch, childListN, rankS);
+        else if (nch <= 64) U = pyr_sort_regs<2>(keysK, cc, nch, childListN, rankS);
+        else if (nch <= 128) U = pyr_sort_regs<4>(keysK, cc, nch, childListN, rankS);
+        else if (nch <= 256) U = pyr_sort_regs<8>(keysK, cc, nch, childListN, rankS);
+        else {
+            int P = 1;
+            while (P < nch) P <<= 1;
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(bump, (unsigned)P);
+            unsigned long long* sk = scratch + __shfl_sync(0xffffffffu, base, 0);
+            for (int i = lane; i < P; i += 32) sk[i] = (i < nch) ? child_key(keysK, cc, i) : ~0ull;
+            __syncwarp();
+            for (int kk = 2; kk <= P; kk <<= 1) {
+                for (int sd = kk >> 1; sd > 0; sd >>= 1) {
+                    for (int i = lane; i < P; i += 32) {
+                        const int j = i ^ sd;
+                        if (j > i) {
+                            const unsigned long long a = sk[i], b = sk[j];
+                            if ((a > b) == ((i & kk) == 0)) {
+                                sk[i] = b;
+                                sk[j] = a;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+            int r = -1;
+            for (int i0 = 0; i0 < nch; i0 += 32) {
+                const int i = i0 + lane;
+                const bool head = i < nch && (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32));
+                const unsigned hb = __ballot_sync(0xffffffffu, head);
+                if (i < nch) {
+                    childListN[cc.cOff + i] = (int)(sk[i] & 0xffffffffull);
+                    rankS[cc.cOff + i] = r + __popc(hb & ((2u << lane) - 1u));
+                }
+                r += __popc(hb);
+            }
+            U = r + 1;
+        }
+        if (lane == 0) cnt[C] = U;
+    }
 }
 
 // Pass 3 (after the exclusive scan of the parent counts → cellOffN): parents get their canonical

@@ -184,6 +184,35 @@ def test_noise_image_dense_grid():
     assert g.M == og.M and np.array_equal(e["keys"], og.keys) and np.array_equal(e["nbr"], og.nbr)
 
 
+@pytest.mark.parametrize("sxy", [8.0, 5.0])
+def test_noise_image_pyramid_bit_exact(sxy):
+    """Dense coarse cells: level-1 coarse cells of up to 4·64 children (the largest register sort,
+    E = 8) and level-2 ones of ~4·256 (noise keeps nearly every halved code distinct), which take
+    the scratch path of k_pyr_sort.  Every level against the oracle's pyramid."""
+    rng = np.random.default_rng(19)
+    rgb = rng.integers(0, 256, (2, 80, 112, 3), dtype=np.uint8)
+    og = O.build_grid(rgb, sxy, 1.0, 1.0)
+    g = fbs.grid_build(dev(rgb), sxy, 1.0, 1.0)
+    assert g.M == og.M
+    info = g.info()
+    levels = {k: g.pyramid_level(k) for k in range(1, info["levels"])}
+    for f in range(rgb.shape[0]):
+        v0, v1 = og.frame_start[f], og.frame_start[f + 1]
+        pyr = O.build_pyramid(og.V[v0:v1])
+        assert info["frame_levels"][f] == pyr.K
+        P1 = O.P_lift(pyr, np.ones(v1 - v0))
+        prev_off = v0
+        for k in range(1, pyr.K):
+            lv = levels[k]
+            seg = np.nonzero((lv["keys"] >> np.uint64(56)).astype(np.int64) == f)[0]
+            off = seg[0]
+            assert np.array_equal(lv["keys"][seg], O.pack_key(pyr.levels[k]))
+            assert np.array_equal(lv["count"][seg], P1[k].astype(np.int64))
+            n_prev = pyr.levels[k - 1].shape[0]
+            assert np.array_equal(lv["parent"][prev_off:prev_off + n_prev] - off, pyr.parents[k - 1])
+            prev_off = off
+
+
 def test_zero_confidence_and_constant_target():
     rgb, t, c = small(K=2)
     g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
