@@ -240,22 +240,24 @@ __global__ void __launch_bounds__(256) k_grid_write(
 }
 
 // ---------------------------------------------------------------- neighbours (B̄ structure)
-// lower bound in a sorted shared-memory segment of n ≤ 64 codes: 6 fixed, branch-free steps
-__device__ __forceinline__ int lower_bound_s(const uint32_t* a, int n, uint32_t q) {
+// position of code q in a sorted shared-memory segment padded to 64 entries with 0xFFFFFFFF
+// (codes are 24-bit, so the padding sorts last and never matches): 6 fixed, branch-free steps
+__device__ __forceinline__ int find_s(const uint32_t* a, uint32_t q) {
     int pos = 0;
 #pragma unroll
     for (int step = 32; step > 0; step >>= 1)
-        if (pos + step <= n && a[pos + step - 1] < q) pos += step;
-    return pos;
+        if (a[pos + step - 1] < q) pos += step;
+    return (a[pos] == q) ? pos : -1;
 }
 
 // One warp per cell: stage the 24-bit codes of the cell and of its x∓ / y∓ neighbour cells in
-// shared memory, then each vertex binary-searches its 10 ±1 neighbours (reading #4).
+// shared memory, then each vertex finds its 10 ±1 neighbours (reading #4): v± are adjacent in the
+// sorted cell, the other 8 are binary searches.
 __global__ void __launch_bounds__(256) k_grid_neighbours(
     const uint64_t* __restrict__ keys, const int* __restrict__ cellOff, int ncx, int ncy,
     int64_t ncells, int4* __restrict__ nbr, int* __restrict__ err) {
     pdl_entry();
-    __shared__ uint32_t sc[kCellsPerBlock][5][kCellMaxPx];
+    __shared__ uint32_t sc[kCellsPerBlock][5][kCellMaxPx + 1];  // + 1: sc[i + 1] of the last entry
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
          c += (int64_t)gridDim.x * kCellsPerBlock) {
@@ -273,27 +275,38 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
                 if (lane == 0) atomicOr(err, 2);
                 ln[s] = kCellMaxPx;
             }
-            for (int i = lane; i < ln[s]; i += 32) sc[warp][s][i] = (uint32_t)(keys[st[s] + i] & 0xffffffu);
+#pragma unroll
+            for (int h = 0; h < kCellMaxPx / 32; ++h) {
+                const int i = lane + 32 * h;
+                sc[warp][s][i] = (i < ln[s]) ? (uint32_t)(keys[st[s] + i] & 0xffffffu) : 0xffffffffu;
+            }
         }
+        if (lane == 0) sc[warp][0][kCellMaxPx] = 0xffffffffu;
         __syncwarp();
         for (int i = lane; i < ln[0]; i += 32) {
             const uint32_t q = sc[warp][0][i];
             const int v = st[0] + i;
             const uint32_t l = (q >> 16) & 255u, u = (q >> 8) & 255u, vv = q & 255u;
-            // slot → (segment, target code, field-in-range)
-            const int seg[10] = {1, 2, 0, 0, 0, 0, 0, 0, 3, 4};
-            const uint32_t tq[10] = {q, q, q - (1u << 16), q + (1u << 16), q - (1u << 8), q + (1u << 8),
-                                     q - 1u, q + 1u, q, q};
-            const bool in[10] = {true, true, l > 0, l < 255, u > 0, u < 255, vv > 0, vv < 255, true, true};
+            // slot order x−, x+, l−, l+, u−, u+, v−, v+, y−, y+.  v± (the least significant field)
+            // are the adjacent entries of the cell's sorted codes when present; the rest are
+            // searched in the staged segment of their cell (x∓: cells c∓1, y∓: c∓ncx, else c).
             int offs[10];
+            const int seg[6] = {1, 2, 0, 0, 0, 0};
+            const uint32_t tq[6] = {q, q, q - (1u << 16), q + (1u << 16), q - (1u << 8), q + (1u << 8)};
+            const bool in[6] = {true, true, l > 0, l < 255, u > 0, u < 255};
 #pragma unroll
-            for (int k = 0; k < 10; ++k) {
-                offs[k] = 0;
+            for (int k = 0; k < 6; ++k) {
                 const int s = seg[k];
-                if (in[k] && ln[s] > 0) {
-                    const int j = lower_bound_s(sc[warp][s], ln[s], tq[k]);
-                    if (j < ln[s] && sc[warp][s][j] == tq[k]) offs[k] = st[s] + j - v;
-                }
+                const int j = in[k] ? find_s(sc[warp][s], tq[k]) : -1;
+                offs[k] = (j >= 0) ? st[s] + j - v : 0;
+            }
+            offs[6] = (vv > 0 && i > 0 && sc[warp][0][i - 1] == q - 1u) ? -1 : 0;
+            offs[7] = (vv < 255 && sc[warp][0][i + 1] == q + 1u) ? 1 : 0;  // i + 1 ≤ 64: padded
+#pragma unroll
+            for (int k = 8; k < 10; ++k) {
+                const int s = k - 5;
+                const int j = find_s(sc[warp][s], q);
+                offs[k] = (j >= 0) ? st[s] + j - v : 0;
             }
             unsigned bx = 0, by = 0;
 #pragma unroll
