@@ -75,11 +75,12 @@ __device__ __forceinline__ uint32_t luv_code(const uint8_t* __restrict__ px, con
 }
 
 __device__ __forceinline__ void cell_of(const CellGeom& g, int64_t c, int& f, int& cy, int& cx) {
-    const int64_t per = (int64_t)g.ncx * g.ncy;
-    f = (int)(c / per);
-    const int64_t r = c - (int64_t)f * per;
-    cy = (int)(r / g.ncx);
-    cx = (int)(r - (int64_t)cy * g.ncx);
+    // 32-bit arithmetic (cell counts < 2^31; a 64-bit division is a ~70-instruction sequence)
+    const unsigned per = (unsigned)g.ncx * (unsigned)g.ncy, cu = (unsigned)c;
+    f = (int)(cu / per);
+    const unsigned r = cu - (unsigned)f * per;
+    cy = (int)(r / (unsigned)g.ncx);
+    cx = (int)(r - (unsigned)cy * (unsigned)g.ncx);
 }
 
 // ---------------------------------------------------------------- level-0 grid build
@@ -183,11 +184,16 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(const int* __restrict_
     }
     __syncthreads();
     int run = (int)s_excl + wex + incl - sum;
+    int64_t fq = frameOff ? base / per : 0, fr = frameOff ? base - fq * per : 0;  // base = fq·per + fr
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
         if (base + i < n) {
             out[base + i] = run;
-            if (frameOff && (base + i) % per == 0) frameOff[(base + i) / per] = run;
+            if (frameOff && fr == 0) frameOff[fq] = run;
+        }
+        if (++fr == per) {
+            fr = 0;
+            ++fq;
         }
         if (base + i == n - 1) {
             out[n] = run + v[i];
@@ -261,9 +267,8 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
          c += (int64_t)gridDim.x * kCellsPerBlock) {
-        const int64_t per = (int64_t)ncx * ncy;
-        const int64_t r = c % per;
-        const int cy = (int)(r / ncx), cx = (int)(r % ncx);
+        const unsigned per = (unsigned)ncx * (unsigned)ncy, r = (unsigned)c % per;
+        const int cy = (int)(r / (unsigned)ncx), cx = (int)(r - (unsigned)cy * (unsigned)ncx);
         int st[5], ln[5];
         const int64_t cc[5] = {c, c - 1, c + 1, c - ncx, c + ncx};
         const bool ok[5] = {true, cx > 0, cx < ncx - 1, cy > 0, cy < ncy - 1};

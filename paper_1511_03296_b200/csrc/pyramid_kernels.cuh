@@ -57,11 +57,11 @@ struct CoarseCell {
 __device__ __forceinline__ CoarseCell coarse_cell(int64_t C, const int* __restrict__ cellOffK, int ncxK, int ncyK,
                                                   int ncxN, int ncyN) {
     CoarseCell cc{};
-    const int64_t per = (int64_t)ncxN * ncyN;
-    cc.f = (int)(C / per);
-    const int64_t r = C - (int64_t)cc.f * per;
-    cc.CY = (int)(r / ncxN);
-    cc.CX = (int)(r - (int64_t)cc.CY * ncxN);
+    const unsigned per = (unsigned)ncxN * (unsigned)ncyN, cu = (unsigned)C;  // 32-bit: cell counts < 2^31
+    cc.f = (int)(cu / per);
+    const unsigned r = cu - (unsigned)cc.f * per;
+    cc.CY = (int)(r / (unsigned)ncxN);
+    cc.CX = (int)(r - (unsigned)cc.CY * (unsigned)ncxN);
     const int cx0 = 2 * cc.CX, cx1 = min(2 * cc.CX + 1, ncxK - 1);
     const int64_t ck0 = ((int64_t)cc.f * ncyK + 2 * cc.CY) * ncxK;
     cc.s0 = cellOffK[ck0 + cx0];

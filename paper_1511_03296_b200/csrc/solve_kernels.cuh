@@ -95,7 +95,10 @@ __device__ __forceinline__ float nbr_nsum(const float* __restrict__ n, int v, in
 // ---------------------------------------------------------------- splat  S p
 // One warp per σxy cell.  The grid build stored each cell's pixels in sorted (code, pixel) order
 // (perm), so the pixels of one vertex are consecutive: each vertex sum is a warp segmented scan
-// in fp64 over the two 32-pixel halves, the halves added in fixed order — deterministic.
+// in fp64 over the two 32-pixel halves, the halves added in fixed order — deterministic.  The
+// tail lane of each segment writes the vertex sum; the one vertex that may span the halves gets
+// half 0's partial (lane 31) carried into half 1's sum.  All of a pixel's loads (vid, c, the
+// first channel) go out in one round trip; later channels are prefetched one ahead.
 // WEIGHTED: Sc = S c and b_k = S(c∘t_k) (Eq. quad_min); otherwise out_k = S p_k.
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict__ cellOff,
@@ -103,7 +106,6 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
                                                const float* __restrict__ c, const float* __restrict__ p, int K,
                                                int64_t M, float* __restrict__ sc_out, float* __restrict__ out) {
     pdl_entry();
-    __shared__ double acc[kCellsPerBlock][kCellMaxPx];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ncells = (int64_t)g.F * g.ncx * g.ncy;
     const size_t HW = (size_t)g.H * g.W;
@@ -114,10 +116,11 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
         const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
         const int w = g.colStart[cx + 1] - x0, h = g.rowStart[cy + 1] - y0;
         const int npx = min(w * h, kCellMaxPx);
-        const int vbeg = cellOff[cell], U = cellOff[cell + 1] - vbeg;
-        size_t pix[2];
-        int rk[2];
-        float cw[2];
+        const float rw = 1.f / (float)w;  // (i + ½)/w is ≥ 1/128 from an integer: exact row
+        const int vbeg = cellOff[cell];
+        const float* pf = p + (size_t)f * K * HW;
+        int pix[2], rk[2];
+        float cw[2], pv[2];
         bool tail[2];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -125,11 +128,14 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
             rk[j] = -1;
             pix[j] = 0;
             cw[j] = 0.f;
+            pv[j] = 0.f;
             if (e < npx) {
                 const int i = perm[(size_t)cell * kCellMaxPx + e];
-                pix[j] = (size_t)(y0 + i / w) * g.W + (x0 + i % w);
+                const int iy = (int)(((float)i + 0.5f) * rw);
+                pix[j] = (y0 + iy) * g.W + (x0 + i - iy * w);
                 rk[j] = vid[(size_t)f * HW + pix[j]] - vbeg;
                 cw[j] = WEIGHTED ? c[(size_t)f * HW + pix[j]] : 1.f;
+                if (K > 0) pv[j] = pf[pix[j]];
             }
         }
         // segment bounds inside each half: lane l's segment starts at the last head ≤ l
@@ -143,36 +149,40 @@ __global__ void __launch_bounds__(256) k_splat(CellGeom g, const int* __restrict
             const int nxt = __shfl_down_sync(0xffffffffu, rk[j], 1);
             tail[j] = (lane == 31) || (rk[j] != nxt);
         }
+        // the vertex spanning the halves: half 0's last segment continues at half 1's lane 0
+        const int rk31 = __shfl_sync(0xffffffffu, rk[0], 31);
+        const int rk32 = __shfl_sync(0xffffffffu, rk[1], 0);
+        const bool span = rk31 >= 0 && rk31 == rk32;
         const int nch = WEIGHTED ? K + 1 : K;
         for (int ch = 0; ch < nch; ++ch) {
             const int k = WEIGHTED ? ch - 1 : ch;  // channel WEIGHTED&&ch==0: Sc; else b_k
-            for (int i = lane; i < U; i += 32) acc[warp][i] = 0.0;
-            __syncwarp();
+            float pn[2] = {0.f, 0.f};
+            const bool data = !(WEIGHTED && ch == 0);
+            if (data && k + 1 < K) {  // prefetch the next channel
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    if (rk[j] >= 0) pn[j] = pf[(size_t)(k + 1) * HW + pix[j]];
+            }
+            double vs[2];
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 double v = 0.0;
-                if (rk[j] >= 0) {
-                    if (WEIGHTED && ch == 0) {
-                        v = (double)cw[j];
-                    } else {
-                        const float pv = p[((size_t)f * K + k) * HW + pix[j]];
-                        v = WEIGHTED ? (double)cw[j] * (double)pv : (double)pv;
-                    }
-                }
+                if (rk[j] >= 0) v = data ? (WEIGHTED ? (double)cw[j] * (double)pv[j] : (double)pv[j]) : (double)cw[j];
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {  // segmented inclusive scan (fixed tree)
                     const double t = __shfl_up_sync(0xffffffffu, v, d);
                     if (lane - d >= sstart[j]) v += t;
                 }
-                if (tail[j] && rk[j] >= 0) acc[warp][rk[j]] += v;  // half 0 then half 1: fixed order
-                __syncwarp();
+                vs[j] = v;
             }
-            for (int i = lane; i < U; i += 32) {
-                const float v = (float)acc[warp][i];
-                if (WEIGHTED && ch == 0) sc_out[vbeg + i] = v;
-                else out[(size_t)k * M + vbeg + i] = v;
+            const double carry = __shfl_sync(0xffffffffu, vs[0], 31);
+            float* dst = data ? out + (size_t)k * M + vbeg : sc_out + vbeg;
+            if (tail[0] && rk[0] >= 0 && !(lane == 31 && span)) dst[rk[0]] = (float)(0.0 + vs[0]);
+            if (tail[1] && rk[1] >= 0) dst[rk[1]] = (float)((span && sstart[1] == 0) ? carry + vs[1] : 0.0 + vs[1]);
+            if (data) {
+                pv[0] = pn[0];
+                pv[1] = pn[1];
             }
-            __syncwarp();
         }
     }
 }
