@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kScanBlock) k_scan_excl(const int* __restrict_
     }
 }
 
-__global__ void __launch_bounds__(256) k_grid_write(
+__global__ void __launch_bounds__(256, 8) k_grid_write(
     const uint8_t* __restrict__ rgb, CellGeom g, const uint8_t* __restrict__ lutL,
     const uint8_t* __restrict__ lutUV, int64_t ncells, const int* __restrict__ cellOff,
     const unsigned long long* __restrict__ heads, const uint8_t* __restrict__ perm, uint64_t* __restrict__ keys,
