@@ -110,14 +110,17 @@ __global__ void __launch_bounds__(256) k_grid_sort(
             npx = kCellMaxPx;
         }
         const uint8_t* base = rgb + (size_t)f * g.H * g.W * 3;
+        const float rw = 1.f / (float)w;  // (i + ½)/w is ≥ 1/128 from an integer: exact row
         uint32_t a0 = 0xffffffffu, a1 = 0xffffffffu;
         if (lane < npx) {
-            const int px = x0 + lane % w, py = y0 + lane / w;
+            const int iy = (int)(((float)lane + 0.5f) * rw);
+            const int px = x0 + lane - iy * w, py = y0 + iy;
             a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)lane;
         }
         if (lane + 32 < npx) {
             const int i = lane + 32;
-            const int px = x0 + i % w, py = y0 + i / w;
+            const int iy = (int)(((float)i + 0.5f) * rw);
+            const int px = x0 + i - iy * w, py = y0 + iy;
             a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)i;
         }
         warp_bitonic64(a0, a1, lane);
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(256, 8) k_grid_write(
         const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
         const int w = g.colStart[cx + 1] - x0;
         const int npx = min(w * (g.rowStart[cy + 1] - y0), kCellMaxPx);
+        const float rw = 1.f / (float)w;
         const unsigned long long H64 = heads[c];
         const unsigned off = (unsigned)cellOff[c];
         const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)cy << 40) | ((uint64_t)cx << 24);
@@ -231,7 +235,8 @@ __global__ void __launch_bounds__(256, 8) k_grid_write(
             const int e = lane + 32 * j;
             if (e >= npx) continue;
             const int i = perm[(size_t)c * kCellMaxPx + e];
-            const int px = x0 + i % w, py = y0 + i / w;
+            const int iy = (int)(((float)i + 0.5f) * rw);
+            const int px = x0 + i - iy * w, py = y0 + iy;
             const unsigned long long upto = (e == 63) ? ~0ull : ((2ull << e) - 1ull);
             const unsigned v = off + (unsigned)__popcll(H64 & upto) - 1u;
             vbase[(size_t)py * g.W + px] = (int)v;
