@@ -144,6 +144,70 @@ void free_all(std::vector<void*>& list, cudaStream_t s) {
     list.clear();
 }
 
+// ---- small host <-> device transfers through mapped pinned memory and a copy kernel.
+// cudaMemcpyAsync queues on the copy engines behind whatever bulk copies other streams have in
+// flight (a caller's 66 MB result read-back or 182 MB input upload), which stalled the grid
+// build's level-size read-backs by up to a millisecond per step in a pipelined caller.  A kernel
+// reading or writing mapped host memory (device address = host address under UVA) does not wait
+// on the copy engines.  Buffers come from a process-wide pool; a returned buffer carries an event
+// recorded on the stream of its last use and is reused only once that event has completed.
+std::mutex g_pin_mu;
+std::vector<PinnedBlock> g_pin_free;
+
+PinnedBlock pinned_get(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_free.size(); ++i) {
+            PinnedBlock b = g_pin_free[i];
+            if (b.bytes >= bytes && (!b.done || cudaEventQuery(b.done) == cudaSuccess)) {
+                g_pin_free.erase(g_pin_free.begin() + i);
+                return b;
+            }
+        }
+    }
+    PinnedBlock b;
+    b.bytes = std::max<size_t>(bytes, 64 * 1024);
+    ck(cudaHostAlloc(&b.p, b.bytes, cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+    ck(cudaEventCreateWithFlags(&b.done, cudaEventDisableTiming), "event");
+    return b;
+}
+
+void pinned_put(PinnedBlock b, cudaStream_t s) {
+    if (!b.p) return;
+    cudaEventRecord(b.done, s);
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(b);
+}
+
+__global__ void k_copy_words(const int* __restrict__ src, int* __restrict__ dst, int64_t n) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+__global__ void k_zero_words(int* __restrict__ dst, int64_t n) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = 0;
+}
+
+// zero `bytes` (a multiple of 4) of device memory with a kernel (cudaMemsetAsync may queue on a copy
+// engine behind a caller's bulk transfers)
+void zero_words(void* dst, size_t bytes, cudaStream_t s) {
+    const int64_t n = (int64_t)(bytes / 4);
+    if (n == 0) return;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+    LAUNCH(k_zero_words, blocks, 256, 0, s, static_cast<int*>(dst), n);
+}
+
+// copy `bytes` (a multiple of 4) between device memory and a mapped pinned block, in stream order
+void copy_words(const void* src, void* dst, size_t bytes, cudaStream_t s) {
+    const int64_t n = (int64_t)(bytes / 4);
+    if (n == 0) return;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+    LAUNCH(k_copy_words, blocks, 256, 0, s, static_cast<const int*>(src), static_cast<int*>(dst), n);
+}
+
 inline int grid_for(int64_t n, int threads = kThreads, int cap_per_sm = 16) {
     int64_t b = (n + threads - 1) / threads;
     const int64_t cap = (int64_t)(g_num_sms > 0 ? g_num_sms : 148) * cap_per_sm;
@@ -210,12 +274,11 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
 
         // scratch: scan tile counter + look-back state (+ error flag, + residual words)
         const int64_t scanTiles = (g->ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems);
-        unsigned* counter = dalloc<unsigned>(A, 1, s);
-        int* err = dalloc<int>(A, 4, s);
-        unsigned long long* state = dalloc<unsigned long long>(A, std::max<int64_t>(scanTiles, 1), s);
-        ck(cudaMemsetAsync(counter, 0, sizeof(unsigned), s), "memset");
-        ck(cudaMemsetAsync(err, 0, 4 * sizeof(int), s), "memset");
-        ck(cudaMemsetAsync(state, 0, std::max<int64_t>(scanTiles, 1) * sizeof(unsigned long long), s), "memset");
+        const int64_t nState = std::max<int64_t>(scanTiles, 1);
+        unsigned long long* state = dalloc<unsigned long long>(A, nState + 3, s);  // + counter, err[4]
+        unsigned* counter = reinterpret_cast<unsigned*>(state + nState);
+        int* err = reinterpret_cast<int*>(state + nState + 1);
+        zero_words(state, (nState + 3) * sizeof(unsigned long long), s);
         g->vid = dalloc<int>(A, N, s);
         uint64_t* keysCap = dalloc<uint64_t>(A, N, s);
         int* mCap = dalloc<int>(A, N + kVecPad, s);
@@ -240,9 +303,13 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // ---- sync 1: vertex counts (sizes the vertex arrays and the pyramid capacities)
         std::vector<int> fo(F + 1);
         int errh[4];
-        ck(cudaMemcpyAsync(fo.data(), g->frameOff, (F + 1) * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
-        ck(cudaMemcpyAsync(errh, err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
+        PinnedBlock rb = pinned_get(((size_t)(F + 1) * (kMaxLevels + 1) + 4) * sizeof(int));  // read-backs
+        int* rbi = static_cast<int*>(rb.p);
+        copy_words(g->frameOff, rbi, (F + 1) * sizeof(int), s);
+        copy_words(err, rbi + F + 1, 4 * sizeof(int), s);
         ck(cudaStreamSynchronize(s), "sync");
+        std::copy(rbi, rbi + F + 1, fo.begin());
+        std::copy(rbi + F + 1, rbi + F + 5, errh);
         if (errh[0]) throw Err(FBS_ELIMIT, "a sigma_xy cell holds more than 64 pixels");
         g->M = fo[F];
         g->frameOffH.assign(fo.begin(), fo.end());
@@ -288,6 +355,17 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         std::vector<int*> lvFrameOffDev(Lmax, nullptr);
         unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
         int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, s) : nullptr;  // parent rank of each sorted child
+        // scan look-back states and (tile counter, scratch bump) pairs of every level: one zeroing
+        std::vector<int64_t> st2Off(Lmax + 1, 0);
+        for (int k = 1; k < Lmax; ++k) {
+            const int64_t nc = (int64_t)F * (((ncx - 1) >> k) + 1) * (((ncy - 1) >> k) + 1);
+            st2Off[k + 1] = st2Off[k] + std::max<int64_t>(1, (nc + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems)) + 1;
+        }
+        unsigned long long* st2All = nullptr;
+        if (Lmax > 1) {
+            st2All = dalloc<unsigned long long>(A, st2Off[Lmax], s);
+            zero_words(st2All, st2Off[Lmax] * sizeof(unsigned long long), s);
+        }
         for (int k = 1; k < Lmax; ++k) {
             Level& L = g->lv[k];
             L.ncx = ((ncx - 1) >> k) + 1;
@@ -302,10 +380,8 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             if (k >= 2) L.cnt1 = dalloc<int>(A, M, s);
             int* cnt2 = dalloc<int>(A, L.ncells, s);
             const int64_t st2n = std::max<int64_t>(1, (L.ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems));
-            unsigned long long* st2 = dalloc<unsigned long long>(A, st2n, s);
-            unsigned* ctr2 = dalloc<unsigned>(A, 2, s);  // scan tile counter, scratch bump
-            ck(cudaMemsetAsync(st2, 0, st2n * sizeof(unsigned long long), s), "memset");
-            ck(cudaMemsetAsync(ctr2, 0, 2 * sizeof(unsigned), s), "memset");
+            unsigned long long* st2 = st2All + st2Off[k];
+            unsigned* ctr2 = reinterpret_cast<unsigned*>(st2 + st2n);  // scan tile counter, scratch bump
             LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
             lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
@@ -322,13 +398,12 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         }
         // ---- sync 2: level sizes
         std::vector<std::vector<int>> lfo(Lmax);
-        for (int k = 1; k < Lmax; ++k) {
-            lfo[k].resize(F + 1);
-            ck(cudaMemcpyAsync(lfo[k].data(), lvFrameOffDev[k], (F + 1) * sizeof(int), cudaMemcpyDeviceToHost, s),
-               "d2h");
-        }
-        ck(cudaMemcpyAsync(errh, err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
+        for (int k = 1; k < Lmax; ++k) copy_words(lvFrameOffDev[k], rbi + (size_t)k * (F + 1), (F + 1) * sizeof(int), s);
+        copy_words(err, rbi + (size_t)Lmax * (F + 1), 4 * sizeof(int), s);
         ck(cudaStreamSynchronize(s), "sync");
+        for (int k = 1; k < Lmax; ++k) lfo[k].assign(rbi + (size_t)k * (F + 1), rbi + (size_t)(k + 1) * (F + 1));
+        std::copy(rbi + (size_t)Lmax * (F + 1), rbi + (size_t)Lmax * (F + 1) + 4, errh);
+        pinned_put(rb, s);
         if (errh[0] & ~8) throw Err(FBS_ECUDA, "internal grid-build check failed (code " + std::to_string(errh[0]) + ")");
         g->bistoch_residual = -1.f;  // computed on request (fbs_grid_export)
         // per-frame level counts: first level with a single vertex (reading #8)
@@ -351,15 +426,34 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             g->lv[k].frameOff.assign(lfo[k].begin(), lfo[k].end());
         }
 
+        // uploads (frame levels, level frame offsets, scan tiles) staged in one mapped pinned block
+        // that lives as long as the grid (no synchronisation for its lifetime)
+        std::vector<int> up;
+        auto stage = [&up](const void* p, size_t bytes) {
+            const size_t at = up.size();
+            up.resize(at + bytes / 4);
+            std::memcpy(up.data() + at, p, bytes);
+            return at;
+        };
+        std::vector<std::pair<size_t, std::pair<void*, size_t>>> upl;  // (offset, (device dst, bytes))
         g->frameLevels = dalloc<int>(A, F, s);
-        ck(cudaMemcpyAsync(g->frameLevels, g->frameLevelsH.data(), F * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
+        upl.push_back({stage(g->frameLevelsH.data(), F * sizeof(int)), {g->frameLevels, F * sizeof(int)}});
         std::vector<int> lfoAll((size_t)L * (F + 1));
         for (int f = 0; f <= F; ++f) lfoAll[f] = fo[f];
         for (int k = 1; k < L; ++k)
             for (int f = 0; f <= F; ++f) lfoAll[(size_t)k * (F + 1) + f] = lfo[k][f];
         g->lvFrameOffDev = dalloc<int>(A, lfoAll.size(), s);
-        ck(cudaMemcpyAsync(g->lvFrameOffDev, lfoAll.data(), lfoAll.size() * sizeof(int), cudaMemcpyHostToDevice, s),
-           "h2d");
+        upl.push_back({stage(lfoAll.data(), lfoAll.size() * sizeof(int)), {g->lvFrameOffDev, lfoAll.size() * sizeof(int)}});
+        auto flush_uploads = [&]() {
+            if (up.empty()) return;
+            PinnedBlock b = pinned_get(up.size() * sizeof(int));
+            g->uploads.push_back(b);
+            std::memcpy(b.p, up.data(), up.size() * sizeof(int));
+            for (auto& e : upl) copy_words(static_cast<int*>(b.p) + e.first, e.second.first, e.second.second, s);
+            up.clear();
+            upl.clear();
+        };
+        flush_uploads();  // the tree kernels below read the level frame offsets
         // ---- tree order of the pyramid (tree_kernels.cuh): depth-first positions of the level-0 and
         // level-1 vertices, so every coarse subtree is one contiguous level-1 range
         std::vector<int> tfo, tframe;
@@ -424,16 +518,15 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             T.tileFrame = dalloc<int>(A, std::max<size_t>(tframe.size(), 1), s);
             T.tileRange = dalloc<int2>(A, std::max<size_t>(trange.size(), 1), s);
             if (!trange.empty())
-                ck(cudaMemcpyAsync(T.tileRange, trange.data(), trange.size() * sizeof(int2), cudaMemcpyHostToDevice, s),
-                   "h2d");
-            ck(cudaMemcpyAsync(T.tileFrameOff, tfo.data(), (F + 1) * sizeof(int), cudaMemcpyHostToDevice, s), "h2d");
+                upl.push_back({stage(trange.data(), trange.size() * sizeof(int2)), {T.tileRange, trange.size() * sizeof(int2)}});
+            upl.push_back({stage(tfo.data(), (F + 1) * sizeof(int)), {T.tileFrameOff, (F + 1) * sizeof(int)}});
             if (!tframe.empty())
-                ck(cudaMemcpyAsync(T.tileFrame, tframe.data(), tframe.size() * sizeof(int), cudaMemcpyHostToDevice, s),
-                   "h2d");
+                upl.push_back({stage(tframe.data(), tframe.size() * sizeof(int)), {T.tileFrame, tframe.size() * sizeof(int)}});
         }
-        ck(cudaStreamSynchronize(s), "sync");  // host vector lifetime for the H2D copy
+        flush_uploads();
     } catch (...) {
         free_all(g->allocs, s);
+        for (auto& b : g->uploads) pinned_put(b, s);
         delete g;
         throw;
     }
@@ -716,8 +809,8 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         return;
     }
     // TOL: device-side per-channel stopping; the host polls the active count one chunk behind
-    int* pin = nullptr;
-    ck(cudaHostAlloc(&pin, 2 * sizeof(int), cudaHostAllocDefault), "cudaHostAlloc");
+    PinnedBlock pb = pinned_get(2 * sizeof(int));  // written by a copy kernel: no copy-engine queue
+    int* pin = static_cast<int*>(pb.p);
     cudaEvent_t ev[2];
     ck(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming), "event");
@@ -728,7 +821,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
             const int nit = std::min(chunk, S->o.max_iters - done);
             for (int i = 0; i < nit; ++i) pcg_iteration(S, a, S->hP, done + i, false, s);
             done += nit;
-            ck(cudaMemcpyAsync(&pin[slot], a.sc_.n_active, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+            copy_words(a.sc_.n_active, &pin[slot], sizeof(int), s);
             ck(cudaEventRecord(ev[slot], s), "event");
             if (pending >= 0) {
                 ck(cudaEventSynchronize(ev[pending]), "event sync");
@@ -741,30 +834,30 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     } catch (...) {
         cudaEventDestroy(ev[0]);
         cudaEventDestroy(ev[1]);
-        cudaFreeHost(pin);
+        pinned_put(pb, s);
         throw;
     }
     cudaEventDestroy(ev[0]);
     cudaEventDestroy(ev[1]);
-    cudaFreeHost(pin);
+    pinned_put(pb, s);
 }
 
 PcgScalars alloc_scalars(std::vector<void*>& A, int FK, cudaStream_t s) {
+    // one allocation, zeroed by one launch: 6 double and 3 int arrays of FK, + the active count
+    double* d = dalloc<double>(A, (size_t)6 * FK + ((size_t)3 * FK + 2) / 2 + 1, s);
     PcgScalars p;
-    p.rho = dalloc<double>(A, FK, s);
-    p.alpha = dalloc<double>(A, FK, s);
-    p.xalpha = dalloc<double>(A, FK, s);
-    p.beta = dalloc<double>(A, FK, s);
-    p.bb = dalloc<double>(A, FK, s);
-    p.rr = dalloc<double>(A, FK, s);
-    p.active = dalloc<int>(A, FK, s);
-    p.iters = dalloc<int>(A, FK, s);
-    p.status = dalloc<int>(A, FK, s);
-    p.n_active = dalloc<int>(A, 1, s);
-    ck(cudaMemsetAsync(p.iters, 0, FK * sizeof(int), s), "memset");
-    ck(cudaMemsetAsync(p.status, 0, FK * sizeof(int), s), "memset");
-    ck(cudaMemsetAsync(p.rr, 0, FK * sizeof(double), s), "memset");
-    ck(cudaMemsetAsync(p.bb, 0, FK * sizeof(double), s), "memset");
+    p.rho = d;
+    p.alpha = d + FK;
+    p.xalpha = d + 2 * (size_t)FK;
+    p.beta = d + 3 * (size_t)FK;
+    p.bb = d + 4 * (size_t)FK;
+    p.rr = d + 5 * (size_t)FK;
+    int* i = reinterpret_cast<int*>(d + 6 * (size_t)FK);
+    p.active = i;
+    p.iters = i + FK;
+    p.status = i + 2 * (size_t)FK;
+    p.n_active = i + 3 * (size_t)FK;
+    zero_words(d, ((size_t)6 * FK + ((size_t)3 * FK + 2) / 2 + 1) * sizeof(double), s);
     return p;
 }
 
@@ -819,8 +912,10 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             const char* e = std::getenv("FBS_PCG_GROUPS");  // A/B measurement: 1 disables the split
             S->nGroups = (e && e[0]) ? std::max(1, std::min(8, std::atoi(e))) : 2;
         }
-        S->sc = dalloc<float>(A, M + kVecPad, s);
-        float* bIn = dalloc<float>(A, (size_t)K * M, s);
+        // b and Sc in one allocation, [b_0 .. b_{K−1}, Sc] with channel stride M: the hierarchical
+        // init lifts exactly these K + 1 channels, so it reads them in place
+        float* bIn = dalloc<float>(A, (size_t)(K + 1) * M + kVecPad, s);
+        S->sc = bIn + (size_t)K * M;
         CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
         // a4: splat Sc, b = S(c∘t)
         LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t,
@@ -837,12 +932,14 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             double* T = dalloc<double>(A, (size_t)F * K * K, s);
             lrRt = dalloc<double>(A, (size_t)F * K * K, s);
             int* tF = dalloc<int>(A, F, s);
-            ck(cudaMemsetAsync(ctr, 0, F * sizeof(unsigned), s), "memset");
+            zero_words(ctr, F * sizeof(unsigned), s);
             LAUNCH(k_gram, F * bpfG, 256, 0, s, bIn, M, K, g->frameOff, bpfG, part, ctr, G);
             LAUNCH(k_pchol, F, 64, 0, s, G, K, o.lowrank_eps, tF, lrRt, T);
-            std::vector<int> tH(F);
-            ck(cudaMemcpyAsync(tH.data(), tF, F * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+            PinnedBlock rb = pinned_get(F * sizeof(int));
+            copy_words(tF, rb.p, F * sizeof(int), s);
             ck(cudaStreamSynchronize(s), "sync");
+            std::vector<int> tH(static_cast<int*>(rb.p), static_cast<int*>(rb.p) + F);
+            pinned_put(rb, s);
             Kc = 1;
             for (int f = 0; f < F; ++f) Kc = std::max(Kc, tH[f]);
             S->lr_rank.assign(tH.begin(), tH.end());
@@ -856,7 +953,6 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const size_t KM = (size_t)Kc * M;
         S->diagA = dalloc<float>(A, M, s);
         S->mu0 = dalloc<float>(A, M, s);
-        S->y0 = dalloc<float>(A, KM, s);
         S->xh = dalloc<float>(A, KM, s);
         S->rh = dalloc<float>(A, KM, s);
         S->dn = dalloc<float2>(A, (size_t)Kc * ((M + 3) & ~3ll) + kVecPad, s);
@@ -890,7 +986,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
         S->counters = dalloc<unsigned>(A, (size_t)F * Kc + F, s);
         S->counters2 = S->counters + (size_t)F * Kc;
-        ck(cudaMemsetAsync(S->counters, 0, ((size_t)F * Kc + F) * sizeof(unsigned), s), "memset");
+        zero_words(S->counters, ((size_t)F * Kc + F) * sizeof(unsigned), s);
         if (hierP || hierI) S->hP = make_hier(S, Kc, o.precond_alpha, o.precond_beta);
         S->fwd = alloc_scalars(A, F * Kc, s);
 
@@ -908,21 +1004,27 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         }
         if (hierI) {
             HierArgs h = make_hier(S, Kc + 1, o.init_alpha, o.init_beta);
-            LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, Kc, S->w0);
+            const float* w0i = bIn;  // [b, Sc] in place (above); the low-rank b is its own array
+            if (lowrank) {
+                LAUNCH(k_fill_init_w0, grid_for(M), kThreads, 0, s, S->b, S->sc, M, Kc, S->w0);
+                w0i = S->w0;
+            }
             if (g->L > 3) {
                 auto km = k_tree_anc_mult<HIER_INIT>;
                 LAUNCH_AS("k_tree_anc_mult<INIT>", km, F * S->bpf2, kThreads, 0, s, h, g->tree.ancId, S->ancMult);
             }
-            tree_lift<HIER_INIT>(S, h, S->w0, s);
+            tree_lift<HIER_INIT>(S, h, w0i, s);
             tree_coarse<HIER_INIT>(S, h, a, 0, s);
-            tree_level0<HIER_INIT>(S, h, a, S->w0, S->xh, 0, s);
+            tree_level0<HIER_INIT>(S, h, a, w0i, S->xh, 0, s);
         }
         if (hierP && g->L > 3) {
             auto km = k_tree_anc_mult<HIER_PCG>;
             LAUNCH_AS("k_tree_anc_mult<PCG>", km, F * S->bpf2, kThreads, 0, s, S->hP, g->tree.ancId, S->ancMult);
         }
-        ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
-        LAUNCH(k_init_dn, grid_for(KM), kThreads, 0, s, S->dn, g->n, M, (int64_t)((M + 3) & ~3ll), Kc);
+        if (sys_out) {  // the initial guess is kept for fbs_system_export only
+            S->y0 = dalloc<float>(A, KM, s);
+            ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
+        }
         // a8: PCG
         run_pcg(S, a, false, s);
         // low rank: Y = Ỹ R̃ (Supp. §4)
@@ -1131,7 +1233,7 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
             if (g->bistoch_residual < 0.f) {  // reporting only: max|n∘B̄n − m| / max m, on request
                 std::vector<void*> tmp;
                 unsigned* d = dalloc<unsigned>(tmp, 2, s);
-                ck(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned), s), "memset");
+                zero_words(d, 2 * sizeof(unsigned), s);
                 LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, d,
                        (float)(2 * g->dims));
                 unsigned h2[2];
@@ -1166,6 +1268,7 @@ int fbs_pyramid_export(fbs_grid g, int level, uint64_t* keys, int32_t* parent, i
 void fbs_grid_destroy(fbs_grid g) {
     if (!g) return;
     free_all(g->allocs, g->stream);
+    for (auto& b : g->uploads) pinned_put(b, g->stream);
     delete g;
 }
 

@@ -13,6 +13,13 @@
 
 namespace fbs {
 
+// a block of mapped pinned host memory from the staging pool (api.cu pinned_get / pinned_put)
+struct PinnedBlock {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t done = nullptr;
+};
+
 constexpr int kD = 5;                // XYLUV dims
 constexpr int kCellMaxPx = 64;       // level-0 cell = one warp, ≤ 2 px per lane
 constexpr int kCellsPerBlock = 8;    // 8 warps, one cell each
@@ -314,6 +321,7 @@ struct TreeOrder {
 
 struct fbs_grid_s {
     int F = 0, H = 0, W = 0;
+    std::vector<fbs::PinnedBlock> uploads;  // mapped pinned staging of the grid's small uploads
     double sxy = 0, sl = 0, suv = 0;
     int ncx = 0, ncy = 0;
     int64_t ncells = 0, N = 0, M = 0;

@@ -244,8 +244,9 @@ __device__ __forceinline__ void write_partials(const VecArgs& a, int f, int j, i
 
 // ---------------------------------------------------------------- assemble (Eq. quad_min)
 // diag(A) = λ n_v Σ_u n_u + Sc_v (PAPER.md:230 at Alg. 1's fixed point; isolated vertex: Sc_v,
-// reading #6), μ0 = 1/diag(A) on live vertices (Jacobi), ‖b‖² per (frame, k), and
-// flat init y_flat = b/Sc (reading #9) or zero init.  Per-frame blocks.
+// reading #6), μ0 = 1/diag(A) on live vertices (Jacobi), ‖b‖² per (frame, k),
+// flat init y_flat = b/Sc (reading #9) or zero init, and the interleaved (d, n)
+// vector with d = 0.  Per-frame blocks.
 __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__ diagA, float* __restrict__ mu0,
                                                   float* __restrict__ w0diag, int init_mode, PcgScalars scal) {
     pdl_entry();
@@ -267,6 +268,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
         for (int v = v0 + j * blockDim.x + threadIdx.x; v < v1; v += a.BPF * blockDim.x) {
             const float b = a.b[off + v];
             bb += (double)b * (double)b;
+            a.dn[(size_t)k * a.ldn + v] = make_float2(0.f, a.n[v]);  // (d, n) with d = 0
             if (init_mode == FBS_INIT_FLAT) {
                 const float S = a.sc[v];
                 a.x[off + v] = (S > 0.f) ? b / S : 0.f;
