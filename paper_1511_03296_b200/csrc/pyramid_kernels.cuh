@@ -158,6 +158,11 @@ __device__ __forceinline__ int pyr_sort_regs(const uint64_t* __restrict__ keysK,
     return __shfl_sync(0xffffffffu, incl, 31);
 }
 
+#ifndef FBS_PYR_REGS_MAX
+#define FBS_PYR_REGS_MAX 128
+#endif
+constexpr int kPyrRegsMax = FBS_PYR_REGS_MAX;  // largest cell sorted in registers (A/B: 128 or 256)
+
 // Pass 1: one warp per coarse cell sorts its (halved code, child id) pairs — in registers for
 // ≤ 256 children (every level-1 cell: 4 level-0 cells of ≤ 64 vertices), else in a global scratch
 // slice from a bump allocator — writes the children grouped by parent in canonical order to the
@@ -178,7 +183,7 @@ __global__ void __launch_bounds__(256) k_pyr_sort(const uint64_t* __restrict__ k
         if (nch <= 32) U = pyr_sort_regs<1>(keysK, cc, nch, childListN, rankS);
         else if (nch <= 64) U = pyr_sort_regs<2>(keysK, cc, nch, childListN, rankS);
         else if (nch <= 128) U = pyr_sort_regs<4>(keysK, cc, nch, childListN, rankS);
-        else if (nch <= 256) U = pyr_sort_regs<8>(keysK, cc, nch, childListN, rankS);
+        else if (kPyrRegsMax >= 256 && nch <= 256) U = pyr_sort_regs<8>(keysK, cc, nch, childListN, rankS);
         else {
             int P = 1;
             while (P < nch) P <<= 1;
