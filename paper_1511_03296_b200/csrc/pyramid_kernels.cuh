@@ -225,10 +225,12 @@ __global__ void __launch_bounds__(256) k_pyr_sort(const uint64_t* __restrict__ k
 }
 
 // Pass 3 (after the exclusive scan of the parent counts → cellOffN): parents get their canonical
-// ids vOff + rank: parent map, parent keys and child-list starts, and (summed by the run head over
-// its children in child order, integers) P(1) = level-0 descendants (countK = nullptr: level 0,
-// one each) and the level-1 descendant counts cnt1 (cnt1K = nullptr: the children are level-1
-// vertices, one each; cnt1N = nullptr: not needed at level 1).  One warp per coarse cell.
+// ids vOff + rank: parent map, parent keys and child-list starts, and (summed over each parent's
+// children in child order, integers) P(1) = level-0 descendants (countK = nullptr: level 0, one
+// each) and the level-1 descendant counts cnt1 (cnt1K = nullptr: the children are level-1
+// vertices, one each; cnt1N = nullptr: not needed at level 1).  One warp per coarse cell, 32
+// sorted children per round: the per-parent sums are warp segmented scans over the rank runs,
+// carried across rounds.
 __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ keysK, const int* __restrict__ cellOffK,
                                                    int ncxK, int ncyK, int ncxN, int ncyN, int64_t ncellsN,
                                                    const int* __restrict__ cellOffN, const int* __restrict__ childListN,
@@ -244,24 +246,52 @@ __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ 
         const int nch = cc.n0 + cc.n1;
         const int vOff = cellOffN[C];
         const uint64_t khi = ((uint64_t)cc.f << 56) | ((uint64_t)cc.CY << 40) | ((uint64_t)cc.CX << 24);
-        for (int i = lane; i < nch; i += 32) {
-            const int gch = childListN[cc.cOff + i];
-            const int r = rankS[cc.cOff + i];
-            parentK[gch] = vOff + r;
-            if (i == 0 || rankS[cc.cOff + i - 1] != r) {
+        int carryR = -1, carry0 = 0, carry1 = 0;  // the run still open at the end of the last round
+        for (int base = 0; base < nch; base += 32) {
+            const int i = base + lane;
+            const bool in = i < nch;
+            int gch = 0, r = -1 - lane, v0 = 0, v1 = 0;  // distinct dummy ranks past the end
+            if (in) {
+                gch = childListN[cc.cOff + i];
+                r = rankS[cc.cOff + i];
+                v0 = countK ? countK[gch] : 1;
+                if (cnt1N) v1 = cnt1K ? cnt1K[gch] : 1;
+                parentK[gch] = vOff + r;
+            }
+            const int rPrev = __shfl_up_sync(0xffffffffu, r, 1);
+            const bool runHead = (lane == 0) || (r != rPrev);  // first of its run in this round
+            if (in && (lane == 0 ? r != carryR : r != rPrev)) {  // first child of parent r
                 keysN[vOff + r] = khi | (uint64_t)halve_code((uint32_t)(keysK[gch] & 0xffffffu));
                 childStartN[vOff + r] = cc.cOff + i;
-                int e = i + 1;
-                while (e < nch && rankS[cc.cOff + e] == r) ++e;  // this parent's children: [i, e)
-                int c0 = 0, c1 = 0;
-                for (int q = i; q < e; ++q) {
-                    const int ch = childListN[cc.cOff + q];
-                    c0 += countK ? countK[ch] : 1;
-                    if (cnt1N) c1 += cnt1K ? cnt1K[ch] : 1;
-                }
-                countN[vOff + r] = c0;
-                if (cnt1N) cnt1N[vOff + r] = c1;
             }
+            if (lane == 0 && carryR >= 0 && r != carryR) {  // the open run ended at the round boundary
+                countN[vOff + carryR] = carry0;
+                if (cnt1N) cnt1N[vOff + carryR] = carry1;
+            }
+            const unsigned hm = __ballot_sync(0xffffffffu, runHead) & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
+            const int sst = 31 - __clz(hm);
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {  // segmented inclusive scans (integers: exact)
+                const int t0 = __shfl_up_sync(0xffffffffu, v0, d);
+                const int t1 = __shfl_up_sync(0xffffffffu, v1, d);
+                if (lane - d >= sst) {
+                    v0 += t0;
+                    v1 += t1;
+                }
+            }
+            if (sst == 0 && r == carryR) {
+                v0 += carry0;
+                v1 += carry1;
+            }
+            const int rNext = __shfl_down_sync(0xffffffffu, r, 1);
+            if (in && (i == nch - 1 || (lane < 31 && rNext != r))) {  // run ends inside this round
+                countN[vOff + r] = v0;
+                if (cnt1N) cnt1N[vOff + r] = v1;
+            }
+            carryR = __shfl_sync(0xffffffffu, r, 31);
+            carry0 = __shfl_sync(0xffffffffu, v0, 31);
+            carry1 = __shfl_sync(0xffffffffu, v1, 31);
+            if (base + 32 >= nch) carryR = -1;  // the last round closed every run
         }
         if (C == ncellsN - 1 && lane == 0) childStartN[cellOffN[ncellsN]] = cc.cOff + nch;
     }
