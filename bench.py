@@ -457,7 +457,40 @@ def main():
         lr_ms = dev_ms(lambda: fbs.solve(g4, t4, c4, w4.lam, precond="hier", init="hier", mode="tol", tol=1e-6,
                                          lowrank_eps=0.01))
         g4.close()
-        extras = {"dt_post_filter_ms": dt_ms,
+        # the other BASELINE.json configs as specified (grid build + solve [+ backward for configs[3]]),
+        # device time per call; TOL-mode solves include the host's active-count polls
+        cfg_rows = {}
+        for name in ("c1", "c2", "c3", "c4"):
+            wc = make(name)
+            rgbc, tc, cc = (torch.from_numpy(a_).to(dev) for a_ in (wc.rgb, wc.t, wc.c))
+            gc_ = torch.from_numpy(wc.g).to(dev) if wc.g is not None else None
+            opts = dict(precond=wc.precond, init=wc.init, mode=wc.mode, tol=wc.tol, max_iters=wc.max_iters)
+            if wc.mode == "fixed":
+                opts["iters"] = wc.iters
+
+            def run_cfg():
+                gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch)
+                if gc_ is not None:
+                    _, S_ = fbs.solve(gg, tc, cc, wc.lam, keep_system=True, **opts)
+                    S_.backward(gc_, tc, cc)
+                    S_.close()
+                else:
+                    fbs.solve(gg, tc, cc, wc.lam, **opts)
+                gg.close()
+
+            ms_c = dev_ms(run_cfg)
+            gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch)
+            _, S_ = fbs.solve(gg, tc, cc, wc.lam, keep_system=True, **opts)
+            pcg_its = int(S_.stats()["iterations"].max())
+            S_.close()
+            gg.close()
+            cfg_rows[name] = {"ms": ms_c, "MP_per_s": wc.pixels / 1e6 / (ms_c / 1e3), "pcg_iterations": pcg_its,
+                              "shape": f"{wc.frames}x{wc.H}x{wc.W}, K={wc.K}",
+                              "solver": f"{wc.precond}+{wc.init}, " +
+                                        (f"fixed {wc.iters} it" if wc.mode == "fixed" else f"tol {wc.tol:g}") +
+                                        (", + backward" if gc_ is not None else "")}
+        extras = {"configs": cfg_rows,
+                  "dt_post_filter_ms": dt_ms,
                   "dt_post_filter": f"{F} frames x1, sigma'_xy = sigma'_rgb = 16, 3 iterations (PAPER.md:329)",
                   "robust_ms_per_irls_round": rb_ms,
                   "robust": f"{F} frames, sigma_gm = 10, hier+hier, {ITERS} PCG iters per round (Supp. Alg. 3)",
