@@ -144,6 +144,20 @@ void free_all(std::vector<void*>& list, cudaStream_t s) {
     list.clear();
 }
 
+// Side streams of the frame-group splits (Alg. 1 and the FIXED-mode PCG), created once per device.
+cudaStream_t group_stream(int dev, int i) {
+    static std::mutex mu;
+    static std::map<int, std::vector<cudaStream_t>> streams;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& v = streams[dev];
+    while ((int)v.size() <= i) {
+        cudaStream_t st;
+        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+        v.push_back(st);
+    }
+    return v[i];
+}
+
 // ---- small host <-> device transfers through mapped pinned memory and a copy kernel.
 // cudaMemcpyAsync queues on the copy engines behind whatever bulk copies other streams have in
 // flight (a caller's 66 MB result read-back or 182 MB input upload), which stalled the grid
@@ -331,11 +345,45 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         if (g->n_bistoch % 2 == 0) std::swap(cur, nxt);  // make the last write land in g->n
         int bsPerSM = 4;  // 4 × (512 threads, 2 × 25 KB stages) per SM: 5.57 → 5.43 ms per bench step against 3
         if (const char* e = std::getenv("FBS_BS_BLOCKS")) bsPerSM = std::max(1, std::min(4, std::atoi(e)));  // A/B
-        for (int it = 0; it < g->n_bistoch; ++it) {
-            const int nch = (int)((M + kBsChunk - 1) / kBsChunk);
-            LAUNCH(k_bistoch, std::max(1, std::min(nch, bsPerSM * (g_num_sms > 0 ? g_num_sms : 148))), kBsThreads, kBsSmem, s,
-                   g->nbr, g->m, cur, nxt, (int)M, it == 0, (float)(2 * g->dims));
-            std::swap(cur, nxt);
+        // frames in Gb groups on Gb streams (frames are independent: no neighbour crosses a frame), so
+        // one group's kernel boundaries overlap the other's work; each group's launches take 1/Gb of
+        // the resident blocks
+        int Gb = std::min(F, 4);  // 1: 5.46, 2: 5.38, 4: 5.34, 8: 5.41 ms per bench step
+        if (const char* e = std::getenv("FBS_BS_GROUPS")) Gb = std::max(1, std::min(F, std::atoi(e)));  // A/B
+        cudaEvent_t bsFork = nullptr;
+        std::vector<cudaEvent_t> bsJoin(Gb, nullptr);
+        if (Gb > 1) {
+            ck(cudaEventCreateWithFlags(&bsFork, cudaEventDisableTiming), "event");
+            ck(cudaEventRecord(bsFork, s), "event");
+        }
+        const int sms = g_num_sms > 0 ? g_num_sms : 148;
+        for (int gi = 0; gi < Gb; ++gi) {
+            const int f0 = (int)((int64_t)F * gi / Gb), f1 = (int)((int64_t)F * (gi + 1) / Gb);
+            const int vlo = fo[f0], vhi = fo[f1];
+            cudaStream_t sg = s;
+            if (Gb > 1) {
+                sg = group_stream(dev, gi);
+                ck(cudaStreamWaitEvent(sg, bsFork, 0), "wait");
+            }
+            float* c2 = cur;
+            float* n2 = nxt;
+            for (int it = 0; it < g->n_bistoch && vhi > vlo; ++it) {
+                const int nch = (vhi + kBsChunk - 1) / kBsChunk - vlo / kBsChunk;
+                LAUNCH(k_bistoch, std::max(1, std::min(nch, std::max(1, bsPerSM * sms / Gb))), kBsThreads, kBsSmem, sg,
+                       g->nbr, g->m, c2, n2, (int)M, vlo, vhi, it == 0, (float)(2 * g->dims));
+                std::swap(c2, n2);
+            }
+            if (Gb > 1) {
+                ck(cudaEventCreateWithFlags(&bsJoin[gi], cudaEventDisableTiming), "event");
+                ck(cudaEventRecord(bsJoin[gi], sg), "event");
+            }
+        }
+        if (Gb > 1) {
+            for (int gi = 0; gi < Gb; ++gi) {
+                ck(cudaStreamWaitEvent(s, bsJoin[gi], 0), "wait");
+                cudaEventDestroy(bsJoin[gi]);
+            }
+            cudaEventDestroy(bsFork);
         }
         if (g->n_bistoch == 0) {
             std::vector<float> ones(M, 1.f);
@@ -756,20 +804,6 @@ void pcg_start(fbs_system S, const VecArgs& a, const HierArgs& h, bool x_zero, c
         else LAUNCH(k2, nb, kThreads, 0, s, as);
         // d = s (Alg. 2 line 3) is the first iteration's k_direction2
     }
-}
-
-// Side streams of the frame-group split (one pair per device, created once).
-cudaStream_t group_stream(int dev, int i) {
-    static std::mutex mu;
-    static std::map<int, std::vector<cudaStream_t>> streams;
-    std::lock_guard<std::mutex> lk(mu);
-    auto& v = streams[dev];
-    while ((int)v.size() <= i) {
-        cudaStream_t st;
-        ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
-        v.push_back(st);
-    }
-    return v[i];
 }
 
 // Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.

@@ -352,12 +352,15 @@ constexpr size_t kBsSmem = 2 * sizeof(BsStage) + 64;
 __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
-                                                 float* __restrict__ nout, int M, int first, float bdiag) {
+                                                 float* __restrict__ nout, int M, int vlo, int vhi, int first,
+                                                 float bdiag) {
     pdl_entry();
     extern __shared__ __align__(128) unsigned char bs_smem[];
     BsStage* st = reinterpret_cast<BsStage*>(bs_smem);
     uint64_t* bar = reinterpret_cast<uint64_t*>(bs_smem + 2 * sizeof(BsStage));
-    const int nChunks = (M + kBsChunk - 1) / kBsChunk;
+    // vertices [vlo, vhi) (whole frames): the chunks covering them; a chunk shared with a
+    // neighbouring range only writes its own vertices (no neighbour crosses a frame)
+    const int cBeg = vlo / kBsChunk, nChunks = (vhi + kBsChunk - 1) / kBsChunk;
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
         bulk_g2s(st[slot].m, m + c0, n4 * 4, &bar[slot]);
         if (!first) bulk_g2s(st[slot].n + (w0 - (c0 - 128)), nin + w0, (w1 - w0) * 4, &bar[slot]);
     };
-    int ci = blockIdx.x;
+    int ci = cBeg + blockIdx.x;
     if (threadIdx.x == 0) {
         if (ci < nChunks) issue(0, ci);
         if (ci + (int)gridDim.x < nChunks) issue(1, ci + gridDim.x);
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
 #pragma unroll
         for (int u = 0; u < kBsChunk / kBsThreads; ++u) {
             const int l = threadIdx.x + kBsThreads * u, v = c0 + l;
-            if (v >= M) continue;
+            if (v < vlo || v >= vhi) continue;
             const int4 nb = S.nb[l];
             float nv, bn;
             if (first) {
