@@ -23,6 +23,15 @@
 
 namespace fbs {
 
+#ifndef FBS_L0B
+#define FBS_L0B 4
+#endif
+#ifndef FBS_UPB
+#define FBS_UPB 4
+#endif
+constexpr int kL0B = FBS_L0B;  // vertices per round of k_tree_level0 (loads in flight per thread)
+constexpr int kUpB = FBS_UPB;  // vertices per round of k_hier_level0
+
 enum { HIER_PCG = 0, HIER_PDA = 1, HIER_INIT = 2, HIER_PLAIN = 3 };
 enum { HSRC_UPDATE = 0, HSRC_RESID = 1, HSRC_RESID0 = 2 };
 
@@ -152,12 +161,12 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
         if (SRC != HSRC_UPDATE || a.sc_.active[fk]) {
             const size_t off = (size_t)k * a.M;
             const float al = (SRC == HSRC_UPDATE) ? (float)a.sc_.alpha[fk] : 0.f;
-            for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += 4 * stride) {
-                float rv[4], mv[4];
+            for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += kUpB * stride) {
+                float rv[kUpB], mv[kUpB];
                 if (SRC == HSRC_UPDATE) {
-                    float xv[4], dv[4], qv[4];
+                    float xv[kUpB], dv[kUpB], qv[kUpB];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kUpB; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
                             if (FINISH_LAST) {
@@ -170,7 +179,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kUpB; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
                             if (FINISH_LAST) a.x[off + v] = xv[u] + al * dv[u];
@@ -179,7 +188,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     }
                 } else {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kUpB; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
                             rv[u] = a.b[off + v];
@@ -189,7 +198,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kUpB; ++u) {
                     const int v = vb + u * stride;
                     if (v >= v1) continue;
                     a.r[off + v] = rv[u];
@@ -477,11 +486,11 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
         if (!dir && xa == 0.f) continue;
         const float be = (MODE == HIER_PCG && !first) ? (float)a.sc_.beta[fk] : 0.f;
         const size_t off = (size_t)k * a.M;
-        for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += 4 * stride) {
-            float sv[4], mv[4], up[4], xv[4];
-            float2 dv[4];
+        for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += kL0B * stride) {
+            float sv[kL0B], mv[kL0B], up[kL0B], xv[kL0B];
+            float2 dv[kL0B];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kL0B; ++u) {
                 const int v = vb + u * stride;
                 if (v < v1) {
                     const int pT = __ldcs(h.parent0T + v);
@@ -500,7 +509,7 @@ __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, cons
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < kL0B; ++u) {
                 const int v = vb + u * stride;
                 if (v >= v1) continue;
                 if (MODE == HIER_INIT) {
