@@ -272,24 +272,30 @@ def main():
                for k, (n, tot) in sorted(prof.items(), key=lambda kv: -kv[1][1])}
     roof = None
     lv = [int(x) for x in info["level_vertices"]]
-    # The FIXED-mode PCG runs its frames as G groups on G streams (api.cu run_pcg): each PCG launch
-    # covers 1/G of the vertices (on average over the groups) and shares the SMs with the other
-    # groups' launches, so its per-launch rate is a lower bound on the kernel's own.
+    # Frame groups run concurrently on their own streams: the FIXED-mode PCG in G groups (api.cu
+    # run_pcg) and Alg. 1 in Gb groups (fbs_grid_build).  A grouped launch covers 1/G of the
+    # vertices (on average over the groups) and shares the SMs with the other groups' launches, so
+    # its per-launch rate is a lower bound on the kernel's own, and the summed event times of a
+    # grouped kernel overstate its share of the step G-fold (wall share ≈ sum / G).
     G = max(1, min(int(os.environ.get("FBS_PCG_GROUPS", "2") or 2), w.frames))
+    Gb = max(1, min(int(os.environ.get("FBS_BS_GROUPS", "4") or 4), w.frames))
     PCG_GROUPED = ("k_spmv2", "k_hier_level0<UPDATE>", "k_tree_lift<PCG>", "k_tree_coarse<PCG>", "k_tree_level0<PCG>",
                    "k_hier_level0<UPDATE,LAST>", "k_hier_level0<RESID>", "k_init_scalars")
 
-    def launch_bytes(k):
-        if k in PCG_GROUPED:
-            b = kernel_bytes(k, M / G, [x / G for x in lv], w.pixels)
-        else:
-            b = kernel_bytes(k, M, lv, w.pixels)
-        return b
+    def groups_of(k):
+        return G if k in PCG_GROUPED else (Gb if k == "k_bistoch" else 1)
 
+    def launch_bytes(k):
+        gk = groups_of(k)
+        return kernel_bytes(k, M / gk, [x / gk for x in lv], w.pixels)
+
+    for k, v in kernels.items():
+        v["frame_groups"] = groups_of(k)
+        v["wall_share_ms_per_step"] = v["ms_per_step"] / groups_of(k)
     cand = [(k, v) for k, v in kernels.items() if launch_bytes(k) is not None]
     if cand:
-        # the dominant kernel = the largest share of the step among kernels with a byte model
-        kname, kv = max(cand, key=lambda kv_: kv_[1]["ms_per_step"])
+        # the dominant kernel = the largest (wall) share of the step among kernels with a byte model
+        kname, kv = max(cand, key=lambda kv_: kv_[1]["wall_share_ms_per_step"])
         bytes_launch = launch_bytes(kname)
         achieved = bytes_launch / (kv["avg_us"] * 1e-6) / 1e9
         peak, peak_src = 6545.6, "MEASURED_PEAKS.json hbm_gbs (measured copy)"
@@ -304,17 +310,17 @@ def main():
                 traffic = json.load(fh).get(kname)
         except Exception:
             pass
-        grouped = kname in PCG_GROUPED
+        gk = groups_of(kname)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": kname, "bytes_per_launch": bytes_launch,
-                "vertices_per_launch": M / G if grouped else M, "frame_groups": G if grouped else 1,
-                "avg_launch_us": kv["avg_us"], "share_of_step": kv["ms_per_step"] / (prof_ms / args.steps),
+                "vertices_per_launch": M / gk, "frame_groups": gk,
+                "avg_launch_us": kv["avg_us"],
+                "share_of_step": kv["wall_share_ms_per_step"] / (prof_ms / args.steps),
                 "peak_source": peak_src}
-        if grouped:
-            roof["note"] = (f"{G} frame groups run their PCG launches concurrently on {G} streams; the average "
-                            "launch duration includes sharing the SMs with the other groups' launches")
-            if traffic is not None:
-                roof["traffic"] = traffic  # profiles/traffic.json: one launch of the prof_pcg.py capture (4 frames)
+        if gk > 1:
+            roof["note"] = (f"{gk} frame groups run their launches concurrently on {gk} streams; the average "
+                            "launch duration includes sharing the SMs with the other groups' launches "
+                            "(traffic: one launch of the 4-frame ncu capture, profiles/traffic.json)")
     for k, v in kernels.items():
         b = launch_bytes(k)
         if b is not None:
@@ -344,18 +350,50 @@ def main():
         stages_ms[st] = stages_ms.get(st, 0.0) + v["ms_per_step"]
     for st in ("grid_build", "bistochastize", "pyramid", "splat_assemble_init", "pcg", "slice"):
         stages_ms.setdefault(st, 0.0)
-    # the PCG kernels of the G frame groups overlap, so their summed launch times exceed the PCG's
-    # share of the step; the rest of the step runs on one stream, so the PCG wall time is estimated
-    # as the timed step minus the other stages' (profiled, hence slightly long) kernel times
+    # Grouped stages (Alg. 1, PCG) overlap their groups, so their summed launch times exceed their
+    # share of the step: their wall times are measured directly, as differences of device-timed
+    # calls — grid build with 20 vs 0 Alg. 1 iterations, solve with 25 vs 1 PCG iterations.
     stages_ms["pcg_kernel_time_sum"] = stages_ms.pop("pcg")
-    pcg_wall = ms / args.steps - sum(v for k, v in stages_ms.items() if k != "pcg_kernel_time_sum")
-    stages_ms["pcg_wall_estimate"] = pcg_wall
-    stages_ms["pcg_wall_estimate_per_iteration"] = pcg_wall / ITERS
+    stages_ms["bistochastize_kernel_time_sum"] = stages_ms.pop("bistochastize")
+
+    def dev_time(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        a_, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a_.record(stream)
+        for _ in range(reps):
+            fn()
+        b_.record(stream)
+        torch.cuda.synchronize()
+        return a_.elapsed_time(b_) / reps
+
+    def gb(nb):
+        def f():
+            gx = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=nb)
+            gx.close()
+        return f
+
+    bs_wall = max(0.0, dev_time(gb(20)) - dev_time(gb(0)))
+    g_w = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=20)
+
+    def sv(iters):
+        return lambda: fbs.solve(g_w, t_d, c_d, LAM, precond="hier", init="hier", mode="fixed", iters=iters, out=x_d)
+
+    pcg24 = max(0.0, dev_time(sv(ITERS)) - dev_time(sv(1)))
+    g_w.close()
+    stages_ms["bistochastize_wall"] = bs_wall
+    stages_ms["pcg_wall_per_iteration"] = pcg24 / (ITERS - 1)
     it_bytes = sum(kernel_bytes(k, M, lv, w.pixels) for k in
                    ("k_spmv2", "k_hier_level0<UPDATE>", "k_tree_lift<PCG>", "k_tree_level0<PCG>"))
-    pcg_iteration_rate = {"algorithmic_bytes": it_bytes, "GBps": it_bytes / (pcg_wall / ITERS * 1e-3) / 1e9,
-                          "note": "all frames, spmv + update + lift + level0 byte models (coarse levels unmodelled) "
-                                  "over the estimated PCG wall time per iteration"}
+    pcg_iteration_rate = {"algorithmic_bytes": it_bytes, "GBps": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9,
+                          "frac": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9 / 6550.7,
+                          "note": "one PCG iteration over all frames (both groups): spmv + update + lift + level0 "
+                                  "byte models (coarse levels unmodelled) over its wall time, measured as "
+                                  "(solve with 25 iterations - solve with 1) / 24"}
+    bistoch_rate = {"algorithmic_bytes": kernel_bytes("k_bistoch", M, lv, w.pixels),
+                    "GBps": 20 * kernel_bytes("k_bistoch", M, lv, w.pixels) / (bs_wall * 1e-3) / 1e9 if bs_wall else None,
+                    "note": "one Alg. 1 iteration over all frames (all groups) over its wall time, measured as "
+                            "(grid build with 20 iterations - grid build with 0) / 20"}
 
     # ---- end to end through the public API with host buffers: every step copies its inputs H2D from
     # pinned memory and its result D2H inside the timed region.  Double-buffered: the H2D of step
@@ -517,7 +555,8 @@ def main():
                 "config": workload_config(args) | {"vertices_per_gpu": M,
                                                    "levels": int(info["levels"])},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "extras": extras,
-                "clocks": clk, "stages_ms_per_step": stages_ms, "pcg_iteration_rate": pcg_iteration_rate, "kernels": kernels,
+                "clocks": clk, "stages_ms_per_step": stages_ms, "pcg_iteration_rate": pcg_iteration_rate,
+                "bistoch_iteration_rate": bistoch_rate, "kernels": kernels,
                 "profiled_ms_per_step": prof_ms / args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -199,6 +199,12 @@ __global__ void k_copy_words(const int* __restrict__ src, int* __restrict__ dst,
         dst[i] = src[i];
 }
 
+__global__ void k_fill_words(int* __restrict__ dst, int64_t n, int value) {
+    pdl_entry();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = value;
+}
+
 __global__ void k_zero_words(int* __restrict__ dst, int64_t n) {
     pdl_entry();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -385,10 +391,11 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             }
             cudaEventDestroy(bsFork);
         }
-        if (g->n_bistoch == 0) {
-            std::vector<float> ones(M, 1.f);
-            ck(cudaMemcpyAsync(g->n, ones.data(), M * sizeof(float), cudaMemcpyHostToDevice, s), "h2d");
-            ck(cudaStreamSynchronize(s), "sync");
+        if (g->n_bistoch == 0) {  // n = 1 (Alg. 1 with no iterations)
+            const float one = 1.f;
+            int bits;
+            std::memcpy(&bits, &one, 4);
+            LAUNCH(k_fill_words, grid_for(M), kThreads, 0, s, reinterpret_cast<int*>(g->n), (int64_t)M, bits);
         }
 
         // ---- pyramid (Supp. Sec. 2), levels 1 .. Lmax-1
