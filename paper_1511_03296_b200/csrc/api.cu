@@ -295,15 +295,16 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // scratch: scan tile counter + look-back state (+ error flag, + residual words)
         const int64_t scanTiles = (g->ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems);
         const int64_t nState = std::max<int64_t>(scanTiles, 1);
-        unsigned long long* state = dalloc<unsigned long long>(A, nState + 3, s);  // + counter, err[4]
+        // + counter, err[4], frameOff[F + 1]: err and the frame offsets are read back together
+        unsigned long long* state = dalloc<unsigned long long>(A, nState + 3 + (F + 2) / 2, s);
         unsigned* counter = reinterpret_cast<unsigned*>(state + nState);
         int* err = reinterpret_cast<int*>(state + nState + 1);
+        g->frameOff = reinterpret_cast<int*>(state + nState + 3);
         zero_words(state, (nState + 3) * sizeof(unsigned long long), s);
         g->vid = dalloc<int>(A, N, s);
         uint64_t* keysCap = dalloc<uint64_t>(A, N, s);
         int* mCap = dalloc<int>(A, N + kVecPad, s);
         g->cellOff = dalloc<int>(A, g->ncells + 1, s);
-        g->frameOff = dalloc<int>(A, F + 1, s);
         CellGeom geo{F, H, W, ncx, ncy, g->colStart, g->rowStart};
         uint8_t* lutL = dalloc<uint8_t>(A, 65536, s);
         uint8_t* lutUV = dalloc<uint8_t>(A, 65536, s);
@@ -325,11 +326,10 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         int errh[4];
         PinnedBlock rb = pinned_get(((size_t)(F + 1) * (kMaxLevels + 1) + 4) * sizeof(int));  // read-backs
         int* rbi = static_cast<int*>(rb.p);
-        copy_words(g->frameOff, rbi, (F + 1) * sizeof(int), s);
-        copy_words(err, rbi + F + 1, 4 * sizeof(int), s);
+        copy_words(err, rbi, (4 + F + 1) * sizeof(int), s);  // err[4] then frameOff (contiguous)
         ck(cudaStreamSynchronize(s), "sync");
-        std::copy(rbi, rbi + F + 1, fo.begin());
-        std::copy(rbi + F + 1, rbi + F + 5, errh);
+        std::copy(rbi, rbi + 4, errh);
+        std::copy(rbi + 4, rbi + 4 + F + 1, fo.begin());
         if (errh[0]) throw Err(FBS_ELIMIT, "a sigma_xy cell holds more than 64 pixels");
         g->M = fo[F];
         g->frameOffH.assign(fo.begin(), fo.end());
@@ -409,6 +409,10 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const uint64_t* keysK = g->keys;
         const int* cellOffK = g->cellOff;
         int ncxK = ncx, ncyK = ncy;
+        // frame offsets of every level in one [Lmax][F + 1] array (row 0: level 0), read back at once
+        // and used by the hierarchy kernels as is
+        int* lvAll = dalloc<int>(A, (size_t)Lmax * (F + 1), s);
+        copy_words(g->frameOff, lvAll, (F + 1) * sizeof(int), s);
         std::vector<int*> lvFrameOffDev(Lmax, nullptr);
         unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
         int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, s) : nullptr;  // parent rank of each sorted child
@@ -441,7 +445,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             unsigned* ctr2 = reinterpret_cast<unsigned*>(st2 + st2n);  // scan tile counter, scratch bump
             LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
-            lvFrameOffDev[k] = dalloc<int>(A, F + 1, s);
+            lvFrameOffDev[k] = lvAll + (size_t)k * (F + 1);
             LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2,
                    (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
             LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
@@ -455,7 +459,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         }
         // ---- sync 2: level sizes
         std::vector<std::vector<int>> lfo(Lmax);
-        for (int k = 1; k < Lmax; ++k) copy_words(lvFrameOffDev[k], rbi + (size_t)k * (F + 1), (F + 1) * sizeof(int), s);
+        if (Lmax > 1) copy_words(lvAll + (F + 1), rbi + (F + 1), (size_t)(Lmax - 1) * (F + 1) * sizeof(int), s);
         copy_words(err, rbi + (size_t)Lmax * (F + 1), 4 * sizeof(int), s);
         ck(cudaStreamSynchronize(s), "sync");
         for (int k = 1; k < Lmax; ++k) lfo[k].assign(rbi + (size_t)k * (F + 1), rbi + (size_t)(k + 1) * (F + 1));
@@ -483,34 +487,32 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             g->lv[k].frameOff.assign(lfo[k].begin(), lfo[k].end());
         }
 
-        // uploads (frame levels, level frame offsets, scan tiles) staged in one mapped pinned block
-        // that lives as long as the grid (no synchronisation for its lifetime)
-        std::vector<int> up;
-        auto stage = [&up](const void* p, size_t bytes) {
-            const size_t at = up.size();
-            up.resize(at + bytes / 4);
-            std::memcpy(up.data() + at, p, bytes);
-            return at;
+        g->lvFrameOffDev = lvAll;  // rows 0 .. L − 1 (row 0 = level 0)
+        // uploads (frame levels, scan tiles): one device block filled from one mapped pinned block
+        // (kept with the grid, so no synchronisation for its lifetime) by one copy kernel
+        struct Upload {
+            const void* src;
+            size_t bytes;
+            void** dst;
         };
-        std::vector<std::pair<size_t, std::pair<void*, size_t>>> upl;  // (offset, (device dst, bytes))
-        g->frameLevels = dalloc<int>(A, F, s);
-        upl.push_back({stage(g->frameLevelsH.data(), F * sizeof(int)), {g->frameLevels, F * sizeof(int)}});
-        std::vector<int> lfoAll((size_t)L * (F + 1));
-        for (int f = 0; f <= F; ++f) lfoAll[f] = fo[f];
-        for (int k = 1; k < L; ++k)
-            for (int f = 0; f <= F; ++f) lfoAll[(size_t)k * (F + 1) + f] = lfo[k][f];
-        g->lvFrameOffDev = dalloc<int>(A, lfoAll.size(), s);
-        upl.push_back({stage(lfoAll.data(), lfoAll.size() * sizeof(int)), {g->lvFrameOffDev, lfoAll.size() * sizeof(int)}});
+        std::vector<Upload> upl;
         auto flush_uploads = [&]() {
-            if (up.empty()) return;
-            PinnedBlock b = pinned_get(up.size() * sizeof(int));
+            size_t total = 0;
+            for (auto& e : upl) total += (e.bytes + 7) & ~size_t(7);
+            if (total == 0) return;
+            char* dev = reinterpret_cast<char*>(dalloc<unsigned long long>(A, total / 8, s));
+            PinnedBlock b = pinned_get(total);
             g->uploads.push_back(b);
-            std::memcpy(b.p, up.data(), up.size() * sizeof(int));
-            for (auto& e : upl) copy_words(static_cast<int*>(b.p) + e.first, e.second.first, e.second.second, s);
-            up.clear();
+            size_t at = 0;
+            for (auto& e : upl) {
+                std::memcpy(static_cast<char*>(b.p) + at, e.src, e.bytes);
+                *e.dst = dev + at;
+                at += (e.bytes + 7) & ~size_t(7);
+            }
+            copy_words(b.p, dev, total, s);
             upl.clear();
         };
-        flush_uploads();  // the tree kernels below read the level frame offsets
+        upl.push_back({g->frameLevelsH.data(), F * sizeof(int), reinterpret_cast<void**>(&g->frameLevels)});
         // ---- tree order of the pyramid (tree_kernels.cuh): depth-first positions of the level-0 and
         // level-1 vertices, so every coarse subtree is one contiguous level-1 range
         std::vector<int> tfo, tframe;
@@ -571,14 +573,11 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
                 throw Err(FBS_ELIMIT, "frame too large for the shared-memory tile scan of the hierarchy");
             T.nTiles1 = tfo[F];
             T.tileFrameOffH = tfo;
-            T.tileFrameOff = dalloc<int>(A, F + 1, s);
-            T.tileFrame = dalloc<int>(A, std::max<size_t>(tframe.size(), 1), s);
-            T.tileRange = dalloc<int2>(A, std::max<size_t>(trange.size(), 1), s);
-            if (!trange.empty())
-                upl.push_back({stage(trange.data(), trange.size() * sizeof(int2)), {T.tileRange, trange.size() * sizeof(int2)}});
-            upl.push_back({stage(tfo.data(), (F + 1) * sizeof(int)), {T.tileFrameOff, (F + 1) * sizeof(int)}});
-            if (!tframe.empty())
-                upl.push_back({stage(tframe.data(), tframe.size() * sizeof(int)), {T.tileFrame, tframe.size() * sizeof(int)}});
+            upl.push_back({tfo.data(), (F + 1) * sizeof(int), reinterpret_cast<void**>(&T.tileFrameOff)});
+            if (trange.empty()) trange.push_back(make_int2(0, 0));
+            if (tframe.empty()) tframe.push_back(0);
+            upl.push_back({trange.data(), trange.size() * sizeof(int2), reinterpret_cast<void**>(&T.tileRange)});
+            upl.push_back({tframe.data(), tframe.size() * sizeof(int), reinterpret_cast<void**>(&T.tileFrame)});
         }
         flush_uploads();
     } catch (...) {
