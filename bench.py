@@ -60,7 +60,7 @@ def kernel_bytes(name, M, lv, N):
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["fbs", "reference"], default="fbs")
     ap.add_argument("--frames-per-gpu", type=int, default=8)
