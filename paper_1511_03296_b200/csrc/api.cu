@@ -144,12 +144,15 @@ void free_all(std::vector<void*>& list, cudaStream_t s) {
     list.clear();
 }
 
-// Side streams of the frame-group splits (Alg. 1 and the FIXED-mode PCG), created once per device.
-cudaStream_t group_stream(int dev, int i) {
+// Side streams of the frame-group splits (Alg. 1 and the FIXED-mode PCG), created once per (device,
+// caller stream).
+cudaStream_t group_stream(int dev, cudaStream_t caller, int i) {
+    // one set per (device, caller stream): solves issued on different caller streams stay
+    // independent instead of serialising on shared side streams
     static std::mutex mu;
-    static std::map<int, std::vector<cudaStream_t>> streams;
+    static std::map<std::pair<int, cudaStream_t>, std::vector<cudaStream_t>> streams;
     std::lock_guard<std::mutex> lk(mu);
-    auto& v = streams[dev];
+    auto& v = streams[{dev, caller}];
     while ((int)v.size() <= i) {
         cudaStream_t st;
         ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -368,7 +371,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             const int vlo = fo[f0], vhi = fo[f1];
             cudaStream_t sg = s;
             if (Gb > 1) {
-                sg = group_stream(dev, gi);
+                sg = group_stream(dev, s, gi);
                 ck(cudaStreamWaitEvent(sg, bsFork, 0), "wait");
             }
             float* c2 = cur;
@@ -828,7 +831,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         ck(cudaEventRecord(fork, s), "event");
         for (int gi = 0; gi < G; ++gi) {
             const int f0 = (int)((int64_t)g->F * gi / G), f1 = (int)((int64_t)g->F * (gi + 1) / G);
-            cudaStream_t sg = group_stream(dev, gi);
+            cudaStream_t sg = group_stream(dev, s, gi);
             ck(cudaStreamWaitEvent(sg, fork, 0), "wait");
             VecArgs ag = a;
             HierArgs hg = S->hP;
