@@ -52,3 +52,39 @@ def zero_conf_pixels(sol):
     """Pixels whose vertex lies in a zero-confidence component (reading #7) — parity unpinned there."""
     zc = O.zero_confidence_components(sol.nbr, sol.sys.Sc)
     return zc[sol.vid]
+
+
+def pcg_fp32_storage(sol, iters, k=0):
+    """Alg. 2 with the oracle's own operators (sol.sys.A, sol.Minv, sol.y0) and
+    every PCG vector rounded to fp32 after it is formed (dots in fp64) — the arithmetic the CUDA
+    path performs, used as the reference where the fixed-count iterate is unstable (reading #29).
+    Returns the sliced per-pixel result of channel k."""
+    f32 = lambda v: v.astype(np.float32).astype(np.float64)  # noqa: E731
+    A, Minv = sol.sys.A, sol.Minv
+    b = sol.sys.b[:, k]
+    x = f32(sol.y0[:, k].astype(np.float64))
+    r = f32(b - A @ x)
+    d = f32(Minv(r))
+    rho = float(r @ d)
+    for _ in range(iters):
+        if rho == 0.0:
+            break
+        q = f32(A @ d)
+        dq = float(d @ q)
+        if dq <= 0.0:
+            break
+        alpha = rho / dq
+        x = f32(x + alpha * d)
+        r = f32(r - alpha * q)
+        s = f32(Minv(r))
+        rho_old, rho = rho, float(r @ s)
+        d = f32(s + (rho / rho_old) * d)
+    return x[sol.vid]
+
+
+def fixed_count_unstable(sol, iters, t, c, k=0):
+    """Pixels where storing the PCG vectors in fp32 alone moves the fixed-count iterate of channel
+    k by more than half the north_star bound (reading #29), and that fp32-storage reference."""
+    x32 = pcg_fp32_storage(sol, iters, k)
+    rng = target_range(t, c)[k]
+    return np.abs(x32 - sol.x[k]) > 0.5 * MAX_TOL * rng, x32
