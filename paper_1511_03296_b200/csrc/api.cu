@@ -815,6 +815,54 @@ void pcg_start(fbs_system S, const VecArgs& a, const HierArgs& h, bool x_zero, c
     }
 }
 
+// TOL iterations 1 … as a device-side loop: a graph whose conditional while node runs one PCG
+// iteration plus k_tol_cond per trip, launched once on s (no host polls, no overshoot, no host
+// synchronisation).  Returns false (nothing launched) if the graph cannot be built.
+bool tol_graph(fbs_system S, const VecArgs& a, cudaStream_t s) {
+    // off by default: measured on configs[0,1,3] it is no faster than the host-polled loop (graph
+    // instantiation per solve costs what the polls cost; the device-side loop adds ~2 µs per trip)
+    const char* e = std::getenv("FBS_TOL_GRAPH");
+    if (!e || e[0] != '1') return false;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t cs = group_stream(dev, s, 7);  // capture stream (nothing executes on it)
+    bool ok = false;
+    if (cudaGraphCreate(&graph, 0) == cudaSuccess) {
+        cudaGraphConditionalHandle h;
+        cudaGraphNodeParams p = {};
+        cudaGraphNode_t node;
+        int* it = dalloc<int>(S->allocs, 1, s);
+        zero_words(it, sizeof(int), s);
+        if (cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault) == cudaSuccess) {
+            p.type = cudaGraphNodeTypeConditional;
+            p.conditional.handle = h;
+            p.conditional.type = cudaGraphCondTypeWhile;
+            p.conditional.size = 1;
+            if (cudaGraphAddNode(&node, graph, nullptr, 0, &p) == cudaSuccess &&
+                cudaStreamBeginCaptureToGraph(cs, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                bool cap = true;
+                try {
+                    pcg_iteration(S, a, S->hP, 1, false, cs);
+                    LAUNCH(k_tol_cond, 1, 32, 0, cs, h, a.sc_.n_active, it, S->o.max_iters + 1);
+                } catch (...) {
+                    cap = false;
+                }
+                cudaGraph_t body = nullptr;
+                if (cudaStreamEndCapture(cs, &body) != cudaSuccess) cap = false;
+                ok = cap && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess &&
+                     cudaGraphLaunch(exec, s) == cudaSuccess;
+            }
+        }
+    }
+    cudaGetLastError();  // a failed attempt leaves no sticky error: fall back to host polling
+    if (exec) cudaGraphExecDestroy(exec);  // freed when the launch completes
+    if (graph) cudaGraphDestroy(graph);
+    return ok;
+}
+
 // Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.
 // FIXED mode with several frames: the frames are split into two groups whose PCGs run on two
 // streams (forked from and joined back to `s`): the frames are independent systems, so one
@@ -854,13 +902,17 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         return;
     }
     // TOL: device-side per-channel stopping; the host polls the active count one chunk behind
+    // (FBS_TOL_GRAPH=1: the loop runs on the device instead, as a CUDA graph with a conditional
+    // while node).
+    pcg_iteration(S, a, S->hP, 0, false, s);  // iteration 0 (Jacobi: d = s) outside the loop
+    if (S->o.max_iters > 1 && tol_graph(S, a, s)) return;
     PinnedBlock pb = pinned_get(2 * sizeof(int));  // written by a copy kernel: no copy-engine queue
     int* pin = static_cast<int*>(pb.p);
     cudaEvent_t ev[2];
     ck(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming), "event");
     ck(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming), "event");
     const int chunk = 8;
-    int done = 0, slot = 0, pending = -1;
+    int done = 1, slot = 0, pending = -1;
     try {
         while (done < S->o.max_iters) {
             const int nit = std::min(chunk, S->o.max_iters - done);

@@ -574,6 +574,16 @@ __global__ void __launch_bounds__(256) k_spmv2_split(VecArgs a) {
     }
 }
 
+// Condition of the TOL loop: another iteration while any (frame, channel) is active (each
+// retires itself at convergence, breakdown or max_iters); `it` bounds it defensively.
+__global__ void k_tol_cond(cudaGraphConditionalHandle h, const int* __restrict__ n_active, int* __restrict__ it,
+                           int max_body) {
+    if (threadIdx.x == 0) {
+        const int i = ++*it;
+        cudaGraphSetConditional(h, (*n_active > 0 && i < max_body) ? 1u : 0u);
+    }
+}
+
 // ---------------------------------------------------------------- slice / export / backward
 // x̂ = Sᵀŷ.  ys planar [K][M] (planar = 1) or canonical [M][K].
 __global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ ys, int64_t M, int K, int F,
