@@ -800,7 +800,7 @@ void pcg_start(fbs_system S, const VecArgs& a, const HierArgs& h, bool x_zero, c
     const VecArgs as = split_args(S, a);
     const int nb = vec_blocks(as);
     const int FKg = a.nf * S->K;  // a group's scalars start at its first frame (restrict_frames)
-    LAUNCH(k_init_scalars, (FKg + 255) / 256, 256, 0, s, a.sc_, FKg, a.nf == S->g->F ? 1 : 0);
+    LAUNCH(k_init_scalars, (FKg + 255) / 256, 256, 0, s, a.sc_, FKg, 1);  // each view has its own count
     if (S->useHierP) {
         // Alg. 2 lines 2-4: r = b − A x, ρ = rᵀM⁻¹r (lift), d = s = M⁻¹r (project)
         if (x_zero) hier_level0<HSRC_RESID0, false>(S, a, s);
@@ -863,20 +863,75 @@ bool tol_graph(fbs_system S, const VecArgs& a, cudaStream_t s) {
     return ok;
 }
 
+// TOL polling for one or more independent PCGs (frame groups) on their own streams: each gets
+// chunks of 8 iterations in turn, and the host reads each one's active count (a copy kernel
+// into mapped pinned memory) one chunk behind; a group whose count reached 0 gets no more.
+struct PcgRun {
+    VecArgs a;
+    HierArgs h;
+    cudaStream_t s;
+};
+void tol_poll(fbs_system S, std::vector<PcgRun>& runs) {
+    const int n = (int)runs.size(), chunk = 8;
+    PinnedBlock pb = pinned_get(2 * n * sizeof(int));
+    int* pin = static_cast<int*>(pb.p);
+    std::vector<cudaEvent_t> ev(2 * n, nullptr);
+    std::vector<int> done(n, 1), slot(n, 0), pending(n, -1);
+    std::vector<char> fin(n, 0);
+    try {
+        for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        for (int left = n; left > 0;) {
+            for (int r = 0; r < n; ++r) {
+                if (fin[r]) continue;
+                const int nit = std::min(chunk, S->o.max_iters - done[r]);
+                for (int i = 0; i < nit; ++i) pcg_iteration(S, runs[r].a, runs[r].h, done[r] + i, false, runs[r].s);
+                done[r] += nit;
+                copy_words(runs[r].a.sc_.n_active, &pin[2 * r + slot[r]], sizeof(int), runs[r].s);
+                ck(cudaEventRecord(ev[2 * r + slot[r]], runs[r].s), "event");
+            }
+            for (int r = 0; r < n; ++r) {
+                if (fin[r]) continue;
+                bool stop = done[r] >= S->o.max_iters;
+                if (pending[r] >= 0) {
+                    ck(cudaEventSynchronize(ev[2 * r + pending[r]]), "event sync");
+                    if (pin[2 * r + pending[r]] == 0) stop = true;
+                }
+                pending[r] = slot[r];
+                slot[r] ^= 1;
+                if (stop) {
+                    fin[r] = 1;
+                    --left;
+                }
+            }
+        }
+        for (auto& r : runs) ck(cudaStreamSynchronize(r.s), "sync");
+    } catch (...) {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        pinned_put(pb, runs[0].s);
+        throw;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    pinned_put(pb, runs[0].s);
+}
+
 // Full PCG (Alg. 2) from the state in a.x (right-hand side a.b); x_zero: x0 = 0.
-// FIXED mode with several frames: the frames are split into two groups whose PCGs run on two
-// streams (forked from and joined back to `s`): the frames are independent systems, so one
-// group's latency-bound kernels overlap the other's bandwidth-bound ones.
+// With several frames, the frames are split into groups whose PCGs run on their own streams
+// (forked from and joined back to `s`): the frames are independent systems, so one group's
+// latency-bound kernels overlap the other's bandwidth-bound ones.  TOL mode: each group has its
+// own active count and stops on its own (tol_poll).
 void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     fbs_grid g = S->g;
     const int G = std::min(S->nGroups, g->F);
-    if (S->o.mode == FBS_MODE_FIXED && G > 1) {
+    const bool tol = S->o.mode == FBS_MODE_TOL;
+    if (G > 1) {
         int dev = 0;
         ck(cudaGetDevice(&dev), "cudaGetDevice");
         cudaEvent_t fork;
         std::vector<cudaEvent_t> join(G);
         ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
         ck(cudaEventRecord(fork, s), "event");
+        std::vector<PcgRun> runs;
         for (int gi = 0; gi < G; ++gi) {
             const int f0 = (int)((int64_t)g->F * gi / G), f1 = (int)((int64_t)g->F * (gi + 1) / G);
             cudaStream_t sg = group_stream(dev, s, gi);
@@ -884,12 +939,20 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
             VecArgs ag = a;
             HierArgs hg = S->hP;
             restrict_frames(S, f0, f1 - f0, ag, hg);
+            ag.sc_.n_active = a.sc_.n_active + 1 + gi;  // the group's own active count
             pcg_start(S, ag, hg, x_zero, sg);
-            for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, ag, hg, i, i == S->o.iters - 1, sg);
+            if (tol) {
+                pcg_iteration(S, ag, hg, 0, false, sg);
+                runs.push_back({ag, hg, sg});
+            } else {
+                for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, ag, hg, i, i == S->o.iters - 1, sg);
+            }
+        }
+        if (tol && S->o.max_iters > 1) tol_poll(S, runs);
+        for (int gi = 0; gi < G; ++gi) {
+            cudaStream_t sg = group_stream(dev, s, gi);
             ck(cudaEventCreateWithFlags(&join[gi], cudaEventDisableTiming), "event");
             ck(cudaEventRecord(join[gi], sg), "event");
-        }
-        for (int gi = 0; gi < G; ++gi) {
             ck(cudaStreamWaitEvent(s, join[gi], 0), "wait");
             cudaEventDestroy(join[gi]);
         }
@@ -897,7 +960,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         return;
     }
     pcg_start(S, a, S->hP, x_zero, s);
-    if (S->o.mode == FBS_MODE_FIXED) {
+    if (!tol) {
         for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, a, S->hP, i, i == S->o.iters - 1, s);
         return;
     }
@@ -905,43 +968,16 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     // (FBS_TOL_GRAPH=1: the loop runs on the device instead, as a CUDA graph with a conditional
     // while node).
     pcg_iteration(S, a, S->hP, 0, false, s);  // iteration 0 (Jacobi: d = s) outside the loop
-    if (S->o.max_iters > 1 && tol_graph(S, a, s)) return;
-    PinnedBlock pb = pinned_get(2 * sizeof(int));  // written by a copy kernel: no copy-engine queue
-    int* pin = static_cast<int*>(pb.p);
-    cudaEvent_t ev[2];
-    ck(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming), "event");
-    ck(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming), "event");
-    const int chunk = 8;
-    int done = 1, slot = 0, pending = -1;
-    try {
-        while (done < S->o.max_iters) {
-            const int nit = std::min(chunk, S->o.max_iters - done);
-            for (int i = 0; i < nit; ++i) pcg_iteration(S, a, S->hP, done + i, false, s);
-            done += nit;
-            copy_words(a.sc_.n_active, &pin[slot], sizeof(int), s);
-            ck(cudaEventRecord(ev[slot], s), "event");
-            if (pending >= 0) {
-                ck(cudaEventSynchronize(ev[pending]), "event sync");
-                if (pin[pending] == 0) break;
-            }
-            pending = slot;
-            slot ^= 1;
-        }
-        ck(cudaStreamSynchronize(s), "sync");
-    } catch (...) {
-        cudaEventDestroy(ev[0]);
-        cudaEventDestroy(ev[1]);
-        pinned_put(pb, s);
-        throw;
-    }
-    cudaEventDestroy(ev[0]);
-    cudaEventDestroy(ev[1]);
-    pinned_put(pb, s);
+    if (S->o.max_iters <= 1 || tol_graph(S, a, s)) return;
+    std::vector<PcgRun> runs{{a, S->hP, s}};
+    tol_poll(S, runs);
 }
 
 PcgScalars alloc_scalars(std::vector<void*>& A, int FK, cudaStream_t s) {
     // one allocation, zeroed by one launch: 6 double and 3 int arrays of FK, + the active count
-    double* d = dalloc<double>(A, (size_t)6 * FK + ((size_t)3 * FK + 2) / 2 + 1, s);
+    // ints: active, iters, status [FK] each, the active count, and one count per frame group (≤ 8)
+    const size_t nD = (size_t)6 * FK + ((size_t)3 * FK + 1 + 8 + 1) / 2 + 1;
+    double* d = dalloc<double>(A, nD, s);
     PcgScalars p;
     p.rho = d;
     p.alpha = d + FK;
@@ -954,7 +990,7 @@ PcgScalars alloc_scalars(std::vector<void*>& A, int FK, cudaStream_t s) {
     p.iters = i + FK;
     p.status = i + 2 * (size_t)FK;
     p.n_active = i + 3 * (size_t)FK;
-    zero_words(d, ((size_t)6 * FK + ((size_t)3 * FK + 2) / 2 + 1) * sizeof(double), s);
+    zero_words(d, nD * sizeof(double), s);
     return p;
 }
 
