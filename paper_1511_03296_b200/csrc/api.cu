@@ -681,23 +681,42 @@ const char* mode_name(int m) {
     return n[m];
 }
 
+// The channel-split view of `a` (block_unit): K > 1 right-hand sides get BPFs blocks each.
+VecArgs split_args(fbs_system S, const VecArgs& a) {
+    VecArgs as = a;
+    if (a.K > 1) {
+        as.ksplit = 1;
+        as.BPF = S->BPFs;
+    }
+    return as;
+}
+int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
+
 // P of the level-0 input in0 [C][M0] to tree-ordered level 1 + prefix scan (k_tree_lift).
+// PCG with K > 1 channels: channel-split kernels (one channel per block group).
 template <int MODE>
 void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s) {
     static const std::string name = std::string("k_tree_lift<") + mode_name(MODE) + ">";
-    auto kern = k_tree_lift<MODE>;
-    LAUNCH_AS(name.c_str(), kern, h.nt, kScanTile, 0, s, h, in0);
+    if (MODE == HIER_PCG && h.C > 1) {
+        auto kern = k_tree_lift<MODE, true>;
+        LAUNCH_AS(name.c_str(), kern, h.nt * h.C, kScanTile, 0, s, h, in0);
+    } else {
+        auto kern = k_tree_lift<MODE, false>;
+        LAUNCH_AS(name.c_str(), kern, h.nt, kScanTile, 0, s, h, in0);
+    }
 }
 
 // coarse values and their projection onto level 2 (k_tree_coarse)
 template <int MODE>
 void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, cudaStream_t s) {
     static const std::string name = std::string("k_tree_coarse<") + mode_name(MODE) + ">";
-    auto kern = k_tree_coarse<MODE>;
+    const bool ks = MODE == HIER_PCG && h.C > 1;
+    auto kern = ks ? k_tree_coarse<MODE, true> : k_tree_coarse<MODE, false>;
     const size_t sm = (size_t)S->g->tree.maxFrameTiles * sizeof(double);
     if (sm > 48 * 1024)
         ck(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "smem attr");
-    LAUNCH_AS(name.c_str(), kern, a.nf * S->bpf2, 256, sm, s, h, a, first);
+    // ks: the finish reads the split level-0 kernel's partials (BPFs per (frame, channel))
+    LAUNCH_AS(name.c_str(), kern, a.nf * S->bpf2 * (ks ? h.C : 1), 256, sm, s, h, ks ? split_args(S, a) : a, first);
 }
 
 // level-0 output (k_tree_level0)
@@ -705,8 +724,14 @@ template <int MODE>
 void tree_level0(fbs_system S, const HierArgs& h, const VecArgs& a, const float* in0, float* out0, int first,
                  cudaStream_t s) {
     static const std::string name = std::string("k_tree_level0<") + mode_name(MODE) + ">";
-    auto kern = k_tree_level0<MODE>;
-    LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, h, a, in0, out0, first);
+    if (MODE == HIER_PCG && a.K > 1) {
+        const VecArgs as = split_args(S, a);
+        auto kern = k_tree_level0<MODE, true>;
+        LAUNCH_AS(name.c_str(), kern, vec_blocks(as), kThreads, 0, s, h, as, in0, out0, first);
+    } else {
+        auto kern = k_tree_level0<MODE, false>;
+        LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, h, a, in0, out0, first);
+    }
 }
 
 // level-0 PCG input w = mask∘r (+ ρ_0, ‖r‖² partials) (k_hier_level0)
@@ -715,8 +740,14 @@ void hier_level0(fbs_system S, const VecArgs& a, cudaStream_t s) {
     static const char* src_names[] = {"UPDATE", "RESID", "RESID0"};
     static const std::string name =
         std::string("k_hier_level0<") + src_names[SRC] + (LAST ? ",LAST>" : ">");
-    auto kern = k_hier_level0<SRC, LAST>;
-    LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, a, S->w0);
+    if (a.K > 1) {
+        const VecArgs as = split_args(S, a);
+        auto kern = k_hier_level0<SRC, LAST, true>;
+        LAUNCH_AS(name.c_str(), kern, vec_blocks(as), kThreads, 0, s, as, S->w0);
+    } else {
+        auto kern = k_hier_level0<SRC, LAST, false>;
+        LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, a, S->w0);
+    }
 }
 
 // s = M⁻¹_hier r and d = s + βd after the level-0 kernel (Alg. 2 lines 10-14)
@@ -756,16 +787,6 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     h.counters += f0;
 }
 
-// The channel-split view of `a` (block_unit): K > 1 right-hand sides get BPFs blocks each.
-VecArgs split_args(fbs_system S, const VecArgs& a) {
-    VecArgs as = a;
-    if (a.K > 1) {
-        as.ksplit = 1;
-        as.BPF = S->BPFs;
-    }
-    return as;
-}
-int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
 
 // q = A d and α (k_spmv2), channel-split
 void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
@@ -1117,9 +1138,9 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->BPFs = (int)std::max<int64_t>(
             1, std::min<int64_t>(S->BPF, ((int64_t)g_num_sms * occ + (int64_t)F * Kc - 1) / ((int64_t)F * Kc)));
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
-        S->counters = dalloc<unsigned>(A, (size_t)F * Kc + F, s);
+        S->counters = dalloc<unsigned>(A, (size_t)2 * F * Kc, s);  // [F][Kc] VecArgs, [Kc][F] HierArgs
         S->counters2 = S->counters + (size_t)F * Kc;
-        zero_words(S->counters, ((size_t)F * Kc + F) * sizeof(unsigned), s);
+        zero_words(S->counters, (size_t)2 * F * Kc * sizeof(unsigned), s);
         if (hierP || hierI) S->hP = make_hier(S, Kc, o.precond_alpha, o.precond_beta);
         S->fwd = alloc_scalars(A, F * Kc, s);
 

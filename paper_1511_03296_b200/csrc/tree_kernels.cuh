@@ -147,15 +147,29 @@ __global__ void k_tree_anc_mult(HierArgs h, const int* __restrict__ ancId, float
 // the FINISH_LAST kernel of the final FIXED-mode iteration.  FINISH_LAST: the
 // final FIXED-mode iteration needs no new direction: its last block per frame records ‖r‖² and
 // the iteration count and retires the channel.
-template <int SRC, bool FINISH_LAST>
+template <int SRC, bool FINISH_LAST, bool KS = false>
 __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restrict__ w0) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    int f, j, kB, kE, ci;  // frame, part, channels [kB, kE), last-block counter index
+    if constexpr (KS) {    // channel split (K > 1): one (frame, channel) per block group
+        const int g = blockIdx.x / a.BPF;
+        j = blockIdx.x - g * a.BPF;
+        f = g / a.K;
+        kB = g - f * a.K;
+        kE = kB + 1;
+        ci = g;
+    } else {
+        f = blockIdx.x / a.BPF;
+        j = blockIdx.x % a.BPF;
+        kB = 0;
+        kE = a.K;
+        ci = f;
+    }
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
     const int stride = a.BPF * blockDim.x;
-    for (int k = 0; k < a.K; ++k) {
+    for (int k = kB; k < kE; ++k) {
         const int fk = f * a.K + k;
         double rho = 0.0, rr = 0.0;
         if (SRC != HSRC_UPDATE || a.sc_.active[fk]) {
@@ -211,8 +225,8 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (FINISH_LAST && last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
-        for (int k = 0; k < a.K; ++k) {
+    if (FINISH_LAST && last_block_of_frame(a.counters + ci, a.BPF, &sflag)) {
+        for (int k = kB; k < kE; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) continue;
             double RR = 0.0;
@@ -266,12 +280,14 @@ __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*
 }
 
 // PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
-template <int MODE>
+template <int MODE, bool KS = false>
 __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0) {
     pdl_entry();
     __shared__ float stage[kScanTile / 32][kLiftStage];
     __shared__ double shs[32];
-    const int t = blockIdx.x;
+    // KS: channel split (K > 1), grid nt · C, one channel per block
+    const int t = KS ? (int)(blockIdx.x % h.nt) : (int)blockIdx.x;
+    const int cB = KS ? (int)(blockIdx.x / h.nt) : 0, cE = KS ? cB + 1 : h.C;
     const int2 tr = h.tileRange[t];  // tree positions [i0, i1) of this tile (one frame)
     const int i0 = tr.x, i1 = tr.y;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -280,7 +296,7 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
     const int wa = min(i0 + 32 * w, i1), wb = min(i0 + 32 * w + 32, i1);
     const int qa = h.csT[wa], qb = h.csT[wb];
     const int myLo = valid ? h.csT[i] : 0, myHi = valid ? h.csT[i + 1] : 0;
-    for (int c = 0; c < h.C; ++c) {
+    for (int c = cB; c < cE; ++c) {
         const float* src = in0 + (size_t)c * h.M0;
         float acc = 0.f;
         for (int qc = qa; qc < qb; qc += kLiftStage) {
@@ -347,13 +363,17 @@ __device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int f, doub
 // PDA (one thread per coarse vertex of every level ≥ 1... levels ≥ 2 here, level 1 in the lift):
 //   μ_k = z_w(k; α, β) P(1)_k / P(diag A)_k, 0 where the denominator is 0
 //   (reading #10) or above the frame's top level.
-template <int MODE>
+template <int MODE, bool KS = false>
 __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
     pdl_entry();
     extern __shared__ double tb[];  // [tiles of the frame]
     __shared__ double shd[32];
     __shared__ int sflag;
-    const int f = blockIdx.x / h.bpf2, j = blockIdx.x % h.bpf2;
+    // KS: channel split (K > 1), grid nf · bpf2 · C, one channel per block group
+    const int nfb = KS ? (int)(gridDim.x / h.C) : (int)gridDim.x;
+    const int bx = KS ? (int)(blockIdx.x % nfb) : (int)blockIdx.x;
+    const int cB = KS ? (int)(blockIdx.x / nfb) : 0, cE = KS ? cB + 1 : h.C;
+    const int f = bx / h.bpf2, j = bx % h.bpf2;
     const int F1 = h.F + 1;
     const int fb = h.lvFrameOff[F1 + f];
     const int top = h.L - 1;
@@ -361,7 +381,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
     const int stride = h.bpf2 * blockDim.x;
     const int lv = (top >= 2) ? 2 : 1;  // level of the threads' vertices
     const int a0 = h.lvFrameOff[lv * F1 + f], a1 = h.lvFrameOff[lv * F1 + f + 1];
-    for (int c = 0; c < h.C; ++c) {
+    for (int c = cB; c < cE; ++c) {
         const int fk = f * a.K + c;
         const bool act = (MODE != HIER_PCG) || first || a.sc_.active[fk];
         double rho = 0.0;
@@ -443,8 +463,8 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
             if (threadIdx.x == 0) h.partial2[((size_t)f * h.bpf2 + j) * h.C + c] = rho;
         }
     }
-    if (MODE == HIER_PCG && last_block_of_frame(h.counters + f, h.bpf2, &sflag)) {
-        for (int c = 0; c < a.K; ++c) {
+    if (MODE == HIER_PCG && last_block_of_frame(h.counters + (KS ? (size_t)cB * h.F : 0) + f, h.bpf2, &sflag)) {
+        for (int c = (KS ? cB : 0); c < (KS ? cE : a.K); ++c) {
             const int fk = f * a.K + c;
             if (!first && !a.sc_.active[fk]) continue;
             double R = 0.0, RR = 0.0;
@@ -468,16 +488,30 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
 // PCG:   d = s + βd with s = mask∘(μ0 r + acc1) (Alg. 2 line 14; first: d = s, line 3)
 // PLAIN: out0 = mask∘(μ0 in0 + acc1[parent])
 // INIT:  out0_k = (in0_k + acc1_k[parent]) / (in0_K + acc1_K[parent]), 0 where the denominator is 0
-template <int MODE>
+template <int MODE, bool KS = false>
 __global__ void __launch_bounds__(256) k_tree_level0(HierArgs h, VecArgs a, const float* __restrict__ in0,
                                                    float* __restrict__ out0, int first) {
     pdl_entry();
-    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    int f, j, kB, kE, ci;  // frame, part, channels [kB, kE), last-block counter index
+    if constexpr (KS) {    // channel split (K > 1): one (frame, channel) per block group
+        const int g = blockIdx.x / a.BPF;
+        j = blockIdx.x - g * a.BPF;
+        f = g / a.K;
+        kB = g - f * a.K;
+        kE = kB + 1;
+        ci = g;
+    } else {
+        f = blockIdx.x / a.BPF;
+        j = blockIdx.x % a.BPF;
+        kB = 0;
+        kE = a.K;
+        ci = f;
+    }
     const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
     const int stride = a.BPF * blockDim.x;
     const int K = (MODE == HIER_INIT) ? h.C - 1 : a.K;
     auto acc1 = [&](int c, int pT) { return h.acc1T[(size_t)c * h.M1 + pT]; };
-    for (int k = 0; k < K; ++k) {
+    for (int k = KS ? kB : 0; k < (KS ? kE : K); ++k) {
         const int fk = f * a.K + k;
         // PCG: this iteration's x += αd (Alg. 2 line 8, deferred from the update kernel) for every
         // channel the SpMV advanced, even one that stopped since; the new direction for active ones
