@@ -693,11 +693,11 @@ VecArgs split_args(fbs_system S, const VecArgs& a) {
 int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
 
 // P of the level-0 input in0 [C][M0] to tree-ordered level 1 + prefix scan (k_tree_lift).
-// PCG with K > 1 channels: channel-split kernels (one channel per block group).
+// PCG and hierarchical init with K > 1 channels: channel-split kernels (one channel per block group).
 template <int MODE>
 void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s) {
     static const std::string name = std::string("k_tree_lift<") + mode_name(MODE) + ">";
-    if (MODE == HIER_PCG && h.C > 1) {
+    if ((MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2)) {
         auto kern = k_tree_lift<MODE, true>;
         LAUNCH_AS(name.c_str(), kern, h.nt * h.C, kScanTile, 0, s, h, in0);
     } else {
@@ -710,7 +710,7 @@ void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s
 template <int MODE>
 void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, cudaStream_t s) {
     static const std::string name = std::string("k_tree_coarse<") + mode_name(MODE) + ">";
-    const bool ks = MODE == HIER_PCG && h.C > 1;
+    const bool ks = (MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2);
     auto kern = ks ? k_tree_coarse<MODE, true> : k_tree_coarse<MODE, false>;
     const size_t sm = (size_t)S->g->tree.maxFrameTiles * sizeof(double);
     if (sm > 48 * 1024)
@@ -724,7 +724,7 @@ template <int MODE>
 void tree_level0(fbs_system S, const HierArgs& h, const VecArgs& a, const float* in0, float* out0, int first,
                  cudaStream_t s) {
     static const std::string name = std::string("k_tree_level0<") + mode_name(MODE) + ">";
-    if (MODE == HIER_PCG && a.K > 1) {
+    if ((MODE == HIER_PCG || MODE == HIER_INIT) && a.K > 1) {
         const VecArgs as = split_args(S, a);
         auto kern = k_tree_level0<MODE, true>;
         LAUNCH_AS(name.c_str(), kern, vec_blocks(as), kThreads, 0, s, h, as, in0, out0, first);
