@@ -355,13 +355,13 @@ def main():
             v["algorithmic_GBps"] = b / (v["avg_us"] * 1e-6) / 1e9
     def stage_of(name):
         for prefix, st in (("k_axis_bins", "grid_build"), ("k_bin_lut", "grid_build"), ("k_grid_", "grid_build"),
-                           ("k_scan_excl", "grid_build"), ("k_frame_offsets", "grid_build"),
+                           ("k_scan_excl", "grid_build"),
                            ("k_bistoch", "bistochastize"),
-                           ("k_pyr_", "pyramid"), ("k_lift_count", "pyramid"), ("k_tree_top", "pyramid"),
+                           ("k_pyr_", "pyramid"), ("k_tree_top", "pyramid"),
                            ("k_tree_down", "pyramid"), ("k_tree_finish", "pyramid"),
                            ("k_tree_anc_mult", "splat_assemble_init"), ("k_tree_anc", "pyramid"),
                            ("k_splat", "splat_assemble_init"), ("k_assemble", "splat_assemble_init"),
-                           ("k_fill_init_w0", "splat_assemble_init"), ("k_init_dn", "splat_assemble_init"),
+                           ("k_fill_init_w0", "splat_assemble_init"),
                            ("k_tree_lift<PDA>", "splat_assemble_init"),
                            ("k_tree_coarse<PDA>", "splat_assemble_init"), ("k_tree_lift<INIT>", "splat_assemble_init"),
                            ("k_tree_coarse<INIT>", "splat_assemble_init"), ("k_tree_level0<INIT>", "splat_assemble_init"),

@@ -297,23 +297,4 @@ __global__ void __launch_bounds__(256) k_pyr_write(const uint64_t* __restrict__ 
     }
 }
 
-// P(1) at level k+1 from level k (segment sums over the child lists; integers, exact).
-__global__ void k_lift_count(const int* __restrict__ countK, const int* __restrict__ childStart,
-                             const int* __restrict__ childList, int Mn, int* __restrict__ countN) {
-    pdl_entry();
-    for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < Mn; p += gridDim.x * blockDim.x) {
-        int s = 0;
-        for (int j = childStart[p]; j < childStart[p + 1]; ++j) s += countK ? countK[childList[j]] : 1;
-        countN[p] = s;
-    }
-}
-
-// frame offsets of a level from its cell offsets: frameOff[f] = cellOff[f * ncx * ncy]
-__global__ void k_frame_offsets(const int* __restrict__ cellOff, int F, int64_t cellsPerFrame,
-                                int* __restrict__ frameOff) {
-    pdl_entry();
-    const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    if (f <= F) frameOff[f] = cellOff[(int64_t)f * cellsPerFrame];
-}
-
 }  // namespace fbs

@@ -394,13 +394,8 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
 }
 
 // ---------------------------------------------------------------- streaming PCG kernels
-// dn[k][v] = (d, n_v): the direction interleaved with n, so the SpMV's neighbour terms
-// n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
-__global__ void k_init_dn(float2* __restrict__ dn, const float* __restrict__ n, int64_t M, int64_t ldn, int K) {
-    pdl_entry();
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x)
-        dn[(i / M) * ldn + i % M] = make_float2(0.f, n[i % M]);
-}
+// dn[k][v] = (d, n_v) (initialised by k_assemble): the direction interleaved with n, so the
+// SpMV's neighbour terms n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
 
 // Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
 __global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
