@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
 }
 
 // Alg. 2 lines 8-12 (Jacobi):  x += αd;  r −= αq;  s = M⁻¹r = r/diag(A);  ρ_new = rᵀs.
-__global__ void __launch_bounds__(256) k_update(VecArgs a) {
+__global__ void __launch_bounds__(256, 8) k_update(VecArgs a) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(256) k_update(VecArgs a) {
 // SpMV's neighbour terms n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
 
 // Alg. 2 line 14:  d = s + βd  (first: d = s, line 3).
-__global__ void __launch_bounds__(256) k_direction2(VecArgs a, int first) {
+__global__ void __launch_bounds__(256, 8) k_direction2(VecArgs a, int first) {
     pdl_entry();
     const BlockUnit bu = block_unit(a);
     const int f = bu.f, j = bu.j;
