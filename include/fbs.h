@@ -62,6 +62,8 @@ typedef struct fbs_system_s* fbs_system;
 /* bits of the `status` word returned by fbs_system_stats */
 #define FBS_ST_BREAKDOWN 1     /* a (frame, channel) stopped on ρ = 0 or dᵀq ≤ 0 (reading #11) */
 #define FBS_ST_NOTCONVERGED 2  /* TOL mode: max_iters reached before ‖r‖ ≤ tol‖b‖           */
+#define FBS_ST_NEG_CONF 4      /* some confidence c < 0 (the paper requires c ≥ 0) */
+#define FBS_ST_NONFINITE 8     /* a non-finite c, t (forward) or dL/dx (backward) entered S      */
 
 /* ---------------------------------------------------------------- options */
 typedef struct {
@@ -104,7 +106,8 @@ void fbs_default_solve_opts(fbs_solve_opts* o);
  *             (⌊x/σxy⌋, ⌊y/σxy⌋, ⌊Yn/256σl⌋, ⌊Un/256σuv⌋, ⌊Vn/256σuv⌋), each one IEEE
  *             fp64 division then floor (reading #2).
  * Then runs opts->n_bistoch iterations of Alg. 1 and (if opts->build_pyramid) builds the
- * pyramid of PAPER.md:745-766 (reading #8).  Synchronises `stream` once at the end.
+ * pyramid of PAPER.md:745-766 (reading #8).  Synchronises `stream` twice, for the vertex and
+ * the pyramid level counts (host allocation sizes); the rest is enqueued asynchronously.
  * Errors: FBS_EINVAL if a pointer is NULL, frames ∉ [1, 256], height or width ∉
  * [1, 65535·σxy], σxy < 1, σl < 1 or σuv < 1 (8-bit key fields), or a σxy cell would hold
  * more than 64 pixels (σxy > 8); FBS_ELIMIT (see above); FBS_ENOMEM; FBS_ECUDA. */

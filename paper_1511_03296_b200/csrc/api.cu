@@ -1071,9 +1071,11 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         float* bIn = dalloc<float>(A, (size_t)(K + 1) * M + kVecPad, s);
         S->sc = bIn + (size_t)K * M;
         CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
+        S->inflags = dalloc<int>(A, 1, s);  // FBS_ST_NEG_CONF / FBS_ST_NONFINITE from the splats
+        zero_words(S->inflags, sizeof(int), s);
         // a4: splat Sc, b = S(c∘t)
         LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t,
-               K, M, S->sc, bIn);
+               K, M, S->sc, bIn, S->inflags);
         // optional low-rank reduction of B (Supp. §4): Kc reduced channels
         int Kc = K;
         double* lrRt = nullptr;
@@ -1285,7 +1287,7 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
     CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
     // u = S g (∂f/∂b = A⁻¹(S ∂f/∂x̂)), solved from x0 = 0 (reading #14)
     LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, g_dldx, K,
-           M, nullptr, S->u);
+           M, nullptr, S->u, S->inflags);
     VecArgs a = make_args(S, S->bwd, S->xb, S->u);
     const VecArgs as = split_args(S, a);
     // k_assemble here only zeroes x and forms ‖u‖² (diag(A), μ0 are recomputed from the same inputs)
@@ -1457,6 +1459,8 @@ int fbs_system_stats(fbs_system S, int32_t* iters, double* relres, int32_t* bwd_
         const int FK = S->g->F * S->K;
         std::vector<double> rr(FK), bb(FK);
         std::vector<int> st(FK), st2(FK, 0);
+        int inflags = 0;
+        ck(cudaMemcpyAsync(&inflags, S->inflags, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaMemcpyAsync(rr.data(), S->fwd.rr, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaMemcpyAsync(bb.data(), S->fwd.bb, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaMemcpyAsync(st.data(), S->fwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
@@ -1471,7 +1475,7 @@ int fbs_system_stats(fbs_system S, int32_t* iters, double* relres, int32_t* bwd_
         if (relres)
             for (int i = 0; i < FK; ++i) relres[i] = bb[i] > 0 ? std::sqrt(rr[i] / bb[i]) : std::sqrt(rr[i]);
         if (status) {
-            int acc = 0;
+            int acc = inflags;
             for (int i = 0; i < FK; ++i) acc |= st[i] | st2[i];
             *status = acc;
         }
@@ -1533,7 +1537,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
         float* planar = dalloc<float>(tmp, KM, s);
         CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
         LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, p, K,
-               g->M, nullptr, planar);
+               g->M, nullptr, planar, nullptr);
         LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, K, out);
         free_all(tmp, s);
     });

@@ -104,7 +104,8 @@ template <bool WEIGHTED>
 __global__ void __launch_bounds__(256, 6) k_splat(CellGeom g, const int* __restrict__ cellOff,
                                                const int* __restrict__ vid, const uint8_t* __restrict__ perm,
                                                const float* __restrict__ c, const float* __restrict__ p, int K,
-                                               int64_t M, float* __restrict__ sc_out, float* __restrict__ out) {
+                                               int64_t M, float* __restrict__ sc_out, float* __restrict__ out,
+                                               int* __restrict__ flags) {
     pdl_entry();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ncells = (int64_t)g.F * g.ncx * g.ncy;
@@ -138,6 +139,17 @@ __global__ void __launch_bounds__(256, 6) k_splat(CellGeom g, const int* __restr
                 if (K > 0) pv[j] = pf[pix[j]];
             }
         }
+        if (flags) {  // input checks (status bits of fbs_system_stats): c < 0, non-finite c or t
+            int bad = 0;
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                if (rk[j] >= 0) {
+                    if (WEIGHTED && cw[j] < 0.f) bad |= FBS_ST_NEG_CONF;
+                    if (!isfinite(cw[j]) || !isfinite(pv[j])) bad |= FBS_ST_NONFINITE;
+                }
+            bad = __reduce_or_sync(0xffffffffu, bad);
+            if (bad && lane == 0) atomicOr(flags, bad);
+        }
         // segment bounds inside each half: lane l's segment starts at the last head ≤ l
         int sstart[2];
 #pragma unroll
@@ -162,6 +174,14 @@ __global__ void __launch_bounds__(256, 6) k_splat(CellGeom g, const int* __restr
 #pragma unroll
                 for (int j = 0; j < 2; ++j)
                     if (rk[j] >= 0) pn[j] = pf[(size_t)(k + 1) * HW + pix[j]];
+            }
+            if (flags && data && k > 0) {  // the later channels' targets
+                int bad = 0;
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    if (rk[j] >= 0 && !isfinite(pv[j])) bad = FBS_ST_NONFINITE;
+                bad = __reduce_or_sync(0xffffffffu, bad);
+                if (bad && lane == 0) atomicOr(flags, bad);
             }
             double vs[2];
 #pragma unroll

@@ -213,6 +213,28 @@ def test_noise_image_pyramid_bit_exact(sxy):
             prev_off = off
 
 
+def test_input_check_status_bits():
+    """Negative confidence and non-finite inputs are flagged in the stats status word
+    (FBS_ST_NEG_CONF = 4, FBS_ST_NONFINITE = 8), not silently solved."""
+    rgb, t, c = small(K=1)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    _, s = fbs.solve(g, dev(t), dev(c), 5.0, keep_system=True, mode="fixed", iters=3)
+    assert s.stats()["status"] & 12 == 0
+    c2 = c.copy()
+    c2[0, 3, 4] = -0.5
+    _, s = fbs.solve(g, dev(t), dev(c2), 5.0, keep_system=True, mode="fixed", iters=3)
+    assert s.stats()["status"] & 4
+    t2 = t.copy()
+    t2[0, 0, 5, 6] = np.nan
+    _, s = fbs.solve(g, dev(t2), dev(c), 5.0, keep_system=True, mode="fixed", iters=3)
+    assert s.stats()["status"] & 8
+    _, s = fbs.solve(g, dev(t), dev(c), 5.0, keep_system=True, mode="fixed", iters=3)
+    gr = np.zeros_like(t)
+    gr[0, 0, 1, 1] = np.inf
+    s.backward(dev(gr), dev(t), dev(c))
+    assert s.stats()["status"] & 8
+
+
 def test_zero_confidence_and_constant_target():
     rgb, t, c = small(K=2)
     g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
