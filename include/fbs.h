@@ -95,6 +95,23 @@ typedef struct {
                           /* the mass, Y = (A⁻¹Q̃)R̃ (reading #26); 0 = off (default)            */
 } fbs_solve_opts;
 
+/* ---------------------------------------------------------------- device memory
+ * Handles allocate their internal buffers stream-ordered on the stream they are created on.
+ * By default that is cudaMallocAsync / cudaFreeAsync on the device's default memory pool; a
+ * caller may route them through its own allocator (e.g. PyTorch's caching allocator):
+ *   alloc(bytes, ctx, stream) → device pointer usable in stream order on `stream` (NULL: fails
+ *                               the call with FBS_ENOMEM);
+ *   free(ptr, ctx, stream)    → release; all work the library enqueued on its buffers is
+ *                               ordered on `stream` before this point.
+ * fbs_set_allocator applies to handles created afterwards (a handle keeps the allocator it was
+ * created with); NULL restores the default.  Not thread-safe against concurrent handle creation. */
+typedef struct {
+    void* (*alloc)(size_t bytes, void* ctx, fbs_stream stream);
+    void (*free)(void* ptr, void* ctx, fbs_stream stream);
+    void* ctx;
+} fbs_allocator;
+int fbs_set_allocator(const fbs_allocator* a);
+
 void fbs_default_grid_opts(fbs_grid_opts* o);
 void fbs_default_solve_opts(fbs_solve_opts* o);
 

@@ -18,6 +18,7 @@ from .fbs import (  # noqa: F401
     slice_,
     solve,
     solve_robust,
+    use_torch_allocator,
     splat,
     version,
 )

@@ -24,6 +24,14 @@ namespace fbs {
 
 std::atomic<long long> g_launches{0};
 
+// the process allocator for handles created from now on (fbs_set_allocator)
+std::mutex g_alloc_mu;
+fbs_allocator g_allocator{};
+fbs_allocator current_allocator() {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    return g_allocator;
+}
+
 namespace {
 
 thread_local std::string t_err;
@@ -131,17 +139,25 @@ void device_setup(int* dev) {
 }
 
 template <class T>
-T* dalloc(std::vector<void*>& list, size_t count, cudaStream_t s) {
+T* dalloc(AllocList& list, size_t count, cudaStream_t s) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    ck(cudaMallocAsync(&p, count * sizeof(T), s), "cudaMallocAsync");
-    list.push_back(p);
+    if (list.al.alloc) {
+        p = list.al.alloc(count * sizeof(T), list.al.ctx, reinterpret_cast<fbs_stream>(s));
+        if (!p) throw Err(FBS_ENOMEM, "caller allocator returned NULL");
+    } else {
+        ck(cudaMallocAsync(&p, count * sizeof(T), s), "cudaMallocAsync");
+    }
+    list.ptrs.push_back(p);
     return static_cast<T*>(p);
 }
 
-void free_all(std::vector<void*>& list, cudaStream_t s) {
-    for (void* p : list) cudaFreeAsync(p, s);
-    list.clear();
+void free_all(AllocList& list, cudaStream_t s) {
+    for (void* p : list.ptrs) {
+        if (list.al.free) list.al.free(p, list.al.ctx, reinterpret_cast<fbs_stream>(s));
+        else cudaFreeAsync(p, s);
+    }
+    list.ptrs.clear();
 }
 
 // Side streams of the frame-group splits (Alg. 1 and the FIXED-mode PCG), created once per (device,
@@ -994,7 +1010,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     tol_poll(S, runs);
 }
 
-PcgScalars alloc_scalars(std::vector<void*>& A, int FK, cudaStream_t s) {
+PcgScalars alloc_scalars(AllocList& A, int FK, cudaStream_t s) {
     // one allocation, zeroed by one launch: 6 double and 3 int arrays of FK, + the active count
     // ints: active, iters, status [FK] each, the active count, and one count per frame group (≤ 8)
     const size_t nD = (size_t)6 * FK + ((size_t)3 * FK + 1 + 8 + 1) / 2 + 1;
@@ -1213,7 +1229,7 @@ static void robust_impl(fbs_grid g, const float* t, int K, const float* c_init, 
     if (K != 1) throw Err(FBS_EINVAL, "the robust solver takes scalar targets (K = 1)");
     if (!(sigma_gm > 0.0) || !std::isfinite(sigma_gm)) throw Err(FBS_EINVAL, "sigma_gm must be finite and > 0");
     if (n_irls < 1) throw Err(FBS_EINVAL, "n_irls must be >= 1");
-    std::vector<void*> tmp;
+    AllocList tmp;
     float* c = (n_irls > 1 || c_out) ? (c_out ? c_out : dalloc<float>(tmp, g->N, s)) : nullptr;
     try {
         const float* cur = c_init;
@@ -1241,7 +1257,7 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
     if (!(sigma_s > 0.0) || !(sigma_r > 0.0) || n_iters < 1) throw Err(FBS_EINVAL, "sigma_s, sigma_r > 0, n_iters >= 1");
     int dev = 0;
     device_setup(&dev);
-    std::vector<void*> tmp;
+    AllocList tmp;
     try {
         const size_t NP = (size_t)F * H * W, NS = NP * K;
         float* Dx = dalloc<float>(tmp, NP, s);
@@ -1379,7 +1395,7 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
         if (m) ck(cudaMemcpyAsync(m, g->m, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
         if (n) ck(cudaMemcpyAsync(n, g->n, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
         if (nbr) {
-            std::vector<void*> tmp;
+            AllocList tmp;
             int* d = dalloc<int>(tmp, (size_t)M * 10, s);
             LAUNCH(k_export_nbr, grid_for(M), kThreads, 0, s, g->nbr, (int)M, d);
             ck(cudaMemcpyAsync(nbr, d, (size_t)M * 40, cudaMemcpyDeviceToHost, s), "d2h");
@@ -1387,7 +1403,7 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
         }
         if (res) {
             if (g->bistoch_residual < 0.f) {  // reporting only: max|n∘B̄n − m| / max m, on request
-                std::vector<void*> tmp;
+                AllocList tmp;
                 unsigned* d = dalloc<unsigned>(tmp, 2, s);
                 zero_words(d, 2 * sizeof(unsigned), s);
                 LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, d,
@@ -1490,7 +1506,7 @@ int fbs_system_export(fbs_system S, float* sc, float* b, float* diagA, float* y0
         const int64_t M = g->M;
         const int K = S->K;
         const size_t KM = (size_t)K * M;
-        std::vector<void*> tmp;
+        AllocList tmp;
         float* d = dalloc<float>(tmp, KM, s);
         auto vk = [&](const float* src, float* host) {
             LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, src, M, K, d);
@@ -1532,7 +1548,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
         if (!g || !p || !out) throw Err(FBS_EINVAL, "null pointer");
         if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
         cudaStream_t s = (cudaStream_t)stream;
-        std::vector<void*> tmp;
+        AllocList tmp;
         const size_t KM = (size_t)K * g->M;
         float* planar = dalloc<float>(tmp, KM, s);
         CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
@@ -1555,7 +1571,7 @@ int fbs_system_apply_A(fbs_system S, const float* y, float* out, fbs_stream stre
         if (!S || !y || !out) throw Err(FBS_EINVAL, "null pointer");
         cudaStream_t s = (cudaStream_t)stream;
         fbs_grid g = S->g;
-        std::vector<void*> tmp;
+        AllocList tmp;
         const size_t KM = (size_t)S->K * g->M;
         float* ys = dalloc<float>(tmp, KM, s);
         LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, y, nullptr, g->M, S->K, ys);
@@ -1570,7 +1586,7 @@ int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_strea
         if (!S || !r || !out) throw Err(FBS_EINVAL, "null pointer");
         cudaStream_t s = (cudaStream_t)stream;
         fbs_grid g = S->g;
-        std::vector<void*> tmp;
+        AllocList tmp;
         const size_t KM = (size_t)S->K * g->M;
         float* w = dalloc<float>(tmp, KM, s);
         LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, r, S->mu0, g->M, S->K, w);
@@ -1591,6 +1607,14 @@ int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_strea
 
 const char* fbs_last_error(void) { return t_err.c_str(); }
 int fbs_version(void) { return 1; }
+
+int fbs_set_allocator(const fbs_allocator* a) {
+    return guard("fbs_set_allocator", [&] {
+        if (a && (!a->alloc || !a->free)) throw Err(FBS_EINVAL, "allocator needs both alloc and free");
+        std::lock_guard<std::mutex> lk(g_alloc_mu);
+        g_allocator = a ? *a : fbs_allocator{};
+    });
+}
 int64_t fbs_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int fbs_profile_enable(int on) {

@@ -13,6 +13,15 @@
 
 namespace fbs {
 
+// The device buffers of a handle (or of one call's scratch) and the allocator they come from:
+// the process allocator current when the list is created (api.cu fbs_set_allocator); alloc ==
+// nullptr means cudaMallocAsync / cudaFreeAsync.
+fbs_allocator current_allocator();
+struct AllocList {
+    std::vector<void*> ptrs;
+    fbs_allocator al = current_allocator();
+};
+
 // a block of mapped pinned host memory from the staging pool (api.cu pinned_get / pinned_put)
 struct PinnedBlock {
     void* p = nullptr;
@@ -352,7 +361,7 @@ struct fbs_grid_s {
     int64_t maxFrameM2 = 0;
     int* lvFrameOffDev = nullptr;  // [L][F + 1]
     fbs::TreeOrder tree;           // tree order of the pyramid (L > 1)
-    std::vector<void*> allocs;
+    fbs::AllocList allocs;
 };
 
 struct fbs_system_s {
@@ -397,5 +406,5 @@ struct fbs_system_s {
     fbs::HierArgs hP{};
     bool has_backward = false;
     std::vector<int> lr_rank;  // low-rank solves: kept rank t_f per frame
-    std::vector<void*> allocs;
+    fbs::AllocList allocs;
 };

@@ -23,7 +23,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 FBS_OK, FBS_EINVAL, FBS_ENOMEM, FBS_ECUDA, FBS_ELIMIT, FBS_ESTATE = range(6)
-FBS_ST_BREAKDOWN, FBS_ST_NOTCONVERGED = 1, 2
+FBS_ST_BREAKDOWN, FBS_ST_NOTCONVERGED, FBS_ST_NEG_CONF, FBS_ST_NONFINITE = 1, 2, 4, 8
 PRECOND = {"jacobi": 0, "hier": 1}
 INIT = {"flat": 0, "hier": 1, "zero": 2}
 MODE = {"fixed": 0, "tol": 1}
@@ -38,6 +38,14 @@ class SolveOpts(C.Structure):
                 ("tol", C.c_double), ("max_iters", C.c_int), ("precond_alpha", C.c_double),
                 ("precond_beta", C.c_double), ("init_alpha", C.c_double), ("init_beta", C.c_double),
                 ("lowrank_eps", C.c_double)]
+
+
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", C.c_void_p)]
 
 
 _vp, _i, _d, _i64 = C.c_void_p, C.c_int, C.c_double, C.c_int64
@@ -63,6 +71,7 @@ _SIGS = {
     "fbs_system_apply_precond": (_i, [_vp, _vp, _vp, _vp]),
     "fbs_last_error": (C.c_char_p, []),
     "fbs_version": (_i, []),
+    "fbs_set_allocator": (_i, [C.POINTER(Allocator)]),
     "fbs_launch_count": (_i64, []),
     "fbs_profile_enable": (_i, [_i]),
     "fbs_profile_report": (_i, [C.c_char_p, C.c_size_t]),
@@ -360,6 +369,34 @@ def blur(grid: Grid, v: torch.Tensor, stream=None) -> torch.Tensor:
     out = torch.empty_like(v)
     _check(_lib.fbs_blur(grid.handle, _ptr(v), _ptr(out), _stream(stream)))
     return out
+
+
+_torch_alloc_refs = None  # keeps the ctypes callbacks alive while registered
+
+
+def use_torch_allocator(enable: bool = True):
+    """Route the device buffers of handles created from now on through PyTorch's caching
+    allocator (stream-ordered on the handle's stream); False restores cudaMallocAsync."""
+    global _torch_alloc_refs
+    if not enable:
+        _check(_lib.fbs_set_allocator(None))
+        _torch_alloc_refs = None
+        return
+
+    def _alloc(nbytes, ctx, stream):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device=torch.cuda.current_device(),
+                                                      stream=int(stream or 0))
+        except Exception:  # noqa: BLE001 (the C side reports FBS_ENOMEM)
+            return None
+
+    def _free(ptr, ctx, stream):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    refs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    a = Allocator(refs[0], refs[1], None)
+    _check(_lib.fbs_set_allocator(C.byref(a)))
+    _torch_alloc_refs = (refs, a)
 
 
 def header_symbols():

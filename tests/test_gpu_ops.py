@@ -235,6 +235,31 @@ def test_input_check_status_bits():
     assert s.stats()["status"] & 8
 
 
+def test_torch_caching_allocator():
+    """Handles created after use_torch_allocator() take their buffers from PyTorch's caching
+    allocator (visible in torch.cuda.memory_allocated) and return them on close; results are
+    unchanged."""
+    rgb, t, c = small(K=2)
+    g0 = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    x0 = fbs.solve(g0, dev(t), dev(c), 5.0, mode="fixed", iters=10)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    fbs.use_torch_allocator(True)
+    try:
+        g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+        torch.cuda.synchronize()
+        held = torch.cuda.memory_allocated() - before
+        assert held > 0
+        x = fbs.solve(g, dev(t), dev(c), 5.0, mode="fixed", iters=10)
+        assert torch.equal(x, x0)
+        g.close()
+        del x
+        torch.cuda.synchronize()
+    finally:
+        fbs.use_torch_allocator(False)
+    assert torch.cuda.memory_allocated() <= before + 4096
+
+
 def test_zero_confidence_and_constant_target():
     rgb, t, c = small(K=2)
     g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
