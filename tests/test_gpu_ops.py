@@ -306,6 +306,28 @@ def test_many_frames():
         assert mx <= MAX_TOL and rms <= RMS_TOL
 
 
+@pytest.mark.parametrize("mode", ["fixed", "tol"])
+@pytest.mark.parametrize("pc", ["hier+hier", "jacobi+flat"])
+def test_frame_groups_times_channel_split(mode, pc):
+    """Several frames (frame groups on side streams) × several channels (channel-split kernels,
+    per-(frame, channel) counters and scalars), against per-frame oracle solves."""
+    precond, init = pc.split("+")
+    rgb, t, c = small(K=3, frames=5, W=70, H=45, cells=7)
+    og = O.build_grid(rgb, 8.0, 4.0, 3.0)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    x, S = fbs.solve(g, dev(t), dev(c), 7.0, keep_system=True, precond=precond, init=init, mode=mode, iters=25,
+                     tol=1e-6)
+    x = x.cpu().numpy()
+    it = S.stats()["iterations"]
+    for f in range(5):
+        sol = O.solve_frame(og, f, t[f].reshape(3, -1).astype(float), c[f].ravel().astype(float), 7.0,
+                            O.SolveOptions(precond=precond, init=init, mode=mode, iters=25, tol=1e-6))
+        mx, rms = compare_x(x[f].reshape(3, -1), sol.x, t[f].reshape(3, -1).astype(float), c[f].ravel().astype(float))
+        assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
+        if mode == "fixed":
+            assert np.all(it[f] == np.minimum(25, sol.iterations))
+
+
 def test_error_paths():
     rgb, t, c = small(K=1)
     with pytest.raises(fbs.FbsError) as e:
