@@ -42,7 +42,8 @@ if os.path.exists(p):
                       "--steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extras",
            "note": "cold-cache serialised per-launch times over the warm-up, timed and profiled passes (3 steps); "
                    "compare shares, not absolutes. Template ids: k_tree_*<0> = PCG, <1> = PDA, <2> = INIT; "
-                   "k_hier_level0<0,0> = UPDATE, <1,0> = RESID, <2,0> = RESID0, <0,1> = UPDATE,LAST.",
+                   "k_hier_level0<0,0> = UPDATE, <1,0> = RESID, <2,0> = RESID0, <0,1> = UPDATE,LAST; a trailing "
+                   "false/true is the channel-split flag (K > 1).",
            "total_ns": all_ns, "launches": len(seq),
            "kernels": {k: {"launches": c, "total_ns": t, "share": round(t / all_ns, 4)}
                        for k, (c, t) in sorted(tot.items(), key=lambda kv: -kv[1][1])}}
@@ -67,9 +68,15 @@ if os.path.exists(p):
         x, unit = v.split()
         return float(x.replace(",", "")) * {"Mbyte": 1e6, "Kbyte": 1e3, "Gbyte": 1e9, "byte": 1.0}[unit]
 
+    def short_name(kname):
+        base = kname.split("(")[0]
+        for k, v in names.items():  # template instances may carry extra flags (e.g. <0, 0, false>)
+            if base == k or base.startswith(k[:-1] + ", "):
+                return v
+        return None
+
     for rec in summary(p):
-        base = rec["Kernel Name"].split("(")[0]
-        short = names.get(base)
+        short = short_name(rec["Kernel Name"])
         if not short:
             continue
         with open(os.path.join(dst, f"{tag}_ncu_{short}.json"), "w") as fh:
