@@ -6,6 +6,8 @@
 #include <cmath>
 #include <functional>
 #include <map>
+#include <chrono>
+#include <cstdio>
 #include <mutex>
 #include <cstdio>
 #include <cstring>
@@ -293,6 +295,16 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
 
     int dev = 0;
     device_setup(&dev);
+    // FBS_HOST_TIMING=1: host-side timestamps of the grid build (diagnostic)
+    static const bool host_timing = std::getenv("FBS_HOST_TIMING") && std::getenv("FBS_HOST_TIMING")[0] == '1';
+    auto t_prev = std::chrono::steady_clock::now();
+    auto HT = [&](const char* what) {
+        if (!host_timing) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[fbs host] %-28s %8.1f us\n", what,
+                     std::chrono::duration<double, std::micro>(now - t_prev).count());
+        t_prev = now;
+    };
     fbs_grid g = new fbs_grid_s();
     try {
         g->F = F; g->H = H; g->W = W; g->sxy = sxy; g->sl = sl; g->suv = suv;
@@ -346,7 +358,9 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         PinnedBlock rb = pinned_get(((size_t)(F + 1) * (kMaxLevels + 1) + 4) * sizeof(int));  // read-backs
         int* rbi = static_cast<int*>(rb.p);
         copy_words(err, rbi, (4 + F + 1) * sizeof(int), s);  // err[4] then frameOff (contiguous)
+        HT("before sync1");
         ck(cudaStreamSynchronize(s), "sync");
+        HT("sync1 wait");
         std::copy(rbi, rbi + 4, errh);
         std::copy(rbi + 4, rbi + 4 + F + 1, fo.begin());
         if (errh[0]) throw Err(FBS_ELIMIT, "a sigma_xy cell holds more than 64 pixels");
@@ -359,6 +373,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         const int64_t M = g->M;
 
         g->nbr = dalloc<int4>(A, M + kVecPad, s);
+        HT("after sync1 -> neighbours");
         LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
                g->ncells, g->nbr, err);
 
@@ -480,7 +495,9 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         std::vector<std::vector<int>> lfo(Lmax);
         if (Lmax > 1) copy_words(lvAll + (F + 1), rbi + (F + 1), (size_t)(Lmax - 1) * (F + 1) * sizeof(int), s);
         copy_words(err, rbi + (size_t)Lmax * (F + 1), 4 * sizeof(int), s);
+        HT("before sync2");
         ck(cudaStreamSynchronize(s), "sync");
+        HT("sync2 wait");
         for (int k = 1; k < Lmax; ++k) lfo[k].assign(rbi + (size_t)k * (F + 1), rbi + (size_t)(k + 1) * (F + 1));
         std::copy(rbi + (size_t)Lmax * (F + 1), rbi + (size_t)Lmax * (F + 1) + 4, errh);
         pinned_put(rb, s);
@@ -549,6 +566,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             T.csT = dalloc<int>(A, M1 + 1, s);
             T.tord1 = dalloc<int>(A, M1, s);
             T.parent0T = dalloc<int>(A, M, s);
+            HT("after sync2 -> tree_top");
             LAUNCH(k_tree_top, 1, 256, 0, s, g->lvFrameOffDev, F, top, start[top], top >= 2 ? T.rng[top] : nullptr,
                    top >= 2 ? cnt1[top] : nullptr);
             for (int k = top; k >= 1; --k) {
