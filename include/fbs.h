@@ -162,13 +162,18 @@ void fbs_grid_destroy(fbs_grid g);
 /* ---------------------------------------------------------------- solve */
 /* Solve A y = b for K channels sharing one A (reading #13) and slice.
  *   t_dev      float [frames][K][H][W]   targets
- *   c_dev      float [frames][H][W]      confidences, ≥ 0 (not checked on device)
+ *   c_dev      float [frames][H][W]      confidences, ≥ 0 (c < 0 and non-finite c, t are flagged in
+ *                                        the status bits FBS_ST_NEG_CONF / FBS_ST_NONFINITE)
  *   lambda     > 0                       smoothness weight λ
  *   x_dev      float [frames][K][H][W]   output x̂ = Sᵀŷ (may alias nothing else)
  *   y_dev      float [M][K] or NULL      bilateral-space solution ŷ
  *   sys_out    receives the system handle (A-state, M⁻¹, ŷ) for fbs_solve_backward and
  *              the stats/export calls; NULL = destroy it after the solve.
- * Each (frame, channel) runs its own PCG scalars and stopping rule (reading #13).
+ * Each (frame, channel) runs its own PCG scalars and stopping rule (reading #13).  The frames are
+ * split into groups whose PCGs run concurrently on side streams forked from and joined to
+ * `stream` (they are independent systems); FIXED mode only enqueues work, TOL mode polls each
+ * group's active count from the host one 8-iteration chunk behind and returns when all have
+ * stopped (FBS_TOL_GRAPH=1: a device-side CUDA-graph loop instead, no host polls).
  * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4); the reduced solve
  * runs max_f t_f channels (one extra host synchronisation), and sys_out must then be NULL.
  * Errors: FBS_EINVAL (NULL pointer, K ∉ [1, 64], λ ≤ 0 or not finite, HIER precond/init
