@@ -1093,7 +1093,11 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         // in the dependent-launch gaps (8: 6.60 ms, 16: 6.21 ms per bench step; one group: equal)
         int occ = 16;
         if (const char* e = std::getenv("FBS_BPF_OCC")) occ = std::max(1, std::min(64, std::atoi(e)));  // A/B
-        const int64_t want = (g->maxFrameM + kThreads - 1) / kThreads;
+        // at least 2 vertices per thread: single-frame solves get fewer, fuller blocks (configs[1,2]:
+        // 3.09 → 2.79 and 1.54 → 1.46 ms; 4: 2.93 / 1.58); the bench batch is capped by occupancy
+        int vpt = 2;
+        if (const char* e = std::getenv("FBS_VPT")) vpt = std::max(1, std::min(64, std::atoi(e)));  // A/B
+        const int64_t want = (g->maxFrameM + (int64_t)kThreads * vpt - 1) / ((int64_t)kThreads * vpt);
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
         S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
         {
