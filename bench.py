@@ -534,8 +534,12 @@ def main():
             if wc.mode == "fixed":
                 opts["iters"] = wc.iters
 
+            # the pyramid only serves the hierarchical preconditioner / init (Jacobi configs skip it)
+            pyr = wc.precond == "hier" or wc.init == "hier"
+
             def run_cfg():
-                gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch)
+                gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch,
+                                    build_pyramid=pyr)
                 if gc_ is not None:
                     _, S_ = fbs.solve(gg, tc, cc, wc.lam, keep_system=True, **opts)
                     S_.backward(gc_, tc, cc)
@@ -545,13 +549,15 @@ def main():
                 gg.close()
 
             ms_c = dev_ms(run_cfg)
-            gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch)
+            gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch,
+                                build_pyramid=pyr)
             _, S_ = fbs.solve(gg, tc, cc, wc.lam, keep_system=True, **opts)
             pcg_its = int(S_.stats()["iterations"].max())
             S_.close()
             gg.close()
             cfg_rows[name] = {"ms": ms_c, "MP_per_s": wc.pixels / 1e6 / (ms_c / 1e3), "pcg_iterations": pcg_its,
                               "shape": f"{wc.frames}x{wc.H}x{wc.W}, K={wc.K}",
+                              "pyramid_built": pyr,
                               "solver": f"{wc.precond}+{wc.init}, " +
                                         (f"fixed {wc.iters} it" if wc.mode == "fixed" else f"tol {wc.tol:g}") +
                                         (", + backward" if gc_ is not None else "")}
