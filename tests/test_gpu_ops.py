@@ -346,6 +346,28 @@ def test_error_paths():
     fbs.solve(g2, dev(t), dev(c), 1.0, precond="jacobi", init="flat")  # fine without a pyramid
 
 
+def test_frame_field_limits():
+    """256 frames (the 8-bit frame field of the key, reading #3) build bit-exactly, including
+    frame 255, and solve frame-independently; 257 frames are rejected."""
+    rng = np.random.default_rng(256)
+    rgb = rng.integers(0, 256, (256, 9, 10, 3), dtype=np.uint8)
+    og = O.build_grid(rgb, 4.0, 8.0, 8.0)
+    g = fbs.grid_build(dev(rgb), 4.0, 8.0, 8.0)
+    e = g.export()
+    assert g.M == og.M and np.array_equal(e["keys"], og.keys) and np.array_equal(e["nbr"], og.nbr)
+    assert int(e["keys"][-1] >> np.uint64(56)) == 255
+    t = rng.uniform(0, 1, (256, 1, 9, 10)).astype(np.float32)
+    c = np.ones((256, 9, 10), np.float32)
+    x = fbs.solve(g, dev(t), dev(c), 2.0, precond="hier", init="hier", mode="fixed", iters=10).cpu().numpy()
+    for f in (0, 128, 255):
+        sol = O.solve_frame(og, f, t[f].reshape(1, -1).astype(float), c[f].ravel().astype(float), 2.0,
+                            O.SolveOptions(precond="hier", init="hier", mode="fixed", iters=10))
+        mx, rms = compare_x(x[f].reshape(1, -1), sol.x, t[f].reshape(1, -1).astype(float), c[f].ravel().astype(float))
+        assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
+    with pytest.raises(fbs.FbsError):
+        fbs.grid_build(dev(np.zeros((257, 4, 4, 3), np.uint8)), 4.0, 8.0, 8.0)
+
+
 def test_launch_counter_and_profile():
     rgb, t, c = small(K=1)
     n0 = fbs.launch_count()
