@@ -1284,7 +1284,8 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
         const size_t NP = (size_t)F * H * W, NS = NP * K;
         float* Dx = dalloc<float>(tmp, NP, s);
         float* Dy = dalloc<float>(tmp, NP, s);
-        LAUNCH(k_dt_dist, grid_for((int64_t)NP), kThreads, 0, s, rgb, F, H, W, (float)(sigma_s / sigma_r), Dx, Dy);
+        LAUNCH(k_dt_dist, dim3((W + kThreads - 1) / kThreads, std::min(F * H, 65535)), kThreads, 0, s, rgb, F, H, W,
+               (float)(sigma_s / sigma_r), Dx, Dy);
         if (out != in) ck(cudaMemcpyAsync(out, in, NS * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
         const size_t perWarp = 2 * (size_t)(W + 32) * sizeof(float);
         const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / perWarp));

@@ -11,14 +11,16 @@
 
 namespace fbs {
 
-// d_x = 1 + ratio Σ_c |I_c(x) − I_c(x−1)| (1 at x = 0), d_y likewise; [F][H][W]
+// d_x = 1 + ratio Σ_c |I_c(x) − I_c(x−1)| (1 at x = 0), d_y likewise; [F][H][W].
+// Grid (⌈W/blockDim⌉, ≤ 65535): rows strided over blockIdx.y, no per-pixel index divisions.
 __global__ void k_dt_dist(const uint8_t* __restrict__ rgb, int F, int H, int W, float ratio, float* __restrict__ Dx,
                           float* __restrict__ Dy) {
     pdl_entry();
-    const int64_t N = (int64_t)F * H * W;
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N; p += (int64_t)gridDim.x * blockDim.x) {
-        const int x = (int)(p % W);
-        const int y = (int)((p / W) % H);
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= W) return;
+    for (int row = blockIdx.y; row < F * H; row += gridDim.y) {  // row = f·H + y
+        const int y = row % H;
+        const int64_t p = (int64_t)row * W + x;
         const uint8_t* c = rgb + 3 * p;
         float dx = 0.f, dy = 0.f;
         if (x > 0) {
