@@ -1295,6 +1295,25 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
                "smem attr");
         const int64_t lines = (int64_t)F * K * H;
         const int rowBlocks = (int)std::max<int64_t>(1, std::min<int64_t>((lines + nw - 1) / nw, 148 * 32));
+        // column passes as row passes on the transpose (FBS_DT_COLS=1: the in-place column kernel)
+        const bool viaT = !(std::getenv("FBS_DT_COLS") && std::getenv("FBS_DT_COLS")[0] == '1');
+        float* sT = nullptr;
+        float* DyT = nullptr;
+        const size_t perWarpT = 2 * (size_t)(H + 32) * sizeof(float);
+        const int nwT = (int)std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / perWarpT));
+        const size_t smemT = perWarpT * nwT;
+        const int64_t linesT = (int64_t)F * K * W;
+        const int rowBlocksT = (int)std::max<int64_t>(1, std::min<int64_t>((linesT + nwT - 1) / nwT, 148 * 32));
+        const dim3 tb(32, 8), tgN((W + 31) / 32, (H + 31) / 32, F * K), tgT((H + 31) / 32, (W + 31) / 32, F * K);
+        if (viaT) {
+            sT = dalloc<float>(tmp, NS, s);
+            DyT = dalloc<float>(tmp, NP, s);
+            LAUNCH(k_dt_transpose, dim3((W + 31) / 32, (H + 31) / 32, F), tb, 0, s, Dy, DyT, H, W);
+            if (std::max(smem, smemT) > 48 * 1024)
+                ck(cudaFuncSetAttribute((const void*)k_dt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)std::max(smem, smemT)),
+                   "smem attr");
+        }
         const int colThreads = 32 * std::max(1, std::min(32, H));  // ≥ 1 row per warp chunk
         const int64_t colTiles = (int64_t)F * K * ((W + 31) / 32);
         const int colBlocks = (int)std::max<int64_t>(1, std::min<int64_t>(colTiles, 148 * 8));
@@ -1302,7 +1321,13 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
             const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, n_iters - i) / std::sqrt(std::pow(4.0, n_iters) - 1.0);
             const float lna = (float)(-std::sqrt(2.0) / sig);  // ln a_i
             LAUNCH(k_dt_rows, rowBlocks, 32 * nw, smem, s, out, Dx, F, K, H, W, lna);
-            LAUNCH(k_dt_cols, colBlocks, colThreads, 0, s, out, Dy, F, K, H, W, lna);
+            if (viaT) {
+                LAUNCH(k_dt_transpose, tgN, tb, 0, s, out, sT, H, W);
+                LAUNCH(k_dt_rows, rowBlocksT, 32 * nwT, smemT, s, sT, DyT, F, K, W, H, lna);
+                LAUNCH(k_dt_transpose, tgT, tb, 0, s, sT, out, W, H);
+            } else {
+                LAUNCH(k_dt_cols, colBlocks, colThreads, 0, s, out, Dy, F, K, H, W, lna);
+            }
         }
     } catch (...) {
         free_all(tmp, s);

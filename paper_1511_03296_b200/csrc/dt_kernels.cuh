@@ -36,6 +36,24 @@ __global__ void k_dt_dist(const uint8_t* __restrict__ rgb, int F, int H, int W, 
     }
 }
 
+// Transpose of P planes [H][W] → [W][H] through 32×32 shared-memory tiles (coalesced both ways);
+// block (32, 8), grid (⌈W/32⌉, ⌈H/32⌉, P).  The column passes run as row passes on the transpose.
+__global__ void k_dt_transpose(const float* __restrict__ in, float* __restrict__ out, int H, int W) {
+    pdl_entry();
+    __shared__ float tile[32][33];
+    const size_t plane = (size_t)blockIdx.z * H * W;
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int y = y0 + j, x = x0 + threadIdx.x;
+        if (y < H && x < W) tile[j][threadIdx.x] = in[plane + (size_t)y * W + x];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += 8) {
+        const int x = x0 + j, y = y0 + threadIdx.x;  // out[x][y]
+        if (x < W && y < H) out[plane + (size_t)x * H + y] = tile[threadIdx.x][j];
+    }
+}
+
 constexpr int kDtB = 8;  // loads issued together before their dependent steps
 
 // composition of affine maps J ↦ A J + B: (later ∘ earlier)
