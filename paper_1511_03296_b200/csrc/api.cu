@@ -54,6 +54,7 @@ void ck(cudaError_t e, const char* what) {
 struct ProfRec {
     const char* name;
     cudaEvent_t a, b;
+    cudaStream_t s;
 };
 std::atomic<int> g_prof_on{0};
 std::vector<ProfRec> g_prof;
@@ -77,7 +78,7 @@ struct ProfScope {
     ProfScope(const char* name, cudaStream_t st) : s(st) {
         if (!g_prof_on.load(std::memory_order_relaxed)) return;
         std::lock_guard<std::mutex> lk(g_prof_mu);
-        ProfRec r{name, ev_get(), ev_get()};
+        ProfRec r{name, ev_get(), ev_get(), st};
         ck(cudaEventRecord(r.a, s), "cudaEventRecord");
         g_prof.push_back(r);
         idx = (int)g_prof.size() - 1;
@@ -1693,6 +1694,20 @@ int fbs_profile_report(char* buf, size_t len) {
             auto& e = acc[r.name];
             e.first += 1;
             e.second += ms;
+        }
+        // FBS_TIMELINE=<path>: every profiled launch as CSV (name, stream, start, duration in µs
+        // relative to the first one) for overlap analysis
+        if (const char* tl = std::getenv("FBS_TIMELINE")) {
+            if (FILE* fh = std::fopen(tl, "w")) {
+                std::fprintf(fh, "name,stream,start_us,dur_us\n");
+                for (auto& r : fbs::g_prof) {
+                    float t0 = 0.f, d = 0.f;
+                    cudaEventElapsedTime(&t0, fbs::g_prof.front().a, r.a);
+                    cudaEventElapsedTime(&d, r.a, r.b);
+                    std::fprintf(fh, "%s,%p,%.3f,%.3f\n", r.name, (void*)r.s, 1e3 * t0, 1e3 * d);
+                }
+                std::fclose(fh);
+            }
         }
         js = "{";
         bool first = true;
