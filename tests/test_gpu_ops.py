@@ -368,6 +368,40 @@ def test_frame_field_limits():
         fbs.grid_build(dev(np.zeros((257, 4, 4, 3), np.uint8)), 4.0, 8.0, 8.0)
 
 
+def test_empty_inputs_rejected():
+    """Empty batches, planes and channel counts are argument errors (FBS_EINVAL), not crashes."""
+    with pytest.raises(fbs.FbsError) as e:
+        fbs.grid_build(dev(np.zeros((0, 8, 8, 3), np.uint8)), 8.0, 4.0, 3.0)
+    assert e.value.code == 1
+    for shape in [(1, 0, 8, 3), (1, 8, 0, 3)]:
+        with pytest.raises(fbs.FbsError):
+            fbs.grid_build(dev(np.zeros(shape, np.uint8)), 8.0, 4.0, 3.0)
+    rgb, t, c = small(K=1)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    with pytest.raises(fbs.FbsError):
+        fbs.solve(g, dev(np.zeros((1, 0, rgb.shape[1], rgb.shape[2]), np.float32)), dev(c), 1.0)  # K = 0
+
+
+@pytest.mark.parametrize("value", [0, 128, 255])
+def test_constant_image(value):
+    """A flat reference: one vertex per σxy cell (plus none in l, u, v), grid bit-exact, and the
+    solve equals the oracle's (the degenerate case where only x/y neighbours exist)."""
+    rgb = np.full((2, 37, 53, 3), value, np.uint8)
+    og = O.build_grid(rgb, 8.0, 4.0, 3.0)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    e = g.export()
+    assert g.M == og.M == 2 * 5 * 7 and np.array_equal(e["keys"], og.keys) and np.array_equal(e["nbr"], og.nbr)
+    rng = np.random.default_rng(value)
+    t = rng.uniform(0, 1, (2, 1, 37, 53)).astype(np.float32)
+    c = rng.uniform(0.1, 1, (2, 37, 53)).astype(np.float32)
+    x = fbs.solve(g, dev(t), dev(c), 3.0, precond="hier", init="hier", mode="tol", tol=1e-6).cpu().numpy()
+    for f in range(2):
+        sol = O.solve_frame(og, f, t[f].reshape(1, -1).astype(float), c[f].ravel().astype(float), 3.0,
+                            O.SolveOptions(precond="hier", init="hier", mode="tol", tol=1e-6))
+        mx, rms = compare_x(x[f].reshape(1, -1), sol.x, t[f].reshape(1, -1).astype(float), c[f].ravel().astype(float))
+        assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
+
+
 def test_launch_counter_and_profile():
     rgb, t, c = small(K=1)
     n0 = fbs.launch_count()
