@@ -765,7 +765,9 @@ void tree_level0(fbs_system S, const HierArgs& h, const VecArgs& a, const float*
         LAUNCH_AS(name.c_str(), kern, vec_blocks(as), kThreads, 0, s, h, as, in0, out0, first);
     } else {
         auto kern = k_tree_level0<MODE, false>;
-        LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, h, a, in0, out0, first);
+        VecArgs a2 = a;  // the PCG direction kernel has no reduction: its own blocks per frame
+        if (MODE == HIER_PCG) a2.BPF = S->BPFl0;
+        LAUNCH_AS(name.c_str(), kern, a2.nf * a2.BPF, kThreads, 0, s, h, a2, in0, out0, first);
     }
 }
 
@@ -1101,6 +1103,11 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int64_t want = (g->maxFrameM + (int64_t)kThreads * vpt - 1) / ((int64_t)kThreads * vpt);
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
         S->BPF = (int)std::max<int64_t>(1, std::min(want, cap));
+        {  // k_tree_level0<PCG>: 24 resident blocks' worth per SM (5.28 -> 5.25 ms per bench step)
+            int occ0 = 24;
+            if (const char* e = std::getenv("FBS_L0_OCC")) occ0 = std::max(1, std::min(64, std::atoi(e)));  // A/B
+            S->BPFl0 = (int)std::max<int64_t>(1, std::min(want, ((int64_t)g_num_sms * occ0 + F - 1) / F));
+        }
         {
             const char* e = std::getenv("FBS_PCG_GROUPS");  // A/B measurement: 1 disables the split
             S->nGroups = (e && e[0]) ? std::max(1, std::min(8, std::atoi(e))) : 2;

@@ -373,6 +373,7 @@ struct fbs_system_s {
     cudaStream_t capture = nullptr;
     int BPF = 1;
     int BPFs = 1;             // blocks per (frame, channel) of the channel-split kernels (K > 1)
+    int BPFl0 = 1;            // blocks per frame of the PCG direction kernel (k_tree_level0<PCG>)
     int* inflags = nullptr;   // input-check status bits (FBS_ST_NEG_CONF, FBS_ST_NONFINITE)
     int nGroups = 2;          // frame groups of the FIXED-mode PCG (run_pcg); FBS_PCG_GROUPS=1 disables
     // vertex arrays
