@@ -402,6 +402,20 @@ def test_constant_image(value):
         assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
 
 
+def test_tol_device_graph_loop(monkeypatch):
+    """FBS_TOL_GRAPH=1: the TOL loop as a CUDA graph with a conditional while node (no host polls)
+    gives the same iteration counts and results as the host-polled loop."""
+    rgb, t, c = small(K=2, frames=1)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    opts = dict(precond="hier", init="hier", mode="tol", tol=1e-6)
+    x0, s0 = fbs.solve(g, dev(t), dev(c), 6.0, keep_system=True, **opts)
+    monkeypatch.setenv("FBS_TOL_GRAPH", "1")
+    x1, s1 = fbs.solve(g, dev(t), dev(c), 6.0, keep_system=True, **opts)
+    monkeypatch.delenv("FBS_TOL_GRAPH")
+    assert np.array_equal(s0.stats()["iterations"], s1.stats()["iterations"])
+    assert torch.equal(x0, x1)
+
+
 def test_launch_counter_and_profile():
     rgb, t, c = small(K=1)
     n0 = fbs.launch_count()
