@@ -1183,8 +1183,13 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             }
             if (g->L > 3) S->ancMult = dalloc<float>(A, (size_t)(g->L - 3) * g->lv[2].M, s);
         }
-        S->BPFs = (int)std::max<int64_t>(
-            1, std::min<int64_t>(S->BPF, ((int64_t)g_num_sms * occ + (int64_t)F * Kc - 1) / ((int64_t)F * Kc)));
+        {  // channel-split kernels: at least vptS vertices per thread (more blocks in flight per SM)
+            int vptS = 4;
+            if (const char* e = std::getenv("FBS_VPT_SPLIT")) vptS = std::max(1, std::min(64, std::atoi(e)));  // A/B
+            const int64_t wantS = (g->maxFrameM + (int64_t)kThreads * vptS - 1) / ((int64_t)kThreads * vptS);
+            S->BPFs = (int)std::max<int64_t>(
+                1, std::min<int64_t>({S->BPF, wantS, ((int64_t)g_num_sms * occ + (int64_t)F * Kc - 1) / ((int64_t)F * Kc)}));
+        }
         S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
         S->counters = dalloc<unsigned>(A, (size_t)2 * F * Kc, s);  // [F][Kc] VecArgs, [Kc][F] HierArgs
         S->counters2 = S->counters + (size_t)F * Kc;
