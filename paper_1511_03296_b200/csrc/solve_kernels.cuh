@@ -93,9 +93,9 @@ __device__ __forceinline__ float apply_A_row(const float* __restrict__ y, const 
 __device__ __forceinline__ float nbr_nsum(const float* __restrict__ n, int v, int4 nb) { return nbr_sum(n, v, nb); }
 
 // ---------------------------------------------------------------- splat  S p
-// Segment sums in fp64 (then rounded to the fp32 vertex vectors).  -DFBS_SPLAT_F32 sums in fp32
-// instead: 197 → 165 µs for the bench batch, parity tests still pass, kept off for accuracy.
-#ifndef FBS_SPLAT_F32
+// Segment sums in fp32 in a fixed order ("fp32 sums in fixed order"); a
+// vertex sums ≤ 64 pixels.  -DFBS_SPLAT_F64 sums in fp64 instead (197 vs 165 µs for the bench batch).
+#ifdef FBS_SPLAT_F64
 using SplatAcc = double;
 #else
 using SplatAcc = float;
