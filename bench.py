@@ -53,6 +53,7 @@ def kernel_bytes(name, M, lv, N):
         "k_grid_neighbours": 24 * M,   # keys 8 + nbr write 16
         "k_splat<true>": 12 * N + 8 * M,  # vid 4 + c 4 + t 4 per px; Sc, b per vertex
         "k_slice": 8 * N,              # vid 4 + x 4 per px
+        "k_slice4": 8 * N,             # the same, 4 px per thread
     }
     return table.get(name)
 

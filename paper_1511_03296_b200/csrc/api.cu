@@ -825,6 +825,17 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
 }
 
 
+// a9: x = Sᵀy; 4 pixels per thread when the frame size and x allow it
+void slice(fbs_grid g, const float* y, int64_t M, int K, int planar, float* x, cudaStream_t s) {
+    const int64_t HW = (int64_t)g->H * g->W;
+    if (HW % 4 == 0 && ((uintptr_t)x & 15) == 0 && g->F <= 65535) {
+        const dim3 grid((unsigned)((HW / 4 + kThreads - 1) / kThreads), (unsigned)g->F);
+        LAUNCH(k_slice4, grid, kThreads, 0, s, g->vid, y, M, K, HW, planar, x);
+    } else {
+        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, y, M, K, g->F, HW, planar, x);
+    }
+}
+
 // q = A d and α (k_spmv2), channel-split
 void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
     const VecArgs as = split_args(S, a);
@@ -1242,7 +1253,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             ysol = yfull;
         }
         // a9: slice
-        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, ysol, M, K, F, (int64_t)g->H * g->W, 1, x);
+        slice(g, ysol, M, K, 1, x, s);
         if (y) LAUNCH(k_export_vk, grid_for((size_t)K * M), kThreads, 0, s, ysol, M, K, y);
     } catch (...) {
         free_all(S->allocs, s);
@@ -1600,7 +1611,7 @@ int fbs_slice(fbs_grid g, const float* y, int K, float* x, fbs_stream stream) {
         if (!g || !y || !x) throw Err(FBS_EINVAL, "null pointer");
         if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
         cudaStream_t s = (cudaStream_t)stream;
-        LAUNCH(k_slice, grid_for(g->N), kThreads, 0, s, g->vid, y, g->M, K, g->F, (int64_t)g->H * g->W, 0, x);
+        slice(g, y, g->M, K, 0, x, s);
     });
 }
 

@@ -623,6 +623,29 @@ __global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ y
     }
 }
 
+// k_slice for HW % 4 == 0 and a 16-byte-aligned output: 4 pixels per thread (one 16-byte vid
+// load, 4 independent gathers, one 16-byte store per channel), the frame from blockIdx.y (no
+// 64-bit division per pixel).
+__global__ void k_slice4(const int* __restrict__ vid, const float* __restrict__ ys, int64_t M, int K, int64_t HW,
+                         int planar, float* __restrict__ out) {
+    pdl_entry();
+    const int f = blockIdx.y;
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (i >= HW) return;
+    const int4 v = __ldcs(reinterpret_cast<const int4*>(vid + (size_t)f * HW + i));
+    for (int k = 0; k < K; ++k) {
+        float4 y;
+        if (planar) {
+            const float* yk = ys + (size_t)k * M;
+            y = make_float4(yk[v.x], yk[v.y], yk[v.z], yk[v.w]);
+        } else {
+            y = make_float4(ys[(size_t)v.x * K + k], ys[(size_t)v.y * K + k], ys[(size_t)v.z * K + k],
+                            ys[(size_t)v.w * K + k]);
+        }
+        __stcs(reinterpret_cast<float4*>(out + ((size_t)f * K + k) * HW + i), y);
+    }
+}
+
 // Alg. 3 line 4-5: e = x̂ − t, c = 2σ² / (σ² + e²)² per pixel (K = 1).
 __global__ void k_gm_weight(const float* __restrict__ x, const float* __restrict__ t, int64_t N, float s2,
                             float* __restrict__ c) {
