@@ -108,7 +108,7 @@ using SplatAcc = float;
 // first channel) go out in one round trip; later channels are prefetched one ahead.
 // WEIGHTED: Sc = S c and b_k = S(c∘t_k) (Eq. quad_min); otherwise out_k = S p_k.
 template <bool WEIGHTED>
-__global__ void __launch_bounds__(256, 6) k_splat(CellGeom g, const int* __restrict__ cellOff,
+__global__ void __launch_bounds__(256, 8) k_splat(CellGeom g, const int* __restrict__ cellOff,
                                                const int* __restrict__ vid, const uint8_t* __restrict__ perm,
                                                const float* __restrict__ c, const float* __restrict__ p, int K,
                                                int64_t M, float* __restrict__ sc_out, float* __restrict__ out,
