@@ -70,7 +70,50 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without CUDA: shard the frames over the ranks (gloo), reduce a fake "
+                         "per-rank time with the max-over-ranks path and print what each rank owns")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        return s_.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec this script as N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1, exactly as the driver would launch it, and pass rank 0's
+    JSON line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world) -> int:
+    """--dry-run: the multi-rank plumbing of the real arm (shard_frames, reduce_max, rank-0 print)
+    over gloo, with rank r reporting a fake device time of 1 + r ms."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    frames = shard_frames(rank, args.frames_per_gpu)
+    ms = reduce_max(1.0 + rank, world)
+    owned = [None] * world
+    if world > 1:
+        dist.all_gather_object(owned, frames)
+    else:
+        owned = [frames]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_requested": args.gpus, "frames": owned,
+                          "max_ms": ms, "config": workload_config(args, world)}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
 
 
 # --------------------------------------------------------------------------- clocks
@@ -178,19 +221,19 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args),
+            "config": workload_config(args, world),
             "cpu_baseline": {"value": value, "unit": "MP/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def workload_config(args):
+def workload_config(args, world=1):
     return {"workload": f"c5_batch: {args.frames_per_gpu} independent {args.width}x{args.height} RGB frames per GPU "
                         f"(300-cell Voronoi + gradients + noise 3, planar depth with 5% outliers), "
                         f"sigma=(8,4,3), lambda=128, Alg.1 x20, hier precond+init, {ITERS} PCG iters, K=1",
             "frames_per_gpu": args.frames_per_gpu, "width": args.width, "height": args.height,
-            "parallelism": f"frames sharded over {args.gpus} rank(s), no collective on the solve path",
+            "parallelism": f"frames sharded over {world} rank(s) (one per GPU), no collective on the solve path",
             "l2": "inputs larger than L2 (rgb+t+c = 11 B/px, 182 MB per GPU-step > 126 MB L2)"}
 
 
@@ -218,12 +261,20 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not (args.impl == "reference" and not args.dry_run):
+        return relaunch(args)  # one process per GPU, as the driver's torchrun launch
+    if world != args.gpus and args.impl != "reference":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks")
+    if args.dry_run:
+        return run_dry(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
     import torch
     import torch.distributed as dist
 
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPU(s)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -539,8 +590,13 @@ def main():
         # the other BASELINE.json configs as specified (grid build + solve [+ backward for configs[3]]),
         # device time per call; TOL-mode solves include the host's active-count polls
         cfg_rows = {}
-        for name in ("c1", "c2", "c3", "c4"):
-            wc = make(name)
+        # configs[2] is run both ways BASELINE.json names: fixed 25 (c3) and to tol 1e-6 (c3_tol)
+        for name, over in (("c1", {}), ("c2", {}), ("c3", {}), ("c3_tol", {"mode": "tol", "max_iters": 5000}),
+                           ("c4", {})):
+            wc = make(name.split("_")[0])
+            if over:
+                import dataclasses
+                wc = dataclasses.replace(wc, **over)
             rgbc, tc, cc = (torch.from_numpy(a_).to(dev) for a_ in (wc.rgb, wc.t, wc.c))
             gc_ = torch.from_numpy(wc.g).to(dev) if wc.g is not None else None
             opts = dict(precond=wc.precond, init=wc.init, mode=wc.mode, tol=wc.tol, max_iters=wc.max_iters)
@@ -621,7 +677,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(args) | {"vertices_per_gpu": M,
+                "config": workload_config(args, world) | {"vertices_per_gpu": M,
                                                    "levels": int(info["levels"])},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "extras": extras,
                 "clocks": clk, "stages_ms_per_step": stages_ms, "pcg_iteration_rate": pcg_iteration_rate,

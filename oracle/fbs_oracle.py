@@ -626,6 +626,13 @@ def solve_frame_lowrank(grid: Grid, f: int, t: np.ndarray, c: np.ndarray, lam: f
 
 
 # ----------------------------------------------------------------------------- domain transform (post-filter)
+def dt_sigmas(sigma_s: float, n_iters: int = 3) -> np.ndarray:
+    """σ_i of pass i = 1..N of the recursive domain transform (reading #28, Gastal & Oliveira
+    2011 as restated in SPEC.md:465-505):  σ_i = σ_s √3 2^(N−i) / √(4^N − 1)."""
+    N = n_iters
+    return np.array([sigma_s * np.sqrt(3.0) * 2.0 ** (N - i) / np.sqrt(4.0 ** N - 1.0) for i in range(1, N + 1)])
+
+
 def dt_filter(signal: np.ndarray, rgb: np.ndarray, sigma_s: float, sigma_r: float, n_iters: int = 3) -> np.ndarray:
     """Edge-aware post-filter of the solver output: the recursive-filter (RF) domain transform of
     Gastal & Oliveira 2011, which the paper cites and applies to every result (PAPER.md:329,
@@ -646,9 +653,7 @@ def dt_filter(signal: np.ndarray, rgb: np.ndarray, sigma_s: float, sigma_r: floa
     dy[1:, :] = np.abs(np.diff(I, axis=0)).sum(axis=2)
     Dx = 1.0 + sigma_s / sigma_r * dx
     Dy = 1.0 + sigma_s / sigma_r * dy
-    N = n_iters
-    for i in range(1, N + 1):
-        sig = sigma_s * np.sqrt(3.0) * 2.0 ** (N - i) / np.sqrt(4.0 ** N - 1.0)
+    for sig in dt_sigmas(sigma_s, n_iters):
         a = np.exp(-np.sqrt(2.0) / sig)
         V = a ** Dx
         for x in range(1, W):

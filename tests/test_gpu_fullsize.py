@@ -1,6 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
-configs[1..3] run whole against the fp64 oracle (each oracle solve takes seconds).  configs[4]
+configs[1..3] run whole against the fp64 oracle in every solver mode BASELINE.json names for them
+(each oracle solve takes seconds to a minute), with the grid compared bit-exactly (keys, vid, m,
+nbr).  configs[4]
 (the bench workload, 8 × 1920×1080) runs as the bench does — all 8 frames in one grid and one
 solve, so the frame-group split of Alg. 1 (4 groups) and of the PCG (2 groups) and the blocks
 per frame are the bench's — and frames 0, 3 and 7 (one from each end and one inside a group)
@@ -8,6 +10,8 @@ are compared with the oracle run on those frames alone: frames are independent s
 (reading #12), so a frame's batched result must match its own solve.  Every frame is checked for
 finite output and the fixed iteration count.
 """
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -40,8 +44,29 @@ def frame_grid_equal(e, og, f_gpu_start, f_gpu_end, HW, f):
     assert np.array_equal(e["vid"][f * HW:(f + 1) * HW] - v0, og.vid)
 
 
-def test_bench_workload_frames_vs_oracle():
-    w = make("c5")  # configs[4]: 8 frames of 1920×1080, hier + hier, fixed 25 iterations
+def compare_fixed_or_tol(x_frame, sol, w, t, c, zc):
+    """north_star's bounds on one frame.  FIXED: reading #29 (the fp32-storage run of the oracle's
+    Alg. 2 is the reference at the few pixels where the fp64 fixed-count iterate is unstable);
+    TOL: the fp64 oracle on every pixel outside zero-confidence components (reading #7)."""
+    HW = t.shape[1]
+    if w.mode == "fixed":
+        unstable, x32 = fixed_count_unstable(sol, w.iters, t, c) if w.K == 1 else (np.zeros(HW, bool), None)
+        assert unstable.sum() <= 1e-5 * HW, unstable.sum()
+        mx, rms = compare_x(x_frame, sol.x, t, c, exclude=zc | unstable)
+        assert mx <= MAX_TOL and rms <= RMS_TOL, (mx, rms)
+        if x32 is not None:
+            mx, rms = compare_x(x_frame, x32[None], t, c, exclude=zc)
+            assert mx <= MAX_TOL and rms <= RMS_TOL, ("fp32-storage reference", mx, rms)
+    else:
+        mx, rms = compare_x(x_frame, sol.x, t, c, exclude=zc)
+        assert mx <= MAX_TOL and rms <= RMS_TOL, (mx, rms)
+
+
+@pytest.mark.parametrize("mode", ["fixed", "tol"])
+def test_bench_workload_frames_vs_oracle(mode):
+    """configs[4] in the bench's launch configuration: fixed 25 iterations (the headline) and run
+    to relative residual 1e-6 ("tol 1e-6 also reported")."""
+    w = dataclasses.replace(make("c5"), mode=mode)  # 8 frames of 1920×1080, hier + hier
     F, HW = w.frames, w.H * w.W
     g = fbs.grid_build(dev(w.rgb), w.sigma_xy, w.sigma_l, w.sigma_uv, n_bistoch=w.n_bistoch)
     x, sysm = fbs.solve(g, dev(w.t), dev(w.c), w.lam, keep_system=True, **gpu_opts(w))
@@ -49,7 +74,10 @@ def test_bench_workload_frames_vs_oracle():
     x = x.cpu().numpy()
     assert np.all(np.isfinite(x))
     st = sysm.stats()
-    assert np.all(st["iterations"] == w.iters) and np.all(st["status"] & ~2 == 0)
+    if mode == "fixed":
+        assert np.all(st["iterations"] == w.iters) and np.all(st["status"] & ~2 == 0)
+    else:
+        assert st["status"] == 0 and np.all(st["iterations"] < w.max_iters)
     e = g.export()
     fo = np.concatenate([[0], np.cumsum(g.info()["frame_vertices"])])
     for f in (0, 3, 7):
@@ -57,42 +85,55 @@ def test_bench_workload_frames_vs_oracle():
                            oracle_opts(w))
         frame_grid_equal(e, og, int(fo[f]), int(fo[f + 1]), HW, f)
         sol = sols[0]
-        assert sol.iterations[0] == w.iters
+        if mode == "fixed":
+            assert sol.iterations[0] == w.iters
         t = w.t[f].reshape(w.K, HW).astype(np.float64)
         c = w.c[f].reshape(HW).astype(np.float64)
-        zc = zero_conf_pixels(sol)
-        # reading #29: at 25 iterations a handful of pixels (isolated low-confidence vertices) sit
-        # on an iterate that any 1e-8 relative perturbation of the vectors moves by ~2.6e-3·range;
-        # there the fp32-storage run of the oracle's Alg. 2 is the reference, elsewhere the fp64
-        # oracle itself
-        unstable, x32 = fixed_count_unstable(sol, w.iters, t, c)
-        assert unstable.sum() <= 1e-5 * HW, unstable.sum()
-        mx, rms = compare_x(x[f].reshape(w.K, HW), sol.x, t, c, exclude=zc | unstable)
-        assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
-        mx, rms = compare_x(x[f].reshape(w.K, HW), x32[None], t, c, exclude=zc)
-        assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
+        compare_fixed_or_tol(x[f].reshape(w.K, HW), sol, w, t, c, zero_conf_pixels(sol))
 
 
-@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
-def test_full_config_vs_oracle(name):
-    w = make(name)
+# Every solver mode BASELINE.json names for configs[1..3], at full size:
+#   configs[1] depth refinement: hier + hier to tol 1e-6 (as specified), and fixed 25;
+#   configs[2] depth SR: fixed 25 and tol 1e-6 (hier + hier, the paper's default), and Jacobi +
+#              flat to tol 1e-6 as the ablation;
+#   configs[3] multichannel: Jacobi + flat and hier + hier, to tol 1e-6, each with the backward.
+FULL_CASES = [
+    ("c2", {}),
+    ("c2", {"mode": "fixed", "iters": 25}),
+    ("c3", {}),
+    ("c3", {"mode": "tol", "max_iters": 5000}),
+    ("c3", {"mode": "tol", "precond": "jacobi", "init": "flat", "max_iters": 5000}),
+    ("c4", {}),
+    ("c4", {"precond": "hier", "init": "hier"}),
+]
+
+
+@pytest.mark.parametrize("name,over", FULL_CASES,
+                         ids=[f"{n}-" + ("-".join(f"{k}={v}" for k, v in o.items()) or "default") for n, o in FULL_CASES])
+def test_full_config_vs_oracle(name, over):
+    w = dataclasses.replace(make(name), **over)
     HW = w.H * w.W
-    g = fbs.grid_build(dev(w.rgb), w.sigma_xy, w.sigma_l, w.sigma_uv, n_bistoch=w.n_bistoch)
+    pyr = w.precond == "hier" or w.init == "hier"
+    g = fbs.grid_build(dev(w.rgb), w.sigma_xy, w.sigma_l, w.sigma_uv, n_bistoch=w.n_bistoch, build_pyramid=pyr)
     t, c = dev(w.t), dev(w.c)
     x, sysm = fbs.solve(g, t, c, w.lam, keep_system=True, **gpu_opts(w))
     x = x.cpu().numpy()
     og, sols = O.solve(w.rgb, w.t, w.c, w.sigma_xy, w.sigma_l, w.sigma_uv, w.lam, oracle_opts(w))
     e = g.export()
-    assert g.M == og.M and np.array_equal(e["keys"], og.keys) and np.array_equal(e["nbr"], og.nbr)
+    # the grid, bit-exact at full size: vertex count, keys, per-pixel vertex ids, counts, neighbours
+    assert g.M == og.M
+    assert np.array_equal(e["keys"], og.keys) and np.array_equal(e["vid"], og.vid)
+    assert np.array_equal(e["m"], og.m) and np.array_equal(e["nbr"], og.nbr)
     sol = sols[0]
     tt = w.t[0].reshape(w.K, HW).astype(np.float64)
     cc = w.c[0].reshape(HW).astype(np.float64)
     zc = zero_conf_pixels(sol)
-    mx, rms = compare_x(x[0].reshape(w.K, HW), sol.x, tt, cc, exclude=zc)
-    assert mx <= MAX_TOL and rms <= RMS_TOL, (mx, rms)
+    compare_fixed_or_tol(x[0].reshape(w.K, HW), sol, w, tt, cc, zc)
     st = sysm.stats()
     if w.mode == "fixed":
         assert np.all(st["iterations"][0] == np.minimum(w.iters, sol.iterations))
+    else:
+        assert st["status"] & 2 == 0, "TOL solve did not converge"
     if w.g is not None:  # configs[3]: the backward pass as well
         dt, dc = sysm.backward(dev(w.g), t, c)
         dt, dc = dt.cpu().numpy(), dc.cpu().numpy()

@@ -45,6 +45,29 @@ def test_gray_yuv(worked):
     assert np.array_equal(Y, 256 * k.astype(np.int64)) and np.all(U == 32768) and np.all(V == 32768)
 
 
+def test_bt601_primaries(worked):
+    """Reading #1 pinned on the channel order: the numerators of pure R, G and B (golden, derived
+    from BT.601's Kr, Kb), and on random colours the oracle's (l, u − 128, v − 128) agree with
+    BT.601 evaluated from its defining constants (Y = Kr R + (1−Kr−Kb) G + Kb B,
+    U = (B − Y)/(2(1 − Kb)), V = (R − Y)/(2(1 − Kr))) to within the 8-bit coefficient rounding
+    (≤ ½/256 per coefficient, × 3 × 255).  An RGB↔BGR swap or a U↔V swap fails both."""
+    ex = worked["bt601_primaries"]
+    for rgb, nums in ex["cases"]:
+        Y, U, V = O.yuv_numerators(np.array([rgb], np.uint8))
+        assert (int(Y[0]), int(U[0]), int(V[0])) == tuple(nums)
+    kr, kb = ex["Kr"], ex["Kb"]
+    px = np.random.default_rng(11).integers(0, 256, (4096, 3)).astype(np.uint8)
+    R, G, B = (px[:, i].astype(np.float64) for i in range(3))
+    Yr = kr * R + (1 - kr - kb) * G + kb * B
+    Ur = (B - Yr) / (2 * (1 - kb))
+    Vr = (R - Yr) / (2 * (1 - kr))
+    Y, U, V = O.yuv_numerators(px)
+    bound = 3 * 255 * 0.5 / 256
+    assert np.abs(Y / 256 - Yr).max() <= bound
+    assert np.abs(U / 256 - 128 - Ur).max() <= bound
+    assert np.abs(V / 256 - 128 - Vr).max() <= bound
+
+
 @pytest.mark.parametrize("sxy,num,den", [(8.0, 1, 8), (7.5, 2, 15), (3.0, 1, 3), (1.0, 1, 1)])
 @pytest.mark.parametrize("sl,suv", [(8.0, 8.0), (4.0, 3.0), (4.0, 4.0), (1.0, 1.0)])
 def test_bins_equal_integer_floor(sxy, num, den, sl, suv):
@@ -395,6 +418,51 @@ def test_hier_4x1_closed_form(worked):
     expect = e0 / dA[0] + ex["w1"] * 2 / (dA[0] + dA[1]) * np.array([1, 1, 0, 0]) \
         + ex["w2"] * 4 / dA.sum() * np.ones(4)
     assert np.allclose(s.Minv(e0), expect, rtol=1e-14)
+
+
+def test_hier_init_4x1_closed_form(worked):
+    """y_hier at the paper's α = 4, β = 0 on the 4×1 line, against the closed
+    form derived by hand in tests/golden (each vertex one pixel: b = c∘t, Sc = c).  Every coarse
+    term is live here, so P(1) multiplied instead of divided, a shifted level index in z_w, a
+    dropped level or swapped numerator/denominator all fail."""
+    ex = worked["hier_init_4x1_line"]
+    rgb = const_image(ex["rgb"], ex["H"], ex["W"])
+    rng = np.random.default_rng(21)
+    c = rng.uniform(0.2, 1.5, 4)
+    t = rng.uniform(-3.0, 5.0, (1, 4))
+    _, s = frame_solve(rgb, t, c, ex["sigma_xy"], ex["sigma_l"], ex["sigma_uv"], 3.0,
+                       precond="jacobi", init="hier", mode="fixed", iters=0)
+    b, Sc = c * t[0], c
+    w1, w2 = ex["w1"], ex["w2"]
+    expect = np.empty(4)
+    for v, (p0, p1) in enumerate(ex["pairs"]):
+        num = b[v] + w1 * (b[p0] + b[p1]) / 2 + w2 * b.sum() / 4
+        den = Sc[v] + w1 * (Sc[p0] + Sc[p1]) / 2 + w2 * Sc.sum() / 4
+        expect[v] = num / den
+    assert np.allclose(s.y0[:, 0], expect, rtol=1e-14, atol=0)
+    assert np.allclose(s.y[:, 0], expect, rtol=1e-14, atol=0)  # 0 PCG iterations
+
+
+def test_diagA_closed_forms(worked):
+    """diag(A): (a) the 2-vertex worked example's diagonal [2, 2]; (b) it equals
+    the diagonal of the explicitly assembled sparse A; (c) at Alg. 1's fixed point n∘B̄n = m it
+    equals λ n_v Σ_{u∈N(v)} n_u + Sc_v (the edge-weight form — an independent route through the
+    neighbour lists), up to λ × the bistochastization residual."""
+    ex = worked["two_vertex_line"]
+    rgb = const_image(ex["rgb"], ex["H"], ex["W"])
+    _, s = frame_solve(rgb, [ex["t"]], ex["c"], ex["sigma_xy"], ex["sigma_l"], ex["sigma_uv"], ex["lam"])
+    assert np.allclose(s.sys.diagA, np.diag(ex["A"]), rtol=1e-12)
+    rgb, t, c, sxy, sl, suv = tiny_case(seed=5)
+    lam = 7.0
+    grid = O.build_grid(rgb, sxy, sl, suv)
+    s = O.solve_frame(grid, 0, t, c, lam, O.SolveOptions(mode="fixed", iters=0, n_bistoch=80))
+    assert np.allclose(s.sys.diagA, s.sys.A.diagonal(), rtol=1e-13, atol=1e-13)
+    nsum = np.array([sum(s.n[u] for u in row if u >= 0) for row in s.nbr])
+    Sc_direct = np.bincount(s.vid, weights=c, minlength=grid.M)
+    closed = lam * s.n * nsum + Sc_direct
+    assert s.bistoch_residual < 1e-12
+    assert np.abs(s.sys.diagA - closed).max() <= 1e-9 * lam * s.m.max()
+    assert np.sum(nsum > 0) > 0.5 * grid.M  # most vertices have neighbours: the test has teeth
 
 
 def test_hier_degenerations():

@@ -1,5 +1,6 @@
 """Oracle pins for the domain-transform post-filter (reading #28)."""
 import numpy as np
+import pytest
 import scipy.linalg as sla
 
 import oracle as O
@@ -67,3 +68,30 @@ def test_edge_preserving():
     # and without the guide edge the step is smoothed out
     flat = O.dt_filter(f, np.zeros_like(rgb), 8.0, 4.0)
     assert abs(flat[0, H // 2, W // 2 - 2] - 50.0) < 30.0 and flat[0, H // 2, W // 2 - 2] > 5.0
+
+
+def test_sigma_schedule_sums_to_sigma_s():
+    """The schedule's defining property (Gastal & Oliveira 2011, reading #28): the N passes'
+    variances add up to the requested σ_s² (Σ σ_i² = σ_s²), each pass halves the previous
+    pass's σ (the widest kernel first)."""
+    for ss, N in ((8.0, 3), (30.0, 3), (5.0, 1), (12.0, 5)):
+        sig = O.dt_sigmas(ss, N)
+        assert len(sig) == N
+        assert np.sum(sig ** 2) == pytest.approx(ss * ss, rel=1e-12)
+        assert np.allclose(sig[:-1] / sig[1:], 2.0, rtol=1e-12)
+
+
+def test_impulse_response_variance_on_flat_guide():
+    """Behavioural pin of the whole filter on a flat guide (d ≡ 1): each pass's causal +
+    anticausal recursion has an impulse response of variance 2a/(1−a)² ≈ σ_i² (a = e^{−√2/σ_i}),
+    so the filtered impulse keeps unit mass and its variance along x is ≈ σ_s² (within 1.5 % for
+    σ_s ≥ 8) — a wrong normalisation or base of the schedule fails."""
+    W = 1601
+    for ss in (8.0, 30.0):
+        f = np.zeros((1, 1, W))
+        f[0, 0, W // 2] = 1.0
+        out = O.dt_filter(f, np.zeros((1, W, 3), np.uint8), ss, 10.0)[0, 0]
+        xs = np.arange(W) - W // 2
+        assert out.sum() == pytest.approx(1.0, abs=1e-9)
+        var = float(np.sum(out * xs * xs))
+        assert var == pytest.approx(ss * ss, rel=0.015)
