@@ -51,7 +51,8 @@ def build(force: bool = False, verbose: bool = False, out: str = None) -> str:
     target = out or LIB
     if not force and out is None and not stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, "-I", INCLUDE, os.path.join(CSRC, "api.cu"), "-o", target + ".tmp"]
+    extra = os.environ.get("FBS_NVCC_DEFS", "").split()  # A/B builds: e.g. "-DFBS_SP_CHUNK=512"
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, "-I", INCLUDE, os.path.join(CSRC, "api.cu"), "-o", target + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)

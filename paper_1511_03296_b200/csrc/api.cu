@@ -148,6 +148,11 @@ T* dalloc(AllocList& list, size_t count, cudaStream_t s) {
     if (list.al.alloc) {
         p = list.al.alloc(count * sizeof(T), list.al.ctx, reinterpret_cast<fbs_stream>(s));
         if (!p) throw Err(FBS_ENOMEM, "caller allocator returned NULL");
+        // vector loads (int4 / float4) and cp.async.bulk copies need 16-byte-aligned buffers (fbs.h)
+        if (reinterpret_cast<uintptr_t>(p) & 15) {
+            list.al.free(p, list.al.ctx, reinterpret_cast<fbs_stream>(s));
+            throw Err(FBS_EINVAL, "caller allocator returned a pointer that is not 16-byte aligned");
+        }
     } else {
         ck(cudaMallocAsync(&p, count * sizeof(T), s), "cudaMallocAsync");
     }
@@ -828,7 +833,7 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
 // a9: x = Sᵀy; 4 pixels per thread when the frame size and x allow it
 void slice(fbs_grid g, const float* y, int64_t M, int K, int planar, float* x, cudaStream_t s) {
     const int64_t HW = (int64_t)g->H * g->W;
-    if (HW % 4 == 0 && ((uintptr_t)x & 15) == 0 && g->F <= 65535) {
+    if (HW % 4 == 0 && ((uintptr_t)x & 15) == 0 && ((uintptr_t)g->vid & 15) == 0 && g->F <= 65535) {
         const dim3 grid((unsigned)((HW / 4 + kThreads - 1) / kThreads), (unsigned)g->F);
         LAUNCH(k_slice4, grid, kThreads, 0, s, g->vid, y, M, K, HW, planar, x);
     } else {

@@ -102,7 +102,8 @@ using SplatAcc = float;
 #endif
 // One warp per σxy cell.  The grid build stored each cell's pixels in sorted (code, pixel) order
 // (perm), so the pixels of one vertex are consecutive: each vertex sum is a warp segmented scan
-// in fp64 over the two 32-pixel halves, the halves added in fixed order — deterministic.  The
+// (SplatAcc: fp32, or fp64 with -DFBS_SPLAT_F64) over the two 32-pixel halves, the halves added
+// in fixed order — deterministic.  The
 // tail lane of each segment writes the vertex sum; the one vertex that may span the halves gets
 // half 0's partial (lane 31) carried into half 1's sum.  All of a pixel's loads (vid, c, the
 // first channel) go out in one round trip; later channels are prefetched one ahead.
@@ -600,6 +601,7 @@ __global__ void __launch_bounds__(256) k_spmv2_split(VecArgs a) {
 // retires itself at convergence, breakdown or max_iters); `it` bounds it defensively.
 __global__ void k_tol_cond(cudaGraphConditionalHandle h, const int* __restrict__ n_active, int* __restrict__ it,
                            int max_body) {
+    pdl_entry();  // launched with PDL like every kernel: wait for the iteration's last atomicSub
     if (threadIdx.x == 0) {
         const int i = ++*it;
         cudaGraphSetConditional(h, (*n_active > 0 && i < max_body) ? 1u : 0u);

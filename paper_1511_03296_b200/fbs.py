@@ -117,6 +117,24 @@ def _dev_tensor(x: torch.Tensor, dtype: torch.dtype, name: str, ndim: int) -> to
     return x.contiguous()
 
 
+def _out_tensor(out: Optional[torch.Tensor], like: torch.Tensor, name: str = "out") -> torch.Tensor:
+    """A caller-supplied output buffer must be exactly what the kernels write: CUDA float32,
+    contiguous, the shape of `like`, on `like`'s device (the C side cannot check any of this)."""
+    if out is None:
+        return torch.empty_like(like)
+    if not isinstance(out, torch.Tensor) or not out.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if out.dtype != torch.float32:
+        raise TypeError(f"{name} must be torch.float32, got {out.dtype}")
+    if tuple(out.shape) != tuple(like.shape):
+        raise ValueError(f"{name} must have shape {tuple(like.shape)}, got {tuple(out.shape)}")
+    if not out.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if out.device != like.device:
+        raise ValueError(f"{name} is on {out.device}, the inputs on {like.device}")
+    return out
+
+
 def launch_count() -> int:
     """Kernels launched by libfbs.so in this process (monotone)."""
     return int(_lib.fbs_launch_count())
@@ -299,7 +317,7 @@ def solve(grid: Grid, t: torch.Tensor, c: torch.Tensor, lam: float, want_y: bool
     F, K, H, W = t.shape
     if (F, H, W) != (grid.frames, grid.H, grid.W) or tuple(c.shape) != (F, H, W):
         raise ValueError("t/c shapes do not match the grid")
-    x = torch.empty_like(t) if out is None else out
+    x = _out_tensor(out, t)
     y = torch.empty((grid.M, K), dtype=torch.float32, device=t.device) if want_y else None
     o = make_opts(**opts)
     h = C.c_void_p()
@@ -322,7 +340,7 @@ def solve_robust(grid: Grid, t: torch.Tensor, c_init: torch.Tensor, lam: float, 
     F, K, H, W = t.shape
     if (F, H, W) != (grid.frames, grid.H, grid.W) or tuple(c_init.shape) != (F, H, W):
         raise ValueError("t/c_init shapes do not match the grid")
-    x = torch.empty_like(t) if out is None else out
+    x = _out_tensor(out, t)
     w = torch.empty_like(c_init) if want_weights else None
     o = make_opts(**opts)
     _check(_lib.fbs_solve_robust(grid.handle, _ptr(t), K, _ptr(c_init), float(lam), C.byref(o), float(sigma_gm),
@@ -341,7 +359,7 @@ def dt_filter(rgb: torch.Tensor, x: torch.Tensor, sigma_s: float, sigma_r: float
     F, K, H, W = x.shape
     if tuple(rgb.shape) != (F, H, W, 3):
         raise ValueError("rgb must be [F][H][W][3] matching x")
-    y = torch.empty_like(x) if out is None else out
+    y = _out_tensor(out, x)
     _check(_lib.fbs_dt_filter(_ptr(rgb), F, H, W, _ptr(x), K, float(sigma_s), float(sigma_r), int(n_iters), _ptr(y),
                               _stream(stream)))
     return y
@@ -371,16 +389,17 @@ def blur(grid: Grid, v: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
-_torch_alloc_refs = None  # keeps the ctypes callbacks alive while registered
+# Every (callbacks, Allocator) pair ever registered stays alive for the life of the process:
+# handles copy the allocator's function pointers when they are created and call them again when
+# destroyed, possibly after the allocator was replaced or disabled.
+_torch_alloc_refs = []
 
 
 def use_torch_allocator(enable: bool = True):
     """Route the device buffers of handles created from now on through PyTorch's caching
     allocator (stream-ordered on the handle's stream); False restores cudaMallocAsync."""
-    global _torch_alloc_refs
     if not enable:
         _check(_lib.fbs_set_allocator(None))
-        _torch_alloc_refs = None
         return
 
     def _alloc(nbytes, ctx, stream):
@@ -395,8 +414,8 @@ def use_torch_allocator(enable: bool = True):
 
     refs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
     a = Allocator(refs[0], refs[1], None)
+    _torch_alloc_refs.append((refs, a))
     _check(_lib.fbs_set_allocator(C.byref(a)))
-    _torch_alloc_refs = (refs, a)
 
 
 def header_symbols():

@@ -260,6 +260,51 @@ def test_torch_caching_allocator():
     assert torch.cuda.memory_allocated() <= before + 4096
 
 
+def test_allocator_callbacks_outlive_replacement():
+    """A handle created under one registered allocator is destroyed after that allocator was
+    replaced and then disabled: its callbacks must still be alive (fbs.py keeps every registered
+    pair), so close() returns the buffers instead of jumping into a freed ctypes thunk."""
+    rgb, t, c = small(K=1)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    fbs.use_torch_allocator(True)
+    try:
+        g1 = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+        fbs.use_torch_allocator(True)  # a second registration replaces the first
+        g2 = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    finally:
+        fbs.use_torch_allocator(False)
+    import gc
+    gc.collect()
+    x = fbs.solve(g1, dev(t), dev(c), 5.0, mode="fixed", iters=5)
+    g1.close()
+    g2.close()
+    del x
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() <= before + 4096
+
+
+def test_out_buffers_validated():
+    """A caller-supplied out= of the wrong shape, dtype, layout or device is rejected before any
+    kernel writes through it."""
+    rgb, t, c = small(K=2)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    T, Cc = dev(t), dev(c)
+    good = torch.empty_like(T)
+    fbs.solve(g, T, Cc, 5.0, mode="fixed", iters=3, out=good)
+    for bad, exc in ((torch.empty(T.shape[0], 1, *T.shape[2:], device="cuda"), ValueError),
+                     (torch.empty_like(T, dtype=torch.float64), TypeError),
+                     (torch.empty(T.shape[::-1], device="cuda").permute(3, 2, 1, 0), ValueError),
+                     (torch.empty_like(T, device="cpu"), TypeError)):
+        with pytest.raises(exc):
+            fbs.solve(g, T, Cc, 5.0, mode="fixed", iters=3, out=bad)
+        with pytest.raises(exc):
+            fbs.dt_filter(dev(rgb), T, 8.0, 8.0, out=bad)
+    T1 = T[:, :1].contiguous()
+    with pytest.raises(ValueError):
+        fbs.solve_robust(g, T1, Cc, 5.0, 10.0, 1, mode="fixed", iters=3, out=torch.empty_like(T))
+
+
 def test_zero_confidence_and_constant_target():
     rgb, t, c = small(K=2)
     g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
