@@ -587,6 +587,22 @@ def main():
         lr_r_ms = dev_ms(lambda: fbs.solve(g4, t4r, c4, w4.lam, precond="hier", init="hier", mode="tol",
                                            tol=1e-6, lowrank_eps=0.01))
         g4.close()
+        # the reduction at scale: 2 frames of the workload with 21 channels mixed from 4 planar maps,
+        # hier+hier fixed 25 — the full solve's channel-split kernels scale with K here, the reduced
+        # one solves t_f ≈ 4 live channels (Supp. §4)
+        w2 = make("c5", frames=2, W=args.width, H=args.height)
+        rng2 = np.random.default_rng(22)
+        maps = np.stack([w2.t[:, 0], np.clip(w2.t[:, 0] * 0.5 + 40, 0, 255), 255 - w2.t[:, 0],
+                         rng2.uniform(0, 1, w2.t[:, 0].shape).astype(np.float32) * 10], axis=1)
+        mix2 = rng2.uniform(0, 1, (21, 4)).astype(np.float32)
+        t21 = torch.from_numpy(np.ascontiguousarray(np.einsum("kj,fjhw->fkhw", mix2, maps))).to(dev)
+        rgb2, c2 = torch.from_numpy(w2.rgb).to(dev), torch.from_numpy(w2.c).to(dev)
+        g2 = fbs.grid_build(rgb2, *SIGMAS, n_bistoch=20)
+        big_full_ms = dev_ms(lambda: fbs.solve(g2, t21, c2, LAM, precond="hier", init="hier", mode="fixed", iters=ITERS))
+        big_lr_ms = dev_ms(lambda: fbs.solve(g2, t21, c2, LAM, precond="hier", init="hier", mode="fixed", iters=ITERS,
+                                             lowrank_eps=0.01))
+        g2.close()
+        del t21
         # the other BASELINE.json configs as specified (grid build + solve [+ backward for configs[3]]),
         # device time per call; TOL-mode solves include the host's active-count polls
         cfg_rows = {}
@@ -653,6 +669,9 @@ def main():
                   "configs3_full_solve_ms": full_ms, "configs3_lowrank_solve_ms": lr_ms,
                   "rank4_full_solve_ms": full_r_ms, "rank4_lowrank_solve_ms": lr_r_ms,
                   "rank4": "configs[3]'s grid with 21 channels mixed from 4 of its target maps: full vs eps = 0.01",
+                  "rank4_2frames_full_solve_ms": big_full_ms, "rank4_2frames_lowrank_solve_ms": big_lr_ms,
+                  "rank4_2frames": f"2 workload frames ({args.width}x{args.height}), 21 channels mixed from 4 maps, "
+                                   "hier+hier fixed 25: full vs eps = 0.01 (solve only)",
                   "lowrank": "configs[3] 500x375, K = 21, hier+hier to tol 1e-6: full vs eps = 0.01 (Supp. §4)"}
 
     # ---- CPU baseline: the oracle as it stands, one frame, host cores (rank 0, N = 1 only)

@@ -734,15 +734,16 @@ int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
 
 // P of the level-0 input in0 [C][M0] to tree-ordered level 1 + prefix scan (k_tree_lift).
 // PCG and hierarchical init with K > 1 channels: channel-split kernels (one channel per block group).
+// active: PCG mode, the per-(frame, channel) flags of the running solve (inactive channels skip)
 template <int MODE>
-void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s) {
+void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s, const int* active = nullptr) {
     static const std::string name = std::string("k_tree_lift<") + mode_name(MODE) + ">";
     if ((MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2)) {
         auto kern = k_tree_lift<MODE, true>;
-        LAUNCH_AS(name.c_str(), kern, h.nt * h.C, kScanTile, 0, s, h, in0);
+        LAUNCH_AS(name.c_str(), kern, h.nt * h.C, kScanTile, 0, s, h, in0, active);
     } else {
         auto kern = k_tree_lift<MODE, false>;
-        LAUNCH_AS(name.c_str(), kern, h.nt, kScanTile, 0, s, h, in0);
+        LAUNCH_AS(name.c_str(), kern, h.nt, kScanTile, 0, s, h, in0, active);
     }
 }
 
@@ -794,7 +795,7 @@ void hier_level0(fbs_system S, const VecArgs& a, cudaStream_t s) {
 
 // s = M⁻¹_hier r and d = s + βd after the level-0 kernel (Alg. 2 lines 10-14)
 void hier_precond_direction(fbs_system S, const VecArgs& a, const HierArgs& h, int first, cudaStream_t s) {
-    tree_lift<HIER_PCG>(S, h, S->w0, s);
+    tree_lift<HIER_PCG>(S, h, S->w0, s, a.sc_.active);
     tree_coarse<HIER_PCG>(S, h, a, first, s);
     tree_level0<HIER_PCG>(S, h, a, nullptr, nullptr, first, s);
 }
@@ -807,7 +808,7 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     a.nf = nf;
     a.frameOff += f0;
     a.counters += (size_t)f0 * K;
-    a.partial += (size_t)f0 * S->BPF * 2 * K;
+    a.partial += (size_t)f0 * std::max(S->BPF, S->BPFk) * 2 * K;
     PcgScalars& q = a.sc_;
     q.rho += f0 * K;
     q.alpha += f0 * K;
@@ -820,6 +821,7 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     q.status += f0 * K;
     const int t0 = g->tree.tileFrameOffH.empty() ? 0 : g->tree.tileFrameOffH[f0];
     h.nt = g->tree.tileFrameOffH.empty() ? 0 : g->tree.tileFrameOffH[f0 + nf] - t0;
+    h.f0 = f0;
     h.lvFrameOff += f0;  // [L][F+1] row-major: k·(F+1) + f0 + f
     h.frameLevels += f0;
     h.tileFrameOff += f0;  // tile ids stay global (tileFrameOff[f] − tileFrameOff[0] is group-local)
@@ -841,8 +843,22 @@ void slice(fbs_grid g, const float* y, int64_t M, int K, int planar, float* x, c
     }
 }
 
-// q = A d and α (k_spmv2), channel-split
+// q = A d and α: k_spmv2 (K = 1), k_spmv_kjoint / k_spmv2_split (K > 1)
+// K > 1: the channel-split kernel (default) or, with FBS_SPMV_K=joint, the channel-joint one
+// (one nbr read per vertex for all channels; 89 vs 19 µs per launch on configs[3])
+bool spmv_kjoint() {
+    const char* e = std::getenv("FBS_SPMV_K");
+    return e && std::strcmp(e, "joint") == 0;
+}
+VecArgs with_bpf(VecArgs a, int bpf) {
+    a.BPF = bpf;
+    return a;
+}
 void spmv(fbs_system S, const VecArgs& a, cudaStream_t s) {
+    if (a.K > 1 && spmv_kjoint()) {
+        LAUNCH(k_spmv_kjoint, a.nf * S->BPFk, kThreads, 0, s, a.BPF == S->BPFk ? a : with_bpf(a, S->BPFk));
+        return;
+    }
     const VecArgs as = split_args(S, a);
     auto kern = as.ksplit ? k_spmv2_split : k_spmv2;
     LAUNCH_AS("k_spmv2", kern, vec_blocks(as), kThreads, 0, s, as);
@@ -1153,14 +1169,10 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             zero_words(ctr, F * sizeof(unsigned), s);
             LAUNCH(k_gram, F * bpfG, 256, 0, s, bIn, M, K, g->frameOff, bpfG, part, ctr, G);
             LAUNCH(k_pchol, F, 64, 0, s, G, K, o.lowrank_eps, tF, lrRt, T);
-            PinnedBlock rb = pinned_get(F * sizeof(int));
-            copy_words(tF, rb.p, F * sizeof(int), s);
-            ck(cudaStreamSynchronize(s), "sync");
-            std::vector<int> tH(static_cast<int*>(rb.p), static_cast<int*>(rb.p) + F);
-            pinned_put(rb, s);
-            Kc = 1;
-            for (int f = 0; f < F; ++f) Kc = std::max(Kc, tH[f]);
-            S->lr_rank.assign(tH.begin(), tH.end());
+            // no host synchronisation: the reduced solve carries K channels; those at or above a
+            // frame's kept rank t_f get zero right-hand sides (zero columns of T), so they are
+            // converged at iteration 0 and every PCG kernel skips them (per-(frame, channel) flags)
+            S->lr_rank = tF;
             S->b = dalloc<float>(A, (size_t)Kc * M, s);
             LAUNCH(k_reduce_rhs, F * S->BPF, kThreads, 0, s, bIn, M, K, Kc, g->frameOff, S->BPF, T, S->b);
         } else {
@@ -1206,7 +1218,11 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             S->BPFs = (int)std::max<int64_t>(
                 1, std::min<int64_t>({S->BPF, wantS, ((int64_t)g_num_sms * occ + (int64_t)F * Kc - 1) / ((int64_t)F * Kc)}));
         }
-        S->partial = dalloc<double>(A, (size_t)F * S->BPF * 2 * Kc, s);
+        // channel-joint SpMV (K > 1): a warp per vertex, ≥ 4 vertices per warp, within the
+        // partials' [F][BPF] capacity
+        S->BPFk = (int)std::max<int64_t>(
+            1, std::min<int64_t>(((int64_t)g_num_sms * occ + F - 1) / F, (g->maxFrameM + 31) / 32));
+        S->partial = dalloc<double>(A, (size_t)F * std::max(S->BPF, S->BPFk) * 2 * Kc, s);
         S->counters = dalloc<unsigned>(A, (size_t)2 * F * Kc, s);  // [F][Kc] VecArgs, [Kc][F] HierArgs
         S->counters2 = S->counters + (size_t)F * Kc;
         zero_words(S->counters, (size_t)2 * F * Kc * sizeof(unsigned), s);

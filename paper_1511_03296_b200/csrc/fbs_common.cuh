@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <climits>
 
 #include <atomic>
 #include <cuda/atomic>
@@ -282,6 +283,7 @@ struct HierArgs {
                             // and per-tile pointers shifted to the group, api.cu)
     int L;                  // levels incl. base (max over frames)
     int F;
+    int f0;                 // first frame of this launch's frame group (tileFrame holds global frames)
     int C;                  // channels carried through the pyramid
     const int* frameLevels;
     const int* lvFrameOff;  // [L][F+1] per-level frame vertex offsets (tree order keeps frames)
@@ -374,6 +376,7 @@ struct fbs_system_s {
     int BPF = 1;
     int BPFs = 1;             // blocks per (frame, channel) of the channel-split kernels (K > 1)
     int BPFl0 = 1;            // blocks per frame of the PCG direction kernel (k_tree_level0<PCG>)
+    int BPFk = 1;             // blocks per frame of the channel-joint SpMV (k_spmv_kjoint, K > 1)
     int* inflags = nullptr;   // input-check status bits (FBS_ST_NEG_CONF, FBS_ST_NONFINITE)
     int nGroups = 2;          // frame groups of the FIXED-mode PCG (run_pcg); FBS_PCG_GROUPS=1 disables
     // vertex arrays
@@ -406,6 +409,6 @@ struct fbs_system_s {
     bool useHierP = false;
     fbs::HierArgs hP{};
     bool has_backward = false;
-    std::vector<int> lr_rank;  // low-rank solves: kept rank t_f per frame
+    int* lr_rank = nullptr;    // low-rank solves: kept rank t_f per frame (device)
     fbs::AllocList allocs;
 };

@@ -528,6 +528,96 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
     }
 }
 
+// q_k = A d_k for all K channels of a frame with ONE read of the neighbour structure per vertex
+// (north_star: "K-channel right-hand sides are solved jointly, sharing one neighbour-index
+// read"): a warp per vertex, a lane per channel (k = lane, lane + 32).  The warp's 16-byte nbr
+// and Sc loads are one broadcast transaction; each lane gathers its own channel's (d, n).  dᵀq_k
+// partials: per lane in registers, then a fixed-order sum over the block's warps (deterministic);
+// the last block of the frame finishes every channel's α as k_spmv2 does.
+__global__ void __launch_bounds__(256) k_spmv_kjoint(VecArgs a) {
+    pdl_entry();
+    __shared__ double sdq[kThreads / 32][kMaxK];
+    __shared__ double shd[32];
+    __shared__ int sflag;
+    const int f = blockIdx.x / a.BPF, j = blockIdx.x % a.BPF;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int WPB = kThreads / 32;
+    double dq[2] = {0.0, 0.0};
+    bool act[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int k = lane + 32 * h;
+        act[h] = k < a.K && a.sc_.active[f * a.K + k];
+    }
+    for (int v = v0 + j * WPB + warp; v < v1; v += a.BPF * WPB) {
+        const int4 nb = __ldcs(a.nbr + v);  // the same address in every lane: one transaction
+        const float scv = __ldcs(a.sc + v);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!act[h]) continue;
+            const int k = lane + 32 * h;
+            const float2* dn = a.dn + (size_t)k * a.ldn;
+            const float2 me = dn[v];
+            float acc = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int o = near_off(nb, e);
+                if (o) {
+                    const float2 u = __ldg(dn + v + o);
+                    acc += u.y * (me.x - u.x);
+                }
+            }
+            if (nb.z) {
+                const float2 u = __ldg(dn + v + nb.z);
+                acc += u.y * (me.x - u.x);
+            }
+            if (nb.w) {
+                const float2 u = __ldg(dn + v + nb.w);
+                acc += u.y * (me.x - u.x);
+            }
+            const float q = a.lam * me.y * acc + scv * me.x;
+            a.q[(size_t)k * a.M + v] = q;
+            dq[h] += (double)me.x * (double)q;
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        if (lane + 32 * h < a.K) sdq[warp][lane + 32 * h] = dq[h];
+    __syncthreads();
+    for (int k = threadIdx.x; k < a.K; k += blockDim.x) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < WPB; ++w) t += sdq[w][k];
+        a.partial[((size_t)f * a.BPF + j) * 2 * a.K + 2 * k] = t;
+    }
+    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
+        for (int k = 0; k < a.K; ++k) {
+            const int fk = f * a.K + k;
+            if (!a.sc_.active[fk]) {
+                if (threadIdx.x == 0) a.sc_.xalpha[fk] = 0.0;
+                continue;
+            }
+            double DQ = 0.0;
+            for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
+                DQ += __ldcg(a.partial + ((size_t)f * a.BPF + jj) * 2 * a.K + 2 * k);
+            DQ = block_sum(DQ, shd);
+            if (threadIdx.x == 0) {
+                if (DQ <= 0.0) {
+                    a.sc_.active[fk] = 0;
+                    a.sc_.alpha[fk] = 0.0;
+                    a.sc_.xalpha[fk] = 0.0;
+                    atomicOr(a.sc_.status + fk, FBS_ST_BREAKDOWN);
+                    atomicSub(a.sc_.n_active, 1);
+                } else {
+                    a.sc_.alpha[fk] = a.sc_.rho[fk] / DQ;
+                    a.sc_.xalpha[fk] = a.sc_.alpha[fk];
+                }
+            }
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_spmv2_split(VecArgs a) {
     pdl_entry();
     __shared__ double shd[32];

@@ -281,7 +281,8 @@ __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*
 
 // PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
 template <int MODE, bool KS = false>
-__global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0) {
+__global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0,
+                                                       const int* __restrict__ active) {
     pdl_entry();
     __shared__ float stage[kScanTile / 32][kLiftStage];
     __shared__ double shs[32];
@@ -297,6 +298,8 @@ __global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float
     const int qa = h.csT[wa], qb = h.csT[wb];
     const int myLo = valid ? h.csT[i] : 0, myHi = valid ? h.csT[i + 1] : 0;
     for (int c = cB; c < cE; ++c) {
+        // PCG: a (frame, channel) that has stopped needs no lift (the coarse and level-0 passes skip it)
+        if (MODE == HIER_PCG && active && !active[(h.tileFrame[t] - h.f0) * h.C + c]) continue;
         const float* src = in0 + (size_t)c * h.M0;
         float acc = 0.f;
         for (int qc = qa; qc < qb; qc += kLiftStage) {

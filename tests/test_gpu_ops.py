@@ -337,6 +337,28 @@ def test_many_channels_k64():
     assert mx <= MAX_TOL and rms <= RMS_TOL
 
 
+@pytest.mark.parametrize("pc", ["hier+hier", "jacobi+flat"])
+def test_channel_joint_spmv(monkeypatch, pc):
+    """The channel-joint SpMV (FBS_SPMV_K=joint: one neighbour-structure read per vertex for all K
+    channels, north_star) gives the oracle's solution like the default channel-split kernel."""
+    precond, init = pc.split("+")
+    rgb, t, c = small(K=5, frames=2, W=50, H=37, cells=6)
+    og = O.build_grid(rgb, 8.0, 4.0, 3.0)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    monkeypatch.setenv("FBS_SPMV_K", "joint")
+    l0 = fbs.launch_count()
+    fbs.profile_reset()
+    fbs.profile_enable(True)
+    x = fbs.solve(g, dev(t), dev(c), 7.0, precond=precond, init=init, mode="fixed", iters=20).cpu().numpy()
+    fbs.profile_enable(False)
+    assert "k_spmv_kjoint" in fbs.profile_report() and fbs.launch_count() > l0
+    for f in range(2):
+        sol = O.solve_frame(og, f, t[f].reshape(5, -1).astype(float), c[f].ravel().astype(float), 7.0,
+                            O.SolveOptions(precond=precond, init=init, mode="fixed", iters=20))
+        mx, rms = compare_x(x[f].reshape(5, -1), sol.x, t[f].reshape(5, -1).astype(float), c[f].ravel().astype(float))
+        assert mx <= MAX_TOL and rms <= RMS_TOL, (f, mx, rms)
+
+
 def test_many_frames():
     rgb, t, c = small(K=1, frames=17, W=24, H=16, cells=4)
     og = O.build_grid(rgb, 8.0, 4.0, 3.0)
