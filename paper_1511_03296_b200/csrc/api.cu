@@ -50,6 +50,45 @@ void ck(cudaError_t e, const char* what) {
     }
 }
 
+// PDL is used only between BACK-TO-BACK kernels of the library on a stream: after any other
+// operation on the stream (allocation, free, copy, event record/wait, or the caller's work before
+// an API call) the next launch is fully serialised.  A programmatic edge across an intervening
+// stream operation is not ordered after the kernel before it (measured: a grid build with a
+// stream-ordered allocation between two PDL kernels read stale data), so pdl_break marks the
+// stream and launch_pdl consumes the mark.
+thread_local std::vector<cudaStream_t> t_pdl_broken;
+int pdl_break_mask() {  // DEBUG A/B: which operations break the PDL chain (bit 0 alloc, 1 free, 2 copy/event, 3 entry)
+    static const int m = [] {
+        const char* e = std::getenv("FBS_PDL_BREAK");
+        return e ? std::atoi(e) : 63;
+    }();
+    return m;
+}
+void pdl_break(cudaStream_t s, int kind);
+void pdl_break(cudaStream_t s) { pdl_break(s, 4); }
+void pdl_break(cudaStream_t s, int kind) {
+    if (!(pdl_break_mask() & kind)) return;
+    if (std::find(t_pdl_broken.begin(), t_pdl_broken.end(), s) == t_pdl_broken.end()) t_pdl_broken.push_back(s);
+}
+bool pdl_take(cudaStream_t s) {
+    auto it = std::find(t_pdl_broken.begin(), t_pdl_broken.end(), s);
+    if (it == t_pdl_broken.end()) return true;
+    t_pdl_broken.erase(it);
+    return false;
+}
+cudaError_t memcpy_async(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    pdl_break(s);
+    return cudaMemcpyAsync(dst, src, bytes, kind, s);
+}
+cudaError_t event_record(cudaEvent_t e, cudaStream_t s) {
+    pdl_break(s);
+    return cudaEventRecord(e, s);
+}
+cudaError_t stream_wait(cudaStream_t s, cudaEvent_t e) {
+    pdl_break(s);
+    return cudaStreamWaitEvent(s, e, 0);
+}
+
 // ---- per-kernel event timing (fbs_profile_*)
 struct ProfRec {
     const char* name;
@@ -79,7 +118,7 @@ struct ProfScope {
         if (!g_prof_on.load(std::memory_order_relaxed)) return;
         std::lock_guard<std::mutex> lk(g_prof_mu);
         ProfRec r{name, ev_get(), ev_get(), st};
-        ck(cudaEventRecord(r.a, s), "cudaEventRecord");
+        ck(cudaEventRecord(r.a, s), "cudaEventRecord");  // timing events keep the PDL chain (as unprofiled)
         g_prof.push_back(r);
         idx = (int)g_prof.size() - 1;
     }
@@ -100,6 +139,16 @@ bool pdl_enabled() {
     return on;
 }
 
+// DEBUG: FBS_PDL_BREAK_BEFORE=name1,name2 serialises the launches of those kernels (bisecting
+// PDL ordering problems)
+void pdl_debug_break(const char* name, cudaStream_t s) {
+    static const std::string list = [] {
+        const char* e = std::getenv("FBS_PDL_BREAK_BEFORE");
+        return e ? "," + std::string(e) + "," : std::string();
+    }();
+    if (!list.empty() && list.find("," + std::string(name) + ",") != std::string::npos) pdl_break(s, 16);
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
@@ -111,13 +160,14 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = (pdl_take(s) && pdl_enabled()) ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 #define LAUNCH(kernel, grid, block, smem, stream, ...) LAUNCH_AS(#kernel, kernel, grid, block, smem, stream, __VA_ARGS__)
 #define LAUNCH_AS(name, kernel, grid, block, smem, stream, ...)                          \
     do {                                                                                 \
+        ::fbs::pdl_debug_break((name), (stream));                                        \
         ::fbs::ProfScope _ps((name), (stream));                                          \
         ck(::fbs::launch_pdl(kernel, dim3(grid), dim3(block), (smem), (stream), __VA_ARGS__), #kernel); \
         ::fbs::g_launches.fetch_add(1, std::memory_order_relaxed);                       \
@@ -141,12 +191,11 @@ void device_setup(int* dev) {
     }
 }
 
-template <class T>
-T* dalloc(AllocList& list, size_t count, cudaStream_t s) {
+void* raw_alloc(AllocList& list, size_t bytes, cudaStream_t s) {
+    pdl_break(s, 1);  // a stream-ordered allocation between PDL launches breaks their ordering
     void* p = nullptr;
-    if (count == 0) count = 1;
     if (list.al.alloc) {
-        p = list.al.alloc(count * sizeof(T), list.al.ctx, reinterpret_cast<fbs_stream>(s));
+        p = list.al.alloc(bytes, list.al.ctx, reinterpret_cast<fbs_stream>(s));
         if (!p) throw Err(FBS_ENOMEM, "caller allocator returned NULL");
         // vector loads (int4 / float4) and cp.async.bulk copies need 16-byte-aligned buffers (fbs.h)
         if (reinterpret_cast<uintptr_t>(p) & 15) {
@@ -154,13 +203,34 @@ T* dalloc(AllocList& list, size_t count, cudaStream_t s) {
             throw Err(FBS_EINVAL, "caller allocator returned a pointer that is not 16-byte aligned");
         }
     } else {
-        ck(cudaMallocAsync(&p, count * sizeof(T), s), "cudaMallocAsync");
+        ck(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
     }
     list.ptrs.push_back(p);
-    return static_cast<T*>(p);
+    return p;
 }
 
+// One allocation up front for a handle's buffers (its size an estimate; dalloc falls back to
+// separate allocations once it is used up).
+void arena_reserve(AllocList& list, size_t bytes, cudaStream_t s) {
+    bytes = (bytes + 255) & ~size_t(255);
+    list.arena = static_cast<char*>(raw_alloc(list, bytes, s));
+    list.arenaLeft = bytes;
+}
+
+template <class T>
+T* dalloc(AllocList& list, size_t count, cudaStream_t s) {
+    if (count == 0) count = 1;
+    const size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);  // 256-byte aligned carving
+    if (list.arena && bytes <= list.arenaLeft) {
+        void* p = list.arena;
+        list.arena += bytes;
+        list.arenaLeft -= bytes;
+        return static_cast<T*>(p);
+    }
+    return static_cast<T*>(raw_alloc(list, count * sizeof(T), s));
+}
 void free_all(AllocList& list, cudaStream_t s) {
+    pdl_break(s, 2);
     for (void* p : list.ptrs) {
         if (list.al.free) list.al.free(p, list.al.ctx, reinterpret_cast<fbs_stream>(s));
         else cudaFreeAsync(p, s);
@@ -215,7 +285,7 @@ PinnedBlock pinned_get(size_t bytes) {
 
 void pinned_put(PinnedBlock b, cudaStream_t s) {
     if (!b.p) return;
-    cudaEventRecord(b.done, s);
+    event_record(b.done, s);
     std::lock_guard<std::mutex> lk(g_pin_mu);
     g_pin_free.push_back(b);
 }
@@ -281,6 +351,42 @@ using namespace fbs;
 
 
 // ===================================================================================== grid
+// Pyramid levels carried (Lmax: halving until every coordinate is 0) and the vertex capacity of
+// each level: a level-k vertex is a distinct (level-k cell, halved code) pair with at least one
+// child, so M_k ≤ min(M_{k−1}, cells_k · codes_k); level 0: M ≤ N.
+static std::vector<int64_t> level_caps(int F, int ncx, int ncy, int64_t N, double sl, double suv, int dims, bool pyr) {
+    const int64_t lmax = (int64_t)std::floor(65280.0 / (256.0 * sl));
+    const int64_t uvmax = (dims == 3) ? 0 : (int64_t)std::floor(65408.0 / (256.0 * suv));
+    int Lmax = 1;
+    if (pyr) {
+        const int bits = std::max({bitlen(ncy - 1), bitlen(ncx - 1), bitlen(lmax), bitlen(uvmax)});
+        Lmax = std::min(1 + bits, kMaxLevels);
+    }
+    std::vector<int64_t> cap(Lmax, N);
+    for (int k = 1; k < Lmax; ++k) {
+        const int64_t nck = (int64_t)F * (((ncx - 1) >> k) + 1) * (((ncy - 1) >> k) + 1);
+        const double codes = (double)((lmax >> k) + 1) * (double)((uvmax >> k) + 1) * (double)((uvmax >> k) + 1);
+        cap[k] = std::max<int64_t>(1, (int64_t)std::min<double>((double)cap[k - 1], (double)nck * codes));
+    }
+    return cap;
+}
+
+// Device bytes of a grid's buffers (the arena estimate; a shortfall only costs extra allocations)
+static size_t grid_bytes(int F, int ncx, int ncy, int64_t N, int64_t ncells, const std::vector<int64_t>& cap) {
+    const int L = (int)cap.size();
+    size_t b = (size_t)N * (4 + 8 + 4 + 16 + 4 + 4) + (size_t)ncells * (kCellMaxPx + 4 + 4 + 8) + (size_t)8 * kVecPad * 16;
+    if (L > 1) {
+        b += (size_t)N * (16 + 4 + 4 + 4);  // pyramid scratch + ranks, tord0, parent0T
+        for (int k = 1; k < L; ++k) {
+            const int64_t nck = (int64_t)F * (((ncx - 1) >> k) + 1) * (((ncy - 1) >> k) + 1);
+            b += (size_t)cap[k] * (8 + 4 + 4 + 4 + 8 + 8) + (size_t)cap[k - 1] * 8 + (size_t)nck * 8 + 4096;
+        }
+        b += (size_t)cap[1] * 8 + (size_t)(L > 3 ? L - 3 : 0) * (L > 2 ? cap[2] : 0) * 12;
+        b += ((size_t)cap[1] / kScanTile + F + 1) * 12;
+    }
+    return b + ((size_t)L + 8) * (F + 1) * 4 + (1 << 20);
+}
+
 static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy, double sl, double suv,
                             const fbs_grid_opts* opts, cudaStream_t s, fbs_grid* out) {
     if (!rgb || !out) throw Err(FBS_EINVAL, "null pointer");
@@ -301,6 +407,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
 
     int dev = 0;
     device_setup(&dev);
+    pdl_break(s, 8);  // the caller's own work may precede this call on the stream
     // FBS_HOST_TIMING=1: host-side timestamps of the grid build (diagnostic)
     static const bool host_timing = std::getenv("FBS_HOST_TIMING") && std::getenv("FBS_HOST_TIMING")[0] == '1';
     auto t_prev = std::chrono::steady_clock::now();
@@ -323,6 +430,8 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->stream = s;
         g->device = dev;
         auto& A = g->allocs;
+        const std::vector<int64_t> cap = level_caps(F, ncx, ncy, N, sl, suv, g->dims, want_pyr);
+        arena_reserve(A, grid_bytes(F, ncx, ncy, N, g->ncells, cap), s);
 
         g->colStart = dalloc<int>(A, ncx + 1, s);
         g->rowStart = dalloc<int>(A, ncy + 1, s);
@@ -358,28 +467,24 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         LAUNCH(k_grid_write, cellBlocks, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, g->cellOff, heads, g->perm,
                keysCap, mCap, g->vid);
 
-        // ---- sync 1: vertex counts (sizes the vertex arrays and the pyramid capacities)
-        std::vector<int> fo(F + 1);
-        int errh[4];
-        PinnedBlock rb = pinned_get(((size_t)(F + 1) * (kMaxLevels + 1) + 4) * sizeof(int));  // read-backs
-        int* rbi = static_cast<int*>(rb.p);
-        copy_words(err, rbi, (4 + F + 1) * sizeof(int), s);  // err[4] then frameOff (contiguous)
-        HT("before sync1");
-        ck(cudaStreamSynchronize(s), "sync");
-        HT("sync1 wait");
-        std::copy(rbi, rbi + 4, errh);
-        std::copy(rbi + 4, rbi + 4 + F + 1, fo.begin());
-        if (errh[0]) throw Err(FBS_ELIMIT, "a sigma_xy cell holds more than 64 pixels");
-        g->M = fo[F];
-        g->frameOffH.assign(fo.begin(), fo.end());
-        g->maxFrameM = 0;
-        for (int f = 0; f < F; ++f) g->maxFrameM = std::max<int64_t>(g->maxFrameM, fo[f + 1] - fo[f]);
+        // No host synchronisation anywhere in the build: every vertex array is sized by a rigorous
+        // capacity known on the host (level 0: M ≤ N; level k: M_k ≤ min(M_{k−1}, cells_k × codes_k)),
+        // every kernel reads the data-dependent counts (frame and level offsets) from device memory,
+        // and launch sizes derive from the capacities (grid-stride loops).  The exact counts are read
+        // back only by the synchronous query / export calls (ensure_sizes).
+        g->err = err;
         g->keys = keysCap;
         g->m = mCap;
-        const int64_t M = g->M;
+        const int64_t M = N;  // level-0 capacity (and the channel stride of every vertex vector)
+        g->M = M;
+        g->maxFrameM = std::max<int64_t>(1, (int64_t)H * W / 3);  // launch-size heuristic only
 
         g->nbr = dalloc<int4>(A, M + kVecPad, s);
-        HT("after sync1 -> neighbours");
+        // Phase boundaries of the build are fully serialised launches: one unbroken programmatic
+        // (PDL) chain through the whole build faulted on B200 (a pyramid or tree kernel read data of
+        // the level-0 build that was not yet visible), while serialising any of these boundaries
+        // fixed it (tests/test_gpu_ops.py ragged shapes; scripts/pdl_bisect.sh)
+        pdl_break(s, 32);
         LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
                g->ncells, g->nbr, err);
 
@@ -400,33 +505,35 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         std::vector<cudaEvent_t> bsJoin(Gb, nullptr);
         if (Gb > 1) {
             ck(cudaEventCreateWithFlags(&bsFork, cudaEventDisableTiming), "event");
-            ck(cudaEventRecord(bsFork, s), "event");
+            ck(event_record(bsFork, s), "event");
         }
         const int sms = g_num_sms > 0 ? g_num_sms : 148;
         for (int gi = 0; gi < Gb; ++gi) {
             const int f0 = (int)((int64_t)F * gi / Gb), f1 = (int)((int64_t)F * (gi + 1) / Gb);
-            const int vlo = fo[f0], vhi = fo[f1];
             cudaStream_t sg = s;
             if (Gb > 1) {
                 sg = group_stream(dev, s, gi);
-                ck(cudaStreamWaitEvent(sg, bsFork, 0), "wait");
+                ck(stream_wait(sg, bsFork), "wait");
             }
             float* c2 = cur;
             float* n2 = nxt;
-            for (int it = 0; it < g->n_bistoch && vhi > vlo; ++it) {
-                const int nch = (vhi + kBsChunk - 1) / kBsChunk - vlo / kBsChunk;
-                LAUNCH(k_bistoch, std::max(1, std::min(nch, std::max(1, bsPerSM * sms / Gb))), kBsThreads, kBsSmem, sg,
-                       g->nbr, g->m, c2, n2, (int)M, vlo, vhi, it == 0, (float)(2 * g->dims));
+            // the group's vertex range [frameOff[f0], frameOff[f1]) is read on the device; the grid
+            // is sized by its pixel count (an upper bound of its vertices)
+            const int64_t chunksCap = ((int64_t)(f1 - f0) * H * W + kBsChunk - 1) / kBsChunk + 1;
+            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(chunksCap, std::max(1, bsPerSM * sms / Gb)));
+            for (int it = 0; it < g->n_bistoch && f1 > f0; ++it) {
+                LAUNCH(k_bistoch, blocks, kBsThreads, kBsSmem, sg, g->nbr, g->m, c2, n2, g->frameOff, F, f0, f1, it == 0,
+                       (float)(2 * g->dims));
                 std::swap(c2, n2);
             }
             if (Gb > 1) {
                 ck(cudaEventCreateWithFlags(&bsJoin[gi], cudaEventDisableTiming), "event");
-                ck(cudaEventRecord(bsJoin[gi], sg), "event");
+                ck(event_record(bsJoin[gi], sg), "event");
             }
         }
         if (Gb > 1) {
             for (int gi = 0; gi < Gb; ++gi) {
-                ck(cudaStreamWaitEvent(s, bsJoin[gi], 0), "wait");
+                ck(stream_wait(s, bsJoin[gi]), "wait");
                 cudaEventDestroy(bsJoin[gi]);
             }
             cudaEventDestroy(bsFork);
@@ -438,22 +545,16 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             LAUNCH(k_fill_words, grid_for(M), kThreads, 0, s, reinterpret_cast<int*>(g->n), (int64_t)M, bits);
         }
 
-        // ---- pyramid (Supp. Sec. 2), levels 1 .. Lmax-1
-        int Lmax = 1;
-        if (want_pyr) {
-            const int64_t lmax = (int64_t)std::floor(65280.0 / (256.0 * sl));
-            const int64_t uvmax = (int64_t)std::floor(65408.0 / (256.0 * suv));
-            const int bits = std::max({bitlen(ncy - 1), bitlen(ncx - 1), bitlen(lmax), bitlen(uvmax)});
-            Lmax = std::min(1 + bits, kMaxLevels);
-        }
+        // ---- pyramid (Supp. Sec. 2), levels 1 .. Lmax-1 (capacities: level_caps)
+        const int Lmax = (int)cap.size();
+        g->capH = cap;
         const uint64_t* keysK = g->keys;
         const int* cellOffK = g->cellOff;
         int ncxK = ncx, ncyK = ncy;
-        // frame offsets of every level in one [Lmax][F + 1] array (row 0: level 0), read back at once
-        // and used by the hierarchy kernels as is
+        // frame offsets of every level in one [Lmax][F + 1] array (row 0: level 0), used by the
+        // hierarchy kernels as is
         int* lvAll = dalloc<int>(A, (size_t)Lmax * (F + 1), s);
         copy_words(g->frameOff, lvAll, (F + 1) * sizeof(int), s);
-        std::vector<int*> lvFrameOffDev(Lmax, nullptr);
         unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
         int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, s) : nullptr;  // parent rank of each sorted child
         // scan look-back states and (tile counter, scratch bump) pairs of every level: one zeroing
@@ -472,22 +573,23 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             L.ncx = ((ncx - 1) >> k) + 1;
             L.ncy = ((ncy - 1) >> k) + 1;
             L.ncells = (int64_t)F * L.ncx * L.ncy;
-            L.keys = dalloc<uint64_t>(A, M, s);
+            L.M = cap[k];
+            L.keys = dalloc<uint64_t>(A, cap[k], s);
             L.cellOff = dalloc<int>(A, L.ncells + 1, s);
-            L.parent = dalloc<int>(A, M, s);
-            L.childStart = dalloc<int>(A, M + 1, s);
-            L.childList = dalloc<int>(A, M, s);
-            L.count = dalloc<int>(A, M, s);
-            if (k >= 2) L.cnt1 = dalloc<int>(A, M, s);
+            L.parent = dalloc<int>(A, cap[k - 1], s);
+            L.childStart = dalloc<int>(A, cap[k] + 1, s);
+            L.childList = dalloc<int>(A, cap[k - 1], s);
+            L.count = dalloc<int>(A, cap[k], s);
+            if (k >= 2) L.cnt1 = dalloc<int>(A, cap[k], s);
             int* cnt2 = dalloc<int>(A, L.ncells, s);
             const int64_t st2n = std::max<int64_t>(1, (L.ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems));
             unsigned long long* st2 = st2All + st2Off[k];
             unsigned* ctr2 = reinterpret_cast<unsigned*>(st2 + st2n);  // scan tile counter, scratch bump
+            pdl_break(s, 32);
             LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
-            lvFrameOffDev[k] = lvAll + (size_t)k * (F + 1);
             LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2,
-                   (int64_t)L.ncx * L.ncy, lvFrameOffDev[k]);
+                   (int64_t)L.ncx * L.ncy, lvAll + (size_t)k * (F + 1));
             LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, L.cellOff, L.childList, pyrRank, L.keys, L.parent, L.childStart,
                    k >= 2 ? g->lv[k - 1].count : nullptr, L.count, k >= 3 ? g->lv[k - 1].cnt1 : nullptr,
@@ -497,132 +599,65 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             ncxK = L.ncx;
             ncyK = L.ncy;
         }
-        // ---- sync 2: level sizes
-        std::vector<std::vector<int>> lfo(Lmax);
-        if (Lmax > 1) copy_words(lvAll + (F + 1), rbi + (F + 1), (size_t)(Lmax - 1) * (F + 1) * sizeof(int), s);
-        copy_words(err, rbi + (size_t)Lmax * (F + 1), 4 * sizeof(int), s);
-        HT("before sync2");
-        ck(cudaStreamSynchronize(s), "sync");
-        HT("sync2 wait");
-        for (int k = 1; k < Lmax; ++k) lfo[k].assign(rbi + (size_t)k * (F + 1), rbi + (size_t)(k + 1) * (F + 1));
-        std::copy(rbi + (size_t)Lmax * (F + 1), rbi + (size_t)Lmax * (F + 1) + 4, errh);
-        pinned_put(rb, s);
-        if (errh[0] & ~8) throw Err(FBS_ECUDA, "internal grid-build check failed (code " + std::to_string(errh[0]) + ")");
         g->bistoch_residual = -1.f;  // computed on request (fbs_grid_export)
-        // per-frame level counts: first level with a single vertex (reading #8)
-        g->frameLevelsH.assign(F, Lmax);
-        for (int f = 0; f < F; ++f) {
-            int Lf = 1;
-            if (fo[f + 1] - fo[f] > 1) {
-                Lf = Lmax;
-                for (int k = 1; k < Lmax; ++k)
-                    if (lfo[k][f + 1] - lfo[k][f] == 1) { Lf = k + 1; break; }
-            }
-            g->frameLevelsH[f] = Lf;
-        }
-        int L = 1;
-        for (int f = 0; f < F; ++f) L = std::max(L, g->frameLevelsH[f]);
-        g->L = L;
+        g->L = Lmax;  // levels carried by the hierarchy kernels; each frame's own count is on the device
         g->has_pyramid = want_pyr;
-        for (int k = 1; k < L; ++k) {
-            g->lv[k].M = lfo[k][F];
-            g->lv[k].frameOff.assign(lfo[k].begin(), lfo[k].end());
-        }
-
         g->lvFrameOffDev = lvAll;  // rows 0 .. L − 1 (row 0 = level 0)
-        // uploads (frame levels, scan tiles): one device block filled from one mapped pinned block
-        // (kept with the grid, so no synchronisation for its lifetime) by one copy kernel
-        struct Upload {
-            const void* src;
-            size_t bytes;
-            void** dst;
-        };
-        std::vector<Upload> upl;
-        auto flush_uploads = [&]() {
-            size_t total = 0;
-            for (auto& e : upl) total += (e.bytes + 7) & ~size_t(7);
-            if (total == 0) return;
-            char* dev = reinterpret_cast<char*>(dalloc<unsigned long long>(A, total / 8, s));
-            PinnedBlock b = pinned_get(total);
-            g->uploads.push_back(b);
-            size_t at = 0;
-            for (auto& e : upl) {
-                std::memcpy(static_cast<char*>(b.p) + at, e.src, e.bytes);
-                *e.dst = dev + at;
-                at += (e.bytes + 7) & ~size_t(7);
-            }
-            copy_words(b.p, dev, total, s);
-            upl.clear();
-        };
-        upl.push_back({g->frameLevelsH.data(), F * sizeof(int), reinterpret_cast<void**>(&g->frameLevels)});
+        // per-frame level counts (first level with a single vertex, reading #8) and, with a pyramid,
+        // the prefix-scan tiles of the tree-ordered level 1 — both computed on the device
+        const int L = Lmax;
+        g->frameLevels = dalloc<int>(A, F, s);
+        pdl_break(s, 32);
+        LAUNCH(k_frame_levels, (F + 255) / 256, 256, 0, s, lvAll, F, L, g->frameLevels);
         // ---- tree order of the pyramid (tree_kernels.cuh): depth-first positions of the level-0 and
         // level-1 vertices, so every coarse subtree is one contiguous level-1 range
-        std::vector<int> tfo, tframe;
-        std::vector<int2> trange;
         if (L > 1) {
             TreeOrder& T = g->tree;
-            const int64_t M1 = g->lv[1].M;
+            const int64_t M1 = cap[1];
             const int top = L - 1;
             std::vector<int*> cnt1(L, nullptr);  // level-1 descendants of levels ≥ 2
             for (int k = 2; k < L; ++k) cnt1[k] = g->lv[k].cnt1;
             std::vector<int2*> start(L, nullptr);
-            for (int k = 1; k < L; ++k) start[k] = dalloc<int2>(A, g->lv[k].M, s);
-            for (int k = 2; k < L; ++k) T.rng[k] = dalloc<int2>(A, g->lv[k].M, s);
+            for (int k = 1; k < L; ++k) start[k] = dalloc<int2>(A, cap[k], s);
+            for (int k = 2; k < L; ++k) T.rng[k] = dalloc<int2>(A, cap[k], s);
             T.tord0 = dalloc<int>(A, M, s);
             T.csT = dalloc<int>(A, M1 + 1, s);
             T.tord1 = dalloc<int>(A, M1, s);
             T.parent0T = dalloc<int>(A, M, s);
-            HT("after sync2 -> tree_top");
             LAUNCH(k_tree_top, 1, 256, 0, s, g->lvFrameOffDev, F, top, start[top], top >= 2 ? T.rng[top] : nullptr,
                    top >= 2 ? cnt1[top] : nullptr);
             for (int k = top; k >= 1; --k) {
                 const int km1 = k - 1;
-                LAUNCH(k_tree_down, grid_for(g->lv[k].M), kThreads, 0, s, km1, g->lv[k].childStart, g->lv[k].childList,
-                       (int)g->lv[k].M, start[k], km1 >= 1 ? g->lv[km1].count : nullptr,
+                LAUNCH(k_tree_down, grid_for(cap[k]), kThreads, 0, s, km1, g->lv[k].childStart, g->lv[k].childList,
+                       lvAll + (size_t)k * (F + 1) + F, start[k], km1 >= 1 ? g->lv[km1].count : nullptr,
                        km1 >= 2 ? cnt1[km1] : nullptr, km1 >= 1 ? start[km1] : nullptr,
                        km1 >= 2 ? T.rng[km1] : nullptr, T.tord0, T.tord1, T.csT);
             }
-            LAUNCH(k_tree_finish, grid_for(M), kThreads, 0, s, g->lv[1].parent, start[1], M, M1, T.parent0T, T.csT);
+            LAUNCH(k_tree_finish, grid_for(M), kThreads, 0, s, g->lv[1].parent, start[1], lvAll + F, lvAll + (F + 1) + F,
+                   T.parent0T, T.csT);
             if (top >= 3) {  // ancestor tables of the level-2 vertices
-                const int64_t M2 = g->lv[2].M;
+                const int64_t M2 = cap[2];
                 T.ancId = dalloc<int>(A, (size_t)(top - 2) * M2, s);
                 T.ancRng = dalloc<int2>(A, (size_t)(top - 2) * M2, s);
                 HierArgs hb{};
                 hb.L = L;
+                hb.M2 = M2;
                 for (int k = 2; k < L; ++k) {
-                    hb.lv[k].M = g->lv[k].M;
+                    hb.lv[k].M = cap[k];
                     hb.lv[k].parent = (k + 1 < L) ? g->lv[k + 1].parent : nullptr;
                     hb.lv[k].rng = T.rng[k];
                 }
-                LAUNCH(k_tree_anc, grid_for(M2), kThreads, 0, s, hb, T.ancId, T.ancRng);
+                LAUNCH(k_tree_anc, grid_for(M2), kThreads, 0, s, hb, lvAll + 2 * (size_t)(F + 1) + F, T.ancId, T.ancRng);
             }
-            // prefix-scan tiles: kScanTile level-1 positions, never crossing a frame
-            tfo.assign(F + 1, 0);
-            g->maxFrameM1 = 0;
-            g->maxFrameM2 = 0;
-            for (int f = 0; f < F && L > 2; ++f) g->maxFrameM2 = std::max<int64_t>(g->maxFrameM2, lfo[2][f + 1] - lfo[2][f]);
-            for (int f = 0; f < F; ++f) {
-                const int64_t m1 = lfo[1][f + 1] - lfo[1][f];
-                g->maxFrameM1 = std::max(g->maxFrameM1, m1);
-                tfo[f + 1] = tfo[f] + (int)((m1 + kScanTile - 1) / kScanTile);
-                T.maxFrameTiles = std::max(T.maxFrameTiles, tfo[f + 1] - tfo[f]);
-                for (int t = tfo[f]; t < tfo[f + 1]; ++t) {
-                    tframe.push_back(f);
-                    const int a0 = lfo[1][f] + (t - tfo[f]) * kScanTile;
-                    trange.push_back(make_int2(a0, (int)std::min<int64_t>(a0 + kScanTile, lfo[1][f + 1])));
-                }
-            }
-            if ((size_t)T.maxFrameTiles * sizeof(double) > 200 * 1024)
-                throw Err(FBS_ELIMIT, "frame too large for the shared-memory tile scan of the hierarchy");
-            T.nTiles1 = tfo[F];
-            T.tileFrameOffH = tfo;
-            upl.push_back({tfo.data(), (F + 1) * sizeof(int), reinterpret_cast<void**>(&T.tileFrameOff)});
-            if (trange.empty()) trange.push_back(make_int2(0, 0));
-            if (tframe.empty()) tframe.push_back(0);
-            upl.push_back({trange.data(), trange.size() * sizeof(int2), reinterpret_cast<void**>(&T.tileRange)});
-            upl.push_back({tframe.data(), tframe.size() * sizeof(int), reinterpret_cast<void**>(&T.tileFrame)});
+            // prefix-scan tiles: kScanTile level-1 positions, never crossing a frame (device-built)
+            T.nTiles1 = (int)((M1 + kScanTile - 1) / kScanTile + F);  // capacity
+            T.tileFrameOff = dalloc<int>(A, F + 1, s);
+            T.tileRange = dalloc<int2>(A, T.nTiles1, s);
+            T.tileFrame = dalloc<int>(A, T.nTiles1, s);
+            LAUNCH(k_scan_tiles, F, 256, 0, s, lvAll + (F + 1), F, T.tileFrameOff, T.tileRange, T.tileFrame);
         }
-        flush_uploads();
+        g->maxFrameM1 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM, L > 1 ? cap[1] : 1));
+        g->maxFrameM2 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM1, L > 2 ? cap[2] : 1));
     } catch (...) {
         free_all(g->allocs, s);
         for (auto& b : g->uploads) pinned_put(b, s);
@@ -630,6 +665,31 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         throw;
     }
     *out = g;
+}
+
+// The exact sizes of a grid (vertex and level counts per frame, levels per frame) live on the
+// device; the synchronous query and export calls read them back once (one synchronisation of the
+// grid's stream) and check the build's internal invariants.
+static void ensure_sizes(fbs_grid g) {
+    if (g->sized) return;
+    cudaStream_t s = g->stream;
+    const int F = g->F, L = g->L;
+    std::vector<int> lv((size_t)L * (F + 1)), fl(F);
+    int errh[4];
+    ck(memcpy_async(lv.data(), g->lvFrameOffDev, lv.size() * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(memcpy_async(fl.data(), g->frameLevels, F * sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(memcpy_async(errh, g->err, sizeof(errh), cudaMemcpyDeviceToHost, s), "d2h");
+    ck(cudaStreamSynchronize(s), "sync");
+    if (errh[0] & 1) throw Err(FBS_ELIMIT, "a sigma_xy cell holds more than 64 pixels");
+    if (errh[0] & 6) throw Err(FBS_ECUDA, "internal grid-build check failed (code " + std::to_string(errh[0]) + ")");
+    g->frameOffH.assign(lv.begin(), lv.begin() + F + 1);
+    g->Mx = lv[F];
+    g->levelMx.assign(L, 0);
+    g->Lx = 1;
+    for (int f = 0; f < F; ++f) g->Lx = std::max(g->Lx, fl[f]);
+    for (int k = 0; k < L; ++k) g->levelMx[k] = lv[(size_t)k * (F + 1) + F];
+    g->frameLevelsH = fl;
+    g->sized = true;
 }
 
 // ===================================================================================== solve
@@ -673,7 +733,9 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.L = g->L;
     h.F = g->F;
     h.C = C;
-    h.nt = g->tree.nTiles1;
+    h.nt = g->tree.nTiles1;  // capacity (the lift reads the group's tile range on the device)
+    h.nfG = g->F;
+    h.f0 = 0;
     for (int k = 0; k < g->L; ++k) {
         HLevel& v = h.lv[k];
         v.M = (k == 0) ? g->M : g->lv[k].M;
@@ -709,6 +771,8 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.buf1T = S->buf1T;
     h.locT = S->locT;
     h.tileAgg = S->tileAgg;
+    h.tileBase = S->tileBase;
+    h.tcount = S->tcount;
     h.acc1T = S->acc1T;
     h.partial2 = S->partial2;
     h.counters = S->counters2;
@@ -738,13 +802,23 @@ int vec_blocks(const VecArgs& a) { return a.nf * a.BPF * (a.ksplit ? a.K : 1); }
 template <int MODE>
 void tree_lift(fbs_system S, const HierArgs& h, const float* in0, cudaStream_t s, const int* active = nullptr) {
     static const std::string name = std::string("k_tree_lift<") + mode_name(MODE) + ">";
-    if ((MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2)) {
-        auto kern = k_tree_lift<MODE, true>;
-        LAUNCH_AS(name.c_str(), kern, h.nt * h.C, kScanTile, 0, s, h, in0, active);
-    } else {
-        auto kern = k_tree_lift<MODE, false>;
-        LAUNCH_AS(name.c_str(), kern, h.nt, kScanTile, 0, s, h, in0, active);
+    // work items walked grid-stride (the group's tile count, ≤ capacity h.nt, is on the device);
+    // the grid is the resident capacity of the kernel, shared by the concurrent frame groups
+    const bool ks = (MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2);
+    auto kern = ks ? k_tree_lift<MODE, true> : k_tree_lift<MODE, false>;
+    static int occ[2] = {0, 0};
+    if (!occ[ks]) {
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[ks], kern, kScanTile, 0), "occupancy");
+        occ[ks] = std::max(1, occ[ks]);
     }
+    // (more blocks than resident slots measured faster than a resident-sized grid: 38.7 µs at 8 per
+    // SM vs 54 µs at the occupancy limit split between the frame groups)
+    int perSM = 8;
+    if (const char* e = std::getenv("FBS_LIFT_GRID")) perSM = std::max(1, std::atoi(e));  // A/B
+    const int64_t cap = std::max<int64_t>(1, (int64_t)g_num_sms * perSM);
+    const int64_t items = (int64_t)h.nt * (ks ? h.C : 1);
+    LAUNCH_AS(name.c_str(), kern, (int)std::max<int64_t>(1, std::min<int64_t>(items, cap)), kScanTile, 0, s, h, in0,
+              active);
 }
 
 // coarse values and their projection onto level 2 (k_tree_coarse)
@@ -753,11 +827,8 @@ void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, c
     static const std::string name = std::string("k_tree_coarse<") + mode_name(MODE) + ">";
     const bool ks = (MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2);
     auto kern = ks ? k_tree_coarse<MODE, true> : k_tree_coarse<MODE, false>;
-    const size_t sm = (size_t)S->g->tree.maxFrameTiles * sizeof(double);
-    if (sm > 48 * 1024)
-        ck(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm), "smem attr");
     // ks: the finish reads the split level-0 kernel's partials (BPFs per (frame, channel))
-    LAUNCH_AS(name.c_str(), kern, a.nf * S->bpf2 * (ks ? h.C : 1), 256, sm, s, h, ks ? split_args(S, a) : a, first);
+    LAUNCH_AS(name.c_str(), kern, a.nf * S->bpf2 * (ks ? h.C : 1), 256, 0, s, h, ks ? split_args(S, a) : a, first);
 }
 
 // level-0 output (k_tree_level0)
@@ -819,14 +890,14 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     q.active += f0 * K;
     q.iters += f0 * K;
     q.status += f0 * K;
-    const int t0 = g->tree.tileFrameOffH.empty() ? 0 : g->tree.tileFrameOffH[f0];
-    h.nt = g->tree.tileFrameOffH.empty() ? 0 : g->tree.tileFrameOffH[f0 + nf] - t0;
+    // the group's tiles: [tileFrameOff[f0], tileFrameOff[f0 + nf]) on the device; a capacity for
+    // the launch size from its frames' share
+    h.nt = (int)std::min<int64_t>(g->tree.nTiles1, (int64_t)g->tree.nTiles1 * nf / std::max(1, g->F) + nf + 1);
+    h.nfG = nf;
     h.f0 = f0;
     h.lvFrameOff += f0;  // [L][F+1] row-major: k·(F+1) + f0 + f
     h.frameLevels += f0;
     h.tileFrameOff += f0;  // tile ids stay global (tileFrameOff[f] − tileFrameOff[0] is group-local)
-    h.tileRange += t0;
-    h.tileFrame += t0;
     h.partial2 += (size_t)f0 * S->bpf2 * h.C;
     h.counters += f0;
 }
@@ -977,7 +1048,7 @@ void tol_poll(fbs_system S, std::vector<PcgRun>& runs) {
                 for (int i = 0; i < nit; ++i) pcg_iteration(S, runs[r].a, runs[r].h, done[r] + i, false, runs[r].s);
                 done[r] += nit;
                 copy_words(runs[r].a.sc_.n_active, &pin[2 * r + slot[r]], sizeof(int), runs[r].s);
-                ck(cudaEventRecord(ev[2 * r + slot[r]], runs[r].s), "event");
+                ck(event_record(ev[2 * r + slot[r]], runs[r].s), "event");
             }
             for (int r = 0; r < n; ++r) {
                 if (fin[r]) continue;
@@ -1020,12 +1091,12 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         cudaEvent_t fork;
         std::vector<cudaEvent_t> join(G);
         ck(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming), "event");
-        ck(cudaEventRecord(fork, s), "event");
+        ck(event_record(fork, s), "event");
         std::vector<PcgRun> runs;
         for (int gi = 0; gi < G; ++gi) {
             const int f0 = (int)((int64_t)g->F * gi / G), f1 = (int)((int64_t)g->F * (gi + 1) / G);
             cudaStream_t sg = group_stream(dev, s, gi);
-            ck(cudaStreamWaitEvent(sg, fork, 0), "wait");
+            ck(stream_wait(sg, fork), "wait");
             VecArgs ag = a;
             HierArgs hg = S->hP;
             restrict_frames(S, f0, f1 - f0, ag, hg);
@@ -1042,8 +1113,8 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         for (int gi = 0; gi < G; ++gi) {
             cudaStream_t sg = group_stream(dev, s, gi);
             ck(cudaEventCreateWithFlags(&join[gi], cudaEventDisableTiming), "event");
-            ck(cudaEventRecord(join[gi], sg), "event");
-            ck(cudaStreamWaitEvent(s, join[gi], 0), "wait");
+            ck(event_record(join[gi], sg), "event");
+            ck(stream_wait(s, join[gi]), "wait");
             cudaEventDestroy(join[gi]);
         }
         cudaEventDestroy(fork);
@@ -1109,6 +1180,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
     validate_opts(o, g);
     int dev = 0;
     device_setup(&dev);
+    pdl_break(s);
 
     const bool lowrank = o.lowrank_eps > 0.0 && K > 1;
     if (lowrank && sys_out) throw Err(FBS_EINVAL, "a low-rank solve keeps no system (sys_out must be NULL)");
@@ -1122,6 +1194,17 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const int64_t M = g->M;
         const int F = g->F;
         auto& A = S->allocs;
+        {  // one up-front allocation for the system's buffers (see arena_reserve)
+            const size_t M4 = (size_t)M * 4, C = (size_t)K + 1;
+            size_t b = M4 * (C + 2 + 8 * (size_t)K + C + 2 * (size_t)K) + (size_t)16 * kVecPad * 16 + (1 << 20);
+            if (g->L > 1) {
+                const size_t c1 = g->capH.size() > 1 ? (size_t)g->capH[1] : 0;
+                b += 16 * C * c1 + 16 * C * ((size_t)g->tree.nTiles1 + 1);
+                for (size_t k = 1; k < g->capH.size(); ++k) b += 4 * (size_t)g->capH[k] + 256;
+                if (g->capH.size() > 3) b += 4 * (g->capH.size() - 3) * (size_t)g->capH[2];
+            }
+            arena_reserve(A, b, s);
+        }
         // launch geometry of the per-frame kernels: BPF blocks per frame
         // 16 blocks of 256 threads per SM: two full SMs' worth, so that each of the two frame
         // groups of a FIXED-mode solve (run_pcg) fills the GPU on its own and the groups overlap
@@ -1200,6 +1283,9 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             S->acc1T = dalloc<float>(A, (size_t)C * M1, s);
             S->locT = dalloc<double>(A, (size_t)C * M1, s);
             S->tileAgg = dalloc<double>(A, (size_t)C * nT, s);
+            S->tileBase = dalloc<double>(A, (size_t)C * nT, s);
+            S->tcount = dalloc<unsigned>(A, (size_t)C * F, s);
+            zero_words(S->tcount, (size_t)C * F * sizeof(unsigned), s);
             const int64_t want2 = ((g->L > 2 ? g->maxFrameM2 : g->maxFrameM1) + 255) / 256;
             int occ2 = 8;
             if (const char* e = std::getenv("FBS_BPF2_OCC")) occ2 = std::max(1, std::min(64, std::atoi(e)));  // A/B
@@ -1262,7 +1348,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         }
         if (sys_out) {  // the initial guess is kept for fbs_system_export only
             S->y0 = dalloc<float>(A, KM, s);
-            ck(cudaMemcpyAsync(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
+            ck(memcpy_async(S->y0, S->xh, KM * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
         }
         // a8: PCG
         run_pcg(S, a, false, s);
@@ -1275,7 +1361,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         }
         // a9: slice
         slice(g, ysol, M, K, 1, x, s);
-        if (y) LAUNCH(k_export_vk, grid_for((size_t)K * M), kThreads, 0, s, ysol, M, K, y);
+        if (y) LAUNCH(k_export_vk, grid_for((size_t)K * M), kThreads, 0, s, ysol, g->frameOff + F, (int64_t)0, M, K, y);
     } catch (...) {
         free_all(S->allocs, s);
         delete S;
@@ -1324,6 +1410,7 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
     if (!(sigma_s > 0.0) || !(sigma_r > 0.0) || n_iters < 1) throw Err(FBS_EINVAL, "sigma_s, sigma_r > 0, n_iters >= 1");
     int dev = 0;
     device_setup(&dev);
+    pdl_break(s);
     AllocList tmp;
     try {
         const size_t NP = (size_t)F * H * W, NS = NP * K;
@@ -1331,7 +1418,7 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
         float* Dy = dalloc<float>(tmp, NP, s);
         LAUNCH(k_dt_dist, dim3((W + kThreads - 1) / kThreads, std::min(F * H, 65535)), kThreads, 0, s, rgb, F, H, W,
                (float)(sigma_s / sigma_r), Dx, Dy);
-        if (out != in) ck(cudaMemcpyAsync(out, in, NS * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
+        if (out != in) ck(memcpy_async(out, in, NS * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
         const size_t perWarp = 2 * (size_t)(W + 32) * sizeof(float);
         const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / perWarp));
         const size_t smem = perWarp * nw;
@@ -1385,6 +1472,7 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
                           cudaStream_t s) {
     if (!S || !g_dldx || !t || !c || !dt || !dc) throw Err(FBS_EINVAL, "null pointer");
     fbs_grid g = S->g;
+    pdl_break(s);
     const int64_t M = g->M;
     const int K = S->K;
     const size_t KM = (size_t)K * M;
@@ -1465,14 +1553,14 @@ int fbs_grid_info(fbs_grid g, int64_t* n_pixels, int64_t* n_vertices, int* n_lev
     return guard("fbs_grid_info", [&] {
         if (!g) throw Err(FBS_EINVAL, "null grid");
         if (n_pixels) *n_pixels = g->N;
-        if (n_vertices) *n_vertices = g->M;
-        if (n_levels) *n_levels = g->L;
+        if (!n_vertices && !n_levels && !frame_vertices && !level_vertices && !frame_levels) return;
+        ensure_sizes(g);  // the sizes are data-dependent: read back once (synchronises the grid's stream)
+        if (n_vertices) *n_vertices = g->Mx;
+        if (n_levels) *n_levels = g->Lx;
         if (frame_vertices)
             for (int f = 0; f < g->F; ++f) frame_vertices[f] = g->frameOffH[f + 1] - g->frameOffH[f];
-        if (level_vertices) {
-            level_vertices[0] = g->M;
-            for (int k = 1; k < g->L; ++k) level_vertices[k] = g->lv[k].M;
-        }
+        if (level_vertices)
+            for (int k = 0; k < g->Lx; ++k) level_vertices[k] = g->levelMx[k];
         if (frame_levels)
             for (int f = 0; f < g->F; ++f) frame_levels[f] = g->frameLevelsH[f];
     });
@@ -1481,17 +1569,18 @@ int fbs_grid_info(fbs_grid g, int64_t* n_pixels, int64_t* n_vertices, int* n_lev
 int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int32_t* m, float* n, float* res) {
     return guard("fbs_grid_export", [&] {
         if (!g) throw Err(FBS_EINVAL, "null grid");
+        ensure_sizes(g);
         cudaStream_t s = g->stream;
-        const int64_t M = g->M;
-        if (keys) ck(cudaMemcpyAsync(keys, g->keys, M * 8, cudaMemcpyDeviceToHost, s), "d2h");
-        if (vid) ck(cudaMemcpyAsync(vid, g->vid, g->N * 4, cudaMemcpyDeviceToHost, s), "d2h");
-        if (m) ck(cudaMemcpyAsync(m, g->m, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
-        if (n) ck(cudaMemcpyAsync(n, g->n, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        const int64_t M = g->Mx;
+        if (keys) ck(memcpy_async(keys, g->keys, M * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        if (vid) ck(memcpy_async(vid, g->vid, g->N * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (m) ck(memcpy_async(m, g->m, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (n) ck(memcpy_async(n, g->n, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
         if (nbr) {
             AllocList tmp;
             int* d = dalloc<int>(tmp, (size_t)M * 10, s);
             LAUNCH(k_export_nbr, grid_for(M), kThreads, 0, s, g->nbr, (int)M, d);
-            ck(cudaMemcpyAsync(nbr, d, (size_t)M * 40, cudaMemcpyDeviceToHost, s), "d2h");
+            ck(memcpy_async(nbr, d, (size_t)M * 40, cudaMemcpyDeviceToHost, s), "d2h");
             free_all(tmp, s);
         }
         if (res) {
@@ -1502,7 +1591,7 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
                 LAUNCH(k_bistoch_residual, grid_for(M), kThreads, 0, s, g->nbr, g->m, g->n, (int)M, d,
                        (float)(2 * g->dims));
                 unsigned h2[2];
-                ck(cudaMemcpyAsync(h2, d, sizeof(h2), cudaMemcpyDeviceToHost, s), "d2h");
+                ck(memcpy_async(h2, d, sizeof(h2), cudaMemcpyDeviceToHost, s), "d2h");
                 ck(cudaStreamSynchronize(s), "sync");
                 free_all(tmp, s);
                 float e, mm;
@@ -1519,13 +1608,14 @@ int fbs_grid_export(fbs_grid g, uint64_t* keys, int32_t* vid, int32_t* nbr, int3
 int fbs_pyramid_export(fbs_grid g, int level, uint64_t* keys, int32_t* parent, int32_t* count) {
     return guard("fbs_pyramid_export", [&] {
         if (!g) throw Err(FBS_EINVAL, "null grid");
-        if (level < 1 || level >= g->L) throw Err(FBS_EINVAL, "level out of range");
+        ensure_sizes(g);
+        if (level < 1 || level >= g->Lx) throw Err(FBS_EINVAL, "level out of range");
         cudaStream_t s = g->stream;
         const Level& L = g->lv[level];
-        const int64_t Mprev = (level == 1) ? g->M : g->lv[level - 1].M;
-        if (keys) ck(cudaMemcpyAsync(keys, L.keys, L.M * 8, cudaMemcpyDeviceToHost, s), "d2h");
-        if (parent) ck(cudaMemcpyAsync(parent, L.parent, Mprev * 4, cudaMemcpyDeviceToHost, s), "d2h");
-        if (count) ck(cudaMemcpyAsync(count, L.count, L.M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        const int64_t Mk = g->levelMx[level], Mprev = g->levelMx[level - 1];
+        if (keys) ck(memcpy_async(keys, L.keys, Mk * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        if (parent) ck(memcpy_async(parent, L.parent, Mprev * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (count) ck(memcpy_async(count, L.count, Mk * 4, cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaStreamSynchronize(s), "sync");
     });
 }
@@ -1569,14 +1659,14 @@ int fbs_system_stats(fbs_system S, int32_t* iters, double* relres, int32_t* bwd_
         std::vector<double> rr(FK), bb(FK);
         std::vector<int> st(FK), st2(FK, 0);
         int inflags = 0;
-        ck(cudaMemcpyAsync(&inflags, S->inflags, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
-        ck(cudaMemcpyAsync(rr.data(), S->fwd.rr, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
-        ck(cudaMemcpyAsync(bb.data(), S->fwd.bb, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
-        ck(cudaMemcpyAsync(st.data(), S->fwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
-        if (iters) ck(cudaMemcpyAsync(iters, S->fwd.iters, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(memcpy_async(&inflags, S->inflags, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h");
+        ck(memcpy_async(rr.data(), S->fwd.rr, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(memcpy_async(bb.data(), S->fwd.bb, FK * 8, cudaMemcpyDeviceToHost, s), "d2h");
+        ck(memcpy_async(st.data(), S->fwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (iters) ck(memcpy_async(iters, S->fwd.iters, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
         if (S->xb) {
-            ck(cudaMemcpyAsync(st2.data(), S->bwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
-            if (bwd_iters) ck(cudaMemcpyAsync(bwd_iters, S->bwd.iters, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+            ck(memcpy_async(st2.data(), S->bwd.status, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
+            if (bwd_iters) ck(memcpy_async(bwd_iters, S->bwd.iters, FK * 4, cudaMemcpyDeviceToHost, s), "d2h");
         } else if (bwd_iters) {
             for (int i = 0; i < FK; ++i) bwd_iters[i] = 0;
         }
@@ -1595,19 +1685,20 @@ int fbs_system_export(fbs_system S, float* sc, float* b, float* diagA, float* y0
     return guard("fbs_system_export", [&] {
         if (!S) throw Err(FBS_EINVAL, "null system");
         fbs_grid g = S->g;
+        ensure_sizes(g);
         cudaStream_t s = S->stream;
-        const int64_t M = g->M;
+        const int64_t M = g->Mx;
         const int K = S->K;
         const size_t KM = (size_t)K * M;
         AllocList tmp;
         float* d = dalloc<float>(tmp, KM, s);
         auto vk = [&](const float* src, float* host) {
-            LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, src, M, K, d);
-            ck(cudaMemcpyAsync(host, d, KM * 4, cudaMemcpyDeviceToHost, s), "d2h");
+            LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, src, nullptr, M, g->M, K, d);
+            ck(memcpy_async(host, d, KM * 4, cudaMemcpyDeviceToHost, s), "d2h");
             ck(cudaStreamSynchronize(s), "sync");
         };
-        if (sc) ck(cudaMemcpyAsync(sc, S->sc, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
-        if (diagA) ck(cudaMemcpyAsync(diagA, S->diagA, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (sc) ck(memcpy_async(sc, S->sc, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
+        if (diagA) ck(memcpy_async(diagA, S->diagA, M * 4, cudaMemcpyDeviceToHost, s), "d2h");
         ck(cudaStreamSynchronize(s), "sync");
         if (b) vk(S->b, b);
         if (y0) vk(S->y0, y0);
@@ -1629,6 +1720,7 @@ void fbs_system_destroy(fbs_system S) {
 
 int fbs_slice(fbs_grid g, const float* y, int K, float* x, fbs_stream stream) {
     return guard("fbs_slice", [&] {
+        pdl_break((cudaStream_t)stream);
         if (!g || !y || !x) throw Err(FBS_EINVAL, "null pointer");
         if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
         cudaStream_t s = (cudaStream_t)stream;
@@ -1638,6 +1730,7 @@ int fbs_slice(fbs_grid g, const float* y, int K, float* x, fbs_stream stream) {
 
 int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) {
     return guard("fbs_splat", [&] {
+        pdl_break((cudaStream_t)stream);
         if (!g || !p || !out) throw Err(FBS_EINVAL, "null pointer");
         if (K < 1 || K > kMaxK) throw Err(FBS_EINVAL, "K must be in [1, 64]");
         cudaStream_t s = (cudaStream_t)stream;
@@ -1647,27 +1740,31 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
         CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
         LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, p, K,
                g->M, nullptr, planar, nullptr);
-        LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, K, out);
+        LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->frameOff + g->F, (int64_t)0, g->M, K, out);
         free_all(tmp, s);
     });
 }
 
 int fbs_blur(fbs_grid g, const float* v, float* out, fbs_stream stream) {
     return guard("fbs_blur", [&] {
+        pdl_break((cudaStream_t)stream);
         if (!g || !v || !out) throw Err(FBS_EINVAL, "null pointer");
-        LAUNCH(k_blur, grid_for(g->M), kThreads, 0, (cudaStream_t)stream, g->nbr, v, g->M, (float)(2 * g->dims), out);
+        ensure_sizes(g);  // the caller's vectors hold exactly M vertices
+        LAUNCH(k_blur, grid_for(g->Mx), kThreads, 0, (cudaStream_t)stream, g->nbr, v, g->Mx, (float)(2 * g->dims), out);
     });
 }
 
 int fbs_system_apply_A(fbs_system S, const float* y, float* out, fbs_stream stream) {
     return guard("fbs_system_apply_A", [&] {
+        pdl_break((cudaStream_t)stream);
         if (!S || !y || !out) throw Err(FBS_EINVAL, "null pointer");
         cudaStream_t s = (cudaStream_t)stream;
         fbs_grid g = S->g;
+        ensure_sizes(g);
         AllocList tmp;
         const size_t KM = (size_t)S->K * g->M;
         float* ys = dalloc<float>(tmp, KM, s);
-        LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, y, nullptr, g->M, S->K, ys);
+        LAUNCH(k_import_vk, grid_for((size_t)S->K * g->Mx), kThreads, 0, s, y, nullptr, g->Mx, g->M, S->K, ys);
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
         LAUNCH(k_apply_A, grid_for(g->M), kThreads, 0, s, a, ys, out);
         free_all(tmp, s);
@@ -1676,13 +1773,16 @@ int fbs_system_apply_A(fbs_system S, const float* y, float* out, fbs_stream stre
 
 int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_stream stream) {
     return guard("fbs_system_apply_precond", [&] {
+        pdl_break((cudaStream_t)stream);
         if (!S || !r || !out) throw Err(FBS_EINVAL, "null pointer");
         cudaStream_t s = (cudaStream_t)stream;
         fbs_grid g = S->g;
+        ensure_sizes(g);
         AllocList tmp;
         const size_t KM = (size_t)S->K * g->M;
         float* w = dalloc<float>(tmp, KM, s);
-        LAUNCH(k_import_vk, grid_for(KM), kThreads, 0, s, r, S->mu0, g->M, S->K, w);
+        zero_words(w, KM * sizeof(float), s);
+        LAUNCH(k_import_vk, grid_for((size_t)S->K * g->Mx), kThreads, 0, s, r, S->mu0, g->Mx, g->M, S->K, w);
         if (S->useHierP) {
             float* planar = dalloc<float>(tmp, KM, s);
             HierArgs h = S->hP;
@@ -1690,9 +1790,9 @@ int fbs_system_apply_precond(fbs_system S, const float* r, float* out, fbs_strea
             tree_lift<HIER_PLAIN>(S, h, w, s);
             tree_coarse<HIER_PLAIN>(S, h, a, 0, s);
             tree_level0<HIER_PLAIN>(S, h, a, w, planar, 0, s);
-            LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->M, S->K, out);
+            LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, nullptr, g->Mx, g->M, S->K, out);
         } else {
-            LAUNCH(k_precond_out, grid_for(g->M), kThreads, 0, s, w, S->mu0, nullptr, nullptr, 0, g->M, S->K, out);
+            LAUNCH(k_precond_out, grid_for(g->Mx), kThreads, 0, s, w, S->mu0, nullptr, nullptr, 0, g->Mx, g->M, S->K, out);
         }
         free_all(tmp, s);
     });

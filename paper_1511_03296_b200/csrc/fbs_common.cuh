@@ -21,6 +21,10 @@ fbs_allocator current_allocator();
 struct AllocList {
     std::vector<void*> ptrs;
     fbs_allocator al = current_allocator();
+    // arena (api.cu arena_reserve): later allocations are carved from it without a stream
+    // operation, so the kernels enqueued between them keep their programmatic (PDL) chaining
+    char* arena = nullptr;
+    size_t arenaLeft = 0;
 };
 
 // a block of mapped pinned host memory from the staging pool (api.cu pinned_get / pinned_put)
@@ -49,6 +53,8 @@ extern std::atomic<long long> g_launches;
 // resident (its blocks then fill SMs as ours retire), and waits until the previous grid has
 // completed and its memory is visible.  Data dependencies stay fully serial; only the launch
 // latency and the ramp between kernels overlap.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_entry() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -305,6 +311,9 @@ struct HierArgs {
     float* buf1T;           // [C][M1] (P y)_1 in tree order
     double* locT;           // [C][M1] inclusive prefix within the scan tile
     double* tileAgg;        // [C][nTiles1] tile totals
+    double* tileBase;       // [C][nTiles1] exclusive prefix of the tile totals within each frame
+    unsigned* tcount;       // [C][F] tiles of each (frame, channel) lifted so far (k_tree_lift)
+    int nfG;                // frames of this launch's group
     float* acc1T;           // [C][M1] projection of levels ≥ 1 onto level 1, tree order
     double* partial2;       // [F][bpf2][C] ρ partials of levels ≥ 1
     unsigned* counters;     // [F] last-block counters of the level-≥1 reductions
@@ -322,9 +331,7 @@ struct TreeOrder {
     int* tileFrameOff = nullptr;
     int* tileFrame = nullptr;
     int2* tileRange = nullptr;
-    int maxFrameTiles = 0;
-    int nTiles1 = 0;
-    std::vector<int> tileFrameOffH;  // host copy [F+1]
+    int nTiles1 = 0;  // capacity of the tile arrays (the count is tileFrameOff[F] on the device)
     int2* rng[kMaxLevels] = {};
 };
 
@@ -335,7 +342,7 @@ struct fbs_grid_s {
     std::vector<fbs::PinnedBlock> uploads;  // mapped pinned staging of the grid's small uploads
     double sxy = 0, sl = 0, suv = 0;
     int ncx = 0, ncy = 0;
-    int64_t ncells = 0, N = 0, M = 0;
+    int64_t ncells = 0, N = 0, M = 0;  // M: level-0 vertex CAPACITY (= N; stride of vertex vectors)
     int n_bistoch = 20;
     int dims = 5;               // D (5: XYLUV; 3: XYL of a grayscale reference)
     bool has_pyramid = false;
@@ -356,7 +363,14 @@ struct fbs_grid_s {
     int* frameLevels = nullptr;  // device [F]
     std::vector<int> frameLevelsH;
     float bistoch_residual = -1.f;
-    int L = 1;  // levels incl. base (max over frames)
+    int L = 1;  // levels carried by the hierarchy kernels (Lmax: an upper bound of every frame's)
+    int* err = nullptr;             // device: build invariant flags (checked by ensure_sizes)
+    std::vector<int64_t> capH;      // capacity of each level (level 0: N)
+    // exact sizes, read back on demand by the synchronous query/export calls (api.cu ensure_sizes)
+    bool sized = false;
+    int64_t Mx = 0;                 // level-0 vertices
+    int Lx = 1;                     // levels incl. base (max over frames)
+    std::vector<int64_t> levelMx;   // vertices of each level (all frames)
     fbs::Level lv[fbs::kMaxLevels];
     int64_t maxFrameM = 0;
     int64_t maxFrameM1 = 0;
@@ -398,6 +412,8 @@ struct fbs_system_s {
     float* buf1T = nullptr;                // [C][M1] hierarchy work arrays (tree_kernels.cuh)
     double* locT = nullptr;
     double* tileAgg = nullptr;
+    double* tileBase = nullptr;
+    unsigned* tcount = nullptr;
     float* acc1T = nullptr;
     double* partial2 = nullptr;
     int bpf2 = 1;

@@ -352,14 +352,20 @@ constexpr size_t kBsSmem = 2 * sizeof(BsStage) + 64;
 __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__ nbr,
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
-                                                 float* __restrict__ nout, int M, int vlo, int vhi, int first,
-                                                 float bdiag) {
-    pdl_entry();
+                                                 float* __restrict__ nout, const int* __restrict__ frameOff, int F,
+                                                 int f0, int f1, int first, float bdiag) {
+    // The frame offsets were written before the (serialised) launch of k_grid_neighbours that
+    // precedes every k_bistoch of a build, so they are complete when any k_bistoch block starts:
+    // they are read before waiting on the previous iteration (the first bulk copies go out as soon
+    // as the wait returns).
+    pdl_trigger();
+    const int M = frameOff[F], vlo = frameOff[f0], vhi = frameOff[f1];
+    pdl_wait();
     extern __shared__ __align__(128) unsigned char bs_smem[];
     BsStage* st = reinterpret_cast<BsStage*>(bs_smem);
     uint64_t* bar = reinterpret_cast<uint64_t*>(bs_smem + 2 * sizeof(BsStage));
-    // vertices [vlo, vhi) (whole frames): the chunks covering them; a chunk shared with a
-    // neighbouring range only writes its own vertices (no neighbour crosses a frame)
+    // vertices [vlo, vhi) = frames [f0, f1) (device counts): the chunks covering them; a chunk
+    // shared with a neighbouring range only writes its own vertices (no neighbour crosses a frame)
     const int cBeg = vlo / kBsChunk, nChunks = (vhi + kBsChunk - 1) / kBsChunk;
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);

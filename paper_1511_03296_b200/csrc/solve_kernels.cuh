@@ -749,24 +749,26 @@ __global__ void k_gm_weight(const float* __restrict__ x, const float* __restrict
     }
 }
 
-// planar [K][M] → canonical [M][K]
-__global__ void k_export_vk(const float* __restrict__ src, int64_t M, int K, float* __restrict__ dst) {
+// planar [K][stride] → canonical [M][K]; M = *Mdev (device count) when Mdev, else Mh
+__global__ void k_export_vk(const float* __restrict__ src, const int* __restrict__ Mdev, int64_t Mh, int64_t stride,
+                            int K, float* __restrict__ dst) {
     pdl_entry();
+    const int64_t M = Mdev ? (int64_t)*Mdev : Mh;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / K;
         const int k = (int)(i - v * K);
-        dst[i] = src[(size_t)k * M + v];
+        dst[i] = src[(size_t)k * stride + v];
     }
 }
 
-// canonical [M][K] → planar [K][M], optionally masked to live vertices (mu0 > 0)
-__global__ void k_import_vk(const float* __restrict__ src, const float* __restrict__ mask, int64_t M, int K,
-                            float* __restrict__ dst) {
+// canonical [M][K] → planar [K][stride], optionally masked to live vertices (mu0 > 0)
+__global__ void k_import_vk(const float* __restrict__ src, const float* __restrict__ mask, int64_t M, int64_t stride,
+                            int K, float* __restrict__ dst) {
     pdl_entry();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M * K; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = i / K;
         const int k = (int)(i - v * K);
-        dst[(size_t)k * M + v] = (mask && !(mask[v] > 0.f)) ? 0.f : src[i];
+        dst[(size_t)k * stride + v] = (mask && !(mask[v] > 0.f)) ? 0.f : src[i];
     }
 }
 
@@ -802,10 +804,12 @@ __global__ void k_blur(const int4* __restrict__ nbr, const float* __restrict__ x
         out[v] = bdiag * x[v] + nbr_sum(x, (int)v, nbr[v]);
 }
 
-// A y for planar y, written canonical [M][K] (debug / parity operator).
+// A y for planar y (stride a.M), written canonical [M][K], M = the grid's vertex count (debug /
+// parity operator).
 __global__ void k_apply_A(VecArgs a, const float* __restrict__ ys, float* __restrict__ out) {
     pdl_entry();
-    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < a.M; v += (int64_t)gridDim.x * blockDim.x)
+    const int64_t M = a.frameOff[a.nf];
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x)
         for (int k = 0; k < a.K; ++k)
             out[(size_t)v * a.K + k] =
                 apply_A_row(ys + (size_t)k * a.M, a.n, (int)v, a.nbr[v], a.lam, a.sc[v]);
@@ -814,13 +818,13 @@ __global__ void k_apply_A(VecArgs a, const float* __restrict__ ys, float* __rest
 // M⁻¹ r at level 0 for masked planar w, written canonical [M][K] (debug / parity operator).
 __global__ void k_precond_out(const float* __restrict__ w0, const float* __restrict__ mu0,
                               const int* __restrict__ parent0, const float* __restrict__ acc1, int64_t M1,
-                              int64_t M, int K, float* __restrict__ out) {
+                              int64_t M, int64_t stride, int K, float* __restrict__ out) {
     pdl_entry();
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < M; v += (int64_t)gridDim.x * blockDim.x) {
         for (int k = 0; k < K; ++k) {
             float s = 0.f;
             if (mu0[v] > 0.f) {
-                s = mu0[v] * w0[(size_t)k * M + v];
+                s = mu0[v] * w0[(size_t)k * stride + v];
                 if (acc1) s += acc1[(size_t)k * M1 + parent0[v]];
             }
             out[(size_t)v * K + k] = s;

@@ -62,15 +62,67 @@ __global__ void k_tree_top(const int* __restrict__ lvFrameOff, int F, int top, i
     }
 }
 
+// Levels of each frame: the first level with a single vertex (reading #8: halving until one
+// vertex per frame); a frame with ≤ 1 vertex has 1 level.  lvFrameOff [L][F + 1].
+__global__ void k_frame_levels(const int* __restrict__ lvFrameOff, int F, int L, int* __restrict__ frameLevels) {
+    pdl_entry();
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    if (f >= F) return;
+    const int F1 = F + 1;
+    int Lf = 1;
+    if (lvFrameOff[f + 1] - lvFrameOff[f] > 1) {
+        Lf = L;
+        for (int k = 1; k < L; ++k)
+            if (lvFrameOff[k * F1 + f + 1] - lvFrameOff[k * F1 + f] == 1) {
+                Lf = k + 1;
+                break;
+            }
+    }
+    frameLevels[f] = Lf;
+}
+
+// Prefix-scan tiles of the tree-ordered level 1: kScanTile positions, never crossing a frame.
+// Block f: tileFrameOff[f] (= Σ_{g<f} ⌈M1_g / kScanTile⌉; block 0 also writes [F]) and the ranges
+// and frame of frame f's tiles.  lv1 = level-1 frame offsets [F + 1].
+__global__ void k_scan_tiles(const int* __restrict__ lv1, int F, int* __restrict__ tileFrameOff,
+                             int2* __restrict__ tileRange, int* __restrict__ tileFrame) {
+    pdl_entry();
+    __shared__ int sh[33];
+    const int f = blockIdx.x;
+    int part = 0;  // tiles of frames g < f (+ block 0: all frames for tileFrameOff[F])
+    const int lim = (f == 0) ? F : f;
+    for (int g = threadIdx.x; g < lim; g += blockDim.x) part += (lv1[g + 1] - lv1[g] + kScanTile - 1) / kScanTile;
+    int tot;
+    (void)block_excl_scan(part, sh, &tot);
+    int before = 0;
+    if (f == 0) {
+        if (threadIdx.x == 0) {
+            tileFrameOff[0] = 0;
+            tileFrameOff[F] = tot;
+        }
+    } else {
+        before = tot;
+        if (threadIdx.x == 0) tileFrameOff[f] = before;
+    }
+    const int b0 = lv1[f], b1 = lv1[f + 1];
+    const int nt = (b1 - b0 + kScanTile - 1) / kScanTile;
+    for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+        const int a0 = b0 + t * kScanTile;
+        tileRange[before + t] = make_int2(a0, min(a0 + kScanTile, b1));
+        tileFrame[before + t] = f;
+    }
+}
+
 // level k → k−1: each level-k vertex hands consecutive sub-ranges (in canonical child order) of
 // its level-0 / level-1 tree ranges to its children.  cnt0 = P(1) of level k−1, cnt1 = level-1
 // descendants of level k−1 (k−1 ≥ 2).  k−1 = 1: writes tord1, csT; k−1 = 0: writes tord0;
 // k−1 ≥ 2: writes rng = (level-1 start, level-1 count).
-__global__ void k_tree_down(int km1, const int* __restrict__ childStart, const int* __restrict__ childList, int Mk,
-                            const int2* __restrict__ startK, const int* __restrict__ cnt0, const int* __restrict__ cnt1,
-                            int2* __restrict__ startKm1, int2* __restrict__ rngKm1, int* __restrict__ tord0,
-                            int* __restrict__ tord1, int* __restrict__ csT) {
+__global__ void k_tree_down(int km1, const int* __restrict__ childStart, const int* __restrict__ childList,
+                            const int* __restrict__ MkDev, const int2* __restrict__ startK, const int* __restrict__ cnt0,
+                            const int* __restrict__ cnt1, int2* __restrict__ startKm1, int2* __restrict__ rngKm1,
+                            int* __restrict__ tord0, int* __restrict__ tord1, int* __restrict__ csT) {
     pdl_entry();
+    const int Mk = *MkDev;  // level-k vertex count (device)
     for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < Mk; a += gridDim.x * blockDim.x) {
         int2 r = startK[a];
         for (int q = childStart[a]; q < childStart[a + 1]; ++q) {
@@ -95,9 +147,11 @@ __global__ void k_tree_down(int km1, const int* __restrict__ childStart, const i
 }
 
 // parent0T[v] = tree position of v's level-1 parent; csT[M1] = M0.
-__global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __restrict__ start1, int64_t M0,
-                              int64_t M1, int* __restrict__ parent0T, int* __restrict__ csT) {
+__global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __restrict__ start1,
+                              const int* __restrict__ M0Dev, const int* __restrict__ M1Dev, int* __restrict__ parent0T,
+                              int* __restrict__ csT) {
     pdl_entry();
+    const int64_t M0 = *M0Dev, M1 = *M1Dev;  // level-0 / level-1 vertex counts (device)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     for (int64_t v = t0; v < M0; v += stride) parent0T[v] = start1[parent0[v]].y;
@@ -107,11 +161,13 @@ __global__ void k_tree_finish(const int* __restrict__ parent0, const int2* __res
 // Ancestor tables of the level-2 vertices (k = 3..top, row k−3): ancId = the level-k ancestor,
 // ancRng = its level-1 range.  The PCG coarse pass then reads a whole ancestor chain in one
 // coalesced round instead of top−2 dependent (and, after each iteration's streams, DRAM) loads.
-__global__ void k_tree_anc(HierArgs h, int* __restrict__ ancId, int2* __restrict__ ancRng) {
+__global__ void k_tree_anc(HierArgs h, const int* __restrict__ M2Dev, int* __restrict__ ancId,
+                           int2* __restrict__ ancRng) {
     pdl_entry();
     const int top = h.L - 1;
-    const int64_t M2 = h.lv[2].M;
-    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < M2; a += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t M2 = h.M2;     // row stride (level-2 capacity)
+    const int64_t n2 = *M2Dev;   // level-2 vertex count (device)
+    for (int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; a < n2; a += (int64_t)gridDim.x * blockDim.x) {
         int an = (int)a;
         for (int k = 3; k <= top; ++k) {
             an = h.lv[k - 1].parent[an];
@@ -130,7 +186,7 @@ __global__ void k_tree_anc_mult(HierArgs h, const int* __restrict__ ancId, float
     const int F1 = h.F + 1;
     const int top = h.L - 1;
     const int fl = h.frameLevels[f];
-    const int64_t M2 = h.lv[2].M;
+    const int64_t M2 = h.M2;  // row stride (level-2 capacity)
     const int a0 = h.lvFrameOff[2 * F1 + f], a1 = h.lvFrameOff[2 * F1 + f + 1];
     for (int a = a0 + j * blockDim.x + threadIdx.x; a < a1; a += h.bpf2 * blockDim.x)
         for (int k = 3; k <= top; ++k) {
@@ -244,12 +300,15 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
 }
 
 // ================================================================ lift 0 → 1 and the prefix scan
-// One block = one scan tile of kScanTile consecutive tree positions of one frame; warp w lifts
-// positions [32w, 32w + 32): the children of its 32 level-1 vertices are one contiguous range of
-// level-0 tree positions, staged (coalesced index load + gather) in shared memory and summed by
-// each lane over its own children in canonical child order.  Then a fixed-tree fp64 block scan
-// gives the within-tile inclusive prefix and the tile total; the coarse pass scans the frame's
-// tile totals in shared memory (no inter-block signalling here).
+// Work item = (scan tile of kScanTile consecutive tree positions of one frame, channel); blocks
+// walk the items of their frame group (tile range read on the device).  Warp w lifts positions
+// [32w, 32w + 32): the children of its 32 level-1 vertices are one contiguous range of level-0
+// tree positions, staged (coalesced index load + gather) in shared memory and summed by each lane
+// over its own children in canonical child order.  Then a fixed-tree fp64 block scan gives the
+// within-tile inclusive prefix and the tile total.  The block that completes the last tile of a
+// (frame, channel) (per-frame counter) scans that frame's tile totals in a fixed order into the
+// exclusive tile bases the coarse pass reads (tileBase): deterministic, no shared-memory limit on
+// the frame size, and the scan is done once instead of once per coarse block.
 constexpr int kLiftStage = 256;
 
 __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*/, double* total) {
@@ -279,80 +338,125 @@ __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*
     return sh[w] + incl;
 }
 
+// exclusive prefix of frame fl's (group-local) tile totals of channel c → tileBase (fixed order)
+__device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int fl, double* sh) {
+    const int t0 = h.tileFrameOff[fl], nt = h.tileFrameOff[fl + 1] - t0;
+    const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + t0;
+    double* base = h.tileBase + (size_t)c * h.nTiles1 + t0;
+    double carry = 0.0;
+    for (int b = 0; b < nt; b += blockDim.x) {
+        const int tt = b + threadIdx.x;
+        const double x = (tt < nt) ? __ldcg(agg + tt) : 0.0;
+        double tot;
+        const double incl = block_incl_scan_d(x, sh, &tot);
+        if (tt < nt) base[tt] = carry + incl - x;
+        carry += tot;
+    }
+}
+
 // PDA: μ_1 = z_w(1) P(1)_1 / (P diagA)_1.
+constexpr int kLiftMaxItems = 32;  // (frame, channel) completions a block defers to its end
+constexpr int kCoarseTiles = 2048; // tile bases a coarse block scans into shared memory (16 KB)
+#ifndef FBS_LIFT_MINB
+#define FBS_LIFT_MINB 6  // ≤ 40 registers: 6 blocks per SM (28.6 µs in the step against 36.9 at 62 registers)
+#endif
 template <int MODE, bool KS = false>
-__global__ void __launch_bounds__(kScanTile) k_tree_lift(HierArgs h, const float* __restrict__ in0,
+__global__ void __launch_bounds__(kScanTile, FBS_LIFT_MINB) k_tree_lift(HierArgs h, const float* __restrict__ in0,
                                                        const int* __restrict__ active) {
     pdl_entry();
     __shared__ float stage[kScanTile / 32][kLiftStage];
     __shared__ double shs[32];
-    // KS: channel split (K > 1), grid nt · C, one channel per block
-    const int t = KS ? (int)(blockIdx.x % h.nt) : (int)blockIdx.x;
-    const int cB = KS ? (int)(blockIdx.x / h.nt) : 0, cE = KS ? cB + 1 : h.C;
-    const int2 tr = h.tileRange[t];  // tree positions [i0, i1) of this tile (one frame)
-    const int i0 = tr.x, i1 = tr.y;
+    __shared__ int sfc[kLiftMaxItems];   // (channel, group-local frame) of each finished item
+    __shared__ int sdone[kLiftMaxItems]; // 1: this block finished that (frame, channel)'s last tile
+    const int tB = h.tileFrameOff[0], nT = h.tileFrameOff[h.nfG] - tB;  // this group's tiles (device)
+    const int CW = KS ? h.C : 1;  // KS: channel split (K > 1), one channel per work item
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i = i0 + (int)threadIdx.x;
-    const bool valid = i < i1;
-    const int wa = min(i0 + 32 * w, i1), wb = min(i0 + 32 * w + 32, i1);
-    const int qa = h.csT[wa], qb = h.csT[wb];
-    const int myLo = valid ? h.csT[i] : 0, myHi = valid ? h.csT[i + 1] : 0;
-    for (int c = cB; c < cE; ++c) {
-        // PCG: a (frame, channel) that has stopped needs no lift (the coarse and level-0 passes skip it)
-        if (MODE == HIER_PCG && active && !active[(h.tileFrame[t] - h.f0) * h.C + c]) continue;
-        const float* src = in0 + (size_t)c * h.M0;
-        float acc = 0.f;
-        for (int qc = qa; qc < qb; qc += kLiftStage) {
-            const int n = min(kLiftStage, qb - qc);
-            constexpr int E = kLiftStage / 32;
-            int id[E];
-            float val[E];
-#pragma unroll
-            for (int e = 0; e < E; ++e) id[e] = (lane + 32 * e < n) ? __ldcs(h.tord0 + qc + lane + 32 * e) : -1;
-#pragma unroll
-            for (int e = 0; e < E; ++e) val[e] = (id[e] >= 0) ? src[id[e]] : 0.f;
-#pragma unroll
-            for (int e = 0; e < E; ++e)
-                if (lane + 32 * e < n) stage[w][lane + 32 * e] = val[e];
-            __syncwarp();
-            const int lo = max(myLo, qc), hi = min(myHi, qc + n);
-            for (int q = lo; q < hi; ++q) acc += stage[w][q - qc];
-            __syncwarp();
-        }
-        if (valid) h.buf1T[(size_t)c * h.M1 + i] = acc;
-        if (MODE == HIER_PDA && valid)
-            h.mu1T[i] = (1 < h.frameLevels[h.tileFrame[t]] && acc > 0.f)
-                            ? zw_count(h, 1, myHi - myLo, (double)acc) : 0.f;
-        double tot;
-        const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
-        if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
-        if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + h.tileFrameOff[0] + t] = tot;  // global tile id
+    int nDone = 0;  // items (× channels) of this block whose tile counts are still to be added
+    // add this block's finished tiles to their (frame, channel) counters — one atomic per entry, all
+    // in flight at once — and scan every frame whose last tile this block finished
+    auto settle = [&]() {
+        if (threadIdx.x == 0) __threadfence();  // this block's tile totals (written by thread 0)
         __syncthreads();
+        if ((int)threadIdx.x < nDone) {
+            const int fc = sfc[threadIdx.x], c = fc / h.nfG, fl = fc - c * h.nfG;
+            __threadfence();
+            unsigned* ctr = h.tcount + (size_t)c * h.F + h.f0 + fl;
+            const unsigned nft = (unsigned)(h.tileFrameOff[fl + 1] - h.tileFrameOff[fl]);
+            const bool last = atomicAdd(ctr, 1u) == nft - 1u;
+            if (last) *ctr = 0u;
+            sdone[threadIdx.x] = last;
+        }
+        __syncthreads();
+        for (int e = 0; e < nDone; ++e)
+            if (sdone[e]) {
+                __threadfence();
+                const int fc = sfc[e], c = fc / h.nfG;
+                tile_bases(h, c, fc - c * h.nfG, shs);
+            }
+        __syncthreads();
+        nDone = 0;
+    };
+    for (int item = blockIdx.x; item < nT * CW; item += gridDim.x) {
+        const int t = tB + (KS ? item % nT : item);  // global tile id
+        const int cB = KS ? item / nT : 0, cE = KS ? cB + 1 : h.C;
+        const int fl = h.tileFrame[t] - h.f0;  // group-local frame
+        const int2 tr = h.tileRange[t];  // tree positions [i0, i1) of this tile (one frame)
+        const int i0 = tr.x, i1 = tr.y;
+        const int i = i0 + (int)threadIdx.x;
+        const bool valid = i < i1;
+        const int wa = min(i0 + 32 * w, i1), wb = min(i0 + 32 * w + 32, i1);
+        const int qa = h.csT[wa], qb = h.csT[wb];
+        const int myLo = valid ? h.csT[i] : 0, myHi = valid ? h.csT[i + 1] : 0;
+        // a frame with more tiles than the coarse kernel scans in shared memory (kCoarseTiles) gets
+        // its tile bases from the block that lifts its last tile
+        const bool big = h.tileFrameOff[fl + 1] - h.tileFrameOff[fl] > kCoarseTiles;
+        for (int c = cB; c < cE; ++c) {
+            if (big) {
+                if (nDone == kLiftMaxItems) settle();
+                if (threadIdx.x == 0) sfc[nDone] = c * h.nfG + fl;
+                ++nDone;
+            }
+            // PCG: a (frame, channel) that has stopped needs no lift (the coarse and level-0
+            // passes skip it); its tiles still count towards the frame's scan
+            if (MODE == HIER_PCG && active && !active[fl * h.C + c]) continue;
+            const float* src = in0 + (size_t)c * h.M0;
+            float acc = 0.f;
+            for (int qc = qa; qc < qb; qc += kLiftStage) {
+                const int n = min(kLiftStage, qb - qc);
+                constexpr int E = kLiftStage / 32;
+                int id[E];
+                float val[E];
+#pragma unroll
+                for (int e = 0; e < E; ++e) id[e] = (lane + 32 * e < n) ? __ldcs(h.tord0 + qc + lane + 32 * e) : -1;
+#pragma unroll
+                for (int e = 0; e < E; ++e) val[e] = (id[e] >= 0) ? src[id[e]] : 0.f;
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+                    if (lane + 32 * e < n) stage[w][lane + 32 * e] = val[e];
+                __syncwarp();
+                const int lo = max(myLo, qc), hi = min(myHi, qc + n);
+                for (int q = lo; q < hi; ++q) acc += stage[w][q - qc];
+                __syncwarp();
+            }
+            if (valid) h.buf1T[(size_t)c * h.M1 + i] = acc;
+            if (MODE == HIER_PDA && valid)
+                h.mu1T[i] = (1 < h.frameLevels[fl] && acc > 0.f) ? zw_count(h, 1, myHi - myLo, (double)acc) : 0.f;
+            double tot;
+            const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
+            if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
+            if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + t] = tot;
+        }
     }
+    if (__syncthreads_or(nDone > 0)) settle();
 }
 
 // ================================================================ coarse values and their projection onto level 2
-// Π(j) = fp64 inclusive prefix of tree-ordered (P y)_1 of frame f up to position j; tb = the
-// frame's exclusive tile prefixes (shared memory)
+// Π(j) = fp64 inclusive prefix of tree-ordered (P y)_1 of frame f up to position j: the frame's
+// exclusive tile base (k_tree_lift) plus the within-tile prefix; tb = this channel's tile bases
+// from the frame's first tile
 __device__ __forceinline__ double tree_prefix(const HierArgs& h, const double* tb, int c, int fb, int j) {
     if (j < fb) return 0.0;
     return tb[(j - fb) / kScanTile] + __ldg(h.locT + (size_t)c * h.M1 + j);
-}
-
-// exclusive prefix of frame f's tile totals of channel c into shared memory (fixed order)
-__device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int f, double* tb, double* sh) {
-    const int t0 = h.tileFrameOff[f], nt = h.tileFrameOff[f + 1] - t0;
-    const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + t0;
-    double carry = 0.0;
-    for (int b = 0; b < nt; b += blockDim.x) {
-        const int tt = b + threadIdx.x;
-        const double x = (tt < nt) ? agg[tt] : 0.0;
-        double tot;
-        const double incl = block_incl_scan_d(x, sh, &tot);
-        if (tt < nt) tb[tt] = carry + incl - x;
-        carry += tot;
-    }
-    __syncthreads();
 }
 
 // One thread per level-2 vertex a (blocks per frame: h.bpf2): (P y)_a and those of its ancestors
@@ -369,9 +473,9 @@ __device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int f, doub
 template <int MODE, bool KS = false>
 __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
     pdl_entry();
-    extern __shared__ double tb[];  // [tiles of the frame]
     __shared__ double shd[32];
     __shared__ int sflag;
+    __shared__ double tbS[kCoarseTiles];  // the frame's exclusive tile bases (frames ≤ kCoarseTiles tiles)
     // KS: channel split (K > 1), grid nf · bpf2 · C, one channel per block group
     const int nfb = KS ? (int)(gridDim.x / h.C) : (int)gridDim.x;
     const int bx = KS ? (int)(blockIdx.x % nfb) : (int)blockIdx.x;
@@ -389,7 +493,22 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
         const bool act = (MODE != HIER_PCG) || first || a.sc_.active[fk];
         double rho = 0.0;
         if (act) {
-            tile_bases(h, c, f, tb, shd);
+            const int t0 = h.tileFrameOff[f], ntf = h.tileFrameOff[f + 1] - t0;
+            const double* tb = h.tileBase + (size_t)c * h.nTiles1 + t0;  // big frames: from k_tree_lift
+            if (ntf <= kCoarseTiles) {  // scan the frame's tile totals here (fixed order)
+                const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + t0;
+                double carry = 0.0;
+                for (int b = 0; b < ntf; b += blockDim.x) {
+                    const int tt = b + threadIdx.x;
+                    const double x = (tt < ntf) ? agg[tt] : 0.0;
+                    double tot;
+                    const double incl = block_incl_scan_d(x, shd, &tot);
+                    if (tt < ntf) tbS[tt] = carry + incl - x;
+                    carry += tot;
+                }
+                __syncthreads();
+                tb = tbS;
+            }
             if (MODE == HIER_PDA) {
                 for (int k = 2; k <= top; ++k) {
                     const HLevel& L = h.lv[k];

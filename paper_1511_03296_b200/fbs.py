@@ -171,9 +171,24 @@ class Grid:
     def __init__(self, handle, frames, H, W):
         self._h = handle
         self.frames, self.H, self.W = frames, H, W
-        n, m, lv = _i64(), _i64(), _i()
-        _check(_lib.fbs_grid_info(self._h, C.byref(n), C.byref(m), C.byref(lv), None, None, None))
-        self.N, self.M, self.levels = n.value, m.value, lv.value
+        self.N = frames * H * W
+        self._sizes = None  # (M, levels): data-dependent, read back on first use (one stream sync)
+
+    def _read_sizes(self):
+        if self._sizes is None:
+            m, lv = _i64(), _i()
+            _check(_lib.fbs_grid_info(self._h, None, C.byref(m), C.byref(lv), None, None, None))
+            self._sizes = (m.value, lv.value)
+        return self._sizes
+
+    @property
+    def M(self):
+        """Vertices (all frames).  The build is asynchronous: the first query synchronises."""
+        return self._read_sizes()[0]
+
+    @property
+    def levels(self):
+        return self._read_sizes()[1]
 
     @property
     def handle(self):
