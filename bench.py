@@ -331,6 +331,36 @@ def main():
     pixels_all = w.pixels * world
     value = pixels_all / 1e6 / (ms / 1e3 / args.steps)
 
+    # ---- the same step captured once into a CUDA graph and replayed (the build and the FIXED-mode
+    # solve only enqueue work, so the whole step is capturable); device time of K replays
+    graph_line = None
+    try:
+        cs = torch.cuda.Stream(dev)
+        cs.wait_stream(stream)
+        with torch.cuda.stream(cs):
+            step()
+        stream.wait_stream(cs)
+        torch.cuda.synchronize()
+        cg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(cg):
+            step()
+        cg.replay()
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            cg.replay()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = max_over_ranks(g0.elapsed_time(g1))
+        graph_line = {"value": pixels_all / 1e6 / (gms / 1e3 / args.steps), "unit": "MP/s",
+                      "ms_per_step": gms / args.steps,
+                      "note": "grid build + solve + release captured once with torch.cuda.graph and replayed"}
+        del cg
+    except Exception as exc:  # noqa: BLE001 (reported, not fatal)
+        graph_line = {"error": str(exc)[:200]}
+
     # ---- per-kernel device times over a second pass of the same K steps (events per launch)
     g_info = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=20)
     M = g_info.M
@@ -634,6 +664,22 @@ def main():
                 gg.close()
 
             ms_c = dev_ms(run_cfg)
+            graph_ms = None
+            if wc.mode == "fixed":  # FIXED-mode steps are enqueue-only: the same call as a CUDA graph
+                try:
+                    cs2 = torch.cuda.Stream(dev)
+                    cs2.wait_stream(stream)
+                    with torch.cuda.stream(cs2):
+                        run_cfg()
+                    stream.wait_stream(cs2)
+                    torch.cuda.synchronize()
+                    gq = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(gq):
+                        run_cfg()
+                    graph_ms = dev_ms(gq.replay, reps=10)
+                    del gq
+                except Exception:  # noqa: BLE001
+                    graph_ms = None
             gg = fbs.grid_build(rgbc, wc.sigma_xy, wc.sigma_l, wc.sigma_uv, n_bistoch=wc.n_bistoch,
                                 build_pyramid=pyr)
             _, S_ = fbs.solve(gg, tc, cc, wc.lam, keep_system=True, **opts)
@@ -641,6 +687,7 @@ def main():
             S_.close()
             gg.close()
             cfg_rows[name] = {"ms": ms_c, "MP_per_s": wc.pixels / 1e6 / (ms_c / 1e3), "pcg_iterations": pcg_its,
+                              "graph_ms": graph_ms,
                               "shape": f"{wc.frames}x{wc.H}x{wc.W}, K={wc.K}",
                               "pyramid_built": pyr,
                               "solver": f"{wc.precond}+{wc.init}, " +
@@ -699,6 +746,7 @@ def main():
                 "config": workload_config(args, world) | {"vertices_per_gpu": M,
                                                    "levels": int(info["levels"])},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "extras": extras,
+                "graph": graph_line,
                 "clocks": clk, "stages_ms_per_step": stages_ms, "pcg_iteration_rate": pcg_iteration_rate,
                 "bistoch_iteration_rate": bistoch_rate, "kernels": kernels,
                 "profiled_ms_per_step": prof_ms / args.steps}

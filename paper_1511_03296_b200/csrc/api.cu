@@ -656,8 +656,10 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             T.tileFrame = dalloc<int>(A, T.nTiles1, s);
             LAUNCH(k_scan_tiles, F, 256, 0, s, lvAll + (F + 1), F, T.tileFrameOff, T.tileRange, T.tileFrame);
         }
-        g->maxFrameM1 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM, L > 1 ? cap[1] : 1));
-        g->maxFrameM2 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM1, L > 2 ? cap[2] : 1));
+        // launch-size heuristics for the level-1 / level-2 kernels: each level typically holds ~1/5
+        // of the vertices below it (Appendix A of SURVEY.md; 1/4 here to err towards more blocks)
+        g->maxFrameM1 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM / 4, L > 1 ? cap[1] : 1));
+        g->maxFrameM2 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM1 / 4, L > 2 ? cap[2] : 1));
     } catch (...) {
         free_all(g->allocs, s);
         for (auto& b : g->uploads) pinned_put(b, s);
