@@ -499,10 +499,22 @@ def main():
     it_bytes = sum(kernel_bytes(k, M, lv, w.pixels) for k in
                    ("k_spmv2", "k_hier_level0<UPDATE>", "k_tree_lift<PCG>", "k_tree_level0<PCG>"))
     pcg_iteration_rate = {"algorithmic_bytes": it_bytes, "GBps": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9,
-                          "frac": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9 / 6550.7,
+                          "frac": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9 / 6550.7,  # of measured copy BW
                           "note": "one PCG iteration over all frames (both groups): spmv + update + lift + level0 "
                                   "byte models (coarse levels unmodelled) over its wall time, measured as "
                                   "(solve with 25 iterations - solve with 1) / 24, median of 5 interleaved rounds"}
+    # SURVEY.md §8(d)'s floor for one hierarchical PCG iteration: s + 4 + 32K B per level-0 vertex
+    # (s = 16 B neighbour structure; diag/M⁻¹; x, r, d read+write; q round trip) plus the pyramid's
+    # 2·r·(4K + 4) + 4r with r = Σ_{k≥1} M_k / M (lift + project + μ), K = 1
+    r_lv = sum(lv[1:]) / max(M, 1)
+    floor_bpv = 16 + 4 + 32 + 2 * r_lv * 8 + 4 * r_lv
+    t_it = pcg24 / (ITERS - 1) * 1e-3
+    pcg_iteration_rate["floor_bytes"] = floor_bpv * M
+    pcg_iteration_rate["floor_bytes_per_vertex"] = floor_bpv
+    pcg_iteration_rate["modelled_bytes_per_vertex"] = it_bytes / max(M, 1)
+    pcg_iteration_rate["floor_GBps"] = floor_bpv * M / t_it / 1e9
+    pcg_iteration_rate["floor_frac"] = floor_bpv * M / t_it / 1e9 / 6550.7
+    pcg_iteration_rate["modelled_over_floor"] = it_bytes / max(floor_bpv * M, 1)
     bistoch_rate = {"algorithmic_bytes": kernel_bytes("k_bistoch", M, lv, w.pixels),
                     "GBps": 20 * kernel_bytes("k_bistoch", M, lv, w.pixels) / (bs_wall * 1e-3) / 1e9 if bs_wall else None,
                     "note": "one Alg. 1 iteration over all frames (all groups) over its wall time, measured as "

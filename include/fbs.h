@@ -11,15 +11,22 @@
  *   solve           PCG, Alg. 2                          PAPER.md:710-742 (Supp. Sec. 1)
  *   slice           x̂ = Sᵀ ŷ                             PAPER.md:137-140 (Eq. solution)
  *   backward        ∂f/∂t, ∂f/∂c by one more solve       PAPER.md:191-201 (Sec. 3)
- * Readings of the paper where it is silent or ambiguous are numbered #1..#19 in
- * DESIGN.md §3 (same numbering as SURVEY.md §8(c)).
+ * Readings of the paper where it is silent or ambiguous are numbered in DESIGN.md §3: #1..#19
+ * follow SURVEY.md §8(c); #20..#29 are this build's own and change what the kernels compute:
+ * #20 difference-form A, #21 σxy cell limit, #22 pyramid cell capacity, #23 ρ from the lift,
+ * #24 coarse lifts as prefix differences, #25 robust objective, #26 low-rank row selection,
+ * #27 D = 3 grid, #28 domain-transform filter, #29 fixed-count parity on unstable iterates.
  *
  * Conventions (all entry points)
  *   - Every pointer argument named *_dev is DEVICE memory owned by the caller and only
  *     borrowed for the enqueued work; pointers named *_host are HOST memory.
- *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).
- *     fbs_grid_build synchronises `stream` once at its end (to learn the data-dependent
- *     vertex and pyramid-level counts); all other compute calls only enqueue.
+ *   - Work is enqueued on `stream` (a cudaStream_t; NULL = legacy default stream).  The
+ *     compute calls only enqueue: fbs_grid_build sizes its buffers by capacities known on the
+ *     host (vertices ≤ pixels, pyramid level k ≤ min(level k−1, cells_k × codes_k)) and its
+ *     kernels read the data-dependent counts on the device, so grid build + FIXED-mode solve
+ *     (+ slice, backward, low-rank) can be captured into a CUDA graph and replayed.  The
+ *     exceptions are stated per call: TOL-mode solves poll the device's active count from the
+ *     host; the query and export calls (fbs_grid_info, *_export, *_stats) synchronise.
  *   - Layouts: RGB is interleaved uint8 [frames][H][W][3]; pixel vectors are planar float
  *     [frames][K][H][W] (pixel p = y·W + x); confidences float [frames][H][W];
  *     vertex vectors are float [M][K] in CANONICAL vertex order: ascending packed key
@@ -29,9 +36,9 @@
  *     fbs_system_stats after the stream has been synchronised.  No exception crosses
  *     the ABI.  There is no CPU fallback: without a CUDA device every call fails with
  *     FBS_ECUDA.
- *   - Handles own their internal device buffers (allocated stream-ordered from the
- *     device's default memory pool) and release them in *_destroy, which enqueues the
- *     frees on the stream the handle was created on.
+ *   - Handles own their internal device buffers (one stream-ordered arena per handle, from the
+ *     device's default memory pool or a caller allocator) and release them in *_destroy, which
+ *     enqueues the frees on the stream the handle was created on.
  *   - Thread safety: a built grid is immutable; concurrent fbs_solve calls on distinct
  *     streams with distinct outputs are allowed.  A system handle must not be used by
  *     two streams at once.
@@ -104,7 +111,9 @@ typedef struct {
  *   free(ptr, ctx, stream)    → release; all work the library enqueued on its buffers is
  *                               ordered on `stream` before this point.
  * fbs_set_allocator applies to handles created afterwards (a handle keeps the allocator it was
- * created with); NULL restores the default.  Not thread-safe against concurrent handle creation. */
+ * created with and calls its free when destroyed, so the callbacks must stay valid until then);
+ * NULL restores the default.  Returned pointers must be 16-byte aligned (vector loads and bulk
+ * copies; FBS_EINVAL otherwise).  Not thread-safe against concurrent handle creation. */
 typedef struct {
     void* (*alloc)(size_t bytes, void* ctx, fbs_stream stream);
     void (*free)(void* ptr, void* ctx, fbs_stream stream);
@@ -123,16 +132,20 @@ void fbs_default_solve_opts(fbs_solve_opts* o);
  *             (⌊x/σxy⌋, ⌊y/σxy⌋, ⌊Yn/256σl⌋, ⌊Un/256σuv⌋, ⌊Vn/256σuv⌋), each one IEEE
  *             fp64 division then floor (reading #2).
  * Then runs opts->n_bistoch iterations of Alg. 1 and (if opts->build_pyramid) builds the
- * pyramid of PAPER.md:745-766 (reading #8).  Synchronises `stream` twice, for the vertex and
- * the pyramid level counts (host allocation sizes); the rest is enqueued asynchronously.
+ * pyramid of PAPER.md:745-766 (reading #8).  Enqueue-only (no host synchronisation): buffers
+ * are sized by capacities (memory ≈ 200 B per pixel with the pyramid), counts live on the device.
  * Errors: FBS_EINVAL if a pointer is NULL, frames ∉ [1, 256], height or width ∉
- * [1, 65535·σxy], σxy < 1, σl < 1 or σuv < 1 (8-bit key fields), or a σxy cell would hold
- * more than 64 pixels (σxy > 8); FBS_ELIMIT (see above); FBS_ENOMEM; FBS_ECUDA. */
+ * [1, 65535·σxy], σl < 1 or σuv < 1 (8-bit key fields), σxy < 1, or σxy > 8: a σxy cell is one
+ * warp of ≤ 64 pixels (reading #21; every setting of the paper uses σxy ≤ 8, PAPER.md:433, :515,
+ * :974); FBS_ENOMEM; FBS_ECUDA.  The build's internal invariant checks (FBS_ELIMIT, FBS_ECUDA)
+ * are reported by the first synchronous query (fbs_grid_info / fbs_grid_export). */
 int fbs_grid_build(const uint8_t* rgb_dev, int frames, int height, int width, double sigma_xy,
                    double sigma_l, double sigma_uv, const fbs_grid_opts* opts, fbs_stream stream,
                    fbs_grid* out);
 
-/* Sizes of a built grid (host outputs; any pointer may be NULL).
+/* Sizes of a built grid (host outputs; any pointer may be NULL).  The counts are data-dependent
+ * and computed on the device: the first call that asks for more than n_pixels synchronises the
+ * grid's stream once (the values are cached with the grid).
  *   frame_vertices_host  int64 [frames]      vertices per frame
  *   level_vertices_host  int64 [n_levels]    Σ over frames of level-k vertex counts
  *   frame_levels_host    int32 [frames]      pyramid levels of each frame (until 1 vertex) */
@@ -174,8 +187,9 @@ void fbs_grid_destroy(fbs_grid g);
  * `stream` (they are independent systems); FIXED mode only enqueues work, TOL mode polls each
  * group's active count from the host one 8-iteration chunk behind and returns when all have
  * stopped (FBS_TOL_GRAPH=1: a device-side CUDA-graph loop instead, no host polls).
- * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4); the reduced solve
- * runs max_f t_f channels (one extra host synchronisation), and sys_out must then be NULL.
+ * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4): the reduced solve
+ * carries K channels of which those at or above the frame's kept rank t_f have zero right-hand
+ * sides and retire at iteration 0 (no host synchronisation); sys_out must then be NULL.
  * Errors: FBS_EINVAL (NULL pointer, K ∉ [1, 64], λ ≤ 0 or not finite, HIER precond/init
  * on a grid built without pyramid, bad opts); FBS_ENOMEM; FBS_ECUDA. */
 int fbs_solve(fbs_grid g, const float* t_dev, int K, const float* c_dev, double lambda,
@@ -234,7 +248,9 @@ int fbs_system_export(fbs_system sys, float* sc_host, float* b_host, float* diag
 
 void fbs_system_destroy(fbs_system sys);
 
-/* ---------------------------------------------------------------- operators (device, async) */
+/* ---------------------------------------------------------------- operators (device, async)
+ * fbs_blur and the fbs_system_apply_* hooks take caller vectors of exactly M vertices: their
+ * first use on a grid reads M back (one synchronisation, as fbs_grid_info). */
 /* x̂ = Sᵀy: y_dev float [M][K] canonical → x_dev float [frames][K][H][W]. */
 int fbs_slice(fbs_grid g, const float* y_dev, int K, float* x_dev, fbs_stream stream);
 /* out = S p: p_dev float [frames][K][H][W] → out_dev float [M][K]. */
