@@ -504,9 +504,10 @@ def main():
                                   "byte models (coarse levels unmodelled) over its wall time, measured as "
                                   "(solve with 25 iterations - solve with 1) / 24, median of 5 interleaved rounds"}
     # SURVEY.md §8(d)'s floor for one hierarchical PCG iteration: s + 4 + 32K B per level-0 vertex
-    # (s = 16 B neighbour structure; diag/M⁻¹; x, r, d read+write; q round trip) plus the pyramid's
-    # 2·r·(4K + 4) + 4r with r = Σ_{k≥1} M_k / M (lift + project + μ), K = 1
-    r_lv = sum(lv[1:]) / max(M, 1)
+    # (s = 16 B neighbour structure; diag/M⁻¹; x, r, d read+write; q round trip) plus the
+    # hierarchy's 2·r·(4K + 4) + 4r with r = Σ_{k≥0} M_k / M (lift + project + μ over all levels,
+    # level 0 included: ≈ 1.23 in the survey), K = 1
+    r_lv = sum(lv) / max(M, 1)
     floor_bpv = 16 + 4 + 32 + 2 * r_lv * 8 + 4 * r_lv
     t_it = pcg24 / (ITERS - 1) * 1e-3
     pcg_iteration_rate["floor_bytes"] = floor_bpv * M
