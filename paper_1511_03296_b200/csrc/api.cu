@@ -499,7 +499,9 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // frames in Gb groups on Gb streams (frames are independent: no neighbour crosses a frame), so
         // one group's kernel boundaries overlap the other's work; each group's launches take 1/Gb of
         // the resident blocks
-        int Gb = std::min(F, 4);  // 1: 5.46, 2: 5.38, 4: 5.34, 8: 5.41 ms per bench step
+        // round 1 (host-sized launches): 1: 5.46, 2: 5.38, 4: 5.34, 8: 5.41 ms per bench step;
+        // round 2 (device-read frame ranges, arena layout): 1: 5.29, 2: 5.23, 4: 5.33 ms
+        int Gb = std::min(F, 2);
         if (const char* e = std::getenv("FBS_BS_GROUPS")) Gb = std::max(1, std::min(F, std::atoi(e)));  // A/B
         cudaEvent_t bsFork = nullptr;
         std::vector<cudaEvent_t> bsJoin(Gb, nullptr);
