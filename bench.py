@@ -388,7 +388,7 @@ def main():
     # its per-launch rate is a lower bound on the kernel's own, and the summed event times of a
     # grouped kernel overstate its share of the step G-fold (wall share ≈ sum / G).
     G = max(1, min(int(os.environ.get("FBS_PCG_GROUPS", "2") or 2), w.frames))
-    Gb = max(1, min(int(os.environ.get("FBS_BS_GROUPS", "4") or 4), w.frames))
+    Gb = max(1, min(int(os.environ.get("FBS_BS_GROUPS", "2") or 2), w.frames))
     PCG_GROUPED = ("k_spmv2", "k_hier_level0<UPDATE>", "k_tree_lift<PCG>", "k_tree_coarse<PCG>", "k_tree_level0<PCG>",
                    "k_hier_level0<UPDATE,LAST>", "k_hier_level0<RESID>", "k_init_scalars")
 
