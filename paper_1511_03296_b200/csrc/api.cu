@@ -740,6 +740,9 @@ HierArgs make_hier(fbs_system S, int C, double alpha, double beta) {
     h.nt = g->tree.nTiles1;  // capacity (the lift reads the group's tile range on the device)
     h.nfG = g->F;
     h.f0 = 0;
+    // FBS_COARSE_TILES (tests): frames with more level-1 scan tiles take the lift's tile-base path
+    h.coarseTiles = kCoarseTiles;
+    if (const char* e = std::getenv("FBS_COARSE_TILES")) h.coarseTiles = std::max(0, std::min(kCoarseTiles, std::atoi(e)));
     for (int k = 0; k < g->L; ++k) {
         HLevel& v = h.lv[k];
         v.M = (k == 0) ? g->M : g->lv[k].M;

@@ -314,6 +314,7 @@ struct HierArgs {
     double* tileBase;       // [C][nTiles1] exclusive prefix of the tile totals within each frame
     unsigned* tcount;       // [C][F] tiles of each (frame, channel) lifted so far (k_tree_lift)
     int nfG;                // frames of this launch's group
+    int coarseTiles;        // frames with more tiles get their tile bases from the lift (≤ kCoarseTiles)
     float* acc1T;           // [C][M1] projection of levels ≥ 1 onto level 1, tree order
     double* partial2;       // [F][bpf2][C] ρ partials of levels ≥ 1
     unsigned* counters;     // [F] last-block counters of the level-≥1 reductions

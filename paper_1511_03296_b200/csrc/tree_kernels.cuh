@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(kScanTile, FBS_LIFT_MINB) k_tree_lift(HierArgs
         const int myLo = valid ? h.csT[i] : 0, myHi = valid ? h.csT[i + 1] : 0;
         // a frame with more tiles than the coarse kernel scans in shared memory (kCoarseTiles) gets
         // its tile bases from the block that lifts its last tile
-        const bool big = h.tileFrameOff[fl + 1] - h.tileFrameOff[fl] > kCoarseTiles;
+        const bool big = h.tileFrameOff[fl + 1] - h.tileFrameOff[fl] > h.coarseTiles;
         for (int c = cB; c < cE; ++c) {
             if (big) {
                 if (nDone == kLiftMaxItems) settle();
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
         if (act) {
             const int t0 = h.tileFrameOff[f], ntf = h.tileFrameOff[f + 1] - t0;
             const double* tb = h.tileBase + (size_t)c * h.nTiles1 + t0;  // big frames: from k_tree_lift
-            if (ntf <= kCoarseTiles) {  // scan the frame's tile totals here (fixed order)
+            if (ntf <= h.coarseTiles) {  // scan the frame's tile totals here (fixed order)
                 const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + t0;
                 double carry = 0.0;
                 for (int b = 0; b < ntf; b += blockDim.x) {

@@ -496,3 +496,19 @@ def test_launch_counter_and_profile():
     assert fbs.launch_count() > n0
     assert rep["k_spmv2"][0] == 3 and rep["k_direction2"][0] == 3 and rep["k_grid_sort"][0] == 1
     assert sum(v[0] for v in rep.values()) == fbs.launch_count() - n0
+
+
+def test_large_frame_tile_base_path(monkeypatch):
+    """Frames with more level-1 scan tiles than the coarse kernel scans in shared memory take their
+    tile bases from the lift's last block (k_tree_lift settle); forcing every frame onto that path
+    (FBS_COARSE_TILES=0) gives bit-identical results, multi-frame and multi-channel."""
+    rgb, t, c = small(K=3, frames=3, W=120, H=90, cells=9)
+    g = fbs.grid_build(dev(rgb), 8.0, 4.0, 3.0)
+    kw = dict(precond="hier", init="hier", mode="fixed", iters=12)
+    x0 = fbs.solve(g, dev(t), dev(c), 6.0, **kw)
+    monkeypatch.setenv("FBS_COARSE_TILES", "0")
+    x1 = fbs.solve(g, dev(t), dev(c), 6.0, **kw)
+    x2 = fbs.solve(g, dev(t[:, :1]), dev(c), 6.0, **kw)
+    monkeypatch.delenv("FBS_COARSE_TILES")
+    x3 = fbs.solve(g, dev(t[:, :1]), dev(c), 6.0, **kw)
+    assert torch.equal(x0, x1) and torch.equal(x2, x3)
