@@ -231,12 +231,15 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
         if (SRC != HSRC_UPDATE || a.sc_.active[fk]) {
             const size_t off = (size_t)k * a.M;
             const float al = (SRC == HSRC_UPDATE) ? (float)a.sc_.alpha[fk] : 0.f;
-            for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += kUpB * stride) {
-                float rv[kUpB], mv[kUpB];
+            // the initial residual applies A per vertex (gathers): one vertex per round keeps its
+            // register count, and with it the occupancy, of a gather kernel
+            constexpr int UB = (SRC == HSRC_RESID) ? 1 : kUpB;
+            for (int vb = v0 + j * blockDim.x + threadIdx.x; vb < v1; vb += UB * stride) {
+                float rv[UB], mv[UB];
                 if (SRC == HSRC_UPDATE) {
-                    float xv[kUpB], dv[kUpB], qv[kUpB];
+                    float xv[UB], dv[UB], qv[UB];
 #pragma unroll
-                    for (int u = 0; u < kUpB; ++u) {
+                    for (int u = 0; u < UB; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
                             if (FINISH_LAST) {
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < kUpB; ++u) {
+                    for (int u = 0; u < UB; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
                             if (FINISH_LAST) a.x[off + v] = xv[u] + al * dv[u];
@@ -258,7 +261,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     }
                 } else {
 #pragma unroll
-                    for (int u = 0; u < kUpB; ++u) {
+                    for (int u = 0; u < UB; ++u) {
                         const int v = vb + u * stride;
                         if (v < v1) {
                             rv[u] = a.b[off + v];
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < kUpB; ++u) {
+                for (int u = 0; u < UB; ++u) {
                     const int v = vb + u * stride;
                     if (v >= v1) continue;
                     a.r[off + v] = rv[u];
