@@ -65,6 +65,10 @@ int pdl_break_mask() {  // DEBUG A/B: which operations break the PDL chain (bit 
     return m;
 }
 void pdl_break(cudaStream_t s, int kind);
+bool pdl_every_level() {  // DEBUG A/B: serialise every pyramid level, not only the first
+    static const bool on = std::getenv("FBS_PDL_EVERY_LEVEL") != nullptr;
+    return on;
+}
 void pdl_break(cudaStream_t s) { pdl_break(s, 4); }
 void pdl_break(cudaStream_t s, int kind) {
     if (!(pdl_break_mask() & kind)) return;
@@ -587,7 +591,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             const int64_t st2n = std::max<int64_t>(1, (L.ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems));
             unsigned long long* st2 = st2All + st2Off[k];
             unsigned* ctr2 = reinterpret_cast<unsigned*>(st2 + st2n);  // scan tile counter, scratch bump
-            pdl_break(s, 32);
+            if (k == 1 || pdl_every_level()) pdl_break(s, 32);
             LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
             LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2,
