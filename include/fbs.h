@@ -185,7 +185,7 @@ void fbs_grid_destroy(fbs_grid g);
  * Each (frame, channel) runs its own PCG scalars and stopping rule (reading #13).  The frames are
  * split into groups whose PCGs run concurrently on side streams forked from and joined to
  * `stream` (they are independent systems); FIXED mode only enqueues work, TOL mode polls each
- * group's active count from the host one 8-iteration chunk behind and returns when all have
+ * group's active count from the host one 4-iteration chunk behind and returns when all have
  * stopped (FBS_TOL_GRAPH=1: a device-side CUDA-graph loop instead, no host polls).
  * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4): the reduced solve
  * carries K channels of which those at or above the frame's kept rank t_f have zero right-hand

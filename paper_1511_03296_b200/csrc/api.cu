@@ -1036,7 +1036,7 @@ bool tol_graph(fbs_system S, const VecArgs& a, cudaStream_t s) {
 }
 
 // TOL polling for one or more independent PCGs (frame groups) on their own streams: each gets
-// chunks of 8 iterations in turn, and the host reads each one's active count (a copy kernel
+// chunks of 4 iterations in turn, and the host reads each one's active count (a copy kernel
 // into mapped pinned memory) one chunk behind; a group whose count reached 0 gets no more.
 struct PcgRun {
     VecArgs a;
@@ -1044,7 +1044,11 @@ struct PcgRun {
     cudaStream_t s;
 };
 void tol_poll(fbs_system S, std::vector<PcgRun>& runs) {
-    const int n = (int)runs.size(), chunk = 8;
+    const int n = (int)runs.size();
+    static const int chunk = [] {
+        const char* e = std::getenv("FBS_TOL_CHUNK");  // A/B
+        return (e && e[0]) ? std::max(1, std::min(64, std::atoi(e))) : 4;  // 4: configs[0,1,3] 2-6 % faster than 8
+    }();
     PinnedBlock pb = pinned_get(2 * n * sizeof(int));
     int* pin = static_cast<int*>(pb.p);
     std::vector<cudaEvent_t> ev(2 * n, nullptr);
