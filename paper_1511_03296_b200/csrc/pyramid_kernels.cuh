@@ -78,8 +78,8 @@ __device__ __forceinline__ CoarseCell coarse_cell(int64_t C, const int* __restri
 
 // Bitonic sort of 32·E keys held in a warp's registers, blocked layout (lane l holds elements
 // l·E .. l·E + E − 1): strides ≥ E exchange across lanes with shuffles, smaller ones inside a lane.
-template <int E>
-__device__ __forceinline__ void warp_bitonic(unsigned long long (&key)[E]) {
+template <int E, typename KeyT = unsigned long long>
+__device__ __forceinline__ void warp_bitonic(KeyT (&key)[E]) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int kk = 2; kk <= 32 * E; kk <<= 1) {
@@ -89,7 +89,7 @@ __device__ __forceinline__ void warp_bitonic(unsigned long long (&key)[E]) {
 #pragma unroll
                 for (int e = 0; e < E; ++e) {
                     const int i = lane * E + e;
-                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, key[e], sd / E);
+                    const KeyT o = __shfl_xor_sync(0xffffffffu, key[e], sd / E);
                     const bool keepMin = ((i & sd) == 0) == ((i & kk) == 0);
                     key[e] = keepMin ? (key[e] < o ? key[e] : o) : (key[e] < o ? o : key[e]);
                 }
@@ -99,7 +99,7 @@ __device__ __forceinline__ void warp_bitonic(unsigned long long (&key)[E]) {
                     const int pe = e ^ sd;
                     if (pe > e) {
                         const bool asc = ((lane * E + e) & kk) == 0;
-                        const unsigned long long a = key[e], b = key[pe];
+                        const KeyT a = key[e], b = key[pe];
                         const bool sw = (a > b) == asc;
                         key[e] = sw ? b : a;
                         key[pe] = sw ? a : b;
@@ -116,26 +116,35 @@ __device__ __forceinline__ unsigned long long child_key(const uint64_t* __restri
     return ((unsigned long long)halve_code((uint32_t)(keysK[gch] & 0xffffffu)) << 32) | (unsigned)gch;
 }
 
-// ≤ 32·E children sorted in registers; heads (first child of each parent code) → parent ranks.
+// ≤ 32·E ≤ 128 children sorted in registers as 32-bit keys (halved code ‖ 7-bit child index in
+// the cell: 64-bit compares ran the math pipe at its limit); the child index orders exactly like the
+// global child id (row 2CY's range precedes row 2CY+1's), so the order equals that of
+// (code, child id).  Heads (first child of each parent code) → parent ranks.
 template <int E>
 __device__ __forceinline__ int pyr_sort_regs(const uint64_t* __restrict__ keysK, const CoarseCell& cc, int nch,
                                              int* __restrict__ childListN, int* __restrict__ rankS) {
+    static_assert(32 * E <= 128, "7-bit child index");
     const int lane = threadIdx.x & 31;
-    unsigned long long key[E];
+    uint32_t key[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         const int i = lane * E + e;
-        key[e] = (i < nch) ? child_key(keysK, cc, i) : ~0ull;
+        uint32_t k = 0xffffffffu;
+        if (i < nch) {
+            const int gch = (i < cc.n0) ? cc.s0 + i : cc.s1 + (i - cc.n0);
+            k = (halve_code((uint32_t)(keysK[gch] & 0xffffffu)) << 7) | (uint32_t)i;
+        }
+        key[e] = k;
     }
-    warp_bitonic<E>(key);
-    const uint32_t hiPrevLane = __shfl_up_sync(0xffffffffu, (uint32_t)(key[E - 1] >> 32), 1);
+    warp_bitonic<E, uint32_t>(key);
+    const uint32_t hiPrevLane = __shfl_up_sync(0xffffffffu, key[E - 1] >> 7, 1);
     int heads = 0;
     unsigned hm = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
         const int i = lane * E + e;
-        const uint32_t prev = (e == 0) ? hiPrevLane : (uint32_t)(key[e - 1] >> 32);
-        const bool head = i < nch && (i == 0 || (uint32_t)(key[e] >> 32) != prev);
+        const uint32_t prev = (e == 0) ? hiPrevLane : (key[e - 1] >> 7);
+        const bool head = i < nch && (i == 0 || (key[e] >> 7) != prev);
         hm |= (unsigned)head << e;
         heads += head;
     }
@@ -151,20 +160,17 @@ __device__ __forceinline__ int pyr_sort_regs(const uint64_t* __restrict__ keysK,
         const int i = lane * E + e;
         if (i < nch) {
             r += (hm >> e) & 1u;
-            childListN[cc.cOff + i] = (int)(key[e] & 0xffffffffull);
+            const int li = (int)(key[e] & 127u);
+            childListN[cc.cOff + i] = (li < cc.n0) ? cc.s0 + li : cc.s1 + (li - cc.n0);
             rankS[cc.cOff + i] = r;
         }
     }
     return __shfl_sync(0xffffffffu, incl, 31);
 }
 
-#ifndef FBS_PYR_REGS_MAX
-#define FBS_PYR_REGS_MAX 128
-#endif
-constexpr int kPyrRegsMax = FBS_PYR_REGS_MAX;  // largest cell sorted in registers (A/B: 128 or 256)
 
-// Pass 1: one warp per coarse cell sorts its (halved code, child id) pairs — in registers for
-// ≤ 256 children (every level-1 cell: 4 level-0 cells of ≤ 64 vertices), else in a global scratch
+// Pass 1: one warp per coarse cell sorts its (halved code, child id) pairs — in registers (32-bit keys) for
+// ≤ 128 children (the typical level-1 cell), else in a global scratch
 // slice from a bump allocator — writes the children grouped by parent in canonical order to the
 // child list, each sorted position's parent rank (rankS) and the cell's parent count.  Warps are
 // independent (no inter-block chain, no shared memory).
@@ -183,7 +189,6 @@ __global__ void __launch_bounds__(256) k_pyr_sort(const uint64_t* __restrict__ k
         if (nch <= 32) U = pyr_sort_regs<1>(keysK, cc, nch, childListN, rankS);
         else if (nch <= 64) U = pyr_sort_regs<2>(keysK, cc, nch, childListN, rankS);
         else if (nch <= 128) U = pyr_sort_regs<4>(keysK, cc, nch, childListN, rankS);
-        else if (kPyrRegsMax >= 256 && nch <= 256) U = pyr_sort_regs<8>(keysK, cc, nch, childListN, rankS);
         else {
             int P = 1;
             while (P < nch) P <<= 1;
