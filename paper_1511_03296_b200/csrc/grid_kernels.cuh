@@ -270,12 +270,16 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
     pdl_entry();
     __shared__ uint32_t sc[kCellsPerBlock][5][kCellMaxPx + 1];  // + 1: sc[i + 1] of the last entry
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
-         c += (int64_t)gridDim.x * kCellsPerBlock) {
-        const unsigned per = (unsigned)ncx * (unsigned)ncy, r = (unsigned)c % per;
+    // 32-bit cell arithmetic (cells ≤ pixels < 2^31); codes are the low words of the keys
+    const uint32_t* keys32 = reinterpret_cast<const uint32_t*>(keys);
+    const int nc = (int)ncells;
+    const unsigned per = (unsigned)ncx * (unsigned)ncy;
+    int bad = 0;
+    for (int c = blockIdx.x * kCellsPerBlock + warp; c < nc; c += gridDim.x * kCellsPerBlock) {
+        const unsigned r = (unsigned)c % per;
         const int cy = (int)(r / (unsigned)ncx), cx = (int)(r - (unsigned)cy * (unsigned)ncx);
         int st[5], ln[5];
-        const int64_t cc[5] = {c, c - 1, c + 1, c - ncx, c + ncx};
+        const int cc[5] = {c, c - 1, c + 1, c - ncx, c + ncx};
         const bool ok[5] = {true, cx > 0, cx < ncx - 1, cy > 0, cy < ncy - 1};
 #pragma unroll
         for (int s = 0; s < 5; ++s) {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
 #pragma unroll
             for (int h = 0; h < kCellMaxPx / 32; ++h) {
                 const int i = lane + 32 * h;
-                sc[warp][s][i] = (i < ln[s]) ? (uint32_t)(keys[st[s] + i] & 0xffffffu) : 0xffffffffu;
+                sc[warp][s][i] = (i < ln[s]) ? (__ldg(keys32 + 2 * (size_t)(st[s] + i)) & 0xffffffu) : 0xffffffffu;
             }
         }
         if (lane == 0) sc[warp][0][kCellMaxPx] = 0xffffffffu;
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int o = offs[k];
-                if (o < -127 || o > 127) atomicOr(err, 4);
+                bad |= (o < -127 || o > 127);
                 const unsigned b = (unsigned)(o & 0xff);
                 if (k < 4) bx |= b << (8 * k); else by |= b << (8 * (k - 4));
             }
@@ -330,6 +334,7 @@ __global__ void __launch_bounds__(256) k_grid_neighbours(
         }
         __syncwarp();
     }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 4);
 }
 
 // ---------------------------------------------------------------- Alg. 1 bistochastization
