@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(256, 8) k_grid_write(
     int* __restrict__ mcount, int* __restrict__ vid) {
     pdl_entry();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t c = (int64_t)blockIdx.x * kCellsPerBlock + warp; c < ncells;
-         c += (int64_t)gridDim.x * kCellsPerBlock) {
+    for (int c = blockIdx.x * kCellsPerBlock + warp; c < (int)ncells;  // cells ≤ pixels < 2^31
+         c += gridDim.x * kCellsPerBlock) {
         int f, cy, cx;
         cell_of(g, c, f, cy, cx);
         const int x0 = g.colStart[cx], y0 = g.rowStart[cy];

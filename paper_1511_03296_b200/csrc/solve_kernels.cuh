@@ -118,8 +118,8 @@ __global__ void __launch_bounds__(256, 8) k_splat(CellGeom g, const int* __restr
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ncells = (int64_t)g.F * g.ncx * g.ncy;
     const size_t HW = (size_t)g.H * g.W;
-    for (int64_t cell = (int64_t)blockIdx.x * kCellsPerBlock + warp; cell < ncells;
-         cell += (int64_t)gridDim.x * kCellsPerBlock) {
+    for (int cell = blockIdx.x * kCellsPerBlock + warp; cell < (int)ncells;  // cells ≤ pixels < 2^31
+         cell += gridDim.x * kCellsPerBlock) {
         int f, cy, cx;
         cell_of(g, cell, f, cy, cx);
         const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
