@@ -57,3 +57,35 @@ def test_step_graph_capture_and_replay(precond):
     torch.cuda.synchronize()
     assert torch.equal(replay_b, x)
     assert not torch.equal(replay_b, eager_a)
+
+
+@pytest.mark.parametrize("lowrank", [False, True])
+def test_build_and_fixed_solve_only_enqueue(lowrank):
+    """fbs_grid_build and a FIXED-mode fbs_solve (with or without the low-rank reduction) return
+    while the stream is still busy: the calls never wait for the device (§8(b) asynchrony)."""
+    import time
+    w = make("c5", frames=2, W=160, H=96, n_cells=12)
+    dev = torch.device("cuda")
+    rgb = torch.from_numpy(w.rgb).to(dev)
+    K = 4 if lowrank else 1
+    t = torch.from_numpy(np.repeat(w.t, K, axis=1)).to(dev)
+    c = torch.from_numpy(w.c).to(dev)
+    kw = dict(precond="hier", init="hier", mode="fixed", iters=10, lowrank_eps=0.01 if lowrank else 0.0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):  # warm-up (one-time set-up: streams, attributes, pools)
+        g = fbs.grid_build(rgb, w.sigma_xy, w.sigma_l, w.sigma_uv)
+        x_ref = fbs.solve(g, t, c, w.lam, **kw)
+        g.close()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        torch.cuda._sleep(int(3e8))  # keep the stream busy for ~0.15 s
+        h0 = time.perf_counter()
+        g = fbs.grid_build(rgb, w.sigma_xy, w.sigma_l, w.sigma_uv)
+        x = fbs.solve(g, t, c, w.lam, **kw)
+        h1 = time.perf_counter()
+        busy = not s.query()
+    torch.cuda.synchronize()
+    assert busy, "the stream finished before the calls returned: nothing was left to enqueue against"
+    assert h1 - h0 < 0.05, f"the calls took {h1 - h0:.3f} s of host time: they waited for the device"
+    assert torch.equal(x, x_ref)
+    g.close()
