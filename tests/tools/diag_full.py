@@ -5,8 +5,9 @@ import sys
 import numpy as np
 import torch
 
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+_ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(_ROOT, "tests"))
+sys.path.insert(0, _ROOT)
 import oracle as O  # noqa: E402
 import paper_1511_03296_b200 as fbs  # noqa: E402
 from parity_util import oracle_opts, target_range, zero_conf_pixels  # noqa: E402

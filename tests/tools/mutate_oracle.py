@@ -1,8 +1,8 @@
 """Mutation check of the oracle's pins: apply one plausible mistake at a time to
 a throw-away copy of oracle/ and show that the CPU pins catch it.
 
-    python scripts/mutate_oracle.py            # all mutations, prints one line each
-    python scripts/mutate_oracle.py --list
+    python tests/tools/mutate_oracle.py            # all mutations, prints one line each
+    python tests/tools/mutate_oracle.py --list
 
 Each mutation copies oracle/, tests/ and workloads/ to a temp dir, edits one line of
 oracle/fbs_oracle.py, runs `pytest -m "not gpu"` on the oracle test files there and records
@@ -16,7 +16,7 @@ import subprocess
 import sys
 import tempfile
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 # (name, old text, new text) — each old text must occur exactly once in oracle/fbs_oracle.py
 MUTATIONS = [
