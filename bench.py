@@ -678,7 +678,7 @@ def main():
 
             ms_c = dev_ms(run_cfg)
             graph_ms = None
-            if wc.mode == "fixed":  # FIXED-mode steps are enqueue-only: the same call as a CUDA graph
+            if True:  # every step is enqueue-only inside a capture (TOL: a device-side loop): as a CUDA graph
                 try:
                     cs2 = torch.cuda.Stream(dev)
                     cs2.wait_stream(stream)

@@ -26,7 +26,8 @@
  *     kernels read the data-dependent counts on the device, so grid build + FIXED-mode solve
  *     (+ slice, backward, low-rank) can be captured into a CUDA graph and replayed.  The
  *     exceptions are stated per call: TOL-mode solves poll the device's active count from the
- *     host; the query and export calls (fbs_grid_info, *_export, *_stats) synchronise.
+ *     host unless the stream is capturing (then a device-side loop is captured); the query and
+ *     export calls (fbs_grid_info, *_export, *_stats) synchronise.
  *   - Layouts: RGB is interleaved uint8 [frames][H][W][3]; pixel vectors are planar float
  *     [frames][K][H][W] (pixel p = y·W + x); confidences float [frames][H][W];
  *     vertex vectors are float [M][K] in CANONICAL vertex order: ascending packed key
@@ -186,7 +187,9 @@ void fbs_grid_destroy(fbs_grid g);
  * split into groups whose PCGs run concurrently on side streams forked from and joined to
  * `stream` (they are independent systems); FIXED mode only enqueues work, TOL mode polls each
  * group's active count from the host one 4-iteration chunk behind and returns when all have
- * stopped (FBS_TOL_GRAPH=1: a device-side CUDA-graph loop instead, no host polls).
+ * stopped; when `stream` is being captured into a CUDA graph it adds a conditional while node
+ * instead (device-side loop, no host polls, replayable); FBS_TOL_GRAPH=1 runs such a loop as its
+ * own graph per solve.
  * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4): the reduced solve
  * carries K channels of which those at or above the frame's kept rank t_f have zero right-hand
  * sides and retire at iteration 0 (no host synchronisation); sys_out must then be NULL.

@@ -1035,6 +1035,52 @@ bool tol_graph(fbs_system S, const VecArgs& a, cudaStream_t s) {
     return ok;
 }
 
+// TOL iterations 1 … inside a CUDA graph the CALLER is capturing on s: a conditional while node
+// is added at the capture's current position (its body: one PCG iteration + k_tol_cond, captured
+// on a side stream), and the capture continues after it.  A TOL solve is then replayable like a
+// FIXED one, with per-channel stopping on the device and no host polls.  Returns false if s is
+// not capturing.
+bool tol_loop_in_capture(fbs_system S, const VecArgs& a, const HierArgs& h, cudaStream_t s, int side) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    ck(cudaStreamIsCapturing(s, &st), "cudaStreamIsCapturing");
+    if (st != cudaStreamCaptureStatusActive) return false;
+    int dev = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    int* it = dalloc<int>(S->allocs, 1, s);
+    zero_words(it, sizeof(int), s);  // captured: re-zeroed at every replay
+    cudaGraph_t graph = nullptr;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    ck(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &ndeps), "cudaStreamGetCaptureInfo");
+    cudaGraphConditionalHandle hc;
+    ck(cudaGraphConditionalHandleCreate(&hc, graph, 1, cudaGraphCondAssignDefault), "conditional handle");
+    cudaGraphNodeParams p = {};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = hc;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    cudaGraphNode_t node;
+    ck(cudaGraphAddNode(&node, graph, deps, ndeps, &p), "conditional node");
+    ck(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies), "capture deps");
+    cudaStream_t cs = group_stream(dev, s, 8 + side);  // body capture stream (nothing executes on it)
+    ck(cudaStreamBeginCaptureToGraph(cs, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeRelaxed),
+       "body capture");
+    try {
+        pdl_break(cs, 8);
+        pcg_iteration(S, a, h, 1, false, cs);
+        LAUNCH(k_tol_cond, 1, 32, 0, cs, hc, a.sc_.n_active, it, S->o.max_iters + 1);
+    } catch (...) {
+        cudaGraph_t body = nullptr;
+        cudaStreamEndCapture(cs, &body);
+        throw;
+    }
+    cudaGraph_t body = nullptr;
+    ck(cudaStreamEndCapture(cs, &body), "body capture end");
+    pdl_break(s, 4);
+    return true;
+}
+
 // TOL polling for one or more independent PCGs (frame groups) on their own streams: each gets
 // chunks of 4 iterations in turn, and the host reads each one's active count (a copy kernel
 // into mapped pinned memory) one chunk behind; a group whose count reached 0 gets no more.
@@ -1124,7 +1170,13 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
                 for (int i = 0; i < S->o.iters; ++i) pcg_iteration(S, ag, hg, i, i == S->o.iters - 1, sg);
             }
         }
-        if (tol && S->o.max_iters > 1) tol_poll(S, runs);
+        if (tol && S->o.max_iters > 1) {
+            // inside the caller's graph capture: a device-side loop per group, else host polls
+            bool captured = true;
+            for (size_t r = 0; r < runs.size() && captured; ++r)
+                captured = tol_loop_in_capture(S, runs[r].a, runs[r].h, runs[r].s, (int)r);
+            if (!captured) tol_poll(S, runs);
+        }
         for (int gi = 0; gi < G; ++gi) {
             cudaStream_t sg = group_stream(dev, s, gi);
             ck(cudaEventCreateWithFlags(&join[gi], cudaEventDisableTiming), "event");
@@ -1144,7 +1196,7 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     // (FBS_TOL_GRAPH=1: the loop runs on the device instead, as a CUDA graph with a conditional
     // while node).
     pcg_iteration(S, a, S->hP, 0, false, s);  // iteration 0 (Jacobi: d = s) outside the loop
-    if (S->o.max_iters <= 1 || tol_graph(S, a, s)) return;
+    if (S->o.max_iters <= 1 || tol_loop_in_capture(S, a, S->hP, s, 0) || tol_graph(S, a, s)) return;
     std::vector<PcgRun> runs{{a, S->hP, s}};
     tol_poll(S, runs);
 }

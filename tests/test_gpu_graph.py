@@ -89,3 +89,46 @@ def test_build_and_fixed_solve_only_enqueue(lowrank):
     assert h1 - h0 < 0.05, f"the calls took {h1 - h0:.3f} s of host time: they waited for the device"
     assert torch.equal(x, x_ref)
     g.close()
+
+
+@pytest.mark.parametrize("frames,precond", [(1, "hier"), (3, "hier"), (1, "jacobi")])
+def test_tol_solve_graph_capture(frames, precond):
+    """Inside a caller's CUDA-graph capture a TOL-mode solve becomes a device-side conditional while
+    loop (no host polls), so the whole TOL step replays too; the replay equals the eager
+    (host-polled) solve bit for bit, including the per-channel iteration counts."""
+    init = "hier" if precond == "hier" else "flat"
+    w = make("c5", frames=frames, W=200, H=120, n_cells=16)
+    dev = torch.device("cuda")
+    rgb, t, c = (torch.from_numpy(a).to(dev) for a in (w.rgb, w.t, w.c))
+    kw = dict(precond=precond, init=init, mode="tol", tol=1e-6, max_iters=500)
+    g0 = fbs.grid_build(rgb, w.sigma_xy, w.sigma_l, w.sigma_uv)
+    x_eager, S0 = fbs.solve(g0, t, c, w.lam, keep_system=True, **kw)
+    it_eager = S0.stats()["iterations"].copy()
+    x = torch.empty_like(t)
+    holder = {}
+
+    def step():
+        g = fbs.grid_build(rgb, w.sigma_xy, w.sigma_l, w.sigma_uv)
+        _, S = fbs.solve(g, t, c, w.lam, keep_system=True, out=x, **kw)
+        holder["S"], holder["g"] = S, g
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    # release the warm-up handles before capturing: destroying a handle enqueues frees on its own
+    # (non-capturing) stream, which a global-mode capture in progress does not allow
+    holder.clear()
+    import gc
+    gc.collect()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    x.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_eager)
+    assert np.array_equal(holder["S"].stats()["iterations"], it_eager)
+    assert np.all(it_eager > 1)
