@@ -1201,10 +1201,28 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     tol_poll(S, runs);
 }
 
+// the per-(frame, channel) PCG scalars of FK pairs: 6 double and 3 int arrays of FK, + the active
+// count and one count per frame group (≤ 8), in scalars_doubles(FK) doubles at d (zeroed by the caller)
+size_t scalars_doubles(int FK) { return (size_t)6 * FK + ((size_t)3 * FK + 1 + 8 + 1) / 2 + 1; }
+PcgScalars scalars_at(double* d, int FK) {
+    PcgScalars p;
+    p.rho = d;
+    p.alpha = d + FK;
+    p.xalpha = d + 2 * (size_t)FK;
+    p.beta = d + 3 * (size_t)FK;
+    p.bb = d + 4 * (size_t)FK;
+    p.rr = d + 5 * (size_t)FK;
+    int* i = reinterpret_cast<int*>(d + 6 * (size_t)FK);
+    p.active = i;
+    p.iters = i + FK;
+    p.status = i + 2 * (size_t)FK;
+    p.n_active = i + 3 * (size_t)FK;
+    return p;
+}
+
 PcgScalars alloc_scalars(AllocList& A, int FK, cudaStream_t s) {
-    // one allocation, zeroed by one launch: 6 double and 3 int arrays of FK, + the active count
-    // ints: active, iters, status [FK] each, the active count, and one count per frame group (≤ 8)
-    const size_t nD = (size_t)6 * FK + ((size_t)3 * FK + 1 + 8 + 1) / 2 + 1;
+    // one allocation, zeroed by one launch
+    const size_t nD = scalars_doubles(FK);
     double* d = dalloc<double>(A, nD, s);
     PcgScalars p;
     p.rho = d;
@@ -1299,8 +1317,20 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         float* bIn = dalloc<float>(A, (size_t)(K + 1) * M + kVecPad, s);
         S->sc = bIn + (size_t)K * M;
         CellGeom geo{F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
-        S->inflags = dalloc<int>(A, 1, s);  // FBS_ST_NEG_CONF / FBS_ST_NONFINITE from the splats
-        zero_words(S->inflags, sizeof(int), s);
+        // every buffer that must start at zero, in one block zeroed by one launch: the input-check
+        // flags (FBS_ST_NEG_CONF / FBS_ST_NONFINITE from the splats), the last-block counters, the
+        // lift's per-(frame, channel) tile counters, the forward PCG scalars, the low-rank Gram counters
+        const size_t zInts = 8 + (size_t)2 * F * K + (size_t)(K + 1) * F + F;
+        const size_t zDoubles = scalars_doubles(F * K);
+        double* zblk = dalloc<double>(A, zDoubles + (zInts + 1) / 2, s);
+        zero_words(zblk, (zDoubles + (zInts + 1) / 2) * sizeof(double), s);
+        S->fwd = scalars_at(zblk, F * K);
+        int* zi = reinterpret_cast<int*>(zblk + zDoubles);
+        S->inflags = zi;
+        S->counters = reinterpret_cast<unsigned*>(zi + 8);  // [F][K] VecArgs, [K][F] HierArgs
+        S->counters2 = S->counters + (size_t)F * K;
+        S->tcount = S->counters + (size_t)2 * F * K;        // [K + 1][F] (k_tree_lift)
+        unsigned* zctr = S->tcount + (size_t)(K + 1) * F;    // [F] (k_gram)
         // a4: splat Sc, b = S(c∘t)
         LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t,
                K, M, S->sc, bIn, S->inflags);
@@ -1311,12 +1341,11 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             const int P = K * (K + 1) / 2;
             const int bpfG = std::min(S->BPF, 64);
             double* part = dalloc<double>(A, (size_t)F * bpfG * P, s);
-            unsigned* ctr = dalloc<unsigned>(A, F, s);
+            unsigned* ctr = zctr;
             double* G = dalloc<double>(A, (size_t)F * K * K, s);
             double* T = dalloc<double>(A, (size_t)F * K * K, s);
             lrRt = dalloc<double>(A, (size_t)F * K * K, s);
             int* tF = dalloc<int>(A, F, s);
-            zero_words(ctr, F * sizeof(unsigned), s);
             LAUNCH(k_gram, F * bpfG, 256, 0, s, bIn, M, K, g->frameOff, bpfG, part, ctr, G);
             LAUNCH(k_pchol, F, 64, 0, s, G, K, o.lowrank_eps, tF, lrRt, T);
             // no host synchronisation: the reduced solve carries K channels; those at or above a
@@ -1351,8 +1380,6 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             S->locT = dalloc<double>(A, (size_t)C * M1, s);
             S->tileAgg = dalloc<double>(A, (size_t)C * nT, s);
             S->tileBase = dalloc<double>(A, (size_t)C * nT, s);
-            S->tcount = dalloc<unsigned>(A, (size_t)C * F, s);
-            zero_words(S->tcount, (size_t)C * F * sizeof(unsigned), s);
             const int64_t want2 = ((g->L > 2 ? g->maxFrameM2 : g->maxFrameM1) + 255) / 256;
             int occ2 = 8;
             if (const char* e = std::getenv("FBS_BPF2_OCC")) occ2 = std::max(1, std::min(64, std::atoi(e)));  // A/B
@@ -1376,11 +1403,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->BPFk = (int)std::max<int64_t>(
             1, std::min<int64_t>(((int64_t)g_num_sms * occ + F - 1) / F, (g->maxFrameM + 31) / 32));
         S->partial = dalloc<double>(A, (size_t)F * std::max(S->BPF, S->BPFk) * 2 * Kc, s);
-        S->counters = dalloc<unsigned>(A, (size_t)2 * F * Kc, s);  // [F][Kc] VecArgs, [Kc][F] HierArgs
-        S->counters2 = S->counters + (size_t)F * Kc;
-        zero_words(S->counters, (size_t)2 * F * Kc * sizeof(unsigned), s);
         if (hierP || hierI) S->hP = make_hier(S, Kc, o.precond_alpha, o.precond_beta);
-        S->fwd = alloc_scalars(A, F * Kc, s);
 
         // a5: assemble (+ flat/zero init)
         VecArgs a = make_args(S, S->fwd, S->xh, S->b);
