@@ -386,9 +386,18 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
         const int w1 = min(c0 + kBsChunk + 128, (M + 3) & ~3);
         const uint32_t bytes = (uint32_t)(n * 16 + n4 * 4 + (first ? 0 : (w1 - w0) * 4));
         mbar_expect_tx(&bar[slot], bytes);
+#ifndef FBS_BS_NO_HINT
+        // the neighbour structure (16 of 28 B per vertex) streams evict-first; m and n, re-read by
+        // every iteration, are kept (evict-last): 30.2 -> 28.5 µs per launch, 5.14 -> 5.10 ms per step
+        bulk_g2s_hint(st[slot].nb, nbr + c0, n * 16, &bar[slot], l2_policy_evict_first());
+        bulk_g2s_hint(st[slot].m, m + c0, n4 * 4, &bar[slot], l2_policy_evict_last());
+        if (!first)
+            bulk_g2s_hint(st[slot].n + (w0 - (c0 - 128)), nin + w0, (w1 - w0) * 4, &bar[slot], l2_policy_evict_last());
+#else
         bulk_g2s(st[slot].nb, nbr + c0, n * 16, &bar[slot]);
         bulk_g2s(st[slot].m, m + c0, n4 * 4, &bar[slot]);
         if (!first) bulk_g2s(st[slot].n + (w0 - (c0 - 128)), nin + w0, (w1 - w0) * 4, &bar[slot]);
+#endif
     };
     int ci = cBeg + blockIdx.x;
     if (threadIdx.x == 0) {
