@@ -86,3 +86,22 @@ if os.path.exists(p):
         json.dump(traffic, fh, indent=1)
     shutil.copy(p, os.path.join(dst, f"{tag}_pcg_iteration.ncu-rep"))
     print("wrote ncu summaries + traffic")
+
+p = os.path.join(src, f"{tag}_build_kernels.ncu-rep")
+if os.path.exists(p):
+    seen = set()
+    for rec in summary(p):
+        base = rec["Kernel Name"].split("(")[0].replace("void ", "")
+        short = base.split("<")[0] + ("_" + base.split("<")[1].rstrip(">").replace(", ", "_") if "<" in base else "")
+        if short in seen:
+            continue
+        seen.add(short)
+        with open(os.path.join(dst, f"{tag}_ncu_{short}.json"), "w") as fh:
+            json.dump(rec, fh, indent=1)
+    shutil.copy(p, os.path.join(dst, f"{tag}_build_kernels.ncu-rep"))
+    print("wrote build-kernel summaries:", sorted(seen))
+
+p = os.path.join(src, "gputest.log")
+if os.path.exists(p):
+    shutil.copy(p, os.path.join(dst, f"{tag}_gputest.log"))
+    print("copied gputest.log")
