@@ -39,9 +39,10 @@ def kernel_bytes(name, M, lv, N):
     lv1 = lv[1] if len(lv) > 1 else 0
     table = {
         "k_spmv2": 32 * M,             # nbr 16 + (d,n) 8 + Sc 4 + q write 4
-        # r rw 8 + q 4 + mu0 4 + w write 4 (x += αd is done by the next direction pass)
-        "k_hier_level0<UPDATE>": 20 * M,
-        # tord0 4 + w gather 4 per level-0 vertex; csT 4 + mu1 4 + (P w)_1 write 4 + prefix write 8 per level-1 vertex
+        # r rw 8 + q 4 + mu0 4 (x += αd is done by the next direction pass; w = mask∘r is r itself
+        # on a forward solve, so it is not written: DESIGN §5)
+        "k_hier_level0<UPDATE>": 16 * M,
+        # tord0 4 + r gather 4 per level-0 vertex; csT 4 + mu1 4 + (P w)_1 write 4 + prefix write 8 per level-1 vertex
         "k_tree_lift<PCG>": 8 * M + 20 * lv1,
         # parent0T 4 + r 4 + mu0 4 + (d,n) rw 16 + x rw 8 (level-1 gathers cache-resident)
         "k_tree_level0<PCG>": 36 * M,

@@ -859,6 +859,14 @@ void tree_level0(fbs_system S, const HierArgs& h, const VecArgs& a, const float*
     }
 }
 
+// where k_hier_level0 stores w = mask∘r: nowhere when r is already masked (S->rMasked; the lift
+// then reads r itself)
+bool w_is_r(fbs_system S) {
+    static const bool off = std::getenv("FBS_WRITE_W") != nullptr;  // A/B: always materialise w
+    return S->rMasked && !off;
+}
+float* lift_w0(fbs_system S) { return w_is_r(S) ? nullptr : S->w0; }
+
 // level-0 PCG input w = mask∘r (+ ρ_0, ‖r‖² partials) (k_hier_level0)
 template <int SRC, bool LAST>
 void hier_level0(fbs_system S, const VecArgs& a, cudaStream_t s) {
@@ -868,16 +876,16 @@ void hier_level0(fbs_system S, const VecArgs& a, cudaStream_t s) {
     if (a.K > 1) {
         const VecArgs as = split_args(S, a);
         auto kern = k_hier_level0<SRC, LAST, true>;
-        LAUNCH_AS(name.c_str(), kern, vec_blocks(as), kThreads, 0, s, as, S->w0);
+        LAUNCH_AS(name.c_str(), kern, vec_blocks(as), kThreads, 0, s, as, lift_w0(S));
     } else {
         auto kern = k_hier_level0<SRC, LAST, false>;
-        LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, a, S->w0);
+        LAUNCH_AS(name.c_str(), kern, a.nf * S->BPF, kThreads, 0, s, a, lift_w0(S));
     }
 }
 
 // s = M⁻¹_hier r and d = s + βd after the level-0 kernel (Alg. 2 lines 10-14)
 void hier_precond_direction(fbs_system S, const VecArgs& a, const HierArgs& h, int first, cudaStream_t s) {
-    tree_lift<HIER_PCG>(S, h, S->w0, s, a.sc_.active);
+    tree_lift<HIER_PCG>(S, h, w_is_r(S) ? a.r : S->w0, s, a.sc_.active);
     tree_coarse<HIER_PCG>(S, h, a, first, s);
     tree_level0<HIER_PCG>(S, h, a, nullptr, nullptr, first, s);
 }
@@ -1370,6 +1378,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         const bool hierP = o.precond == FBS_PRECOND_HIER && g->L > 1;  // L = 1: hier ≡ Jacobi / flat
         const bool hierI = o.init == FBS_INIT_HIER && g->L > 1;
         S->useHierP = hierP;
+        S->rMasked = true;  // b = S(c∘t) and the initial residual are 0 on dead vertices (reading #6)
         if (hierP || hierI) {
             const int C = S->C;
             const int64_t M1 = g->lv[1].M;
@@ -1576,6 +1585,7 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
     LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, g_dldx, K,
            M, nullptr, S->u, S->inflags);
     VecArgs a = make_args(S, S->bwd, S->xb, S->u);
+    S->rMasked = false;  // u = S g need not vanish on dead vertices: the lift reads w = mask∘r
     const VecArgs as = split_args(S, a);
     // k_assemble here only zeroes x and forms ‖u‖² (diag(A), μ0 are recomputed from the same inputs)
     LAUNCH(k_assemble, vec_blocks(as), kThreads, 0, s, as, S->diagA, S->mu0, nullptr, FBS_INIT_ZERO, S->bwd);

@@ -443,6 +443,9 @@ struct fbs_system_s {
     unsigned* counters2 = nullptr; // [F] (HierArgs kernels)
     fbs::PcgScalars fwd, bwd;
     bool useHierP = false;
+    // r is 0 on dead vertices (b = S(c∘t) is, and A's rows are 0 there), so w = mask∘r = r and the
+    // lift reads r instead of a materialised w (forward solves); the backward's u = S g is not
+    bool rMasked = false;
     fbs::HierArgs hP{};
     bool has_backward = false;
     int* lr_rank = nullptr;    // low-rank solves: kept rank t_f per frame (device)

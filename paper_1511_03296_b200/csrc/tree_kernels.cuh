@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
                     if (v >= v1) continue;
                     a.r[off + v] = rv[u];
                     const float w = (mv[u] > 0.f) ? rv[u] : 0.f;
-                    if (!FINISH_LAST) w0[off + v] = w;
+                    if (!FINISH_LAST && w0) w0[off + v] = w;
                     rr += (double)rv[u] * (double)rv[u];
                     rho += (double)mv[u] * (double)w * (double)w;
                 }
