@@ -341,6 +341,34 @@ __device__ __forceinline__ double block_incl_scan_d(double x, double* sh /*[32]*
     return sh[w] + incl;
 }
 
+// The same scan with ONE block barrier: every warp reads all warp totals after it and forms its
+// own offset.  The totals alternate between two buffers (par), so a warp still reading scan i's
+// totals cannot see scan i+1's (which completes a barrier all warps pass only after reading).
+// The additions are the same as block_incl_scan_d's, in the same order (bitwise equal results).
+__device__ __forceinline__ double block_incl_scan_d1(double x, double (*sh)[32], int& par, double* total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    double* b = sh[par];
+    par ^= 1;
+    if (lane == 31) b[w] = incl;
+    __syncthreads();
+    const double s = (lane < nw) ? b[lane] : 0.0;
+    double si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, si, o);
+        if (lane >= o) si += y;
+    }
+    const double excl = __shfl_sync(0xffffffffu, si - s, w);
+    *total = __shfl_sync(0xffffffffu, si, nw - 1);
+    return excl + incl;
+}
+
 // exclusive prefix of frame fl's (group-local) tile totals of channel c → tileBase (fixed order)
 __device__ __forceinline__ void tile_bases(const HierArgs& h, int c, int fl, double* sh) {
     const int t0 = h.tileFrameOff[fl], nt = h.tileFrameOff[fl + 1] - t0;
@@ -369,6 +397,8 @@ __global__ void __launch_bounds__(kScanTile, FBS_LIFT_MINB) k_tree_lift(HierArgs
     pdl_entry();
     __shared__ float stage[kScanTile / 32][kLiftStage];
     __shared__ double shs[32];
+    __shared__ double shs2[2][32];  // block_incl_scan_d1's warp totals
+    int par = 0;
     __shared__ int sfc[kLiftMaxItems];   // (channel, group-local frame) of each finished item
     __shared__ int sdone[kLiftMaxItems]; // 1: this block finished that (frame, channel)'s last tile
     const int tB = h.tileFrameOff[0], nT = h.tileFrameOff[h.nfG] - tB;  // this group's tiles (device)
@@ -445,7 +475,7 @@ __global__ void __launch_bounds__(kScanTile, FBS_LIFT_MINB) k_tree_lift(HierArgs
             if (MODE == HIER_PDA && valid)
                 h.mu1T[i] = (1 < h.frameLevels[fl] && acc > 0.f) ? zw_count(h, 1, myHi - myLo, (double)acc) : 0.f;
             double tot;
-            const double incl = block_incl_scan_d(valid ? (double)acc : 0.0, shs, &tot);
+            const double incl = block_incl_scan_d1(valid ? (double)acc : 0.0, shs2, par, &tot);
             if (valid) h.locT[(size_t)c * h.M1 + i] = incl;
             if (threadIdx.x == 0) h.tileAgg[(size_t)c * h.nTiles1 + t] = tot;
         }
@@ -479,6 +509,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
     __shared__ double shd[32];
     __shared__ int sflag;
     __shared__ double tbS[kCoarseTiles];  // the frame's exclusive tile bases (frames ≤ kCoarseTiles tiles)
+    __shared__ double shd2[2][32];
     // KS: channel split (K > 1), grid nf · bpf2 · C, one channel per block group
     const int nfb = KS ? (int)(gridDim.x / h.C) : (int)gridDim.x;
     const int bx = KS ? (int)(blockIdx.x % nfb) : (int)blockIdx.x;
@@ -501,11 +532,12 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
             if (ntf <= h.coarseTiles) {  // scan the frame's tile totals here (fixed order)
                 const double* agg = h.tileAgg + (size_t)c * h.nTiles1 + t0;
                 double carry = 0.0;
+                int par = 0;
                 for (int b = 0; b < ntf; b += blockDim.x) {
                     const int tt = b + threadIdx.x;
                     const double x = (tt < ntf) ? agg[tt] : 0.0;
                     double tot;
-                    const double incl = block_incl_scan_d(x, shd, &tot);
+                    const double incl = block_incl_scan_d1(x, shd2, par, &tot);
                     if (tt < ntf) tbS[tt] = carry + incl - x;
                     carry += tot;
                 }
