@@ -423,6 +423,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         t_prev = now;
     };
     fbs_grid g = new fbs_grid_s();
+    bool pyrForked = false;  // work was enqueued on the pyramid's side stream
     try {
         g->F = F; g->H = H; g->W = W; g->sxy = sxy; g->sl = sl; g->suv = suv;
         g->ncx = ncx; g->ncy = ncy; g->ncells = (int64_t)F * ncx * ncy; g->N = N;
@@ -483,6 +484,30 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->M = M;
         g->maxFrameM = std::max<int64_t>(1, (int64_t)H * W / 3);  // launch-size heuristic only
 
+        // The pyramid and the tree order need only the keys and the frame and cell offsets, not n:
+        // on small builds (≤ 4 M pixels) they run on a side stream `sp` concurrently with Alg. 1,
+        // whose launches are then latency-bound (configs[2]: 1.35 → 1.30 ms per build + solve).  On
+        // the bench batch Alg. 1 streams at the copy bandwidth and the concurrent pyramid slows it
+        // more than it hides (5.06 vs 4.99 ms per step), so it stays serial there.
+        // FBS_PYR_FORK (A/B): 0 serial, 1 fork after the neighbour search, 2 before it.
+        static const int pyrForkEnv = [] {
+            const char* e = std::getenv("FBS_PYR_FORK");
+            return (e && e[0]) ? std::atoi(e) : -1;
+        }();
+        const int pyrFork = pyrForkEnv >= 0 ? pyrForkEnv : (N <= (4ll << 20) ? 1 : 0);
+        const bool pyrSide = pyrFork != 0 && want_pyr && cap.size() > 1;
+        cudaStream_t sp = s;
+        cudaEvent_t pyrFork0 = nullptr, pyrJoin = nullptr;
+        auto fork_pyramid = [&]() {
+            sp = group_stream(dev, s, 2);
+            pyrForked = true;
+            ck(cudaEventCreateWithFlags(&pyrFork0, cudaEventDisableTiming), "event");
+            ck(event_record(pyrFork0, s), "event");
+            ck(stream_wait(sp, pyrFork0), "wait");
+            cudaEventDestroy(pyrFork0);
+        };
+        if (pyrSide && pyrFork == 2) fork_pyramid();
+
         g->nbr = dalloc<int4>(A, M + kVecPad, s);
         // Phase boundaries of the build are fully serialised launches: one unbroken programmatic
         // (PDL) chain through the whole build faulted on B200 (a pyramid or tree kernel read data of
@@ -491,6 +516,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         pdl_break(s, 32);
         LAUNCH(k_grid_neighbours, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, g->keys, g->cellOff, ncx, ncy,
                g->ncells, g->nbr, err);
+        if (pyrSide && pyrFork == 1) fork_pyramid();
 
         // ---- Alg. 1 (reading #5: fixed n_bistoch iterations)
         g->n = dalloc<float>(A, M + kVecPad, s);
@@ -507,6 +533,16 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // round 2 (device-read frame ranges, arena layout): 1: 5.29, 2: 5.23, 4: 5.33 ms
         int Gb = std::min(F, 2);
         if (const char* e = std::getenv("FBS_BS_GROUPS")) Gb = std::max(1, std::min(F, std::atoi(e)));  // A/B
+        // dynamic chunk scheduling (k_bistoch): one counter per launch, zeroed before the fork
+        static const bool bsDynamic = [] {
+            const char* e = std::getenv("FBS_BS_DYNAMIC");  // A/B
+            return !(e && e[0] == '0');
+        }();
+        unsigned* bsCtr = nullptr;
+        if (bsDynamic && g->n_bistoch > 0) {
+            bsCtr = dalloc<unsigned>(A, (size_t)g->n_bistoch * Gb, s);
+            zero_words(bsCtr, (size_t)g->n_bistoch * Gb * sizeof(unsigned), s);
+        }
         cudaEvent_t bsFork = nullptr;
         std::vector<cudaEvent_t> bsJoin(Gb, nullptr);
         if (Gb > 1) {
@@ -529,7 +565,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(chunksCap, std::max(1, bsPerSM * sms / Gb)));
             for (int it = 0; it < g->n_bistoch && f1 > f0; ++it) {
                 LAUNCH(k_bistoch, blocks, kBsThreads, kBsSmem, sg, g->nbr, g->m, c2, n2, g->frameOff, F, f0, f1, it == 0,
-                       (float)(2 * g->dims));
+                       (float)(2 * g->dims), bsCtr ? bsCtr + (size_t)it * Gb + gi : nullptr);
                 std::swap(c2, n2);
             }
             if (Gb > 1) {
@@ -559,10 +595,10 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         int ncxK = ncx, ncyK = ncy;
         // frame offsets of every level in one [Lmax][F + 1] array (row 0: level 0), used by the
         // hierarchy kernels as is
-        int* lvAll = dalloc<int>(A, (size_t)Lmax * (F + 1), s);
-        copy_words(g->frameOff, lvAll, (F + 1) * sizeof(int), s);
-        unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, s) : nullptr;
-        int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, s) : nullptr;  // parent rank of each sorted child
+        int* lvAll = dalloc<int>(A, (size_t)Lmax * (F + 1), sp);
+        copy_words(g->frameOff, lvAll, (F + 1) * sizeof(int), sp);
+        unsigned long long* pyrScratch = (Lmax > 1) ? dalloc<unsigned long long>(A, 2 * (size_t)M + 2, sp) : nullptr;
+        int* pyrRank = (Lmax > 1) ? dalloc<int>(A, M, sp) : nullptr;  // parent rank of each sorted child
         // scan look-back states and (tile counter, scratch bump) pairs of every level: one zeroing
         std::vector<int64_t> st2Off(Lmax + 1, 0);
         for (int k = 1; k < Lmax; ++k) {
@@ -571,8 +607,8 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         }
         unsigned long long* st2All = nullptr;
         if (Lmax > 1) {
-            st2All = dalloc<unsigned long long>(A, st2Off[Lmax], s);
-            zero_words(st2All, st2Off[Lmax] * sizeof(unsigned long long), s);
+            st2All = dalloc<unsigned long long>(A, st2Off[Lmax], sp);
+            zero_words(st2All, st2Off[Lmax] * sizeof(unsigned long long), sp);
         }
         for (int k = 1; k < Lmax; ++k) {
             Level& L = g->lv[k];
@@ -580,23 +616,23 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             L.ncy = ((ncy - 1) >> k) + 1;
             L.ncells = (int64_t)F * L.ncx * L.ncy;
             L.M = cap[k];
-            L.keys = dalloc<uint64_t>(A, cap[k], s);
-            L.cellOff = dalloc<int>(A, L.ncells + 1, s);
-            L.parent = dalloc<int>(A, cap[k - 1], s);
-            L.childStart = dalloc<int>(A, cap[k] + 1, s);
-            L.childList = dalloc<int>(A, cap[k - 1], s);
-            L.count = dalloc<int>(A, cap[k], s);
-            if (k >= 2) L.cnt1 = dalloc<int>(A, cap[k], s);
-            int* cnt2 = dalloc<int>(A, L.ncells, s);
+            L.keys = dalloc<uint64_t>(A, cap[k], sp);
+            L.cellOff = dalloc<int>(A, L.ncells + 1, sp);
+            L.parent = dalloc<int>(A, cap[k - 1], sp);
+            L.childStart = dalloc<int>(A, cap[k] + 1, sp);
+            L.childList = dalloc<int>(A, cap[k - 1], sp);
+            L.count = dalloc<int>(A, cap[k], sp);
+            if (k >= 2) L.cnt1 = dalloc<int>(A, cap[k], sp);
+            int* cnt2 = dalloc<int>(A, L.ncells, sp);
             const int64_t st2n = std::max<int64_t>(1, (L.ncells + kScanBlock * kScanItems - 1) / (kScanBlock * kScanItems));
             unsigned long long* st2 = st2All + st2Off[k];
             unsigned* ctr2 = reinterpret_cast<unsigned*>(st2 + st2n);  // scan tile counter, scratch bump
-            if (k == 1 || pdl_every_level()) pdl_break(s, 32);
-            LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
+            if (k == 1 || pdl_every_level()) pdl_break(sp, 32);
+            LAUNCH(k_pyr_sort, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, sp, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, ctr2 + 1, pyrScratch, L.childList, pyrRank, cnt2);
-            LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, s, cnt2, L.ncells, L.cellOff, ctr2, st2,
+            LAUNCH(k_scan_excl, (unsigned)st2n, kScanBlock, 0, sp, cnt2, L.ncells, L.cellOff, ctr2, st2,
                    (int64_t)L.ncx * L.ncy, lvAll + (size_t)k * (F + 1));
-            LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, s, keysK, cellOffK, ncxK, ncyK, L.ncx,
+            LAUNCH(k_pyr_write, grid_for(L.ncells * 32, 256, 1 << 20), 256, 0, sp, keysK, cellOffK, ncxK, ncyK, L.ncx,
                    L.ncy, L.ncells, L.cellOff, L.childList, pyrRank, L.keys, L.parent, L.childStart,
                    k >= 2 ? g->lv[k - 1].count : nullptr, L.count, k >= 3 ? g->lv[k - 1].cnt1 : nullptr,
                    k >= 2 ? L.cnt1 : nullptr);
@@ -612,9 +648,9 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // per-frame level counts (first level with a single vertex, reading #8) and, with a pyramid,
         // the prefix-scan tiles of the tree-ordered level 1 — both computed on the device
         const int L = Lmax;
-        g->frameLevels = dalloc<int>(A, F, s);
-        pdl_break(s, 32);
-        LAUNCH(k_frame_levels, (F + 255) / 256, 256, 0, s, lvAll, F, L, g->frameLevels);
+        g->frameLevels = dalloc<int>(A, F, sp);
+        pdl_break(sp, 32);
+        LAUNCH(k_frame_levels, (F + 255) / 256, 256, 0, sp, lvAll, F, L, g->frameLevels);
         // ---- tree order of the pyramid (tree_kernels.cuh): depth-first positions of the level-0 and
         // level-1 vertices, so every coarse subtree is one contiguous level-1 range
         if (L > 1) {
@@ -624,27 +660,27 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
             std::vector<int*> cnt1(L, nullptr);  // level-1 descendants of levels ≥ 2
             for (int k = 2; k < L; ++k) cnt1[k] = g->lv[k].cnt1;
             std::vector<int2*> start(L, nullptr);
-            for (int k = 1; k < L; ++k) start[k] = dalloc<int2>(A, cap[k], s);
-            for (int k = 2; k < L; ++k) T.rng[k] = dalloc<int2>(A, cap[k], s);
-            T.tord0 = dalloc<int>(A, M, s);
-            T.csT = dalloc<int>(A, M1 + 1, s);
-            T.tord1 = dalloc<int>(A, M1, s);
-            T.parent0T = dalloc<int>(A, M, s);
-            LAUNCH(k_tree_top, 1, 256, 0, s, g->lvFrameOffDev, F, top, start[top], top >= 2 ? T.rng[top] : nullptr,
+            for (int k = 1; k < L; ++k) start[k] = dalloc<int2>(A, cap[k], sp);
+            for (int k = 2; k < L; ++k) T.rng[k] = dalloc<int2>(A, cap[k], sp);
+            T.tord0 = dalloc<int>(A, M, sp);
+            T.csT = dalloc<int>(A, M1 + 1, sp);
+            T.tord1 = dalloc<int>(A, M1, sp);
+            T.parent0T = dalloc<int>(A, M, sp);
+            LAUNCH(k_tree_top, 1, 256, 0, sp, g->lvFrameOffDev, F, top, start[top], top >= 2 ? T.rng[top] : nullptr,
                    top >= 2 ? cnt1[top] : nullptr);
             for (int k = top; k >= 1; --k) {
                 const int km1 = k - 1;
-                LAUNCH(k_tree_down, grid_for(cap[k]), kThreads, 0, s, km1, g->lv[k].childStart, g->lv[k].childList,
+                LAUNCH(k_tree_down, grid_for(cap[k]), kThreads, 0, sp, km1, g->lv[k].childStart, g->lv[k].childList,
                        lvAll + (size_t)k * (F + 1) + F, start[k], km1 >= 1 ? g->lv[km1].count : nullptr,
                        km1 >= 2 ? cnt1[km1] : nullptr, km1 >= 1 ? start[km1] : nullptr,
                        km1 >= 2 ? T.rng[km1] : nullptr, T.tord0, T.tord1, T.csT);
             }
-            LAUNCH(k_tree_finish, grid_for(M), kThreads, 0, s, g->lv[1].parent, start[1], lvAll + F, lvAll + (F + 1) + F,
+            LAUNCH(k_tree_finish, grid_for(M), kThreads, 0, sp, g->lv[1].parent, start[1], lvAll + F, lvAll + (F + 1) + F,
                    T.parent0T, T.csT);
             if (top >= 3) {  // ancestor tables of the level-2 vertices
                 const int64_t M2 = cap[2];
-                T.ancId = dalloc<int>(A, (size_t)(top - 2) * M2, s);
-                T.ancRng = dalloc<int2>(A, (size_t)(top - 2) * M2, s);
+                T.ancId = dalloc<int>(A, (size_t)(top - 2) * M2, sp);
+                T.ancRng = dalloc<int2>(A, (size_t)(top - 2) * M2, sp);
                 HierArgs hb{};
                 hb.L = L;
                 hb.M2 = M2;
@@ -653,20 +689,27 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
                     hb.lv[k].parent = (k + 1 < L) ? g->lv[k + 1].parent : nullptr;
                     hb.lv[k].rng = T.rng[k];
                 }
-                LAUNCH(k_tree_anc, grid_for(M2), kThreads, 0, s, hb, lvAll + 2 * (size_t)(F + 1) + F, T.ancId, T.ancRng);
+                LAUNCH(k_tree_anc, grid_for(M2), kThreads, 0, sp, hb, lvAll + 2 * (size_t)(F + 1) + F, T.ancId, T.ancRng);
             }
             // prefix-scan tiles: kScanTile level-1 positions, never crossing a frame (device-built)
             T.nTiles1 = (int)((M1 + kScanTile - 1) / kScanTile + F);  // capacity
-            T.tileFrameOff = dalloc<int>(A, F + 1, s);
-            T.tileRange = dalloc<int2>(A, T.nTiles1, s);
-            T.tileFrame = dalloc<int>(A, T.nTiles1, s);
-            LAUNCH(k_scan_tiles, F, 256, 0, s, lvAll + (F + 1), F, T.tileFrameOff, T.tileRange, T.tileFrame);
+            T.tileFrameOff = dalloc<int>(A, F + 1, sp);
+            T.tileRange = dalloc<int2>(A, T.nTiles1, sp);
+            T.tileFrame = dalloc<int>(A, T.nTiles1, sp);
+            LAUNCH(k_scan_tiles, F, 256, 0, sp, lvAll + (F + 1), F, T.tileFrameOff, T.tileRange, T.tileFrame);
         }
         // launch-size heuristics for the level-1 / level-2 kernels: each level typically holds ~1/5
         // of the vertices below it (Appendix A of SURVEY.md; 1/4 here to err towards more blocks)
         g->maxFrameM1 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM / 4, L > 1 ? cap[1] : 1));
         g->maxFrameM2 = std::max<int64_t>(1, std::min<int64_t>(g->maxFrameM1 / 4, L > 2 ? cap[2] : 1));
+        if (sp != s) {  // join the pyramid's side stream
+            ck(cudaEventCreateWithFlags(&pyrJoin, cudaEventDisableTiming), "event");
+            ck(event_record(pyrJoin, sp), "event");
+            ck(stream_wait(s, pyrJoin), "wait");
+            cudaEventDestroy(pyrJoin);
+        }
     } catch (...) {
+        if (pyrForked) cudaStreamSynchronize(group_stream(dev, s, 2));  // error path: drain it first
         free_all(g->allocs, s);
         for (auto& b : g->uploads) pinned_put(b, s);
         delete g;

@@ -358,7 +358,8 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
                                                  const int* __restrict__ m,
                                                  const float* __restrict__ nin,
                                                  float* __restrict__ nout, const int* __restrict__ frameOff, int F,
-                                                 int f0, int f1, int first, float bdiag) {
+                                                 int f0, int f1, int first, float bdiag,
+                                                 unsigned* __restrict__ chunkCtr) {
     // The frame offsets were written before the (serialised) launch of k_grid_neighbours that
     // precedes every k_bistoch of a build, so they are complete when any k_bistoch block starts:
     // they are read before waiting on the previous iteration (the first bulk copies go out as soon
@@ -399,14 +400,26 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
         if (!first) bulk_g2s(st[slot].n + (w0 - (c0 - 128)), nin + w0, (w1 - w0) * 4, &bar[slot]);
 #endif
     };
-    int ci = cBeg + blockIdx.x;
+    // chunkCtr (dynamic scheduling): blocks take chunks from a per-launch counter, so a block that
+    // starts late (SM slots held by another kernel) takes fewer chunks instead of delaying the
+    // launch (28.5 → 26.0 µs per launch in the bench step); each slot's chunk id travels with its
+    // stage (sci), and a slot with no chunk left completes its barrier with no bytes (sci = −1)
+    volatile int* sci = reinterpret_cast<int*>(bs_smem + 2 * sizeof(BsStage) + 16);
+    auto take = [&](int slot, int guess) {  // thread 0: the slot's chunk, issued (or −1)
+        const int cj = chunkCtr ? cBeg + (int)atomicAdd(chunkCtr, 1u) : guess;
+        sci[slot] = (cj < nChunks) ? cj : -1;
+        if (cj < nChunks) issue(slot, cj);
+        else mbar_expect_tx(&bar[slot], 0);
+    };
     if (threadIdx.x == 0) {
-        if (ci < nChunks) issue(0, ci);
-        if (ci + (int)gridDim.x < nChunks) issue(1, ci + gridDim.x);
+        take(0, cBeg + blockIdx.x);
+        take(1, cBeg + blockIdx.x + gridDim.x);
     }
-    for (int it = 0; ci < nChunks; ++it, ci += gridDim.x) {
+    for (int it = 0;; ++it) {
         const int slot = it & 1;
         mbar_wait(&bar[slot], (it >> 1) & 1);
+        const int ci = sci[slot];
+        if (ci < 0) break;
         const BsStage& S = st[slot];
         const int c0 = ci * kBsChunk;
         float ny[kBsChunk / kBsThreads][2];
@@ -445,8 +458,8 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
             }
             nout[v] = sqrtf(nv * (float)S.m[l] / bn);
         }
-        __syncthreads();  // stage `slot` fully consumed
-        if (threadIdx.x == 0 && ci + 2 * (int)gridDim.x < nChunks) issue(slot, ci + 2 * gridDim.x);
+        __syncthreads();  // stage `slot` fully consumed (and sci[slot] read by every thread)
+        if (threadIdx.x == 0) take(slot, ci + 2 * (int)gridDim.x);
     }
 }
 
