@@ -276,7 +276,7 @@ __device__ __forceinline__ void write_partials(const VecArgs& a, int f, int j, i
 // flat init y_flat = b/Sc (reading #9) or zero init, and the interleaved (d, n)
 // vector with d = 0.  Per-frame blocks.
 __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__ diagA, float* __restrict__ mu0,
-                                                  float* __restrict__ w0diag, int init_mode, PcgScalars scal) {
+                                                  int init_mode, PcgScalars scal) {
     pdl_entry();
     __shared__ double shd[32];
     __shared__ int sflag;
@@ -288,7 +288,6 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
         const bool live = dA > 0.f;
         diagA[v] = dA;
         mu0[v] = live ? 1.f / dA : 0.f;
-        if (w0diag) w0diag[v] = dA;
     }
     for (int k = bu.k0; k < bu.k1; ++k) {
         double bb = 0.0;
