@@ -1558,8 +1558,12 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
         const size_t NP = (size_t)F * H * W, NS = NP * K;
         float* Dx = dalloc<float>(tmp, NP, s);
         float* Dy = dalloc<float>(tmp, NP, s);
-        LAUNCH(k_dt_dist, dim3((W + kThreads - 1) / kThreads, std::min(F * H, 65535)), kThreads, 0, s, rgb, F, H, W,
-               (float)(sigma_s / sigma_r), Dx, Dy);
+        if ((W & 3) == 0 && ((uintptr_t)rgb & 3) == 0)  // four pixels per thread, word loads
+            LAUNCH(k_dt_dist4, dim3((W / 4 + kThreads - 1) / kThreads, std::min(F * H, 65535)), kThreads, 0, s, rgb, F, H,
+                   W, (float)(sigma_s / sigma_r), Dx, Dy);
+        else
+            LAUNCH(k_dt_dist, dim3((W + kThreads - 1) / kThreads, std::min(F * H, 65535)), kThreads, 0, s, rgb, F, H, W,
+                   (float)(sigma_s / sigma_r), Dx, Dy);
         if (out != in) ck(memcpy_async(out, in, NS * sizeof(float), cudaMemcpyDeviceToDevice, s), "d2d");
         const size_t perWarp = 2 * (size_t)(W + 32) * sizeof(float);
         const int nw = (int)std::max<size_t>(1, std::min<size_t>(8, (64 * 1024) / perWarp));
@@ -1569,8 +1573,11 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
                "smem attr");
         const int64_t lines = (int64_t)F * K * H;
         const int rowBlocks = (int)std::max<int64_t>(1, std::min<int64_t>((lines + nw - 1) / nw, 148 * 32));
-        // column passes as row passes on the transpose (FBS_DT_COLS=1: the in-place column kernel)
-        const bool viaT = !(std::getenv("FBS_DT_COLS") && std::getenv("FBS_DT_COLS")[0] == '1');
+        // column passes: register-resident columns (H ≤ 1536), else row passes on the transpose
+        // (FBS_DT_COLS=t / 1 for A/B: the transpose path / the in-place column kernel)
+        const char* dtc = std::getenv("FBS_DT_COLS");
+        const bool colsReg = H <= kDtColChunks * kDtColRows && !(dtc && dtc[0]);
+        const bool viaT = !colsReg && !(dtc && dtc[0] == '1');
         float* sT = nullptr;
         float* DyT = nullptr;
         const size_t perWarpT = 2 * (size_t)(H + 32) * sizeof(float);
@@ -1595,7 +1602,11 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
             const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, n_iters - i) / std::sqrt(std::pow(4.0, n_iters) - 1.0);
             const float lna = (float)(-std::sqrt(2.0) / sig);  // ln a_i
             LAUNCH(k_dt_rows, rowBlocks, 32 * nw, smem, s, out, Dx, F, K, H, W, lna);
-            if (viaT) {
+            if (colsReg) {
+                const int64_t tiles = (int64_t)F * K * ((W + 15) / 16);
+                LAUNCH(k_dt_cols_reg, (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 8)), 1024, 0, s, out, Dy, F,
+                       K, H, W, lna);
+            } else if (viaT) {
                 LAUNCH(k_dt_transpose, tgN, tb, 0, s, out, sT, H, W);
                 LAUNCH(k_dt_rows, rowBlocksT, 32 * nwT, smemT, s, sT, DyT, F, K, W, H, lna);
                 LAUNCH(k_dt_transpose, tgT, tb, 0, s, sT, out, W, H);

@@ -36,6 +36,53 @@ __global__ void k_dt_dist(const uint8_t* __restrict__ rgb, int F, int H, int W, 
     }
 }
 
+// The same for W % 4 = 0, four pixels per thread: the 12 bytes of the 4 pixels (and the byte
+// triple before them) as 32-bit words, the row above likewise, two 16-byte stores.
+__global__ void k_dt_dist4(const uint8_t* __restrict__ rgb, int F, int H, int W, float ratio, float* __restrict__ Dx,
+                           float* __restrict__ Dy) {
+    pdl_entry();
+    const int W4 = W >> 2;
+    const int x4 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (x4 >= W4) return;
+    auto bytes = [](uint32_t w, int i) { return (float)((w >> (8 * i)) & 255u); };
+    for (int row = blockIdx.y; row < F * H; row += gridDim.y) {  // row = f·H + y
+        const int y = row % H;
+        const uint32_t* cw = reinterpret_cast<const uint32_t*>(rgb + ((size_t)row * W + 4 * x4) * 3);
+        uint32_t c[4], u[3], pw = 0;  // c[0..2]: the 4 pixels; pw: the word ending with pixel x − 1
+        c[0] = __ldg(cw);
+        c[1] = __ldg(cw + 1);
+        c[2] = __ldg(cw + 2);
+        if (x4 > 0) pw = __ldg(cw - 1);
+        if (y > 0) {
+            const uint32_t* uw = cw - (size_t)W * 3 / 4;  // W % 4 = 0: the row above is word-aligned
+            u[0] = __ldg(uw);
+            u[1] = __ldg(uw + 1);
+            u[2] = __ldg(uw + 2);
+        }
+        (void)c[3];
+        float px[5][3];  // pixels x − 1 … x + 3 (channel bytes in memory order)
+        px[0][0] = bytes(pw, 1); px[0][1] = bytes(pw, 2); px[0][2] = bytes(pw, 3);
+#pragma unroll
+        for (int q = 0; q < 12; ++q) px[1 + q / 3][q % 3] = bytes(c[q / 4], q % 4);
+        float dx[4], dy[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float d = fabsf(px[i + 1][0] - px[i][0]) + fabsf(px[i + 1][1] - px[i][1]) + fabsf(px[i + 1][2] - px[i][2]);
+            dx[i] = 1.f + ratio * ((x4 > 0 || i > 0) ? d : 0.f);
+            float e = 0.f;
+            if (y > 0) {
+                const int q0 = 3 * i;
+                e = fabsf(px[i + 1][0] - bytes(u[q0 / 4], q0 % 4)) + fabsf(px[i + 1][1] - bytes(u[(q0 + 1) / 4], (q0 + 1) % 4)) +
+                    fabsf(px[i + 1][2] - bytes(u[(q0 + 2) / 4], (q0 + 2) % 4));
+            }
+            dy[i] = 1.f + ratio * e;
+        }
+        const size_t p4 = (size_t)row * W4 + x4;
+        reinterpret_cast<float4*>(Dx)[p4] = make_float4(dx[0], dx[1], dx[2], dx[3]);
+        reinterpret_cast<float4*>(Dy)[p4] = make_float4(dy[0], dy[1], dy[2], dy[3]);
+    }
+}
+
 // Transpose of P planes [H][W] → [W][H] through 32×32 shared-memory tiles (coalesced both ways);
 // block (32, 8), grid (⌈W/32⌉, ⌈H/32⌉, P).  The column passes run as row passes on the transpose.
 __global__ void k_dt_transpose(const float* __restrict__ in, float* __restrict__ out, int H, int W) {
@@ -80,21 +127,54 @@ __global__ void k_dt_rows(float* __restrict__ sig, const float* __restrict__ Dx,
         const int y = (int)(r % H);
         float* line = sig + (size_t)r * W;
         const float* dl = Dx + ((size_t)f * H + y) * W;
-        for (int nb = lane; nb < W; nb += 32 * kDtB) {  // kDtB loads of each array in flight
-            float lv[kDtB], dv[kDtB];
+        if ((W & 3) == 0) {
+            // 16-byte loads (rows start 16-byte aligned when W % 4 = 0): a 1920-pixel line is two
+            // rounds of kDtB loads per lane instead of eight — the loads' latency, not bandwidth,
+            // bounds a warp's line
+            const float4* line4 = reinterpret_cast<const float4*>(line);
+            const float4* dl4 = reinterpret_cast<const float4*>(dl);
+            const int W4 = W >> 2;
+            for (int nb = lane; nb < W4; nb += 32 * kDtB) {
+                float4 lv[kDtB], dv[kDtB];
 #pragma unroll
-            for (int u = 0; u < kDtB; ++u) {
-                const int n = nb + 32 * u;
-                lv[u] = (n < W) ? line[n] : 0.f;
-                dv[u] = (n < W) ? __ldg(dl + n) : 0.f;
+                for (int u = 0; u < kDtB; ++u) {
+                    const int n4 = nb + 32 * u;
+                    lv[u] = (n4 < W4) ? line4[n4] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    dv[u] = (n4 < W4) ? __ldg(dl4 + n4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < kDtB; ++u) {
+                    const int n4 = nb + 32 * u;
+                    if (n4 < W4) {
+                        const float le[4] = {lv[u].x, lv[u].y, lv[u].z, lv[u].w};
+                        const float de[4] = {dv[u].x, dv[u].y, dv[u].z, dv[u].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int n = 4 * n4 + e;
+                            const int pn = n + __float2int_rz(((float)n + 0.5f) * invC);
+                            val[pn] = le[e];
+                            wgt[pn] = (n == 0) ? 0.f : __expf(lna * de[e]);
+                        }
+                    }
+                }
             }
+        } else {
+            for (int nb = lane; nb < W; nb += 32 * kDtB) {  // kDtB loads of each array in flight
+                float lv[kDtB], dv[kDtB];
 #pragma unroll
-            for (int u = 0; u < kDtB; ++u) {
-                const int n = nb + 32 * u;
-                if (n < W) {
-                    const int pn = n + __float2int_rz(((float)n + 0.5f) * invC);
-                    val[pn] = lv[u];
-                    wgt[pn] = (n == 0) ? 0.f : __expf(lna * dv[u]);  // w[0] = 0: the first element keeps its value
+                for (int u = 0; u < kDtB; ++u) {
+                    const int n = nb + 32 * u;
+                    lv[u] = (n < W) ? line[n] : 0.f;
+                    dv[u] = (n < W) ? __ldg(dl + n) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < kDtB; ++u) {
+                    const int n = nb + 32 * u;
+                    if (n < W) {
+                        const int pn = n + __float2int_rz(((float)n + 0.5f) * invC);
+                        val[pn] = lv[u];
+                        wgt[pn] = (n == 0) ? 0.f : __expf(lna * dv[u]);  // w[0] = 0: the first element keeps its value
+                    }
                 }
             }
         }
@@ -236,6 +316,98 @@ __global__ void __launch_bounds__(1024) k_dt_cols(float* __restrict__ sig, const
                     col[(size_t)(yb - u) * W] = J;
                 }
         }
+        __syncthreads();
+    }
+}
+
+// Column pass with the column held in registers (H ≤ kDtColChunks · kDtColRows): one block of
+// 1024 threads per 16 adjacent columns of one (frame, channel) plane; thread (warp w, lane l)
+// owns column l % 16 and chunk 2w + l / 16 of kDtColRows consecutive rows (a warp's loads are
+// two 64-byte row segments).  The chunk's values and weights are read once into registers;
+// causal and anticausal passes compose the chunk's affine maps, scan the column's chunk maps in
+// shared memory (Hillis–Steele, in chunk order) and re-run the chunk from its incoming value;
+// the result is stored once: 12 bytes per pixel (sig read and written, Dy read).
+constexpr int kDtColRows = 18;  // H ≤ 1152 (registers: 64 per thread at 1024 threads)
+constexpr int kDtColChunks = 64;
+__global__ void __launch_bounds__(1024, 1) k_dt_cols_reg(float* __restrict__ sig, const float* __restrict__ Dy, int F,
+                                                         int K, int H, int W, float lna) {
+    pdl_entry();
+    __shared__ float2 cm[kDtColChunks][16];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int col = lane & 15, j = 2 * warp + (lane >> 4);  // chunk index
+    const int tilesX = (W + 15) / 16;
+    const int64_t planes = (int64_t)F * K;
+    const int R = (H + kDtColChunks - 1) / kDtColChunks;  // rows per chunk (≤ kDtColRows)
+    for (int64_t b = blockIdx.x; b < planes * tilesX; b += gridDim.x) {
+        const int64_t pl = b / tilesX;
+        const int x = (int)(b % tilesX) * 16 + col;
+        const int f = (int)(pl / K);
+        const bool ok = x < W;
+        float* cs = sig + (size_t)pl * H * W + (ok ? x : 0);
+        const float* dc = Dy + (size_t)f * H * W + (ok ? x : 0);
+        const int y0 = j * R, y1 = ok ? min(y0 + R, H) : y0;
+        float iv[kDtColRows], wv[kDtColRows];
+#pragma unroll
+        for (int i = 0; i < kDtColRows; ++i) {
+            const int y = y0 + i;
+            const bool in = i < R && y < y1;
+            iv[i] = in ? cs[(size_t)y * W] : 0.f;
+            wv[i] = in ? __ldg(dc + (size_t)y * W) : 0.f;
+        }
+        // the anticausal pass of the chunk's last row needs the next chunk's first weight
+        const float dnext = (ok && y1 < H && y1 == y0 + R) ? __ldg(dc + (size_t)y1 * W) : 0.f;
+#pragma unroll
+        for (int i = 0; i < kDtColRows; ++i) wv[i] = (y0 + i > 0) ? __expf(lna * wv[i]) : 0.f;  // w = 0 at y = 0
+        const float wnx = (y1 < H && y1 == y0 + R) ? __expf(lna * dnext) : 0.f;
+        // causal: row y uses w[y]
+        float2 m = make_float2(1.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < kDtColRows; ++i)
+            if (y0 + i < y1) m = amap_compose(make_float2(wv[i], (1.f - wv[i]) * iv[i]), m);
+        cm[j][col] = m;
+        __syncthreads();
+        // inclusive scan of the column's chunk maps in chunk order (Hillis–Steele, 6 rounds);
+        // the incoming value of chunk j is the earlier chunks' composed map applied to 0
+#pragma unroll
+        for (int r = 1; r < kDtColChunks; r <<= 1) {
+            const float2 t = (j >= r) ? amap_compose(cm[j][col], cm[j - r][col]) : cm[j][col];
+            __syncthreads();
+            cm[j][col] = t;
+            __syncthreads();
+        }
+        float J = (j > 0) ? cm[j - 1][col].y : 0.f;
+#pragma unroll
+        for (int i = 0; i < kDtColRows; ++i)
+            if (y0 + i < y1) {
+                J = wv[i] * J + (1.f - wv[i]) * iv[i];
+                iv[i] = J;
+            }
+        __syncthreads();
+        // anticausal: row y uses w[y + 1] (0 for the last row)
+        m = make_float2(1.f, 0.f);
+#pragma unroll
+        for (int i = kDtColRows - 1; i >= 0; --i)
+            if (y0 + i < y1) {
+                const float w = (i + 1 < kDtColRows && y0 + i + 1 < y1) ? wv[i + 1] : wnx;
+                m = amap_compose(make_float2(w, (1.f - w) * iv[i]), m);
+            }
+        cm[j][col] = m;
+        __syncthreads();
+#pragma unroll
+        for (int r = 1; r < kDtColChunks; r <<= 1) {  // the same in reverse chunk order
+            const float2 t = (j + r < kDtColChunks) ? amap_compose(cm[j][col], cm[j + r][col]) : cm[j][col];
+            __syncthreads();
+            cm[j][col] = t;
+            __syncthreads();
+        }
+        J = (j + 1 < kDtColChunks) ? cm[j + 1][col].y : 0.f;
+#pragma unroll
+        for (int i = kDtColRows - 1; i >= 0; --i)
+            if (y0 + i < y1) {
+                const float w = (i + 1 < kDtColRows && y0 + i + 1 < y1) ? wv[i + 1] : wnx;
+                J = w * J + (1.f - w) * iv[i];
+                cs[(size_t)(y0 + i) * W] = J;
+            }
         __syncthreads();
     }
 }
