@@ -725,6 +725,10 @@ def main():
         extras = {"configs": cfg_rows,
                   "dt_post_filter_ms": dt_ms,
                   "dt_post_filter": f"{F} frames x1, sigma'_xy = sigma'_rgb = 16, 3 iterations (PAPER.md:329)",
+                  # algorithmic bytes: per pixel 11 (distances: rgb 3, Dx, Dy 8) + 8 (input
+                  # copied to the output) + 3 iterations × 2 passes × 12 (value read + write, weight read)
+                  "dt_post_filter_rate": {"bytes_per_pixel": 91, "GBps": 91 * w.pixels / (dt_ms / 1e3) / 1e9,
+                                          "frac": 91 * w.pixels / (dt_ms / 1e3) / 1e9 / 6550.7},
                   "robust_ms_per_irls_round": rb_ms,
                   "robust": f"{F} frames, sigma_gm = 10, hier+hier, {ITERS} PCG iters per round (Supp. Alg. 3)",
                   "configs3_full_solve_ms": full_ms, "configs3_lowrank_solve_ms": lr_ms,
