@@ -1572,6 +1572,13 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
             ck(cudaFuncSetAttribute((const void*)k_dt_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
                "smem attr");
         const int64_t lines = (int64_t)F * K * H;
+        // rows of ≥ 256 pixels (W % 4 = 0): two warps per row (k_dt_rows2; FBS_DT_ROWS1=1 for A/B)
+        const bool rows2 = (W % 4 == 0) && W >= 256 && !std::getenv("FBS_DT_ROWS1");
+        const size_t smem2 = 8 * 2 * (size_t)(((W + 1) / 2 + 3) / 4 * 4 + 33) * sizeof(float);
+        const int rowBlocks2 = (int)std::max<int64_t>(1, std::min<int64_t>((lines + 3) / 4, 148 * 32));
+        if (rows2 && smem2 > 48 * 1024)
+            ck(cudaFuncSetAttribute((const void*)k_dt_rows2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2),
+               "smem attr");
         const int rowBlocks = (int)std::max<int64_t>(1, std::min<int64_t>((lines + nw - 1) / nw, 148 * 32));
         // column passes: register-resident columns (H ≤ 1536), else row passes on the transpose
         // (FBS_DT_COLS=t / 1 for A/B: the transpose path / the in-place column kernel)
@@ -1601,7 +1608,8 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
         for (int i = 1; i <= n_iters; ++i) {
             const double sig = sigma_s * std::sqrt(3.0) * std::pow(2.0, n_iters - i) / std::sqrt(std::pow(4.0, n_iters) - 1.0);
             const float lna = (float)(-std::sqrt(2.0) / sig);  // ln a_i
-            LAUNCH(k_dt_rows, rowBlocks, 32 * nw, smem, s, out, Dx, F, K, H, W, lna);
+            if (rows2) LAUNCH(k_dt_rows2, rowBlocks2, 256, smem2, s, out, Dx, F, K, H, W, lna);
+            else LAUNCH(k_dt_rows, rowBlocks, 32 * nw, smem, s, out, Dx, F, K, H, W, lna);
             if (colsReg) {
                 const int64_t tiles = (int64_t)F * K * ((W + 15) / 16);
                 LAUNCH(k_dt_cols_reg, (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 8)), 1024, 0, s, out, Dy, F,

@@ -222,6 +222,122 @@ __global__ void k_dt_rows(float* __restrict__ sig, const float* __restrict__ Dx,
     }
 }
 
+// Row pass with TWO warps per row (rows of ≥ 256 pixels): warp 2p + h of a block handles half h
+// of row p, [h·Wh, min((h+1)·Wh, W)) with Wh a multiple of 4, staged and chunked exactly as in
+// k_dt_rows.  The halves exchange one value through shared memory per direction: the causal
+// value leaving half 0 (its composed map applied to the row's start, whose weight is 0) and the
+// anticausal value leaving half 1.  Half the shared memory per warp and half the serial chunk
+// walk of k_dt_rows.  Block: 8 warps = 4 rows; every row of a block runs in step (__syncthreads).
+constexpr int kDtB2 = 4;  // 16-byte loads of each array in flight per lane (3 blocks per SM)
+__global__ void __launch_bounds__(256, 3) k_dt_rows2(float* __restrict__ sig, const float* __restrict__ Dx, int F, int K, int H, int W,
+                           float lna) {
+    pdl_entry();
+    extern __shared__ float dt_smem[];
+    __shared__ float xch[2][4];  // [direction][row of the block]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rb = warp >> 1, h = warp & 1;  // row of the block, half
+    const int Wh = ((W + 1) / 2 + 3) & ~3;
+    const int a = h * Wh, b = min(a + Wh, W), L = b - a;  // this warp's elements (L ≥ 1 for W ≥ 8)
+    const int C = (Wh + 31) / 32;
+    const float invC = 1.f / (float)C;
+    const int lpad = Wh + 32 + 1;  // + 1: the next half's first weight (anticausal, half 0)
+    float* val = dt_smem + (size_t)warp * 2 * lpad;
+    float* wgt = val + lpad;
+    const int64_t lines = (int64_t)F * K * H;
+    for (int64_t r0 = (int64_t)blockIdx.x * 4; r0 < lines; r0 += (int64_t)gridDim.x * 4) {
+        const int64_t r = r0 + rb;
+        const bool live = r < lines;
+        float* line = sig + (size_t)(live ? r : 0) * W;
+        const int f = live ? (int)(r / ((int64_t)K * H)) : 0;
+        const int y = live ? (int)(r % H) : 0;
+        const float* dl = Dx + ((size_t)f * H + y) * W;
+        auto pidx = [&](int n) { return n + __float2int_rz(((float)n + 0.5f) * invC); };  // local n
+        if (live) {
+            const float4* line4 = reinterpret_cast<const float4*>(line + a);
+            const float4* dl4 = reinterpret_cast<const float4*>(dl + a);
+            const int L4 = (L + 3) >> 2;
+            for (int nb = lane; nb < L4; nb += 32 * kDtB2) {
+                float4 lv[kDtB2], dv[kDtB2];
+#pragma unroll
+                for (int u = 0; u < kDtB2; ++u) {
+                    const int n4 = nb + 32 * u;
+                    lv[u] = (n4 < L4) ? line4[n4] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    dv[u] = (n4 < L4) ? __ldg(dl4 + n4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < kDtB2; ++u) {
+                    const int n4 = nb + 32 * u;
+                    if (n4 < L4) {
+                        const float le[4] = {lv[u].x, lv[u].y, lv[u].z, lv[u].w};
+                        const float de[4] = {dv[u].x, dv[u].y, dv[u].z, dv[u].w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int n = 4 * n4 + e;  // local (W % 4 = 0: L % 4 = 0)
+                            val[pidx(n)] = le[e];
+                            wgt[pidx(n)] = (a + n == 0) ? 0.f : __expf(lna * de[e]);
+                        }
+                    }
+                }
+            }
+            // w[b] where wnext reads it for half 0's last element (two past its padded index)
+            if (h == 0 && lane == 0) wgt[pidx(L - 1) + 2] = (b < W) ? __expf(lna * __ldg(dl + b)) : 0.f;
+        }
+        __syncwarp();
+        const int n0 = min(lane * C, L), n1 = min(n0 + C, L);
+        const int base = lane * (C + 1);  // padded index of n0
+        // causal: lane chunk maps, warp scan, then the value entering this half
+        float2 m = make_float2(1.f, 0.f);
+        for (int q = base; q < base + (n1 - n0); ++q) m = amap_compose(make_float2(wgt[q], (1.f - wgt[q]) * val[q]), m);
+        float2 incl = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float ax = __shfl_up_sync(0xffffffffu, incl.x, o), ay = __shfl_up_sync(0xffffffffu, incl.y, o);
+            if (lane >= o) incl = amap_compose(incl, make_float2(ax, ay));
+        }
+        if (h == 0 && lane == 31) xch[0][rb] = incl.y;  // half 0 starts at w = 0: its map is (0, J_end)
+        __syncthreads();
+        const float Jin = (h == 0) ? 0.f : xch[0][rb];
+        const float ex = __shfl_up_sync(0xffffffffu, incl.x, 1), ey = __shfl_up_sync(0xffffffffu, incl.y, 1);
+        float J = (lane == 0) ? Jin : ex * Jin + ey;
+        for (int q = base; q < base + (n1 - n0); ++q) {
+            J = wgt[q] * J + (1.f - wgt[q]) * val[q];
+            val[q] = J;
+        }
+        __syncwarp();
+        // anticausal: local n uses w[n+1] (the last element of the row 0; half 0's last element
+        // the staged first weight of half 1)
+        auto wnext = [&](int n, int q) {
+            if (a + n + 1 >= W) return 0.f;
+            return wgt[(n + 1 == n1) ? q + 2 : q + 1];
+        };
+        m = make_float2(1.f, 0.f);
+        for (int n = n1 - 1, q = base + (n1 - 1 - n0); n >= n0; --n, --q) {
+            const float w = wnext(n, q);
+            m = amap_compose(make_float2(w, (1.f - w) * val[q]), m);
+        }
+        incl = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float ax = __shfl_down_sync(0xffffffffu, incl.x, o), ay = __shfl_down_sync(0xffffffffu, incl.y, o);
+            if (lane + o < 32) incl = amap_compose(incl, make_float2(ax, ay));
+        }
+        if (h == 1 && lane == 0) xch[1][rb] = incl.y;  // half 1 ends at w = 0: its map is (0, J_start)
+        __syncthreads();
+        const float Jin2 = (h == 1) ? 0.f : xch[1][rb];
+        const float fx = __shfl_down_sync(0xffffffffu, incl.x, 1), fy = __shfl_down_sync(0xffffffffu, incl.y, 1);
+        J = (lane == 31) ? Jin2 : fx * Jin2 + fy;
+        for (int n = n1 - 1, q = base + (n1 - 1 - n0); n >= n0; --n, --q) {
+            const float w = wnext(n, q);
+            J = w * J + (1.f - w) * val[q];
+            val[q] = J;
+        }
+        __syncwarp();
+        if (live)
+            for (int n = lane; n < L; n += 32) line[a + n] = val[pidx(n)];
+        __syncthreads();
+    }
+}
+
 // Column pass, in place on the row-major sig [F][K][H][W], w = exp(lna · Dy) with Dy [F][H][W]:
 // one block per 32 adjacent columns of one (frame, channel) plane; lane = column (coalesced
 // 128-byte row segments), warp = a chunk of rows.  Each lane composes its chunk's maps, the

@@ -18,11 +18,13 @@ def dev(a):
 
 
 # tall planes (H = 1536, 1600): long column recursions across many warp chunks; H = 1080, 1152:
-# the register-resident column kernel (up to its 64 × 18 rows), 1153: the transpose path
+# the register-resident column kernel (up to its 64 × 18 rows), 1153: the transpose path;
+# W = 260, 1028, 1920: rows of ≥ 256 pixels take two warps per row (k_dt_rows2)
 @pytest.mark.parametrize("H,W,K,ss,sr", [(48, 64, 1, 16.0, 16.0), (37, 203, 2, 4.0, 8.0), (5, 17, 1, 8.0, 4.0),
                                          (130, 9, 3, 32.0, 64.0), (1, 77, 1, 4.0, 4.0), (1600, 40, 1, 16.0, 8.0),
                                          (1536, 33, 1, 8.0, 16.0), (1152, 48, 1, 16.0, 16.0), (1080, 100, 2, 16.0, 8.0),
-                                         (1153, 20, 1, 16.0, 16.0)])
+                                         (1153, 20, 1, 16.0, 16.0), (40, 1920, 1, 16.0, 16.0), (33, 260, 2, 8.0, 4.0),
+                                         (7, 1028, 1, 32.0, 8.0)])
 def test_dt_parity(H, W, K, ss, sr):
     w = make("c2", W=W, H=H, n_cells=6)
     rng = np.random.default_rng(H * 1000 + W)
