@@ -1611,9 +1611,16 @@ static void dt_impl(const uint8_t* rgb, int F, int H, int W, const float* in, in
             if (rows2) LAUNCH(k_dt_rows2, rowBlocks2, 256, smem2, s, out, Dx, F, K, H, W, lna);
             else LAUNCH(k_dt_rows, rowBlocks, 32 * nw, smem, s, out, Dx, F, K, H, W, lna);
             if (colsReg) {
-                const int64_t tiles = (int64_t)F * K * ((W + 15) / 16);
-                LAUNCH(k_dt_cols_reg, (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 8)), 1024, 0, s, out, Dy, F,
-                       K, H, W, lna);
+                static const int colsPer = [] {  // A/B: FBS_DT_COLSPER = 4, 8 or 16
+                    const char* e = std::getenv("FBS_DT_COLSPER");
+                    const int v = e ? std::atoi(e) : 8;
+                    return (v == 4 || v == 16) ? v : 8;
+                }();
+                const int64_t tiles = (int64_t)F * K * ((W + colsPer - 1) / colsPer);
+                const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 148 * 32));
+                if (colsPer == 16) LAUNCH_AS("k_dt_cols_reg", k_dt_cols_reg<16>, blocks, 1024, 0, s, out, Dy, F, K, H, W, lna);
+                else if (colsPer == 4) LAUNCH_AS("k_dt_cols_reg", k_dt_cols_reg<4>, blocks, 256, 0, s, out, Dy, F, K, H, W, lna);
+                else LAUNCH_AS("k_dt_cols_reg", k_dt_cols_reg<8>, blocks, 512, 0, s, out, Dy, F, K, H, W, lna);
             } else if (viaT) {
                 LAUNCH(k_dt_transpose, tgN, tb, 0, s, out, sT, H, W);
                 LAUNCH(k_dt_rows, rowBlocksT, 32 * nwT, smemT, s, sT, DyT, F, K, W, H, lna);

@@ -437,26 +437,27 @@ __global__ void __launch_bounds__(1024) k_dt_cols(float* __restrict__ sig, const
 }
 
 // Column pass with the column held in registers (H ≤ kDtColChunks · kDtColRows): one block of
-// 1024 threads per 16 adjacent columns of one (frame, channel) plane; thread (warp w, lane l)
-// owns column l % 16 and chunk 2w + l / 16 of kDtColRows consecutive rows (a warp's loads are
-// two 64-byte row segments).  The chunk's values and weights are read once into registers;
+// 64·COLS threads per COLS adjacent columns of one (frame, channel) plane; thread (warp w, lane l)
+// owns column l % COLS and chunk w·(32/COLS) + l / COLS of kDtColRows consecutive rows (COLS = 8:
+// a warp's loads are four 32-byte row segments, two blocks per SM).  The chunk's values and weights are read once into registers;
 // causal and anticausal passes compose the chunk's affine maps, scan the column's chunk maps in
 // shared memory (Hillis–Steele, in chunk order) and re-run the chunk from its incoming value;
 // the result is stored once: 12 bytes per pixel (sig read and written, Dy read).
 constexpr int kDtColRows = 18;  // H ≤ 1152 (registers: 64 per thread at 1024 threads)
 constexpr int kDtColChunks = 64;
-__global__ void __launch_bounds__(1024, 1) k_dt_cols_reg(float* __restrict__ sig, const float* __restrict__ Dy, int F,
-                                                         int K, int H, int W, float lna) {
+template <int COLS>  // columns per block: 16 (1024 threads, 64-byte row segments) or 8 (512 threads, 2 blocks/SM)
+__global__ void __launch_bounds__(COLS * kDtColChunks, 1024 / (COLS * kDtColChunks)) k_dt_cols_reg(
+    float* __restrict__ sig, const float* __restrict__ Dy, int F, int K, int H, int W, float lna) {
     pdl_entry();
-    __shared__ float2 cm[kDtColChunks][16];
+    __shared__ float2 cm[kDtColChunks][COLS];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int col = lane & 15, j = 2 * warp + (lane >> 4);  // chunk index
-    const int tilesX = (W + 15) / 16;
+    const int col = lane % COLS, j = warp * (32 / COLS) + lane / COLS;  // chunk index
+    const int tilesX = (W + COLS - 1) / COLS;
     const int64_t planes = (int64_t)F * K;
     const int R = (H + kDtColChunks - 1) / kDtColChunks;  // rows per chunk (≤ kDtColRows)
     for (int64_t b = blockIdx.x; b < planes * tilesX; b += gridDim.x) {
         const int64_t pl = b / tilesX;
-        const int x = (int)(b % tilesX) * 16 + col;
+        const int x = (int)(b % tilesX) * COLS + col;
         const int f = (int)(pl / K);
         const bool ok = x < W;
         float* cs = sig + (size_t)pl * H * W + (ok ? x : 0);
