@@ -465,6 +465,7 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->perm = dalloc<uint8_t>(A, (size_t)g->ncells * kCellMaxPx, s);
         int* cellCnt = dalloc<int>(A, g->ncells, s);
         unsigned long long* heads = dalloc<unsigned long long>(A, g->ncells, s);
+        g->heads = heads;  // kept: the splat ranks its sorted pixels from it
         const int cellBlocks = grid_for(g->ncells * 32, 256, 1 << 20);
         LAUNCH(k_grid_sort, cellBlocks, 256, 0, s, rgb, geo, lutL, lutUV, g->ncells, cellCnt, heads, g->perm, err);
         LAUNCH(k_scan_excl, (unsigned)std::max<int64_t>(scanTiles, 1), kScanBlock, 0, s, cellCnt, g->ncells, g->cellOff,
@@ -1383,7 +1384,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->tcount = S->counters + (size_t)2 * F * K;        // [K + 1][F] (k_tree_lift)
         unsigned* zctr = S->tcount + (size_t)(K + 1) * F;    // [F] (k_gram)
         // a4: splat Sc, b = S(c∘t)
-        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, c, t,
+        LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->heads, g->perm, c, t,
                K, M, S->sc, bIn, S->inflags);
         // optional low-rank reduction of B (Supp. §4): Kc reduced channels
         int Kc = K;
@@ -1651,7 +1652,7 @@ static void backward_impl(fbs_system S, const float* g_dldx, const float* t, con
     }
     CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
     // u = S g (∂f/∂b = A⁻¹(S ∂f/∂x̂)), solved from x0 = 0 (reading #14)
-    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, g_dldx, K,
+    LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->heads, g->perm, nullptr, g_dldx, K,
            M, nullptr, S->u, S->inflags);
     VecArgs a = make_args(S, S->bwd, S->xb, S->u);
     S->rMasked = false;  // u = S g need not vanish on dead vertices: the lift reads w = mask∘r
@@ -1907,7 +1908,7 @@ int fbs_splat(fbs_grid g, const float* p, int K, float* out, fbs_stream stream) 
         const size_t KM = (size_t)K * g->M;
         float* planar = dalloc<float>(tmp, KM, s);
         CellGeom geo{g->F, g->H, g->W, g->ncx, g->ncy, g->colStart, g->rowStart};
-        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->vid, g->perm, nullptr, p, K,
+        LAUNCH(k_splat<false>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->heads, g->perm, nullptr, p, K,
                g->M, nullptr, planar, nullptr);
         LAUNCH(k_export_vk, grid_for(KM), kThreads, 0, s, planar, g->frameOff + g->F, (int64_t)0, g->M, K, out);
         free_all(tmp, s);

@@ -375,7 +375,8 @@ struct fbs_grid_s {
     uint64_t* keys = nullptr;  // [N] capacity (first M valid)
     int* m = nullptr;          // [N] capacity
     int* cellOff = nullptr;    // [ncells + 1]
-    uint8_t* perm = nullptr;   // [ncells][64] sorted position → local pixel (splat order)
+    uint8_t* perm = nullptr;   // [ncells][64] sorted position → the pixel's row·8 + column in its cell
+    unsigned long long* heads = nullptr;  // [ncells] run-head bits of the sorted positions (vertex ranks)
     int4* nbr = nullptr;       // [M] packed neighbour offsets (fbs_common.cuh near_off)
     float* n = nullptr;        // [M]
     int* frameOff = nullptr;   // device [F + 1]

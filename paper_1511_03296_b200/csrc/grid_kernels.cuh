@@ -115,13 +115,13 @@ __global__ void __launch_bounds__(256) k_grid_sort(
         if (lane < npx) {
             const int iy = (int)(((float)lane + 0.5f) * rw);
             const int px = x0 + lane - iy * w, py = y0 + iy;
-            a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)lane;
+            a0 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)(iy << 3 | (lane - iy * w));
         }
         if (lane + 32 < npx) {
             const int i = lane + 32;
             const int iy = (int)(((float)i + 0.5f) * rw);
             const int px = x0 + i - iy * w, py = y0 + iy;
-            a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)i;
+            a1 = (luv_code(base + ((size_t)py * g.W + px) * 3, lutL, lutUV) << 6) | (uint32_t)(iy << 3 | (i - iy * w));
         }
         warp_bitonic64(a0, a1, lane);
         // run heads in sorted order (same code ⇒ same vertex)
@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(256) k_grid_sort(
         const bool h1 = v1 && ((prev1 >> 6) != (a1 >> 6));
         const unsigned hb0 = __ballot_sync(0xffffffffu, h0);
         const unsigned hb1 = __ballot_sync(0xffffffffu, h1);
-        if (v0) perm[(size_t)c * kCellMaxPx + lane] = (uint8_t)(a0 & 63u);  // sorted position → local pixel
+        // sorted position → the pixel's (row, column) in the cell as row·8 + column (w, h ≤ 8): the
+        // same order as the row-major pixel index for equal codes, and no division to decode
+        if (v0) perm[(size_t)c * kCellMaxPx + lane] = (uint8_t)(a0 & 63u);
         if (v1) perm[(size_t)c * kCellMaxPx + lane + 32] = (uint8_t)(a1 & 63u);
         if (lane == 0) {
             cnt[c] = __popc(hb0) + __popc(hb1);
@@ -224,7 +226,6 @@ __global__ void __launch_bounds__(256, 8) k_grid_write(
         const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
         const int w = g.colStart[cx + 1] - x0;
         const int npx = min(w * (g.rowStart[cy + 1] - y0), kCellMaxPx);
-        const float rw = 1.f / (float)w;
         const unsigned long long H64 = heads[c];
         const unsigned off = (unsigned)cellOff[c];
         const uint64_t khi = ((uint64_t)f << 56) | ((uint64_t)cy << 40) | ((uint64_t)cx << 24);
@@ -234,9 +235,8 @@ __global__ void __launch_bounds__(256, 8) k_grid_write(
         for (int j = 0; j < 2; ++j) {
             const int e = lane + 32 * j;
             if (e >= npx) continue;
-            const int i = perm[(size_t)c * kCellMaxPx + e];
-            const int iy = (int)(((float)i + 0.5f) * rw);
-            const int px = x0 + i - iy * w, py = y0 + iy;
+            const int i = perm[(size_t)c * kCellMaxPx + e];  // row·8 + column
+            const int px = x0 + (i & 7), py = y0 + (i >> 3);
             const unsigned long long upto = (e == 63) ? ~0ull : ((2ull << e) - 1ull);
             const unsigned v = off + (unsigned)__popcll(H64 & upto) - 1u;
             vbase[(size_t)py * g.W + px] = (int)v;

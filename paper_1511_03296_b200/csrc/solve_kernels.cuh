@@ -110,7 +110,8 @@ using SplatAcc = float;
 // WEIGHTED: Sc = S c and b_k = S(c∘t_k) (Eq. quad_min); otherwise out_k = S p_k.
 template <bool WEIGHTED>
 __global__ void __launch_bounds__(256, 8) k_splat(CellGeom g, const int* __restrict__ cellOff,
-                                               const int* __restrict__ vid, const uint8_t* __restrict__ perm,
+                                               const unsigned long long* __restrict__ heads,
+                                               const uint8_t* __restrict__ perm,
                                                const float* __restrict__ c, const float* __restrict__ p, int K,
                                                int64_t M, float* __restrict__ sc_out, float* __restrict__ out,
                                                int* __restrict__ flags) {
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(256, 8) k_splat(CellGeom g, const int* __restr
         const int x0 = g.colStart[cx], y0 = g.rowStart[cy];
         const int w = g.colStart[cx + 1] - x0, h = g.rowStart[cy + 1] - y0;
         const int npx = min(w * h, kCellMaxPx);
-        const float rw = 1.f / (float)w;  // (i + ½)/w is ≥ 1/128 from an integer: exact row
+        const unsigned long long H64 = heads[cell];  // run heads of the sorted pixels (k_grid_sort)
         const int vbeg = cellOff[cell];
         const float* pf = p + (size_t)f * K * HW;
         int pix[2], rk[2];
@@ -139,10 +140,12 @@ __global__ void __launch_bounds__(256, 8) k_splat(CellGeom g, const int* __restr
             cw[j] = 0.f;
             pv[j] = 0.f;
             if (e < npx) {
-                const int i = perm[(size_t)cell * kCellMaxPx + e];
-                const int iy = (int)(((float)i + 0.5f) * rw);
-                pix[j] = (y0 + iy) * g.W + (x0 + i - iy * w);
-                rk[j] = vid[(size_t)f * HW + pix[j]] - vbeg;
+                const int i = perm[(size_t)cell * kCellMaxPx + e];  // row·8 + column in the cell
+                pix[j] = (y0 + (i >> 3)) * g.W + (x0 + (i & 7));
+                // the vertex of sorted position e within the cell: its run's rank (= vid − cellOff),
+                // from the head mask instead of a gathered vid load
+                const unsigned long long upto = (e == 63) ? ~0ull : ((2ull << e) - 1ull);
+                rk[j] = __popcll(H64 & upto) - 1;
                 cw[j] = WEIGHTED ? c[(size_t)f * HW + pix[j]] : 1.f;
                 if (K > 0) pv[j] = pf[pix[j]];
             }
