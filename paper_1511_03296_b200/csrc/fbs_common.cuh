@@ -39,7 +39,10 @@ constexpr int kCellMaxPx = 64;       // level-0 cell = one warp, ≤ 2 px per la
 constexpr int kCellsPerBlock = 8;    // 8 warps, one cell each
 constexpr int kCoarseCap = 512;      // children of one pyramid coarse cell sorted in shared memory (larger: global scratch)
 constexpr int kMaxLevels = 24;
-constexpr int kThreads = 256;        // vertex-parallel kernels
+#ifndef FBS_KTHREADS
+#define FBS_KTHREADS 256
+#endif
+constexpr int kThreads = FBS_KTHREADS;  // vertex-parallel kernels
 constexpr int kMaxK = 64;
 constexpr int kVecPad = 512;         // vertex arrays streamed by bulk copies are allocated with this slack
 constexpr int kScanTile = 256;       // tree-ordered level-1 positions per prefix-scan tile (tree_kernels.cuh)
