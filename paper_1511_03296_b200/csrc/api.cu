@@ -883,6 +883,13 @@ void tree_coarse(fbs_system S, const HierArgs& h, const VecArgs& a, int first, c
     const bool ks = (MODE == HIER_PCG && h.C > 1) || (MODE == HIER_INIT && h.C > 2);
     auto kern = ks ? k_tree_coarse<MODE, true> : k_tree_coarse<MODE, false>;
     // ks: the finish reads the split level-0 kernel's partials (BPFs per (frame, channel))
+    if (MODE == HIER_PCG && S->bpf2g > 0) {  // small problems: G = 8 lanes per level-2 vertex
+        HierArgs hg = h;
+        hg.bpf2 = S->bpf2g;
+        auto kg = ks ? k_tree_coarse<HIER_PCG, true, 8> : k_tree_coarse<HIER_PCG, false, 8>;
+        LAUNCH_AS(name.c_str(), kg, a.nf * hg.bpf2 * (ks ? h.C : 1), 256, 0, s, hg, ks ? split_args(S, a) : a, first);
+        return;
+    }
     LAUNCH_AS(name.c_str(), kern, a.nf * S->bpf2 * (ks ? h.C : 1), 256, 0, s, h, ks ? split_args(S, a) : a, first);
 }
 
@@ -961,7 +968,7 @@ void restrict_frames(fbs_system S, int f0, int nf, VecArgs& a, HierArgs& h) {
     h.lvFrameOff += f0;  // [L][F+1] row-major: k·(F+1) + f0 + f
     h.frameLevels += f0;
     h.tileFrameOff += f0;  // tile ids stay global (tileFrameOff[f] − tileFrameOff[0] is group-local)
-    h.partial2 += (size_t)f0 * S->bpf2 * h.C;
+    h.partial2 += (size_t)f0 * std::max(S->bpf2, S->bpf2g) * h.C;
     h.counters += f0;
 }
 
@@ -1438,7 +1445,17 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             if (const char* e = std::getenv("FBS_BPF2_OCC")) occ2 = std::max(1, std::min(64, std::atoi(e)));  // A/B
             const int64_t cap2 = std::max<int64_t>(1, ((int64_t)g_num_sms * occ2 + F - 1) / F);
             S->bpf2 = (int)std::max<int64_t>(1, std::min(want2, cap2));
-            S->partial2 = dalloc<double>(A, (size_t)F * S->bpf2 * C, s);
+            // the PCG coarse pass with 8 lanes per level-2 vertex when all of them fit in about
+            // two resident waves (single frames: configs[1, 2]); FBS_COARSE_G=1 / 8 forces (A/B)
+            {
+                const char* e = std::getenv("FBS_COARSE_G");
+                const int64_t lanes = (int64_t)F * (g->L > 2 ? g->maxFrameM2 : 0) * 8;
+                const bool small = g->L > 2 && lanes <= 2ll * g_num_sms * 4 * 256;
+                const bool on = e ? std::atoi(e) == 8 && g->L > 2 : small;
+                const int64_t capg = std::max<int64_t>(1, ((int64_t)g_num_sms * 4 + F - 1) / F);
+                S->bpf2g = on ? (int)std::max<int64_t>(1, std::min<int64_t>((lanes / F + 255) / 256, capg)) : 0;
+            }
+            S->partial2 = dalloc<double>(A, (size_t)F * std::max(S->bpf2, S->bpf2g) * C, s);
             if (hierP) {
                 for (int k = 1; k < g->L; ++k) S->mu[k] = dalloc<float>(A, g->lv[k].M, s);
             }

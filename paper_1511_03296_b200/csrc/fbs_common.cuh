@@ -441,6 +441,7 @@ struct fbs_system_s {
     float* acc1T = nullptr;
     double* partial2 = nullptr;
     int bpf2 = 1;
+    int bpf2g = 0;            // > 0: the PCG coarse pass runs 8 lanes per level-2 vertex with these blocks per frame
     int C = 1;
     double* partial = nullptr;  // [F][BPF][2K]
     unsigned* counters = nullptr;  // [F][K] (VecArgs kernels)

@@ -503,7 +503,12 @@ __device__ __forceinline__ double tree_prefix(const HierArgs& h, const double* t
 // PDA (one thread per coarse vertex of every level ≥ 1... levels ≥ 2 here, level 1 in the lift):
 //   μ_k = z_w(k; α, β) P(1)_k / P(diag A)_k, 0 where the denominator is 0
 //   (reading #10) or above the frame's top level.
-template <int MODE, bool KS = false>
+// G = 8 (small problems, api.cu): a group of G lanes per level-2 vertex, lane t taking the levels
+// 2 + t, 2 + t + G, …: the ancestor ranges, multipliers and prefix values of all levels go out in
+// one round trip each instead of one round per four levels; the fp32 contributions are summed by
+// the group's first lane in level order (the same additions as G = 1), the children split over
+// the lanes.
+template <int MODE, bool KS = false, int G = 1>
 __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int first) {
     pdl_entry();
     __shared__ double shd[32];
@@ -557,6 +562,52 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
                 }
                 continue;
             }
+            if constexpr (G > 1) {
+                const int lane = threadIdx.x & 31, t = lane % G, gl0 = lane - t;
+                const int gpb = blockDim.x / G;  // vertex groups per block
+                for (int vb = a0 + j * gpb; vb < a1; vb += h.bpf2 * gpb) {  // uniform over the block
+                    const int v = vb + (int)threadIdx.x / G;
+                    const bool valid = v < a1;
+                    const int2 kids = valid ? h.lv[2].rng[v] : make_int2(0, 0);
+                    const int first1 = kids.x;
+                    float acc = 0.f;
+                    for (int kb = 2; kb <= top; kb += G) {  // levels kb + t of every lane
+                        const int k = kb + t;
+                        float cv = 0.f;
+                        if (valid && k <= top) {
+                            int2 r;
+                            float m;
+                            if (k == 2) {
+                                r = kids;
+                                m = (MODE == HIER_INIT) ? init_mult1(h, 2, fl, h.lv[2].count[v]) : h.lv[2].mu[v];
+                            } else {
+                                const size_t o = (size_t)(k - 3) * h.M2 + v;
+                                r = __ldg(h.ancRng + o);
+                                m = __ldg(h.ancMult + o);
+                            }
+                            const double S = tree_prefix(h, tb, c, fb, r.x + r.y - 1) - tree_prefix(h, tb, c, fb, r.x - 1);
+                            cv = m * (float)S;
+                            if (MODE == HIER_PCG && (k == 2 || r.x == first1)) rho += (double)m * S * S;
+                        }
+                        // the group's first lane adds the levels in order (as the G = 1 loop does)
+#pragma unroll
+                        for (int u = 0; u < G; ++u) {
+                            const float cu = __shfl_sync(0xffffffffu, cv, gl0 + u);
+                            if (u == 0 && kb == 2) acc = cu;
+                            else if (kb + u <= top) acc += cu;
+                        }
+                    }
+                    acc = __shfl_sync(0xffffffffu, acc, gl0);
+                    // acc1 for the children, split over the group's lanes
+                    const float* b1 = h.buf1T + (size_t)c * h.M1;
+                    for (int i = kids.x + t; valid && i < kids.x + kids.y; i += G) {
+                        const float m1 = (MODE == HIER_INIT) ? init_mult1(h, 1, fl, h.csT[i + 1] - h.csT[i]) : h.mu1T[i];
+                        const float bv = b1[i];
+                        h.acc1T[(size_t)c * h.M1 + i] = m1 * bv + acc;
+                        if (MODE == HIER_PCG) rho += (double)m1 * (double)bv * (double)bv;
+                    }
+                }
+            } else
             for (int v = a0 + j * blockDim.x + threadIdx.x; v < a1; v += stride) {
                 // level-1 children of v: one contiguous tree range (L = 2: v itself)
                 const int2 kids = (lv == 2) ? h.lv[2].rng[v] : make_int2(v, 1);
