@@ -1450,7 +1450,9 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             {
                 const char* e = std::getenv("FBS_COARSE_G");
                 const int64_t lanes = (int64_t)F * (g->L > 2 ? g->maxFrameM2 : 0) * 8;
-                const bool small = g->L > 2 && lanes <= 2ll * g_num_sms * 4 * 256;
+                // (K = 1 only: with the channel split the blocks × channels outgrow the work — configs[3]
+                // hierarchical 1.98 → 2.27 ms)
+                const bool small = g->L > 2 && Kc == 1 && lanes <= 2ll * g_num_sms * 4 * 256;
                 const bool on = e ? std::atoi(e) == 8 && g->L > 2 : small;
                 const int64_t capg = std::max<int64_t>(1, ((int64_t)g_num_sms * 4 + F - 1) / F);
                 S->bpf2g = on ? (int)std::max<int64_t>(1, std::min<int64_t>((lanes / F + 255) / 256, capg)) : 0;
