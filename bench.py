@@ -521,6 +521,17 @@ def main():
                     "GBps": 20 * kernel_bytes("k_bistoch", M, lv, w.pixels) / (bs_wall * 1e-3) / 1e9 if bs_wall else None,
                     "note": "one Alg. 1 iteration over all frames (all groups) over its wall time, measured as "
                             "(grid build with 20 iterations - grid build with 0) / 20"}
+    if bistoch_rate["GBps"]:
+        bistoch_rate["frac"] = bistoch_rate["GBps"] / 6550.7
+    # the other stages against their algorithmic bytes (DESIGN §7 byte models; summed launch times,
+    # single-stream stages): grid build (sort + write + neighbours) and slice
+    stage_rates = {}
+    for st, names in (("grid_build", ("k_grid_sort", "k_grid_write", "k_grid_neighbours")), ("slice", ("k_slice4",))):
+        ms_ = sum(kernels[n]["ms_per_step"] for n in names if n in kernels)
+        by_ = sum(kernel_bytes(n, M, lv, w.pixels) for n in names if n in kernels)
+        if ms_ > 0:
+            stage_rates[st] = {"ms": ms_, "algorithmic_bytes": by_, "GBps": by_ / (ms_ * 1e-3) / 1e9,
+                               "frac": by_ / (ms_ * 1e-3) / 1e9 / 6550.7}
 
     # ---- end to end through the public API with host buffers: every step copies its inputs H2D from
     # pinned memory and its result D2H inside the timed region.  Double-buffered: the H2D of step
@@ -766,7 +777,7 @@ def main():
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches), "extras": extras,
                 "graph": graph_line,
                 "clocks": clk, "stages_ms_per_step": stages_ms, "pcg_iteration_rate": pcg_iteration_rate,
-                "bistoch_iteration_rate": bistoch_rate, "kernels": kernels,
+                "bistoch_iteration_rate": bistoch_rate, "stage_rates": stage_rates, "kernels": kernels,
                 "profiled_ms_per_step": prof_ms / args.steps}
         print(json.dumps(line), flush=True)
     if world > 1:
