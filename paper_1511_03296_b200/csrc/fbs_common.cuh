@@ -140,20 +140,27 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 // Per-frame "last block done": every block of frame f calls this once after writing its
 // partials; returns true (in all threads) only in the last block to arrive, which then owns
 // the frame's final fixed-order reduction.  Resets the counter for the next launch.
+// One fence per block, by the thread that signals (the grid-barrier pattern): the block barrier
+// orders every thread's partial writes before thread 0's release fence, which is cumulative; the
+// acquire fence before the second barrier covers the last block's reads.  Fencing in every
+// thread made each wait for its own streaming stores (the SpMV's q) to be acknowledged.
 __device__ __forceinline__ bool last_block_of_frame(unsigned* counter, int bpf, int* sflag) {
+#ifdef FBS_FENCE_ALL
     __threadfence();
+#endif
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         unsigned prev = atomicAdd(counter, 1u);
-        *sflag = (prev == (unsigned)(bpf - 1));
+        const bool last = (prev == (unsigned)(bpf - 1));
+        if (last) {
+            __threadfence();
+            *counter = 0u;
+        }
+        *sflag = last;
     }
     __syncthreads();
-    const bool last = *sflag != 0;
-    if (last) {
-        __threadfence();
-        if (threadIdx.x == 0) *counter = 0u;
-    }
-    return last;
+    return *sflag != 0;
 }
 
 // ------------------------------------------------------------------ decoupled look-back scan
