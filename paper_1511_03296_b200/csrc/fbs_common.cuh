@@ -137,6 +137,30 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return r;
 }
 
+// Two deterministic block sums in one pass (one barrier pair instead of two); the same fixed
+// trees as block_sum, so each result is bitwise block_sum's.  `sh` needs 2·blockDim.x/32 ≤ 32
+// doubles.  All threads call; results valid in thread 0.
+__device__ __forceinline__ void block_sum2(double& v0, double& v1, double* sh) {
+    v0 = warp_sum(v0);
+    v1 = warp_sum(v1);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+    __syncthreads();
+    if (l == 0) {
+        sh[w] = v0;
+        sh[16 + w] = v1;
+    }
+    __syncthreads();
+    double r0 = 0.0, r1 = 0.0;
+    if (w == 0) {
+        r0 = (l < nw) ? sh[l] : 0.0;
+        r1 = (l < nw) ? sh[16 + l] : 0.0;
+        r0 = warp_sum(r0);
+        r1 = warp_sum(r1);
+    }
+    v0 = r0;
+    v1 = r1;
+}
+
 // Per-frame "last block done": every block of frame f calls this once after writing its
 // partials; returns true (in all threads) only in the last block to arrive, which then owns
 // the frame's final fixed-order reduction.  Resets the counter for the next launch.

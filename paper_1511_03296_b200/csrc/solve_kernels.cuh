@@ -256,16 +256,17 @@ __device__ void finish_rho(const VecArgs& a, int f, int k0, int k1, bool first, 
             R += __ldcg(pp);
             RR += __ldcg(pp + 1);
         }
-        R = block_sum(R, shd);
-        RR = block_sum(RR, shd);
+        block_sum2(R, RR, shd);
         if (threadIdx.x == 0) finish_rho_one(a, fk, first, R, RR);
     }
 }
 
+// (ONE: v1 is 0 and needs no reduction)
+template <bool ONE = false>
 __device__ __forceinline__ void write_partials(const VecArgs& a, int f, int j, int k, double v0, double v1,
                                                double* shd) {
-    v0 = block_sum(v0, shd);
-    v1 = block_sum(v1, shd);
+    if (ONE) v0 = block_sum(v0, shd);
+    else block_sum2(v0, v1, shd);
     if (threadIdx.x == 0) {
         double* pp = a.partial + ((size_t)f * a.BPF + j) * 2 * a.K + 2 * k;
         pp[0] = v0;
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
                 a.x[off + v] = 0.f;
             }
         }
-        write_partials(a, f, j, k, bb, 0.0, shd);
+        write_partials<true>(a, f, j, k, bb, 0.0, shd);
     }
     if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) {
         for (int k = bu.k0; k < bu.k1; ++k) {
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
                 dq += (double)me.x * (double)q;
             }
         }
-        write_partials(a, f, j, k, dq, 0.0, shd);
+        write_partials<true>(a, f, j, k, dq, 0.0, shd);
     }
     if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
         for (int k = 0; k < a.K; ++k) {
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(256) k_spmv2_split(VecArgs a) {
                 dq += (double)me.x * (double)q;
             }
         }
-        write_partials(a, f, j, k, dq, 0.0, shd);
+        write_partials<true>(a, f, j, k, dq, 0.0, shd);
     }
     if (last_block_of_frame(a.counters + g, a.BPF, &sflag)) {
         for (int k = kb; k < ke; ++k) {

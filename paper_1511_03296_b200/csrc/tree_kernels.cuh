@@ -683,8 +683,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
             }
             for (int jj = threadIdx.x; jj < h.bpf2; jj += blockDim.x)
                 R += __ldcg(h.partial2 + ((size_t)f * h.bpf2 + jj) * h.C + c);
-            R = block_sum(R, shd);
-            RR = block_sum(RR, shd);
+            block_sum2(R, RR, shd);
             if (threadIdx.x == 0) finish_rho_one(a, fk, first != 0, R, RR);
             __syncthreads();
         }
