@@ -187,6 +187,23 @@ __device__ __forceinline__ bool last_block_of_frame(unsigned* counter, int bpf, 
     return *sflag != 0;
 }
 
+// The same handshake when everything the last block reads was written by thread 0 itself (the
+// block-reduced partials of write_partials / block_sum): no barrier before the signal, thread 0
+// fences its own writes; one barrier broadcasts the outcome.
+__device__ __forceinline__ bool last_block_t0(unsigned* counter, int bpf, int* sflag) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const bool last = atomicAdd(counter, 1u) == (unsigned)(bpf - 1);
+        if (last) {
+            __threadfence();
+            *counter = 0u;
+        }
+        *sflag = last;
+    }
+    __syncthreads();
+    return *sflag != 0;
+}
+
 // ------------------------------------------------------------------ decoupled look-back scan
 // Tile state word: bits 63..62 flag (0 none, 1 aggregate, 2 inclusive prefix),
 // bits 61..31 second count (pyramid children), bits 30..0 first count (vertices).

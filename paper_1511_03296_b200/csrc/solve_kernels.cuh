@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(256) k_assemble(VecArgs a, float* __restrict__
         }
         write_partials<true>(a, f, j, k, bb, 0.0, shd);
     }
-    if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) {
+    if (last_block_t0(a.counters + bu.g, a.BPF, &sflag)) {
         for (int k = bu.k0; k < bu.k1; ++k) {
             double R = 0.0;
             for (int jj = threadIdx.x; jj < a.BPF; jj += blockDim.x)
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k_residual0(VecArgs a) {
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, true, shd);
+    if (last_block_t0(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, true, shd);
 }
 
 // Alg. 2 lines 8-12 (Jacobi):  x += αd;  r −= αq;  s = M⁻¹r = r/diag(A);  ρ_new = rᵀs.
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(256, 8) k_update(VecArgs a) {
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (last_block_of_frame(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, false, shd);
+    if (last_block_t0(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, false, shd);
 }
 
 // ---------------------------------------------------------------- streaming PCG kernels
@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(256) k_spmv2(VecArgs a) {
         }
         write_partials<true>(a, f, j, k, dq, 0.0, shd);
     }
-    if (last_block_of_frame(a.counters + f, a.BPF, &sflag)) {
+    if (last_block_t0(a.counters + f, a.BPF, &sflag)) {
         for (int k = 0; k < a.K; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) {
@@ -663,7 +663,7 @@ __global__ void __launch_bounds__(256) k_spmv2_split(VecArgs a) {
         }
         write_partials<true>(a, f, j, k, dq, 0.0, shd);
     }
-    if (last_block_of_frame(a.counters + g, a.BPF, &sflag)) {
+    if (last_block_t0(a.counters + g, a.BPF, &sflag)) {
         for (int k = kb; k < ke; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) {

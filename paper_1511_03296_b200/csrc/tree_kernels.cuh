@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) k_hier_level0(VecArgs a, float* __restric
         }
         write_partials(a, f, j, k, rho, rr, shd);
     }
-    if (FINISH_LAST && last_block_of_frame(a.counters + ci, a.BPF, &sflag)) {
+    if (FINISH_LAST && last_block_t0(a.counters + ci, a.BPF, &sflag)) {
         for (int k = kB; k < kE; ++k) {
             const int fk = f * a.K + k;
             if (!a.sc_.active[fk]) continue;
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(256) k_tree_coarse(HierArgs h, VecArgs a, int 
             if (threadIdx.x == 0) h.partial2[((size_t)f * h.bpf2 + j) * h.C + c] = rho;
         }
     }
-    if (MODE == HIER_PCG && last_block_of_frame(h.counters + (KS ? (size_t)cB * h.F : 0) + f, h.bpf2, &sflag)) {
+    if (MODE == HIER_PCG && last_block_t0(h.counters + (KS ? (size_t)cB * h.F : 0) + f, h.bpf2, &sflag)) {
         for (int c = (KS ? cB : 0); c < (KS ? cE : a.K); ++c) {
             const int fk = f * a.K + c;
             if (!first && !a.sc_.active[fk]) continue;
