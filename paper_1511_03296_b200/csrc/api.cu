@@ -1148,34 +1148,74 @@ struct PcgRun {
     HierArgs h;
     cudaStream_t s;
 };
+// The host's view of a TOL run after a chunk: the active count and, for a single (frame,
+// channel), ‖b‖² and the last ‖r‖² (k_tol_probe copies them into mapped pinned memory).
+struct TolProbe {
+    int n_active;
+    int pad;
+    double bb, rr;
+};
+// Host-polled TOL loop: each run enqueues a chunk of iterations and a probe, then reads the probe
+// of the chunk before (one chunk behind, so the GPU never waits for the host).  A run of a single
+// (frame, channel) sizes its next chunk from the residual's observed rate of decrease: near
+// convergence the chunks shrink to the predicted remainder (≥ 1), so fewer iterations are
+// launched past the stopping point (they change nothing — the retired channel's kernels skip — but
+// each costs its launches).  The iterates and the stopping iteration are the same for any chunking.
 void tol_poll(fbs_system S, std::vector<PcgRun>& runs) {
     const int n = (int)runs.size();
     static const int chunk = [] {
         const char* e = std::getenv("FBS_TOL_CHUNK");  // A/B
         return (e && e[0]) ? std::max(1, std::min(64, std::atoi(e))) : 4;  // 4: configs[0,1,3] 2-6 % faster than 8
     }();
-    PinnedBlock pb = pinned_get(2 * n * sizeof(int));
-    int* pin = static_cast<int*>(pb.p);
+    static const bool adapt = [] {
+        const char* e = std::getenv("FBS_TOL_ADAPT");  // A/B: 0 = fixed chunks
+        return !(e && e[0] == '0');
+    }();
+    PinnedBlock pb = pinned_get(2 * n * sizeof(TolProbe));
+    TolProbe* pin = static_cast<TolProbe*>(pb.p);
     std::vector<cudaEvent_t> ev(2 * n, nullptr);
-    std::vector<int> done(n, 1), slot(n, 0), pending(n, -1);
+    std::vector<int> done(n, 1), slot(n, 0), pending(n, -1), at(2 * n, 0);
     std::vector<char> fin(n, 0);
+    // the last two (iteration, ‖r‖²) observations of single-(frame, channel) runs
+    std::vector<int> it1(n, -1), it2(n, -1);
+    std::vector<double> rr1(n, 0.0), rr2(n, 0.0), bbv(n, 0.0);
     try {
         for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         for (int left = n; left > 0;) {
             for (int r = 0; r < n; ++r) {
                 if (fin[r]) continue;
-                const int nit = std::min(chunk, S->o.max_iters - done[r]);
+                const VecArgs& a = runs[r].a;
+                const bool single = a.nf * a.K == 1;
+                int nit = std::min(chunk, S->o.max_iters - done[r]);
+                if (adapt && single && it1[r] >= 0 && it2[r] > it1[r] && rr2[r] > 0.0 && rr2[r] < rr1[r]) {
+                    // geometric model of ‖r‖² from the last two observations
+                    const double q = std::pow(rr2[r] / rr1[r], 1.0 / (it2[r] - it1[r]));
+                    const double target = a.tol2 * bbv[r];
+                    if (q < 1.0 && target > 0.0) {
+                        const double m = std::ceil(std::log(target / rr2[r]) / std::log(q));
+                        const double rem = m - (double)(done[r] - it2[r]);
+                        if (rem < nit) nit = std::max(1, (int)std::max(1.0, rem));
+                    }
+                }
                 for (int i = 0; i < nit; ++i) pcg_iteration(S, runs[r].a, runs[r].h, done[r] + i, false, runs[r].s);
                 done[r] += nit;
-                copy_words(runs[r].a.sc_.n_active, &pin[2 * r + slot[r]], sizeof(int), runs[r].s);
+                at[2 * r + slot[r]] = done[r];
+                LAUNCH(k_tol_probe, 1, 32, 0, runs[r].s, a.sc_.n_active, single ? a.sc_.bb : nullptr,
+                       single ? a.sc_.rr : nullptr, reinterpret_cast<int*>(&pin[2 * r + slot[r]]));
                 ck(event_record(ev[2 * r + slot[r]], runs[r].s), "event");
             }
             for (int r = 0; r < n; ++r) {
                 if (fin[r]) continue;
                 bool stop = done[r] >= S->o.max_iters;
                 if (pending[r] >= 0) {
-                    ck(cudaEventSynchronize(ev[2 * r + pending[r]]), "event sync");
-                    if (pin[2 * r + pending[r]] == 0) stop = true;
+                    const int ps = 2 * r + pending[r];
+                    ck(cudaEventSynchronize(ev[ps]), "event sync");
+                    if (pin[ps].n_active == 0) stop = true;
+                    it1[r] = it2[r];
+                    rr1[r] = rr2[r];
+                    it2[r] = at[ps];
+                    rr2[r] = pin[ps].rr;
+                    bbv[r] = pin[ps].bb;
                 }
                 pending[r] = slot[r];
                 slot[r] ^= 1;

@@ -701,6 +701,19 @@ __global__ void k_tol_cond(cudaGraphConditionalHandle h, const int* __restrict__
     }
 }
 
+// The host-polled TOL loop's probe (api.cu tol_poll): the active count and, for a single (frame,
+// channel), ‖b‖² and the last ‖r‖², into mapped pinned memory laid out as {int, pad, double, double}.
+__global__ void k_tol_probe(const int* __restrict__ n_active, const double* __restrict__ bb,
+                            const double* __restrict__ rr, int* __restrict__ out) {
+    pdl_entry();
+    if (threadIdx.x == 0) {
+        out[0] = *n_active;
+        double* d = reinterpret_cast<double*>(out + 2);
+        d[0] = bb ? *bb : 0.0;
+        d[1] = rr ? *rr : 0.0;
+    }
+}
+
 // ---------------------------------------------------------------- slice / export / backward
 // x̂ = Sᵀŷ.  ys planar [K][M] (planar = 1) or canonical [M][K].
 __global__ void k_slice(const int* __restrict__ vid, const float* __restrict__ ys, int64_t M, int K, int F,
