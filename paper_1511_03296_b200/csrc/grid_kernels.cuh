@@ -364,7 +364,6 @@ __global__ void __launch_bounds__(kBsThreads) k_bistoch(const int4* __restrict__
     // precedes every k_bistoch of a build, so they are complete when any k_bistoch block starts:
     // they are read before waiting on the previous iteration (the first bulk copies go out as soon
     // as the wait returns).
-    pdl_trigger();
     const int M = frameOff[F], vlo = frameOff[f0], vhi = frameOff[f1];
     pdl_wait();
     extern __shared__ __align__(128) unsigned char bs_smem[];
