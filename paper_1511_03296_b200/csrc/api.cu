@@ -486,16 +486,17 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         g->maxFrameM = std::max<int64_t>(1, (int64_t)H * W / 3);  // launch-size heuristic only
 
         // The pyramid and the tree order need only the keys and the frame and cell offsets, not n:
-        // on small builds (≤ 4 M pixels) they run on a side stream `sp` concurrently with Alg. 1,
-        // whose launches are then latency-bound (configs[2]: 1.35 → 1.30 ms per build + solve).  On
-        // the bench batch Alg. 1 streams at the copy bandwidth and the concurrent pyramid slows it
-        // more than it hides (5.06 vs 4.99 ms per step), so it stays serial there.
+        // they run on a side stream `sp` concurrently with Alg. 1, whose launches are latency-bound
+        // (configs[2]: 1.35 → 1.30 ms per build + solve).  Until the PDL trigger change (kernels
+        // no longer trigger their dependents at entry, fbs_common.cuh) the concurrent pyramid
+        // slowed the bench batch's Alg. 1 more than it hid (5.06 vs 4.99 ms per step); since, it
+        // pays there too: 4.925 → 4.825 ms.
         // FBS_PYR_FORK (A/B): 0 serial, 1 fork after the neighbour search, 2 before it.
         static const int pyrForkEnv = [] {
             const char* e = std::getenv("FBS_PYR_FORK");
             return (e && e[0]) ? std::atoi(e) : -1;
         }();
-        const int pyrFork = pyrForkEnv >= 0 ? pyrForkEnv : (N <= (4ll << 20) ? 1 : 0);
+        const int pyrFork = pyrForkEnv >= 0 ? pyrForkEnv : 1;
         const bool pyrSide = pyrFork != 0 && want_pyr && cap.size() > 1;
         cudaStream_t sp = s;
         cudaEvent_t pyrFork0 = nullptr, pyrJoin = nullptr;
@@ -1395,9 +1396,12 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         // in the dependent-launch gaps (8: 6.60 ms, 16: 6.21 ms per bench step; one group: equal)
         int occ = 16;
         if (const char* e = std::getenv("FBS_BPF_OCC")) occ = std::max(1, std::min(64, std::atoi(e)));  // A/B
-        // at least 2 vertices per thread: single-frame solves get fewer, fuller blocks (configs[1,2]:
-        // 3.09 → 2.79 and 1.54 → 1.46 ms; 4: 2.93 / 1.58); the bench batch is capped by occupancy
-        int vpt = 2;
+        // at least vpt vertices per thread: single-frame solves get fewer, fuller blocks (round 1,
+        // configs[1,2]: 3.09 → 2.79 and 1.54 → 1.46 ms at 2); the bench batch is capped by
+        // occupancy.  Re-measured after the PDL trigger change: 3 for K = 1 (configs[1] 2.13 →
+        // 2.03, configs[2] 1.14 → 1.12 ms; 4 slows configs[0]), 6 for K > 1, where the channel-split
+        // kernels carry the PCG and the unsplit ones want fewer blocks (configs[3] 1.87 → 1.72 ms)
+        int vpt = K > 1 ? 6 : 3;
         if (const char* e = std::getenv("FBS_VPT")) vpt = std::max(1, std::min(64, std::atoi(e)));  // A/B
         const int64_t want = (g->maxFrameM + (int64_t)kThreads * vpt - 1) / ((int64_t)kThreads * vpt);
         const int64_t cap = std::max<int64_t>(1, ((int64_t)g_num_sms * std::max(occ, 1) + F - 1) / F);
