@@ -1384,7 +1384,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             size_t b = M4 * (C + 2 + 8 * (size_t)K + C + 2 * (size_t)K) + (size_t)16 * kVecPad * 16 + (1 << 20);
             if (g->L > 1) {
                 const size_t c1 = g->capH.size() > 1 ? (size_t)g->capH[1] : 0;
-                b += 16 * C * c1 + 16 * C * ((size_t)g->tree.nTiles1 + 1);
+                b += 16 * (C + 1) * c1 + 16 * (C + 1) * ((size_t)g->tree.nTiles1 + 1);  // + the side PDA's level-1 scratch
                 for (size_t k = 1; k < g->capH.size(); ++k) b += 4 * (size_t)g->capH[k] + 256;
                 if (g->capH.size() > 3) b += 4 * (g->capH.size() - 3) * (size_t)g->capH[2];
             }
@@ -1423,7 +1423,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         // every buffer that must start at zero, in one block zeroed by one launch: the input-check
         // flags (FBS_ST_NEG_CONF / FBS_ST_NONFINITE from the splats), the last-block counters, the
         // lift's per-(frame, channel) tile counters, the forward PCG scalars, the low-rank Gram counters
-        const size_t zInts = 8 + (size_t)2 * F * K + (size_t)(K + 1) * F + F;
+        const size_t zInts = 8 + (size_t)2 * F * K + (size_t)(K + 1) * F + F + F;
         const size_t zDoubles = scalars_doubles(F * K);
         double* zblk = dalloc<double>(A, zDoubles + (zInts + 1) / 2, s);
         zero_words(zblk, (zDoubles + (zInts + 1) / 2) * sizeof(double), s);
@@ -1434,6 +1434,7 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         S->counters2 = S->counters + (size_t)F * K;
         S->tcount = S->counters + (size_t)2 * F * K;        // [K + 1][F] (k_tree_lift)
         unsigned* zctr = S->tcount + (size_t)(K + 1) * F;    // [F] (k_gram)
+        unsigned* pdaTcount = zctr + F;                      // [F] (the side PDA lift)
         // a4: splat Sc, b = S(c∘t)
         LAUNCH(k_splat<true>, grid_for(g->ncells * 32, 256, 1 << 20), 256, 0, s, geo, g->cellOff, g->heads, g->perm, c, t,
                K, M, S->sc, bIn, S->inflags);
@@ -1528,10 +1529,34 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
         LAUNCH(k_assemble, vec_blocks(as), kThreads, 0, s, as, S->diagA, S->mu0, init_mode, S->fwd);
         // a6/a7: hierarchical preconditioner multipliers μ_k = z_w P(1) / P(diag A), and init
         // (running the two concurrently on two streams measured slower: 5.10 vs 4.99 ms per step)
+        // With both, the multipliers run on a side stream beside the init (their own level-1
+        // scratch; the two share only the grid's read-only tree): since the PDL trigger change
+        // (fbs_common.cuh) this overlap pays — FBS_PDA_SIDE=0 serialises (A/B).
+        static const bool pdaSideEnv = [] {
+            const char* e = std::getenv("FBS_PDA_SIDE");
+            return !(e && e[0] == '0');
+        }();
+        const bool pdaSide = pdaSideEnv && hierP && hierI;
+        cudaStream_t spda = s;
         if (hierP) {
             HierArgs h = make_hier(S, 1, o.precond_alpha, o.precond_beta);
-            tree_lift<HIER_PDA>(S, h, S->diagA, s);  // (P diag A)_1 (diag A is the lift's input)
-            tree_coarse<HIER_PDA>(S, h, a, 0, s);
+            if (pdaSide) {
+                const int64_t M1 = g->lv[1].M;
+                const int nT = g->tree.nTiles1;
+                h.buf1T = dalloc<float>(A, (size_t)M1, s);
+                h.locT = dalloc<double>(A, (size_t)M1, s);
+                h.tileAgg = dalloc<double>(A, (size_t)nT, s);
+                h.tileBase = dalloc<double>(A, (size_t)nT, s);
+                h.tcount = pdaTcount;
+                spda = group_stream(dev, s, 3);
+                cudaEvent_t ev;
+                ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+                ck(event_record(ev, s), "event");
+                ck(stream_wait(spda, ev), "wait");
+                cudaEventDestroy(ev);
+            }
+            tree_lift<HIER_PDA>(S, h, S->diagA, spda);  // (P diag A)_1 (diag A is the lift's input)
+            tree_coarse<HIER_PDA>(S, h, a, 0, spda);
         }
         if (hierI) {
             HierArgs h = make_hier(S, Kc + 1, o.init_alpha, o.init_beta);
@@ -1547,6 +1572,13 @@ static void solve_impl(fbs_grid g, const float* t, int K, const float* c, double
             tree_lift<HIER_INIT>(S, h, w0i, s);
             tree_coarse<HIER_INIT>(S, h, a, 0, s);
             tree_level0<HIER_INIT>(S, h, a, w0i, S->xh, 0, s);
+        }
+        if (pdaSide) {  // join: the PCG's multipliers come from the side stream
+            cudaEvent_t ev;
+            ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+            ck(event_record(ev, spda), "event");
+            ck(stream_wait(s, ev), "wait");
+            cudaEventDestroy(ev);
         }
         if (hierP && g->L > 3) {
             auto km = k_tree_anc_mult<HIER_PCG>;
