@@ -59,6 +59,16 @@ def kernel_bytes(name, M, lv, N):
     return table.get(name)
 
 
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's measured copy bandwidth, else the profiling guide's
+    fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return 6650.0, "B200_PROFILING.md fallback"
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -409,12 +419,7 @@ def main():
         kname, kv = max(cand, key=lambda kv_: kv_[1]["wall_share_ms_per_step"])
         bytes_launch = launch_bytes(kname)
         achieved = bytes_launch / (kv["avg_us"] * 1e-6) / 1e9
-        peak, peak_src = 6545.6, "MEASURED_PEAKS.json hbm_gbs (measured copy)"
-        try:
-            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
-                peak = float(json.load(fh)["hbm_gbs"])
-        except Exception:
-            peak, peak_src = 6650.0, "B200_PROFILING.md fallback"
+        peak, peak_src = hbm_peak()
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
@@ -480,7 +485,9 @@ def main():
 
     def gb(nb):
         def f():
-            gx = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=nb)
+            # without the pyramid, which otherwise runs beside Alg. 1 on a side stream and would
+            # hide in the 20-iteration build but not in the 0-iteration one
+            gx = fbs.grid_build(rgb_d, *SIGMAS, n_bistoch=nb, build_pyramid=False)
             gx.close()
         return f
 
@@ -500,7 +507,7 @@ def main():
     it_bytes = sum(kernel_bytes(k, M, lv, w.pixels) for k in
                    ("k_spmv2", "k_hier_level0<UPDATE>", "k_tree_lift<PCG>", "k_tree_level0<PCG>"))
     pcg_iteration_rate = {"algorithmic_bytes": it_bytes, "GBps": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9,
-                          "frac": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9 / 6550.7,  # of measured copy BW
+                          "frac": it_bytes / (pcg24 / (ITERS - 1) * 1e-3) / 1e9 / hbm_peak()[0],  # of the measured copy bandwidth
                           "note": "one PCG iteration over all frames (both groups): spmv + update + lift + level0 "
                                   "byte models (coarse levels unmodelled) over its wall time, measured as "
                                   "(solve with 25 iterations - solve with 1) / 24, median of 5 interleaved rounds"}
@@ -515,14 +522,14 @@ def main():
     pcg_iteration_rate["floor_bytes_per_vertex"] = floor_bpv
     pcg_iteration_rate["modelled_bytes_per_vertex"] = it_bytes / max(M, 1)
     pcg_iteration_rate["floor_GBps"] = floor_bpv * M / t_it / 1e9
-    pcg_iteration_rate["floor_frac"] = floor_bpv * M / t_it / 1e9 / 6550.7
+    pcg_iteration_rate["floor_frac"] = floor_bpv * M / t_it / 1e9 / hbm_peak()[0]
     pcg_iteration_rate["modelled_over_floor"] = it_bytes / max(floor_bpv * M, 1)
     bistoch_rate = {"algorithmic_bytes": kernel_bytes("k_bistoch", M, lv, w.pixels),
                     "GBps": 20 * kernel_bytes("k_bistoch", M, lv, w.pixels) / (bs_wall * 1e-3) / 1e9 if bs_wall else None,
                     "note": "one Alg. 1 iteration over all frames (all groups) over its wall time, measured as "
-                            "(grid build with 20 iterations - grid build with 0) / 20"}
+                            "(grid build with 20 iterations - grid build with 0) / 20, both without the pyramid"}
     if bistoch_rate["GBps"]:
-        bistoch_rate["frac"] = bistoch_rate["GBps"] / 6550.7
+        bistoch_rate["frac"] = bistoch_rate["GBps"] / hbm_peak()[0]
     # the other stages against their algorithmic bytes (DESIGN §7 byte models; summed launch times,
     # single-stream stages): grid build (sort + write + neighbours) and slice
     stage_rates = {}
@@ -531,7 +538,7 @@ def main():
         by_ = sum(kernel_bytes(n, M, lv, w.pixels) for n in names if n in kernels)
         if ms_ > 0:
             stage_rates[st] = {"ms": ms_, "algorithmic_bytes": by_, "GBps": by_ / (ms_ * 1e-3) / 1e9,
-                               "frac": by_ / (ms_ * 1e-3) / 1e9 / 6550.7}
+                               "frac": by_ / (ms_ * 1e-3) / 1e9 / hbm_peak()[0]}
 
     # ---- end to end through the public API with host buffers: every step copies its inputs H2D from
     # pinned memory and its result D2H inside the timed region.  Double-buffered: the H2D of step
@@ -745,7 +752,7 @@ def main():
                   # algorithmic bytes: per pixel 11 (distances: rgb 3, Dx, Dy 8) + 8 (input
                   # copied to the output) + 3 iterations × 2 passes × 12 (value read + write, weight read)
                   "dt_post_filter_rate": {"bytes_per_pixel": 91, "GBps": 91 * w.pixels / (dt_ms / 1e3) / 1e9,
-                                          "frac": 91 * w.pixels / (dt_ms / 1e3) / 1e9 / 6550.7},
+                                          "frac": 91 * w.pixels / (dt_ms / 1e3) / 1e9 / hbm_peak()[0]},
                   "robust_ms_per_irls_round": rb_ms,
                   "robust": f"{F} frames, sigma_gm = 10, hier+hier, {ITERS} PCG iters per round (Supp. Alg. 3)",
                   "configs3_full_solve_ms": full_ms, "configs3_lowrank_solve_ms": lr_ms,
