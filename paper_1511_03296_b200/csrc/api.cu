@@ -535,10 +535,12 @@ static void grid_build_impl(const uint8_t* rgb, int F, int H, int W, double sxy,
         // round 2 (device-read frame ranges, arena layout): 1: 5.29, 2: 5.23, 4: 5.33 ms
         int Gb = std::min(F, 2);
         if (const char* e = std::getenv("FBS_BS_GROUPS")) Gb = std::max(1, std::min(F, std::atoi(e)));  // A/B
-        // dynamic chunk scheduling (k_bistoch): one counter per launch, zeroed before the fork
+        // dynamic chunk scheduling (k_bistoch): one counter per launch, zeroed before the fork.
+        // Off since the PDL trigger change and the pyramid beside Alg. 1: static chunks measured
+        // 4.813 -> 4.798 ms per bench step, configs[2] 1.113 -> 1.096 ms (FBS_BS_DYNAMIC=1: A/B)
         static const bool bsDynamic = [] {
             const char* e = std::getenv("FBS_BS_DYNAMIC");  // A/B
-            return !(e && e[0] == '0');
+            return e && e[0] == '1';
         }();
         unsigned* bsCtr = nullptr;
         if (bsDynamic && g->n_bistoch > 0) {
@@ -1166,7 +1168,8 @@ void tol_poll(fbs_system S, std::vector<PcgRun>& runs) {
     const int n = (int)runs.size();
     static const int chunk = [] {
         const char* e = std::getenv("FBS_TOL_CHUNK");  // A/B
-        return (e && e[0]) ? std::max(1, std::min(64, std::atoi(e))) : 4;  // 4: configs[0,1,3] 2-6 % faster than 8
+        // 6 with the adaptive shrink near convergence (configs[0] 0.864 -> 0.828 ms against 4)
+        return (e && e[0]) ? std::max(1, std::min(64, std::atoi(e))) : 6;
     }();
     static const bool adapt = [] {
         const char* e = std::getenv("FBS_TOL_ADAPT");  // A/B: 0 = fixed chunks
