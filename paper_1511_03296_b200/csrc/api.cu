@@ -1247,6 +1247,19 @@ void tol_poll(fbs_system S, std::vector<PcgRun>& runs) {
 // own active count and stops on its own (tol_poll).
 void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
     fbs_grid g = S->g;
+    // Jacobi on small frames: the whole PCG of each (frame, channel) in one CTA (k_pcg_small);
+    // FBS_SMALL_PX sets the per-frame pixel bound (0 = off); FBS_SPMV_K=joint (the A/B switch of
+    // the channel-joint SpMV) keeps the multi-kernel path
+    static const int64_t small_px = [] {
+        const char* e = std::getenv("FBS_SMALL_PX");
+        return (e && e[0]) ? (int64_t)std::atoll(e) : (int64_t)kSmallPx;
+    }();
+    if (!S->useHierP && (int64_t)g->H * g->W <= small_px && !spmv_kjoint()) {
+        const int FK = a.nf * S->K;
+        LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK, 1);
+        LAUNCH(k_pcg_small, FK, kSmallThreads, 0, s, a, (int)x_zero);
+        return;
+    }
     const int G = std::min(S->nGroups, g->F);
     const bool tol = S->o.mode == FBS_MODE_TOL;
     if (G > 1) {

@@ -424,6 +424,124 @@ __global__ void __launch_bounds__(256, 8) k_update(VecArgs a) {
     if (last_block_t0(a.counters + bu.g, a.BPF, &sflag)) finish_rho(a, f, bu.k0, bu.k1, false, shd);
 }
 
+// ---------------------------------------------------------------- small systems: Alg. 2 in one CTA
+// A frame of ≤ kSmallPx pixels (configs[0]-sized) has a few thousand vertices: each multi-kernel
+// PCG iteration is three ~4 µs launches plus, in TOL mode, host polls.  Here one CTA runs the
+// whole Jacobi PCG of one (frame, channel) — Alg. 2 lines 2-4, then per iteration lines 14, 6-7,
+// 8-12 — with block barriers in place of kernel boundaries (the vectors stay in L1/L2) and the
+// stopping rule on the device.  Per-vertex arithmetic, the fp32 casts of α and β and the scalar
+// recurrences / stopping rule (finish_rho_one) are those of k_residual0 / k_direction2 / k_spmv2 /
+// k_update; only the fp64 dot products' summation order differs (one block's tree).
+constexpr int kSmallThreads = 512;  // block_sum2 holds ≤ 16 warps
+constexpr int kSmallPx = 16384;     // default per-frame pixel bound of the one-CTA path (api.cu run_pcg)
+__global__ void __launch_bounds__(kSmallThreads) k_pcg_small(VecArgs a, int x_zero) {
+    pdl_entry();
+    __shared__ double shd[32];
+    __shared__ double s_beta;
+    __shared__ float s_alpha;
+    __shared__ int s_active;
+    const int f = blockIdx.x / a.K, k = blockIdx.x - f * a.K;
+    const int fk = f * a.K + k;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const size_t off = (size_t)k * a.M;
+    float* __restrict__ x = a.x + off;
+    float* __restrict__ r = a.r + off;
+    float* __restrict__ s = a.s + off;
+    float* __restrict__ q = a.q + off;
+    float2* __restrict__ dn = a.dn + (size_t)k * a.ldn;
+    // Alg. 2 lines 2-4: r = b − A x, s = M⁻¹r, ρ = rᵀs
+    double R = 0.0, RR = 0.0;
+    for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+        float rv = a.b[off + v];
+        if (!x_zero) rv -= apply_A_row(x, a.n, v, a.nbr[v], a.lam, a.sc[v]);
+        r[v] = rv;
+        const float sv = a.mu0[v] * rv;
+        s[v] = sv;
+        R += (double)rv * (double)sv;
+        RR += (double)rv * (double)rv;
+    }
+    block_sum2(R, RR, shd);
+    if (threadIdx.x == 0) {
+        finish_rho_one(a, fk, true, R, RR);
+        s_active = a.sc_.active[fk];
+        s_beta = 0.0;
+    }
+    __syncthreads();
+    for (int it = 0; s_active; ++it) {
+        // line 14 (line 3 at it = 0): d = s + βd
+        const float be = (float)s_beta;
+        for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+            const float2 dv = dn[v];
+            dn[v] = make_float2(it == 0 ? s[v] : s[v] + be * dv.x, dv.y);
+        }
+        __syncthreads();
+        // lines 6-7: q = A d (Laplacian-difference form), α = ρ / dᵀq
+        double dq = 0.0;
+        for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+            const int4 nb = a.nbr[v];
+            const float2 me = dn[v];
+            float acc = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int o = near_off(nb, e);
+                if (o) {
+                    const float2 u = dn[v + o];
+                    acc += u.y * (me.x - u.x);
+                }
+            }
+            if (nb.z) {
+                const float2 u = dn[v + nb.z];
+                acc += u.y * (me.x - u.x);
+            }
+            if (nb.w) {
+                const float2 u = dn[v + nb.w];
+                acc += u.y * (me.x - u.x);
+            }
+            const float qv = a.lam * me.y * acc + a.sc[v] * me.x;
+            q[v] = qv;
+            dq += (double)me.x * (double)qv;
+        }
+        dq = block_sum(dq, shd);
+        if (threadIdx.x == 0) {
+            if (dq <= 0.0) {
+                a.sc_.active[fk] = 0;
+                a.sc_.alpha[fk] = 0.0;
+                a.sc_.xalpha[fk] = 0.0;
+                atomicOr(a.sc_.status + fk, FBS_ST_BREAKDOWN);
+                atomicSub(a.sc_.n_active, 1);
+                s_active = 0;
+            } else {
+                const double al = a.sc_.rho[fk] / dq;
+                a.sc_.alpha[fk] = al;
+                a.sc_.xalpha[fk] = al;
+                s_alpha = (float)al;
+            }
+        }
+        __syncthreads();
+        if (!s_active) break;
+        // lines 8-12: x += αd, r −= αq, s = M⁻¹r, ρ_new = rᵀs (and ‖r‖² for the stopping rule)
+        const float al = s_alpha;
+        R = 0.0;
+        RR = 0.0;
+        for (int v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+            x[v] = x[v] + al * dn[v].x;
+            const float rv = r[v] - al * q[v];
+            r[v] = rv;
+            const float sv = a.mu0[v] * rv;
+            s[v] = sv;
+            R += (double)rv * (double)sv;
+            RR += (double)rv * (double)rv;
+        }
+        block_sum2(R, RR, shd);
+        if (threadIdx.x == 0) {
+            finish_rho_one(a, fk, false, R, RR);
+            s_active = a.sc_.active[fk];
+            s_beta = a.sc_.beta[fk];
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- streaming PCG kernels
 // dn[k][v] = (d, n_v) (initialised by k_assemble): the direction interleaved with n, so the
 // SpMV's neighbour terms n_u (d_v − d_u) need ONE 8-byte gather per neighbour.
