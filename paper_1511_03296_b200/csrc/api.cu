@@ -1254,10 +1254,17 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         const char* e = std::getenv("FBS_SMALL_PX");
         return (e && e[0]) ? (int64_t)std::atoll(e) : (int64_t)kSmallPx;
     }();
-    if (!S->useHierP && (int64_t)g->H * g->W <= small_px && !spmv_kjoint()) {
+    // larger frames up to FBS_CLUSTER_PX pixels: a cluster of kPcgCluster CTAs per (frame, channel)
+    static const int64_t cluster_px = [] {
+        const char* e = std::getenv("FBS_CLUSTER_PX");
+        return (e && e[0]) ? (int64_t)std::atoll(e) : (int64_t)kClusterPx;
+    }();
+    const int64_t HWf = (int64_t)g->H * g->W;
+    if (!S->useHierP && (HWf <= small_px || HWf <= cluster_px) && !spmv_kjoint()) {
         const int FK = a.nf * S->K;
         LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK, 1);
-        LAUNCH(k_pcg_small, FK, kSmallThreads, 0, s, a, (int)x_zero);
+        if (HWf <= small_px) LAUNCH(k_pcg_small, FK, kSmallThreads, 0, s, a, (int)x_zero);
+        else LAUNCH(k_pcg_cluster, FK * kPcgCluster, kSmallThreads, 0, s, a, (int)x_zero);
         return;
     }
     const int G = std::min(S->nGroups, g->F);

@@ -12,6 +12,7 @@
 #pragma once
 #include "fbs_common.cuh"
 #include "grid_kernels.cuh"
+#include <cooperative_groups.h>
 
 namespace fbs {
 
@@ -540,6 +541,152 @@ __global__ void __launch_bounds__(kSmallThreads) k_pcg_small(VecArgs a, int x_ze
         }
         __syncthreads();
     }
+}
+
+// Medium frames: the same one-launch Jacobi PCG with a cluster of kPcgCluster CTAs per (frame,
+// channel).  Vertex v of the frame belongs to CTA rank (v − v0) / blockDim mod kPcgCluster; a
+// phase's dot product is each CTA's block tree, its partial left in shared memory, then summed by
+// every CTA over the cluster's ranks in rank order through distributed shared memory — the same
+// value in every CTA, so each CTA takes the same α, β and stopping decision (rank 0 alone writes
+// the global scalars through finish_rho_one).  Three cluster barriers per iteration (after the
+// direction: the SpMV gathers other CTAs' d; after each reduction); the (d, n) vector, shared
+// across CTAs, goes through L2 (ld/st.cg), the per-vertex vectors stay with their owner thread.
+constexpr int kPcgCluster = 8;
+constexpr int kClusterPx = 262144;  // default per-frame pixel bound of the cluster path (api.cu run_pcg)
+__global__ void __cluster_dims__(kPcgCluster, 1, 1) __launch_bounds__(kSmallThreads, 2)
+    k_pcg_cluster(VecArgs a, int x_zero) {
+    namespace cg = cooperative_groups;
+    pdl_entry();
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ double shd[32];
+    __shared__ double part[2][2];  // [slot][value]: slot 0 the SpMV's dᵀq, slot 1 (ρ, ‖r‖²)
+    const int rank = (int)cl.block_rank();
+    const int u = blockIdx.x / kPcgCluster;
+    const int f = u / a.K, k = u - f * a.K;
+    const int fk = f * a.K + k;
+    const int v0 = a.frameOff[f], v1 = a.frameOff[f + 1];
+    const int vbeg = v0 + rank * blockDim.x + threadIdx.x, stride = kPcgCluster * blockDim.x;
+    const size_t off = (size_t)k * a.M;
+    float* __restrict__ x = a.x + off;
+    float* __restrict__ r = a.r + off;
+    float* __restrict__ s = a.s + off;
+    float* __restrict__ q = a.q + off;
+    float2* dn = a.dn + (size_t)k * a.ldn;
+    // cluster-wide sums of slot `sl` (after the barrier that published every CTA's partial)
+    auto cluster_sum = [&](int sl, double& s0, double& s1) {
+        s0 = 0.0;
+        s1 = 0.0;
+        for (int q2 = 0; q2 < kPcgCluster; ++q2) {
+            const double* p = cl.map_shared_rank(&part[sl][0], q2);
+            s0 += p[0];
+            s1 += p[1];
+        }
+    };
+    const double bb = a.sc_.bb[fk];
+    // Alg. 2 lines 2-4
+    double R = 0.0, RR = 0.0;
+    for (int v = vbeg; v < v1; v += stride) {
+        float rv = a.b[off + v];
+        if (!x_zero) rv -= apply_A_row(x, a.n, v, a.nbr[v], a.lam, a.sc[v]);
+        r[v] = rv;
+        const float sv = a.mu0[v] * rv;
+        s[v] = sv;
+        R += (double)rv * (double)sv;
+        RR += (double)rv * (double)rv;
+    }
+    block_sum2(R, RR, shd);
+    if (threadIdx.x == 0) {
+        part[1][0] = R;
+        part[1][1] = RR;
+    }
+    cl.sync();
+    cluster_sum(1, R, RR);
+    if (rank == 0 && threadIdx.x == 0) finish_rho_one(a, fk, true, R, RR);
+    double rho = R;
+    bool active = !(a.tol_mode && RR <= a.tol2 * bb) && R != 0.0 && a.max_iters > 0;
+    double beta = 0.0;
+    for (int it = 0; active; ++it) {
+        const float be = (float)beta;
+        for (int v = vbeg; v < v1; v += stride) {
+            const float2 dv = __ldcg(dn + v);
+            __stcg(dn + v, make_float2(it == 0 ? s[v] : s[v] + be * dv.x, dv.y));
+        }
+        cl.sync();
+        double dq = 0.0;
+        for (int v = vbeg; v < v1; v += stride) {
+            const int4 nb = a.nbr[v];
+            const float2 me = __ldcg(dn + v);
+            float acc = 0.f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int o = near_off(nb, e);
+                if (o) {
+                    const float2 w = __ldcg(dn + v + o);
+                    acc += w.y * (me.x - w.x);
+                }
+            }
+            if (nb.z) {
+                const float2 w = __ldcg(dn + v + nb.z);
+                acc += w.y * (me.x - w.x);
+            }
+            if (nb.w) {
+                const float2 w = __ldcg(dn + v + nb.w);
+                acc += w.y * (me.x - w.x);
+            }
+            const float qv = a.lam * me.y * acc + a.sc[v] * me.x;
+            q[v] = qv;
+            dq += (double)me.x * (double)qv;
+        }
+        dq = block_sum(dq, shd);
+        if (threadIdx.x == 0) {
+            part[0][0] = dq;
+            part[0][1] = 0.0;
+        }
+        cl.sync();
+        double DQ, unused;
+        cluster_sum(0, DQ, unused);
+        if (DQ <= 0.0) {
+            if (rank == 0 && threadIdx.x == 0) {
+                a.sc_.active[fk] = 0;
+                a.sc_.alpha[fk] = 0.0;
+                a.sc_.xalpha[fk] = 0.0;
+                atomicOr(a.sc_.status + fk, FBS_ST_BREAKDOWN);
+                atomicSub(a.sc_.n_active, 1);
+            }
+            break;
+        }
+        const double alpha = rho / DQ;
+        if (rank == 0 && threadIdx.x == 0) {
+            a.sc_.alpha[fk] = alpha;
+            a.sc_.xalpha[fk] = alpha;
+        }
+        const float al = (float)alpha;
+        R = 0.0;
+        RR = 0.0;
+        for (int v = vbeg; v < v1; v += stride) {
+            x[v] = x[v] + al * __ldcg(dn + v).x;
+            const float rv = r[v] - al * q[v];
+            r[v] = rv;
+            const float sv = a.mu0[v] * rv;
+            s[v] = sv;
+            R += (double)rv * (double)sv;
+            RR += (double)rv * (double)rv;
+        }
+        block_sum2(R, RR, shd);
+        if (threadIdx.x == 0) {
+            part[1][0] = R;
+            part[1][1] = RR;
+        }
+        cl.sync();
+        cluster_sum(1, R, RR);
+        if (rank == 0 && threadIdx.x == 0) finish_rho_one(a, fk, false, R, RR);
+        // finish_rho_one's recurrence and stopping rule, taken identically by every CTA
+        beta = R / rho;
+        rho = R;
+        const bool conv = a.tol_mode && RR <= a.tol2 * bb;
+        if (conv || R == 0.0 || it + 1 >= a.max_iters) active = false;
+    }
+    cl.sync();  // no CTA exits while another may still read its partials
 }
 
 // ---------------------------------------------------------------- streaming PCG kernels

@@ -495,7 +495,7 @@ def test_launch_counter_and_profile():
     rep = fbs.profile_report()
     assert fbs.launch_count() > n0
     assert rep["k_grid_sort"][0] == 1
-    if rgb.shape[1] * rgb.shape[2] <= 16384:  # a small-frame Jacobi solve: one CTA per channel
+    if rgb.shape[1] * rgb.shape[2] <= 16384:  # a small-frame Jacobi solve: one CTA per (frame, channel)
         assert rep["k_pcg_small"][0] == 1 and "k_spmv2" not in rep
     else:
         assert rep["k_spmv2"][0] == 3 and rep["k_direction2"][0] == 3

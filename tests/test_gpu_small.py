@@ -1,6 +1,7 @@
-"""The one-CTA Jacobi PCG for small frames (k_pcg_small, api.cu run_pcg) against the oracle and
-against the multi-kernel path of the same library (FBS_SMALL_PX=0, in a subprocess: the bound is
-read once per process).  Same per-vertex arithmetic and stopping rule (Alg. 2;
+"""The one-launch Jacobi PCG for small frames (k_pcg_small: one CTA; k_pcg_cluster: a cluster of 8
+CTAs per (frame, channel); api.cu run_pcg) against the oracle and against the multi-kernel path of
+the same library (FBS_SMALL_PX=0 FBS_CLUSTER_PX=0, in a subprocess: the bounds are read once per
+process).  Same per-vertex arithmetic and stopping rule (Alg. 2;
 reading #11); only the fp64 dot products' summation order differs, so the two paths agree to
 fp32 rounding and stop within one iteration of each other.
 """
@@ -27,6 +28,9 @@ CASES = {
     "c1": dict(name="c1", kw={}),                                              # configs[0]: 48x64
     "c5_3f": dict(name="c5", kw=dict(frames=3, W=120, H=96, n_cells=12)),      # 3 small frames
     "c4_k": dict(name="c4", kw=dict(W=100, H=75, n_cells=8)),                  # K > 1 channels
+    # > 16384 px: the cluster path (k_pcg_cluster, 8 CTAs per (frame, channel))
+    "c5_mid": dict(name="c5", kw=dict(frames=2, W=320, H=240, n_cells=30)),
+    "c4_mid": dict(name="c4", kw=dict(W=300, H=225, n_cells=16)),
 }
 MODES = {
     "tol": dict(precond="jacobi", init="flat", mode="tol", tol=1e-6, max_iters=5000),
@@ -60,7 +64,7 @@ def _multi_kernel(case, mode, backward):
         "np.savez('gpurun_out/_small_ref.npz', **{k: np.asarray(v) for k, v in o.items()})"
     )
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    env = dict(os.environ, FBS_SMALL_PX="0")
+    env = dict(os.environ, FBS_SMALL_PX="0", FBS_CLUSTER_PX="0")
     subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, check=True, timeout=600)
     z = np.load(os.path.join(ROOT, "gpurun_out", "_small_ref.npz"))
     return {k: z[k] for k in z.files}
