@@ -27,7 +27,7 @@
  *     (+ slice, backward, low-rank) can be captured into a CUDA graph and replayed.  The
  *     exceptions are stated per call: TOL-mode solves poll the device's active count from the
  *     host unless the stream is capturing (then a device-side loop is captured) or the solve is
- *     a small-frame Jacobi one (one CTA per (frame, channel), fbs_solve); the query and
+ *     a Jacobi one on frames of ≤ 262144 pixels (one launch, fbs_solve); the query and
  *     export calls (fbs_grid_info, *_export, *_stats) synchronise.
  *   - Layouts: RGB is interleaved uint8 [frames][H][W][3]; pixel vectors are planar float
  *     [frames][K][H][W] (pixel p = y·W + x); confidences float [frames][H][W];
@@ -191,8 +191,9 @@ void fbs_grid_destroy(fbs_grid g);
  * point) behind and returns when all have stopped; when `stream` is being captured into a CUDA
  * graph it adds a conditional while node instead (device-side loop, no host polls, replayable);
  * FBS_TOL_GRAPH=1 runs such a loop as its own graph per solve.  Jacobi solves of frames of
- * ≤ 16384 pixels (FBS_SMALL_PX) run each (frame, channel)'s whole PCG in one CTA instead, in
- * either mode enqueue-only (the stopping rule is decided on the device).
+ * ≤ 16384 pixels (FBS_SMALL_PX) run each (frame, channel)'s whole PCG in one CTA instead, and of
+ * ≤ 262144 pixels (FBS_CLUSTER_PX) in one cluster of 8 CTAs: one launch, in either mode
+ * enqueue-only (the stopping rule is decided on the device).
  * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4): the reduced solve
  * carries K channels of which those at or above the frame's kept rank t_f have zero right-hand
  * sides and retire at iteration 0 (no host synchronisation); sys_out must then be NULL.

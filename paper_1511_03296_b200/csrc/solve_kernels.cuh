@@ -551,9 +551,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_pcg_small(VecArgs a, int x_ze
 // the global scalars through finish_rho_one).  Three cluster barriers per iteration (after the
 // direction: the SpMV gathers other CTAs' d; after each reduction); the (d, n) vector, shared
 // across CTAs, goes through L2 (ld/st.cg), the per-vertex vectors stay with their owner thread.
+#ifndef FBS_CLUSTER_MINB
+#define FBS_CLUSTER_MINB 2  // resident CTAs per SM the register budget allows (A/B: -DFBS_CLUSTER_MINB=3)
+#endif
 constexpr int kPcgCluster = 8;
 constexpr int kClusterPx = 262144;  // default per-frame pixel bound of the cluster path (api.cu run_pcg)
-__global__ void __cluster_dims__(kPcgCluster, 1, 1) __launch_bounds__(kSmallThreads, 2)
+__global__ void __cluster_dims__(kPcgCluster, 1, 1) __launch_bounds__(kSmallThreads, FBS_CLUSTER_MINB)
     k_pcg_cluster(VecArgs a, int x_zero) {
     namespace cg = cooperative_groups;
     pdl_entry();
