@@ -191,9 +191,9 @@ void fbs_grid_destroy(fbs_grid g);
  * point) behind and returns when all have stopped; when `stream` is being captured into a CUDA
  * graph it adds a conditional while node instead (device-side loop, no host polls, replayable);
  * FBS_TOL_GRAPH=1 runs such a loop as its own graph per solve.  Jacobi solves of frames of
- * ≤ 16384 pixels (FBS_SMALL_PX) run each (frame, channel)'s whole PCG in one CTA instead, and of
- * ≤ 262144 pixels (FBS_CLUSTER_PX) in one cluster of 8 CTAs: one launch, in either mode
- * enqueue-only (the stopping rule is decided on the device).
+ * ≤ 8192 pixels (FBS_SMALL_PX) run each (frame, channel)'s whole PCG in one CTA instead, and of
+ * ≤ 98304 pixels (≤ 262144 with ≥ 16 (frame, channel)s; FBS_CLUSTER_PX) in one cluster of 8
+ * CTAs: one launch, in either mode enqueue-only (the stopping rule is decided on the device).
  * opts->lowrank_eps > 0 with K > 1 reduces B per frame first (Supp. §4): the reduced solve
  * carries K channels of which those at or above the frame's kept rank t_f have zero right-hand
  * sides and retire at iteration 0 (no host synchronisation); sys_out must then be NULL.

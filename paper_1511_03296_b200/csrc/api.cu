@@ -1259,9 +1259,13 @@ void run_pcg(fbs_system S, const VecArgs& a, bool x_zero, cudaStream_t s) {
         const char* e = std::getenv("FBS_CLUSTER_PX");
         return (e && e[0]) ? (int64_t)std::atoll(e) : (int64_t)kClusterPx;
     }();
+    // (measured, scripts/ab_cluster_sizes.py: the cluster path wins up to 240x320 at any K, ties
+    // the multi-kernel path at 375x500 with K = 21 and loses 2x there with K ≤ 3, whose 8-24
+    // CTAs leave most SMs idle; so beyond kClusterPxAnyK pixels it needs ≥ 16 (frame, channel)s)
     const int64_t HWf = (int64_t)g->H * g->W;
-    if (!S->useHierP && (HWf <= small_px || HWf <= cluster_px) && !spmv_kjoint()) {
-        const int FK = a.nf * S->K;
+    const int FK = a.nf * S->K;
+    const bool cluster_ok = HWf <= cluster_px && (HWf <= kClusterPxAnyK || FK >= 16);
+    if (!S->useHierP && (HWf <= small_px || cluster_ok) && !spmv_kjoint()) {
         LAUNCH(k_init_scalars, (FK + 255) / 256, 256, 0, s, a.sc_, FK, 1);
         if (HWf <= small_px) LAUNCH(k_pcg_small, FK, kSmallThreads, 0, s, a, (int)x_zero);
         else LAUNCH(k_pcg_cluster, FK * kPcgCluster, kSmallThreads, 0, s, a, (int)x_zero);

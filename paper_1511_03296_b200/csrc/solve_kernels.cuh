@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(256, 8) k_update(VecArgs a) {
 // recurrences / stopping rule (finish_rho_one) are those of k_residual0 / k_direction2 / k_spmv2 /
 // k_update; only the fp64 dot products' summation order differs (one block's tree).
 constexpr int kSmallThreads = 512;  // block_sum2 holds ≤ 16 warps
-constexpr int kSmallPx = 16384;     // default per-frame pixel bound of the one-CTA path (api.cu run_pcg)
+constexpr int kSmallPx = 8192;      // default per-frame pixel bound of the one-CTA path (api.cu run_pcg)
 __global__ void __launch_bounds__(kSmallThreads) k_pcg_small(VecArgs a, int x_zero) {
     pdl_entry();
     __shared__ double shd[32];
@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_pcg_small(VecArgs a, int x_ze
 #endif
 constexpr int kPcgCluster = 8;
 constexpr int kClusterPx = 262144;  // default per-frame pixel bound of the cluster path (api.cu run_pcg)
+constexpr int kClusterPxAnyK = 98304;  // ... for any (frame, channel) count; above it ≥ 16 of them
 __global__ void __cluster_dims__(kPcgCluster, 1, 1) __launch_bounds__(kSmallThreads, FBS_CLUSTER_MINB)
     k_pcg_cluster(VecArgs a, int x_zero) {
     namespace cg = cooperative_groups;

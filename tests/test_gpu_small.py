@@ -28,7 +28,7 @@ CASES = {
     "c1": dict(name="c1", kw={}),                                              # configs[0]: 48x64
     "c5_3f": dict(name="c5", kw=dict(frames=3, W=120, H=96, n_cells=12)),      # 3 small frames
     "c4_k": dict(name="c4", kw=dict(W=100, H=75, n_cells=8)),                  # K > 1 channels
-    # > 16384 px: the cluster path (k_pcg_cluster, 8 CTAs per (frame, channel))
+    # > 8192 px: the cluster path (k_pcg_cluster, 8 CTAs per (frame, channel))
     "c5_mid": dict(name="c5", kw=dict(frames=2, W=320, H=240, n_cells=30)),
     "c4_mid": dict(name="c4", kw=dict(W=300, H=225, n_cells=16)),
 }
