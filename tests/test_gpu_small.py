@@ -56,25 +56,24 @@ def _solve(case, mode, backward=False):
     return w, out
 
 
-def _multi_kernel(case, mode, backward):
+def _multi_kernel(case, mode, backward, out_path):
     code = (
-        "import json, sys, numpy as np; sys.path.insert(0, 'tests'); "
-        "import test_gpu_small as T; import torch; "
+        "import sys, numpy as np; sys.path.insert(0, 'tests'); "
+        "import test_gpu_small as T; "
         f"w, o = T._solve({case!r}, {mode!r}, {backward!r}); "
-        "np.savez('gpurun_out/_small_ref.npz', **{k: np.asarray(v) for k, v in o.items()})"
+        f"np.savez({str(out_path)!r}, **{{k: np.asarray(v) for k, v in o.items()}})"
     )
-    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     env = dict(os.environ, FBS_SMALL_PX="0", FBS_CLUSTER_PX="0")
     subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, check=True, timeout=600)
-    z = np.load(os.path.join(ROOT, "gpurun_out", "_small_ref.npz"))
+    z = np.load(out_path)
     return {k: z[k] for k in z.files}
 
 
 @pytest.mark.parametrize("case", list(CASES))
 @pytest.mark.parametrize("mode", list(MODES))
-def test_small_path_vs_oracle_and_multi_kernel(case, mode):
+def test_small_path_vs_oracle_and_multi_kernel(case, mode, tmp_path):
     w, one = _solve(case, mode, backward=(mode == "tol"))
-    ref = _multi_kernel(case, mode, backward=(mode == "tol"))
+    ref = _multi_kernel(case, mode, (mode == "tol"), tmp_path / "multi_kernel.npz")
     # the one-CTA path ran: 2 launches per solve (scalars + k_pcg_small) plus set-up, against
     # several per PCG iteration on the multi-kernel path
     assert one["launches"] < ref["launches"]
